@@ -1,0 +1,512 @@
+#!/usr/bin/env python3
+"""bench.py — aggregate SPMD jobs/s through the B200 GVM (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vecadd|ep|bs|mm|mixed]
+                    [--procs P] [--impl ours|reference]
+
+One "step" = one SPMD round: each of the P processes sharing a GPU runs one
+job (SND -> STR -> STP -> RCV) through the unchanged client API. Legs:
+
+  value   device-resident: the GVM's batched launch over the P jobs of a step
+          with inputs already in HBM (rotating input sets > 2x L2), CUDA events
+          -> jobs/s; its dominant kernel gives `roofline`.
+  e2e     end to end: P forked SPMD processes (bin/vgpu-spmd) lease VGPUs from
+          a GVM that runs in THIS process (libvgpu.so via ctypes); every step
+          copies the inputs from the workers' host memory through shm, H2D,
+          kernel, D2H and back (bytes counted) -> jobs/s. The headline.
+  native  the non-virtualized baseline: the same P workers with NativeVgpu
+          (one CUDA context per process, pageable copies, time-sliced, no MPS).
+  cpu_baseline  the unmodified reference GVM (oracle/_ref/ref-bench, built
+          from /root/reference sources) on the box's host cores, bounded sample.
+
+Under torchrun (N > 1) every rank runs its own GVM on its GPU (weak scaling,
+P processes per GPU, no data-path collective); times are max over ranks and a
+single NCCL all-gather of per-GPU partial records is the final reduction.
+--impl reference runs only the reference arm (rank 0) and prints its line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import select
+import shutil
+import signal
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; kernel GB/s vs roofline"
+L2_BYTES = 126 << 20
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# ---- distributed plumbing -------------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.torch, self.dist, self.backend = torch, dist, backend
+
+    def barrier(self):
+        if self.torch:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.torch:
+            return x
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.torch:
+            return x
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def bcast(self, obj):
+        if not self.torch:
+            return obj
+        lst = [obj]
+        self.dist.broadcast_object_list(lst, src=0)
+        return lst[0]
+
+    def close(self):
+        if self.torch:
+            self.dist.destroy_process_group()
+
+
+# ---- clocks ------------------------------------------------------------------------
+
+class Clocks:
+    """nvidia-smi sampler over the timed regions (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+        self.windows = []
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        fd, self.path = tempfile.mkstemp(prefix="clocks", suffix=".csv")
+        os.close(fd)
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+             "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+            stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        time.sleep(0.3)
+
+    def mark(self, t0: float, t1: float):
+        self.windows.append((t0, t1))
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.send_signal(signal.SIGTERM)
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        power = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        loaded = [s for s, p in zip(sm, power) if p > 200.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(power) if power else None}
+
+
+# ---- helpers ------------------------------------------------------------------------
+
+def measured_peaks() -> dict:
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs"), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel_kind: str):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(kernel_kind)
+
+
+def spawn_workers(args_list, env):
+    procs = []
+    for a in args_list:
+        procs.append(subprocess.Popen(a, stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, env=env, cwd=REPO))
+    return procs
+
+
+def wait_ready(procs, timeout=300.0):
+    deadline = time.time() + timeout
+    for p in procs:
+        while True:
+            left = deadline - time.time()
+            if left <= 0:
+                raise TimeoutError("worker did not become ready")
+            r, _, _ = select.select([p.stdout], [], [], left)
+            if not r:
+                continue
+            line = p.stdout.readline().decode()
+            if not line:
+                err = p.stderr.read().decode()
+                raise RuntimeError(f"worker exited before READY: {err[-2000:]}")
+            if line.startswith("READY"):
+                break
+            if line.startswith("{"):
+                raise RuntimeError(f"worker failed: {line.strip()}")
+
+
+def collect(procs, timeout=1800.0):
+    out = []
+    for p in procs:
+        so, se = p.communicate(timeout=timeout)
+        lines = [l for l in so.decode().splitlines() if l.startswith("{")]
+        if not lines:
+            raise RuntimeError(f"worker produced no result (rc={p.returncode}): {se.decode()[-2000:]}")
+        out.append(json.loads(lines[-1]))
+    return out
+
+
+def timed_window(results, warmup):
+    """[first finish of the last warm-up round, last finish] in ns."""
+    begin = min((r["t1"][warmup - 1] if warmup else r["t0"][0]) for r in results)
+    end = max(r["t1"][-1] for r in results)
+    return begin, end
+
+
+# ---- legs ----------------------------------------------------------------------------
+
+def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup, device, sizes):
+    """Device-resident throughput of the batched kernel(s) of one step."""
+    by_kind = {}
+    for i in range(procs_per_gpu):
+        w = gid0 + i
+        k = W.kind_of(workload, w)
+        by_kind.setdefault(k, []).append(W.job_input(workload, w, total_workers, sizes))
+    legs = {}
+    ms_step = 0.0
+    launches = 0
+    for k, inputs in by_kind.items():
+        per_set = sum(len(b) + W.output_bytes(k, sizes) for b in inputs)
+        sets = max(2, min(64, -(-2 * L2_BYTES // max(1, per_set)) + 1))
+        if k == "ep":
+            sets = 2
+        r = V.resident_bench(W.PAYLOAD[k], inputs, sets, warmup, steps, device=device)
+        legs[k] = r
+        ms_step += r["ms_per_step"]
+        launches += r["launches_per_step"] * steps
+    dom = max(legs, key=lambda k: legs[k]["kernel_ms_per_launch"] * max(1, legs[k]["launches_per_step"]))
+    return legs, ms_step, launches, dom
+
+
+def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
+                sizes, dist):
+    """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
+    spmd = N.bin_path("vgpu-spmd")
+    inst = f"b200bench{os.getpid()}g{dist.local}"
+    env = dict(os.environ)
+    env["CUDA_VISIBLE_DEVICES"] = env.get("CUDA_VISIBLE_DEVICES", "")
+    if not env["CUDA_VISIBLE_DEVICES"]:
+        env.pop("CUDA_VISIBLE_DEVICES")
+    gvm = None
+    if not native:
+        V.unlink_os_instance(inst, procs)
+        cfg = V.GvmConfig(instance=inst, max_clients=procs, barrier_size=procs,
+                          per_client_shm_bytes=W.region_bytes(workload, sizes),
+                          barrier_window=2000, clock=V.ClockMode.Real, cuda_device=device,
+                          device_sms=148, device_max_kernels=128, device_slots_per_sm=32)
+        gvm = V.GvmDaemon.start_os(cfg)
+    size_args = ["--vecadd-n", str(sizes.vecadd_n), "--ep-m", str(sizes.ep_m),
+                 "--bs-n", str(sizes.bs_n), "--mm-n", str(sizes.mm_n)]
+    args = []
+    for i in range(procs):
+        a = [spmd, "--worker", str(gid0 + i), "--workers", str(total_workers), "--workload",
+             workload, "--rounds", str(warmup + steps)] + size_args
+        a += ["--native", "--device", str(device)] if native else ["--instance", inst]
+        args.append(a)
+    try:
+        ps = spawn_workers(args, env)
+        wait_ready(ps)
+        before = gvm.summary() if gvm else None
+        for p in ps:
+            p.stdin.write(b"g")
+            p.stdin.flush()
+        res = collect(ps)
+        after = gvm.summary() if gvm else None
+        batches = gvm.batches() if gvm else []
+        tasks = gvm.tasks() if gvm else []
+    finally:
+        if gvm:
+            gvm.stop()
+            gvm.close()
+    bad = [r for r in res if not r.get("ok")]
+    if bad:
+        raise RuntimeError(f"worker errors: {bad[:2]}")
+    t0, t1 = timed_window(res, warmup)
+    info = {"results": res, "t0": t0, "t1": t1, "seconds": (t1 - t0) * 1e-9}
+    if gvm:
+        info["launches_total"] = after["kernel_launches"] - before["kernel_launches"]
+        info["batches"] = batches
+        info["tasks"] = tasks
+    if native:
+        info["cold_ms"] = max((r["t1"][0] - r["t_go"]) * 1e-6 for r in res)
+    return info
+
+
+def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
+    """The unmodified reference GVM (oracle/_ref/ref-bench) on host cores."""
+    ref = os.path.join(REPO, "oracle", "_ref", "ref-bench")
+    size_args = ["--vecadd-n", str(sizes.vecadd_n), "--ep-m", str(sizes.ep_m),
+                 "--bs-n", str(sizes.bs_n), "--mm-n", str(sizes.mm_n)]
+    if not os.path.exists(ref):
+        return None
+    # probe one round to size a bounded sample (~budget_s of CPU work)
+    probe = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds", "1",
+                            "--warmup", "0"] + size_args, capture_output=True, text=True,
+                           timeout=1800)
+    one = json.loads(probe.stdout.strip().splitlines()[-1])
+    per_round = max(1e-3, one["seconds"])
+    rounds = max(1, min(200, int(budget_s / per_round)))
+    run = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds",
+                          str(rounds), "--warmup", str(warmup if per_round < budget_s / 4 else 0)]
+                         + size_args, capture_output=True, text=True, timeout=3600)
+    r = json.loads(run.stdout.strip().splitlines()[-1])
+    r["sample"] = (f"reference GVM (oracle/_ref/ref-bench, unmodified libvgpu from /root/reference) "
+                   f"{procs} forked VgpuHandle clients x {rounds} rounds of '{workload}', "
+                   f"virtual clock, OpenMP on all host threads")
+    return r
+
+
+def final_reduce(V, N, dist, record):
+    """The single cross-GPU collective: NCCL all-gather of per-GPU records,
+    folded on the host in rank order (deterministic)."""
+    import ctypes as C
+    libs = N.load()
+    uid = (C.c_uint8 * 128)()
+    if dist.rank == 0:
+        rc = libs.cuda.vgpu_cu_nccl_unique_id(uid)
+        if rc:
+            raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
+    uid_bytes = dist.bcast(bytes(uid))
+    uid = (C.c_uint8 * 128).from_buffer_copy(uid_bytes)
+    dev = C.c_void_p()
+    if libs.cuda.vgpu_cu_open(dist.local, 1, 4096, C.byref(dev)):
+        raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
+    try:
+        if libs.cuda.vgpu_cu_comm_init(dev, uid, dist.world, dist.rank):
+            raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
+        rec = (C.c_double * 4)(*record)
+        allr = (C.c_double * (4 * dist.world))()
+        if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
+            raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
+        folded = [0.0] * 4
+        for r in range(dist.world):
+            for i in range(4):
+                folded[i] = folded[i] + allr[4 * r + i]
+        return folded
+    finally:
+        libs.cuda.vgpu_cu_close(dev)
+
+
+# ---- main -----------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="vecadd", choices=["vecadd", "ep", "bs", "mm", "mixed"])
+    ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-native", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_1511_07658_b200 import _native as N
+    from paper_1511_07658_b200 import vgpu as V
+    from paper_1511_07658_b200 import workloads as W
+
+    dist = Dist()
+    procs = args.procs or W.DEFAULT_PROCS[args.workload]
+    sizes = W.Sizes()
+    world = dist.world
+    config = {"workload": W.CONFIG_NAME[args.workload], "procs_per_gpu": procs,
+              "gpus": world, "global_procs": procs * world, "parallelism": f"gvm-per-gpu x{world}",
+              "l2": "value: rotating input sets > 2x L2 between steps; e2e: inputs re-sent from "
+                    "host memory every step"}
+
+    if args.impl == "reference":
+        if dist.rank == 0:
+            r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s)
+            if r is None:
+                line = {"impl": "reference", "unavailable": "oracle/_ref/ref-bench not built "
+                        "(needs /root/reference at build time)"}
+            else:
+                cores = os.cpu_count()
+                line = {"impl": "reference", "metric": METRIC, "value": r["jobs_per_s"],
+                        "unit": "jobs/s", "higher_is_better": True, "n_gpus": 0, "steps": r["rounds"],
+                        "warmup": r["warmup"], "ms_per_step": r["ms_per_round"], "dtype": "f32",
+                        "data": "synthetic", "scaling": "weak", "vs_baseline": None,
+                        "config": config,
+                        "cpu_baseline": {"value": r["jobs_per_s"], "unit": "jobs/s", "cores": cores,
+                                         "kind": "reference", "sample": r["sample"]},
+                        "e2e": {"value": r["jobs_per_s"], "unit": "jobs/s",
+                                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            print(json.dumps(line), flush=True)
+        dist.close()
+        return
+
+    N.load()
+    if V.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
+    device = dist.local
+    gid0 = dist.rank * procs
+    total_workers = procs * world
+    clocks = Clocks(device) if dist.local == 0 or world == 1 else None
+    if clocks:
+        clocks.start()
+
+    # ---- value: device-resident --------------------------------------------------
+    dist.barrier()
+    t0 = time.time()
+    legs, ms_step, launches_value, dom = leg_value(V, W, args.workload, procs, gid0,
+                                                   total_workers, args.steps, args.warmup,
+                                                   device, sizes)
+    dist.barrier()
+    ms_step_max = dist.max(ms_step)
+    value = procs * world / (ms_step_max * 1e-3)
+    if clocks:
+        clocks.mark(t0, time.time())
+
+    # ---- e2e: virtualized through the GVM ----------------------------------------------
+    dist.barrier()
+    e2e = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                      args.warmup, device, False, sizes, dist)
+    secs = dist.max(e2e["seconds"])
+    e2e_value = procs * world * args.steps / secs
+    kinds = [W.kind_of(args.workload, gid0 + i) for i in range(procs)]
+    h2d = sum(W.input_bytes(k, sizes) for k in kinds)
+    d2h = sum(W.output_bytes(k, sizes) for k in kinds)
+    launches_e2e = int(round(e2e["launches_total"] * args.steps / (args.steps + args.warmup)))
+
+    # ---- native baseline --------------------------------------------------------------
+    native = None
+    if not args.no_native:
+        dist.barrier()
+        nat = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                          args.warmup, device, True, sizes, dist)
+        nsecs = dist.max(nat["seconds"])
+        native = {"value": procs * world * args.steps / nsecs, "unit": "jobs/s",
+                  "cold_turnaround_ms": dist.max(nat["cold_ms"]),
+                  "desc": "NativeVgpu: one CUDA context per process, pageable cudaMemcpy, "
+                          "time-sliced by the driver, no MPS"}
+    clock_info = clocks.stop() if clocks else None
+
+    # ---- final reduction (multi-GPU only) ----------------------------------------------
+    reduce_info = None
+    if world > 1:
+        checks = [int(r["checksum"], 16) & 0xFFFFFFFF for r in e2e["results"]]
+        rec = [float(procs * args.steps), float(sum(checks) % 1000003), e2e["seconds"], ms_step]
+        folded = final_reduce(V, N, dist, rec)
+        reduce_info = {"jobs_all_gpus": folded[0], "collective": "ncclAllGather (NVLink), "
+                       "host fold in rank order"}
+
+    # ---- cpu baseline (rank 0, N = 1) -----------------------------------------------------
+    cpu = None
+    if dist.rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s)
+        if r is not None:
+            cpu = {"value": r["jobs_per_s"], "unit": "jobs/s", "cores": os.cpu_count(),
+                   "kind": "reference", "sample": r["sample"]}
+
+    if dist.rank == 0:
+        d = legs[dom]
+        peaks = measured_peaks()
+        kernel_s = d["kernel_ms_per_launch"] * 1e-3
+        bound = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32"}[dom]
+        if bound == "hbm":
+            achieved = d["algo_bytes_per_launch"] / kernel_s / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
+                    "peak_source": peaks["source"], "kernel": W.PAYLOAD[dom],
+                    "algo_bytes_per_launch": d["algo_bytes_per_launch"],
+                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
+        else:
+            achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
+            roof = {"bound": bound, "achieved": achieved, "peak": None, "unit": "TFLOP/s",
+                    "frac": None, "traffic": ncu_traffic(dom), "kernel": W.PAYLOAD[dom],
+                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
+        line = {
+            "metric": METRIC, "value": value, "unit": "jobs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config,
+            "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h * world, "ms_per_step": secs * 1e3 / args.steps,
+                    "path": "bin/vgpu-spmd x P -> VgpuHandle::run_task -> UDS+shm -> GVM "
+                            "(libvgpu.so) -> per-client CUDA streams"},
+            "native": native,
+            "vs_native": (e2e_value / native["value"]) if native else None,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches_value + launches_e2e,
+            "clocks": clock_info,
+            "final_reduce": reduce_info,
+            "model": {"batches": len(e2e["batches"]),
+                      "model_makespan_us_median": statistics.median(
+                          [b["model_makespan_us"] for b in e2e["batches"]]) if e2e["batches"] else None,
+                      "measured_makespan_us_median": statistics.median(
+                          [b["measured_makespan_us"] for b in e2e["batches"]]) if e2e["batches"] else None,
+                      "style": "PS2" if e2e["batches"] and e2e["batches"][-1]["style"] else "PS1"},
+        }
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

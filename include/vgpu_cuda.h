@@ -1,0 +1,198 @@
+/*
+ * vgpu-b200 — thin C-ABI between the GVM host layer (C++) and the B200
+ * device backend (libvgpu_cuda.so, nvcc -gencode arch=compute_100a,code=sm_100a).
+ *
+ * This replaces, in the reference, the two plug points the GVM dispatches
+ * through:
+ *   - PayloadRegistry::execute / PayloadFn         proj/include/vgpu/payload.hpp:17,:38
+ *     (called from flush_barrier, proj/src/daemon.cpp:413)
+ *   - simulate() as the executor of the work queue proj/include/vgpu/device.hpp:86
+ *     (proj/src/daemon.cpp:384-385; PS-1/PS-2 order proj/src/device.cpp:56-69)
+ * and the completion lane that paced sleeps stood in for
+ *   - completer_loop / apply_completion            proj/src/daemon.cpp:474-585.
+ *
+ * Conventions: plain C types only; integer status returns (0 = ok, codes 3/5/8
+ * deliberately equal vgpu::ErrCode Size/Payload/Internal); no C++ exception
+ * crosses the ABI; host pointers handed to submit stay valid until poll()
+ * reports the task. submit is called from the GVM dispatcher thread only,
+ * poll from the dispatcher too; the notify callback fires on a CUDA-owned
+ * thread and must only signal.
+ */
+#ifndef VGPU_CUDA_H
+#define VGPU_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+enum vgpu_cu_status {
+    VGPU_CU_OK = 0,
+    VGPU_CU_ESIZE = 3,       /* result does not fit / buffer too small       */
+    VGPU_CU_EPAYLOAD = 5,    /* unknown payload id or malformed input bytes  */
+    VGPU_CU_EINTERNAL = 8,   /* CUDA runtime failure (detail: last_error)     */
+    VGPU_CU_ENODEV = 100,    /* no usable CUDA device                         */
+    VGPU_CU_EINVAL = 101,    /* bad argument                                  */
+    VGPU_CU_ENCCL = 102      /* NCCL missing or failed                        */
+};
+
+/* ---- device kernels (payload ids) --------------------------------------- */
+enum vgpu_cu_kernel {
+    VGPU_CU_K_IDENTITY = 0,  /* "identity"      bytes -> bytes (copy only)     */
+    VGPU_CU_K_VADD = 1,      /* "vector-add"    a||b fp32 -> a+b               */
+    VGPU_CU_K_VSCALE = 2,    /* "vector-scale"  x fp32 -> param*x              */
+    VGPU_CU_K_EP = 3,        /* "nas-ep"        vgpu_ep_params -> vgpu_ep_result */
+    VGPU_CU_K_BS = 4,        /* "black-scholes" S||X||T fp32 -> call||put      */
+    VGPU_CU_K_SGEMM = 5,     /* "sgemm"         A||B (n*n fp32) -> A*B         */
+    VGPU_CU_K_COUNT = 6
+};
+
+/* NAS EP job (input, 32 bytes little-endian). The job computes batches
+ * [first_batch, first_batch + n_batches) of the class with 2^m pairs,
+ * 2^mk pairs per batch (NPB: mk = 16). */
+typedef struct vgpu_ep_params {
+    uint32_t m;
+    uint32_t mk;
+    uint64_t first_batch;
+    uint64_t n_batches;
+    uint64_t reserved; /* must be 0 */
+} vgpu_ep_params;
+
+/* NAS EP job result (output, 112 bytes). sx/sy follow the fixed reduction
+ * order documented in DESIGN.md (bit-identical to oracle/vgpu_oracle.c). */
+typedef struct vgpu_ep_result {
+    uint64_t q[10];
+    double sx;
+    double sy;
+    uint64_t pairs;     /* accepted Gaussian pairs = sum(q) */
+    uint64_t n_batches;
+} vgpu_ep_result;
+
+/* Black-Scholes constants (CUDA SDK formulation). */
+#define VGPU_BS_RISKFREE 0.02f
+#define VGPU_BS_VOLATILITY 0.30f
+
+/* ---- one task of a dispatch batch --------------------------------------- */
+typedef struct vgpu_cu_task {
+    uint32_t slot;       /* client slot 1..max_clients: stream + HBM buffers */
+    uint32_t kernel;     /* vgpu_cu_kernel                                    */
+    float param;         /* vector-scale factor                               */
+    uint32_t flags;      /* 0                                                 */
+    const void* h_in;    /* host source (registered region / pinned staging)  */
+    uint64_t in_bytes;
+    void* h_out;         /* host destination of the result                    */
+    uint64_t out_bytes;  /* vgpu_cu_output_size()                             */
+    uint64_t tag;        /* echoed in vgpu_cu_done                            */
+} vgpu_cu_task;
+
+typedef struct vgpu_cu_done {
+    uint64_t tag;
+    uint64_t batch;        /* batch sequence number from submit              */
+    int32_t status;        /* VGPU_CU_OK or error                            */
+    uint32_t slot;
+    float h2d_us;          /* CUDA-event stage durations                     */
+    float comp_us;
+    float d2h_us;
+    float span_us;         /* this task: H2D start -> D2H end                */
+    float batch_span_us;   /* set on the batch's last completion: first H2D
+                              start -> last D2H end over the batch; else 0   */
+    uint32_t batch_done;   /* 1 on the batch's last completion               */
+} vgpu_cu_done;
+
+typedef struct vgpu_cu_stats {
+    uint64_t kernel_launches;  /* our kernels launched by this device handle */
+    uint64_t tasks;            /* tasks submitted                             */
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t batches;
+} vgpu_cu_stats;
+
+typedef struct vgpu_cu_dev vgpu_cu_dev;
+
+/* Open the GVM's device: primary context on `device`, one non-blocking
+ * stream and an in/out HBM buffer pair of slot_bytes per client slot. */
+int vgpu_cu_open(int device, uint32_t max_clients, uint64_t slot_bytes,
+                 vgpu_cu_dev** out);
+void vgpu_cu_close(vgpu_cu_dev* dev);
+
+/* Page-lock a client region (cudaHostRegister) so H2D/D2H DMA it directly. */
+int vgpu_cu_register_region(vgpu_cu_dev* dev, uint32_t slot, void* base,
+                            uint64_t bytes);
+/* Pinned host staging (DataPlane::Snapshot). */
+int vgpu_cu_alloc_pinned(vgpu_cu_dev* dev, uint64_t bytes, void** out);
+void vgpu_cu_free_pinned(vgpu_cu_dev* dev, void* p);
+
+/* Payload id -> kernel; unknown ids return VGPU_CU_EPAYLOAD. */
+int vgpu_cu_payload(const char* id, uint32_t* kernel);
+/* Host-side validation before launch: result size for this input, or
+ * VGPU_CU_EPAYLOAD when the input is malformed (the reference's
+ * PayloadError::MalformedInput). `in` may be NULL except for EP. */
+int vgpu_cu_output_size(uint32_t kernel, const void* in, uint64_t in_bytes,
+                        uint64_t* out_bytes);
+
+/* Enqueue a batch. style 0 = PS-1 (all H2D, then compute — one launch per
+ * kernel kind over the whole batch's task table — then all D2H), 1 = PS-2
+ * (per-stream H2D -> kernel -> D2H triples). Returns immediately. */
+int vgpu_cu_submit_batch(vgpu_cu_dev* dev, int style, const vgpu_cu_task* tasks,
+                         uint32_t n, uint64_t* batch_id);
+/* Collect finished tasks (non-blocking). */
+int vgpu_cu_poll(vgpu_cu_dev* dev, vgpu_cu_done* out, uint32_t cap,
+                 uint32_t* n_out);
+/* Block until at least one task finished or timeout_us passed. */
+int vgpu_cu_wait(vgpu_cu_dev* dev, int64_t timeout_us);
+/* Called (from a CUDA host-callback thread) whenever a task finishes. */
+void vgpu_cu_set_notify(vgpu_cu_dev* dev, void (*fn)(void* ctx, uint32_t slot),
+                        void* ctx);
+int vgpu_cu_get_stats(vgpu_cu_dev* dev, vgpu_cu_stats* out);
+
+/* Synchronous single task in the CALLING process's own context, pageable
+ * host memory, cudaMemcpy + launch + sync: PayloadRegistry::execute() and
+ * the NativeVgpu (non-virtualized) baseline. */
+int vgpu_cu_execute(int device, uint32_t kernel, float param, const void* in,
+                    uint64_t in_bytes, void* out, uint64_t out_cap,
+                    uint64_t* out_bytes);
+/* Kernel launches issued by vgpu_cu_execute in this process. */
+uint64_t vgpu_cu_execute_launches(void);
+
+int vgpu_cu_device_count(int* n);
+const char* vgpu_cu_strerror(int code);
+const char* vgpu_cu_last_error(void); /* thread-local detail of the last failure */
+
+/* ---- device-resident measurement (bench.py `value` and roofline) ------- */
+typedef struct vgpu_cu_resident_result {
+    double ms_total;            /* all timed steps, CUDA events              */
+    double ms_per_step;
+    double kernel_ms_per_launch;/* average duration of the dominant launch  */
+    uint32_t launches_per_step;
+    uint32_t sets;              /* rotating input sets actually used         */
+    uint64_t algo_bytes_per_launch;
+    double algo_flops_per_launch;
+    uint64_t resident_bytes;    /* HBM held by the rotating sets             */
+} vgpu_cu_resident_result;
+
+/* Times `steps` batched launches of `kernel` over n_tasks tasks whose inputs
+ * (copied once from h_inputs[i], in_bytes[i]) sit in HBM; `sets` rotating
+ * copies keep the working set above L2 between steps. */
+int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
+                           uint32_t n_tasks, const void* const* h_inputs,
+                           const uint64_t* in_bytes, uint32_t sets,
+                           uint32_t warmup, uint32_t steps,
+                           vgpu_cu_resident_result* out);
+
+/* ---- multi-GPU: the single final reduction (NCCL over NVLink) --------- */
+#define VGPU_CU_NCCL_ID_BYTES 128
+int vgpu_cu_nccl_unique_id(void* id_out /* VGPU_CU_NCCL_ID_BYTES */);
+int vgpu_cu_comm_init(vgpu_cu_dev* dev, const void* id, int nranks, int rank);
+/* All-gather `bytes` of partial record from every rank into all_out
+ * (nranks * bytes, rank order). Callers fold in rank order on the host. */
+int vgpu_cu_reduce_final(vgpu_cu_dev* dev, const void* partial, uint64_t bytes,
+                         void* all_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VGPU_CUDA_H */

@@ -1,0 +1,120 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes access to oracle/_build/libvgpu_oracle.so (the C restatements in
+vgpu_oracle.c) with numpy helpers. Used by tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline leg as the checker / CPU baseline; never by the
+product path (paper_1511_07658_b200/ does not import this module).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "_build", "libvgpu_oracle.so")
+REF_DIR = os.path.join(HERE, "_ref")
+
+NPB_VERIFY = {  # NPB 3.x EP verification sums (ep.f), epsilon 1e-8
+    24: (-3.247834652034740e3, -6.958407078382297e3),   # class S
+    25: (-2.863319731645753e3, -6.320053679109499e3),   # class W
+    28: (-4.295875165629892e3, -1.580732573678431e4),   # class A
+    30: (4.033815542441498e4, -2.660669192809235e4),    # class B
+}
+
+
+class EpParams(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("mk", C.c_uint32), ("first_batch", C.c_uint64),
+                ("n_batches", C.c_uint64), ("reserved", C.c_uint64)]
+
+
+class EpResult(C.Structure):
+    _fields_ = [("q", C.c_uint64 * 10), ("sx", C.c_double), ("sy", C.c_double),
+                ("pairs", C.c_uint64), ("n_batches", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            subprocess.run(["make", "oracle"], cwd=REPO, check=True,
+                           stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+        L = C.CDLL(LIB)
+        f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+        f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.vo_vector_add.argtypes = [f32p, f32p, f32p, C.c_size_t]
+        L.vo_vector_scale.argtypes = [f32p, f32p, C.c_float, C.c_size_t]
+        L.vo_ep_job.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
+        L.vo_ep_job.restype = C.c_int
+        L.vo_ep_fold.argtypes = [C.POINTER(EpResult), C.c_size_t, C.POINTER(EpResult)]
+        L.vo_black_scholes.argtypes = [f32p, f32p, f32p, C.c_size_t, C.c_double, C.c_double,
+                                       f64p, f64p]
+        L.vo_sgemm.argtypes = [f32p, f32p, C.c_size_t, f64p]
+        _lib = L
+    return _lib
+
+
+def vector_add(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    out = np.empty_like(a)
+    lib().vo_vector_add(out, a, b, a.size)
+    return out
+
+
+def vector_scale(x: np.ndarray, f: float) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty_like(x)
+    lib().vo_vector_scale(out, x, f, x.size)
+    return out
+
+
+def ep_params_bytes(m: int, first: int, count: int, mk: int = 16) -> bytes:
+    return bytes(EpParams(m, mk, first, count, 0))
+
+
+def ep_job(m: int, first: int, count: int, mk: int = 16) -> EpResult:
+    r = EpResult()
+    rc = lib().vo_ep_job(C.byref(EpParams(m, mk, first, count, 0)), C.byref(r))
+    if rc != 0:
+        raise ValueError("bad EP parameters")
+    return r
+
+
+def ep_from_bytes(b: bytes) -> EpResult:
+    return EpResult.from_buffer_copy(b)
+
+
+def ep_fold(parts) -> EpResult:
+    arr = (EpResult * len(parts))(*parts)
+    out = EpResult()
+    lib().vo_ep_fold(arr, len(parts), C.byref(out))
+    return out
+
+
+def black_scholes(S, X, T, r=0.02, v=0.30):
+    S, X, T = (np.ascontiguousarray(a, np.float32) for a in (S, X, T))
+    call = np.empty(S.size, np.float64)
+    put = np.empty(S.size, np.float64)
+    lib().vo_black_scholes(S, X, T, S.size, r, v, call, put)
+    return call, put
+
+
+def sgemm(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    n = A.shape[0]
+    A = np.ascontiguousarray(A, np.float32)
+    B = np.ascontiguousarray(B, np.float32)
+    Cm = np.empty((n, n), np.float64)
+    lib().vo_sgemm(A, B, n, Cm)
+    return Cm
+
+
+def ref_tool(name: str) -> str:
+    """Path of a binary built from the reference sources (oracle/_ref)."""
+    return os.path.join(REF_DIR, name)

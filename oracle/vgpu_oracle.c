@@ -1,0 +1,137 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY (see vgpu_oracle.h). Compiled with
+ * -O2 -ffp-contract=off on x86-64 (SSE2 binary64/binary32, no x87, no FMA).
+ */
+#include "vgpu_oracle.h"
+
+#include <math.h>
+#include <string.h>
+
+#include "../paper_1511_07658_b200/csrc/common/ep_math.h"
+
+/* reference proj/src/payload_kernels.cpp:13-16 */
+void vo_vector_add(float* out, const float* a, const float* b, size_t n) {
+    for (size_t i = 0; i < n; ++i) out[i] = a[i] + b[i];
+}
+
+/* reference proj/src/payload_kernels.cpp:24-27 */
+void vo_vector_scale(float* out, const float* in, float factor, size_t n) {
+    for (size_t i = 0; i < n; ++i) out[i] = in[i] * factor;
+}
+
+/* ---- NAS EP (NPB 3.x ep.f main loop, fixed reduction order) ---------- */
+
+int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
+    memset(r, 0, sizeof *r);
+    if (p->mk < 8 || p->mk > 24 || p->m < p->mk || p->m > 40 || p->reserved != 0) return -1;
+    const uint64_t batches_total = 1ull << (p->m - p->mk);
+    if (p->first_batch > batches_total || p->n_batches > batches_total - p->first_batch) return -1;
+    const uint64_t per_lane = (1ull << p->mk) / VGPU_EP_LANES;
+    const uint64_t lane_skip = ep_powmod46(VGPU_EP_A, 2ull * per_lane);
+    double lsx[VGPU_EP_LANES], lsy[VGPU_EP_LANES];
+    double jsx = 0.0, jsy = 0.0;
+    for (uint64_t b = p->first_batch; b < p->first_batch + p->n_batches; ++b) {
+        const uint64_t seed = vgpu_ep_batch_seed(b, p->mk);
+        uint64_t lane_start = seed;
+        for (unsigned lane = 0; lane < VGPU_EP_LANES; ++lane) {
+            uint64_t v = lane_start;
+            double sx = 0.0, sy = 0.0;
+            for (uint64_t k = 0; k < per_lane; ++k) {
+                const uint64_t xa = ep_mulmod46(v, VGPU_EP_A);
+                const uint64_t xb = ep_mulmod46(xa, VGPU_EP_A);
+                v = xb;
+                double gx, gy;
+                int l;
+                if (vgpu_ep_pair(xa, xb, &gx, &gy, &l)) {
+                    r->q[l] += 1;
+                    sx = sx + gx;
+                    sy = sy + gy;
+                }
+            }
+            lsx[lane] = sx;
+            lsy[lane] = sy;
+            lane_start = ep_mulmod46(lane_start, lane_skip);
+        }
+        for (unsigned stride = 1; stride < VGPU_EP_LANES; stride *= 2)
+            for (unsigned i = 0; i < VGPU_EP_LANES; i += 2 * stride) {
+                lsx[i] = lsx[i] + lsx[i + stride];
+                lsy[i] = lsy[i] + lsy[i + stride];
+            }
+        jsx = jsx + lsx[0];
+        jsy = jsy + lsy[0];
+    }
+    r->sx = jsx;
+    r->sy = jsy;
+    for (int i = 0; i < 10; ++i) r->pairs += r->q[i];
+    r->n_batches = p->n_batches;
+    return 0;
+}
+
+void vo_ep_fold(const vgpu_ep_result* parts, size_t n, vgpu_ep_result* out) {
+    memset(out, 0, sizeof *out);
+    double sx = 0.0, sy = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+        for (int i = 0; i < 10; ++i) out->q[i] += parts[j].q[i];
+        sx = sx + parts[j].sx;
+        sy = sy + parts[j].sy;
+        out->pairs += parts[j].pairs;
+        out->n_batches += parts[j].n_batches;
+    }
+    out->sx = sx;
+    out->sy = sy;
+}
+
+/* ---- Black-Scholes (CUDA SDK formulation, binary64) -------------------- */
+
+static double cnd64(double d) {
+    const double A1 = 0.31938153, A2 = -0.356563782, A3 = 1.781477937,
+                 A4 = -1.821255978, A5 = 1.330274429;
+    const double RSQRT2PI = 0.39894228040143267793994605993438;
+    const double K = 1.0 / (1.0 + 0.2316419 * fabs(d));
+    double c = RSQRT2PI * exp(-0.5 * d * d) * (K * (A1 + K * (A2 + K * (A3 + K * (A4 + K * A5)))));
+    if (d > 0) c = 1.0 - c;
+    return c;
+}
+
+void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,
+                      double R, double V, double* call, double* put) {
+    for (size_t i = 0; i < n; ++i) {
+        const double s = S[i], x = X[i], t = T[i];
+        const double sqrtT = sqrt(t);
+        const double d1 = (log(s / x) + (R + 0.5 * V * V) * t) / (V * sqrtT);
+        const double d2 = d1 - V * sqrtT;
+        const double c1 = cnd64(d1), c2 = cnd64(d2);
+        const double expRT = exp(-R * t);
+        call[i] = s * c1 - x * expRT * c2;
+        put[i] = x * expRT * (1.0 - c2) - s * (1.0 - c1);
+    }
+}
+
+/* ---- SGEMM (binary64 accumulation, i-k-j order) ------------------------ */
+
+void vo_sgemm(const float* A, const float* B, size_t n, double* C) {
+    for (size_t i = 0; i < n * n; ++i) C[i] = 0.0;
+    for (size_t i = 0; i < n; ++i)
+        for (size_t k = 0; k < n; ++k) {
+            const double a = A[i * n + k];
+            const float* brow = B + k * n;
+            double* crow = C + i * n;
+            for (size_t j = 0; j < n; ++j) crow[j] += a * (double)brow[j];
+        }
+}
+
+/* ---- deterministic generator ---------------------------------------------- */
+
+uint64_t vo_rng_next(uint64_t* s) {
+    uint64_t x = *s ? *s : 0x9E3779B97F4A7C15ull;
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    *s = x;
+    return x * 0x2545F4914F6CDD1Dull;
+}
+
+float vo_rng_uniform(uint64_t* s, float lo, float hi) {
+    const double u = (double)(vo_rng_next(s) >> 11) * (1.0 / 9007199254740992.0);
+    return (float)(lo + (hi - lo) * u);
+}

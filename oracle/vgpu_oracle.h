@@ -1,0 +1,57 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY. Never linked into, loaded by or called
+ * from the product path (paper_1511_07658_b200/). Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * use it, as the checker.
+ *
+ * CPU restatements of the reference's arithmetic for the GVM hot path:
+ *   vector add / scale   proj/src/payload_kernels.cpp:13-16, :24-27 (serial twins)
+ *                        — PINNED: bit-exact vs the reference itself (oracle/_ref)
+ *                          and its goldens (proj/tests/test_payload.cpp:26-79).
+ *   NAS EP               no reference arithmetic (proj/src/bench/profiles.cpp:27,:31 are
+ *                        timing-only); restated from NPB 3.x EP (ep.f) —
+ *                        PINNED against the published NPB verification sums
+ *                        (classes S, W, A; epsilon 1e-8) in tests/golden/.
+ *   Black-Scholes        no reference arithmetic (profiles.cpp:39); CUDA-SDK
+ *                        formulation in binary64 — parity UNPINNED by the
+ *                        reference (tolerance-checked: L1 relative <= 1e-6).
+ *   SGEMM                no reference arithmetic (profiles.cpp:35); binary64
+ *                        accumulation — parity UNPINNED by the reference
+ *                        (relative Frobenius <= 1e-5 for FP32 SIMT).
+ */
+#ifndef VGPU_ORACLE_H
+#define VGPU_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../include/vgpu_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+void vo_vector_add(float* out, const float* a, const float* b, size_t n);
+void vo_vector_scale(float* out, const float* in, float factor, size_t n);
+
+/* One EP job with the documented fixed reduction order:
+ * 256 lanes per batch, each lane sums its pairs sequentially, lanes combine
+ * in a binary tree, batches accumulate sequentially in batch order. */
+int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r);
+/* Fold job results in order (the GVM / rank-order host fold). */
+void vo_ep_fold(const vgpu_ep_result* parts, size_t n, vgpu_ep_result* out);
+
+void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,
+                      double riskfree, double volatility, double* call, double* put);
+
+void vo_sgemm(const float* A, const float* B, size_t n, double* C);
+
+/* deterministic generators shared by tests and bench (xorshift64*) */
+uint64_t vo_rng_next(uint64_t* state);
+float vo_rng_uniform(uint64_t* state, float lo, float hi);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

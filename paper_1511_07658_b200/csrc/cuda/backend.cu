@@ -1,0 +1,1114 @@
+// libvgpu_cuda.so — the B200 device backend behind include/vgpu_cuda.h.
+//
+// Replaces the reference's executor (sequential CPU payloads on the
+// dispatcher thread, proj/src/daemon.cpp:400-426) and its paced completion
+// lane (:532-585) with real device work:
+//   * one primary CUDA context per GVM (the paper's single context);
+//   * per client slot: a non-blocking stream (CUDA_DEVICE_MAX_CONNECTIONS
+//     = 32 so up to 32 slots get their own hardware queue — without it the
+//     Fermi-style false serialization of §4.2.1 reappears), an in/out HBM
+//     buffer pair and an EP scratch area carved from ONE arena allocation;
+//   * client regions page-locked in place (cudaHostRegister), so H2D/D2H
+//     DMA straight between the shm region and HBM;
+//   * a batch is enqueued in the paper's issue order — PS-1: every H2D, then
+//     ONE launch per kernel kind covering all tasks (task table in the
+//     parameter space; the lead stream waits on the other tasks' H2D events,
+//     the other streams wait on the launch's end event), then every D2H;
+//     PS-2: per-stream H2D -> kernel -> D2H triples;
+//   * completion: a host function after each task's D2H queues the slot and
+//     rings the daemon's notify callback; poll() turns CUDA events into
+//     per-stage times (the paper's t_in / t_comp / t_out) and batch spans.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "vgpu_cuda.h"
+#include "k_bs.cuh"
+#include "k_ep.cuh"
+#include "k_sgemm.cuh"
+#include "k_stream.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    set_err("%s: %s", what, cudaGetErrorString(e));
+    return VGPU_CU_EINTERNAL;
+}
+
+#define CK(call)                                                  \
+    do {                                                          \
+        const cudaError_t ck_e_ = (call);                         \
+        if (ck_e_ != cudaSuccess) return cuda_fail(ck_e_, #call); \
+    } while (0)
+
+constexpr std::uint64_t kEpMaxBatchesPerJob = 1ull << 16;
+constexpr std::uint64_t kEpTicketBytes = 256;
+constexpr std::uint64_t kScratchBytes = kEpTicketBytes + sizeof(vgk::EpPartial) * kEpMaxBatchesPerJob;
+constexpr std::uint64_t kAlign = 2ull << 20;  // 2 MiB: TLB-page aligned slot buffers
+
+std::uint64_t round_up(std::uint64_t v, std::uint64_t a) { return (v + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+// ---- payload contracts (host-side validation before launch) ----------------
+
+int ep_check(const vgpu_ep_params& p) {
+    if (p.reserved != 0 || p.mk < 8 || p.mk > 24 || p.m < p.mk || p.m > 40) {
+        set_err("nas-ep: bad class parameters m=%u mk=%u", p.m, p.mk);
+        return VGPU_CU_EPAYLOAD;
+    }
+    const std::uint64_t total = 1ull << (p.m - p.mk);
+    if (p.first_batch > total || p.n_batches > total - p.first_batch) {
+        set_err("nas-ep: batches [%llu, +%llu) outside the class (%llu batches)",
+                (unsigned long long)p.first_batch, (unsigned long long)p.n_batches,
+                (unsigned long long)total);
+        return VGPU_CU_EPAYLOAD;
+    }
+    if (p.n_batches > kEpMaxBatchesPerJob) {
+        set_err("nas-ep: at most %llu batches per job", (unsigned long long)kEpMaxBatchesPerJob);
+        return VGPU_CU_EPAYLOAD;
+    }
+    return VGPU_CU_OK;
+}
+
+std::uint64_t isqrt(std::uint64_t v) {
+    std::uint64_t r = static_cast<std::uint64_t>(std::sqrt(static_cast<double>(v)));
+    while (r * r > v) --r;
+    while ((r + 1) * (r + 1) <= v) ++r;
+    return r;
+}
+
+// ---- device jobs and launches ------------------------------------------------
+
+struct DevJob {
+    std::uint32_t kernel = 0;
+    float param = 0.0f;
+    const std::uint8_t* in = nullptr;
+    std::uint64_t in_bytes = 0;
+    std::uint8_t* out = nullptr;
+    std::uint64_t out_bytes = 0;
+    std::uint8_t* scratch = nullptr;
+    vgpu_ep_params ep{};
+};
+
+// Launch every job (all of one kernel kind) on `s`; counts launches.
+cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t n,
+                        cudaStream_t s, std::uint64_t* launches) {
+    using namespace vgk;
+    switch (kernel) {
+        case VGPU_CU_K_IDENTITY:
+            for (std::uint32_t i = 0; i < n; ++i)
+                if (jobs[i].in_bytes) {
+                    const cudaError_t e = cudaMemcpyAsync(jobs[i].out, jobs[i].in, jobs[i].in_bytes,
+                                                          cudaMemcpyDeviceToDevice, s);
+                    if (e != cudaSuccess) return e;
+                }
+            return cudaSuccess;
+        case VGPU_CU_K_VADD:
+        case VGPU_CU_K_VSCALE: {
+            const bool add = kernel == VGPU_CU_K_VADD;
+            for (std::uint32_t b = 0; b < n; b += kMaxTableJobs) {
+                StreamTable t{};
+                std::uint32_t ctas = 0;
+                for (std::uint32_t i = b; i < std::min(n, b + kMaxTableJobs); ++i) {
+                    const std::uint64_t elems = add ? jobs[i].in_bytes / 8 : jobs[i].in_bytes / 4;
+                    if (elems == 0) continue;
+                    StreamJob& j = t.job[t.njobs++];
+                    j.a = reinterpret_cast<const float*>(jobs[i].in);
+                    j.b = add ? j.a + elems : nullptr;
+                    j.out = reinterpret_cast<float*>(jobs[i].out);
+                    j.n = elems;
+                    j.factor = jobs[i].param;
+                    j.cta_begin = ctas;
+                    j.vec_ok = aligned16(j.a) && aligned16(j.out) && (!add || aligned16(j.b));
+                    ctas += static_cast<std::uint32_t>((elems + kStreamChunk - 1) / kStreamChunk);
+                }
+                if (!ctas) continue;
+                if (add)
+                    stream_table_kernel<true><<<ctas, kStreamThreads, 0, s>>>(t);
+                else
+                    stream_table_kernel<false><<<ctas, kStreamThreads, 0, s>>>(t);
+                ++*launches;
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        case VGPU_CU_K_EP: {
+            for (std::uint32_t b = 0; b < n; b += kMaxEpJobs) {
+                EpTable t{};
+                std::uint32_t ctas = 0;
+                for (std::uint32_t i = b; i < std::min(n, b + kMaxEpJobs); ++i) {
+                    const vgpu_ep_params& p = jobs[i].ep;
+                    if (p.n_batches == 0) {
+                        const cudaError_t e = cudaMemsetAsync(jobs[i].out, 0, sizeof(vgpu_ep_result), s);
+                        if (e != cudaSuccess) return e;
+                        continue;
+                    }
+                    EpJob& j = t.job[t.njobs++];
+                    j.out = reinterpret_cast<vgpu_ep_result*>(jobs[i].out);
+                    j.ticket = reinterpret_cast<std::uint32_t*>(jobs[i].scratch);
+                    j.partials = reinterpret_cast<EpPartial*>(jobs[i].scratch + kEpTicketBytes);
+                    j.first_batch = p.first_batch;
+                    j.n_batches = p.n_batches;
+                    j.batch_seed0 = vgpu_ep_batch_seed(p.first_batch, p.mk);
+                    j.batch_skip = ep_powmod46(VGPU_EP_A, 2ull << p.mk);
+                    j.ppl = static_cast<std::uint32_t>((1ull << p.mk) / VGPU_EP_LANES);
+                    j.lane_skip = ep_powmod46(VGPU_EP_A, 2ull * j.ppl);
+                    j.cta_begin = ctas;
+                    ctas += static_cast<std::uint32_t>(p.n_batches);
+                }
+                if (!ctas) continue;
+                ep_table_kernel<<<ctas, kEpThreads, 0, s>>>(t);
+                ++*launches;
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        case VGPU_CU_K_BS: {
+            for (std::uint32_t b = 0; b < n; b += kMaxBsJobs) {
+                BsTable t{};
+                t.R = VGPU_BS_RISKFREE;
+                t.V = VGPU_BS_VOLATILITY;
+                std::uint32_t ctas = 0;
+                for (std::uint32_t i = b; i < std::min(n, b + kMaxBsJobs); ++i) {
+                    const std::uint64_t opts = jobs[i].in_bytes / 12;
+                    if (opts == 0) continue;
+                    BsJob& j = t.job[t.njobs++];
+                    const float* base = reinterpret_cast<const float*>(jobs[i].in);
+                    float* out = reinterpret_cast<float*>(jobs[i].out);
+                    j.S = base;
+                    j.X = base + opts;
+                    j.T = base + 2 * opts;
+                    j.call = out;
+                    j.put = out + opts;
+                    j.n = opts;
+                    j.vec_ok = (opts % 4 == 0) && aligned16(base) && aligned16(out);
+                    j.cta_begin = ctas;
+                    ctas += static_cast<std::uint32_t>((opts + kBsChunk - 1) / kBsChunk);
+                }
+                if (!ctas) continue;
+                bs_table_kernel<<<ctas, kBsThreads, 0, s>>>(t);
+                ++*launches;
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+        case VGPU_CU_K_SGEMM: {
+            GemmTable fast{}, gen{};
+            std::uint32_t fast_tiles = 0, gen_tiles = 0;
+            auto flush = [&](GemmTable& t, std::uint32_t& tiles, bool is_fast) -> cudaError_t {
+                if (!t.njobs) return cudaSuccess;
+                if (is_fast)
+                    sgemm128_kernel<<<dim3(tiles, t.njobs), kGemmThreads, 0, s>>>(t);
+                else
+                    sgemm_generic_kernel<<<dim3(tiles, t.njobs),
+                                           dim3(kGemmSmallTile, kGemmSmallTile), 0, s>>>(t);
+                ++*launches;
+                t.njobs = 0;
+                tiles = 0;
+                return cudaGetLastError();
+            };
+            for (std::uint32_t i = 0; i < n; ++i) {
+                const std::uint32_t dim = static_cast<std::uint32_t>(isqrt(jobs[i].in_bytes / 8));
+                if (dim == 0) continue;
+                const bool is_fast = dim % kGemmBM == 0 &&
+                                     aligned16(jobs[i].in) && aligned16(jobs[i].out);
+                GemmTable& t = is_fast ? fast : gen;
+                std::uint32_t& tiles = is_fast ? fast_tiles : gen_tiles;
+                GemmJob& j = t.job[t.njobs++];
+                j.A = reinterpret_cast<const float*>(jobs[i].in);
+                j.B = j.A + static_cast<std::size_t>(dim) * dim;
+                j.C = reinterpret_cast<float*>(jobs[i].out);
+                j.n = dim;
+                const std::uint32_t per = is_fast ? dim / kGemmBM
+                                                  : (dim + kGemmSmallTile - 1) / kGemmSmallTile;
+                j.tiles = per * per;
+                tiles = std::max(tiles, j.tiles);
+                if (t.njobs == kMaxGemmJobs) {
+                    const cudaError_t e = flush(t, tiles, is_fast);
+                    if (e != cudaSuccess) return e;
+                }
+            }
+            cudaError_t e = flush(fast, fast_tiles, true);
+            if (e != cudaSuccess) return e;
+            return flush(gen, gen_tiles, false);
+        }
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+// Algorithmic work of one job (roofline numerators).
+void job_work(const DevJob& j, std::uint64_t* bytes, double* flops) {
+    switch (j.kernel) {
+        case VGPU_CU_K_IDENTITY: *bytes += 2 * j.in_bytes; break;
+        case VGPU_CU_K_VADD: *bytes += j.in_bytes + j.in_bytes / 2; *flops += j.in_bytes / 8.0; break;
+        case VGPU_CU_K_VSCALE: *bytes += 2 * j.in_bytes; *flops += j.in_bytes / 4.0; break;
+        case VGPU_CU_K_BS: *bytes += (j.in_bytes / 12) * 20; break;
+        case VGPU_CU_K_EP:
+            *bytes += sizeof(vgpu_ep_params) + sizeof(vgpu_ep_result);
+            *flops += static_cast<double>(j.ep.n_batches) * (2.0 * (1ull << j.ep.mk));  // uniforms (NPB Mop)
+            break;
+        case VGPU_CU_K_SGEMM: {
+            const double d = static_cast<double>(isqrt(j.in_bytes / 8));
+            *bytes += j.in_bytes + j.in_bytes / 2;
+            *flops += 2.0 * d * d * d;
+            break;
+        }
+        default: break;
+    }
+}
+
+// ---- NCCL, loaded on demand (the only cross-GPU collective) ------------------
+
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::mutex mu;
+    std::lock_guard lk(mu);
+    if (api.tried) return api;
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy;
+    return api;
+}
+
+}  // namespace
+
+// ---- the device handle ----------------------------------------------------------
+
+enum { kEvH2d0, kEvH2d1, kEvC0, kEvC1, kEvD2h0, kEvD2h1, kEvCount };
+
+struct SlotState {
+    vgpu_cu_dev* dev = nullptr;
+    std::uint32_t index = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[kEvCount] = {};
+    std::uint8_t* d_in = nullptr;
+    std::uint8_t* d_out = nullptr;
+    std::uint8_t* d_scratch = nullptr;
+    void* reg_base = nullptr;
+    // in flight
+    bool busy = false;
+    std::uint64_t tag = 0;
+    std::uint64_t batch = 0;
+    bool has_h2d = false, has_comp = false;
+    cudaEvent_t comp0 = nullptr, comp1 = nullptr;
+};
+
+struct BatchRec {
+    cudaEvent_t anchor = nullptr;
+    std::uint32_t remaining = 0;
+    float first = 1e30f, last = -1e30f;
+    std::vector<cudaEvent_t> pooled;
+};
+
+struct vgpu_cu_dev {
+    int device = 0;
+    std::uint32_t max_clients = 0;
+    std::uint64_t slot_bytes = 0;
+    std::uint8_t* arena = nullptr;
+    std::vector<SlotState> slots;  // [0] unused
+    cudaStream_t anchor_stream = nullptr;
+    std::vector<cudaEvent_t> event_pool;
+    std::map<std::uint64_t, BatchRec> batches;
+    std::uint64_t next_batch = 1;
+    std::vector<void*> pinned;
+
+    std::mutex cb_mu;
+    std::condition_variable cb_cv;
+    std::vector<std::uint32_t> finished;
+    std::mutex notify_mu;
+    void (*notify_fn)(void*, std::uint32_t) = nullptr;
+    void* notify_ctx = nullptr;
+
+    std::atomic<std::uint64_t> launches{0}, tasks{0}, h2d_bytes{0}, d2h_bytes{0}, nbatches{0};
+
+    ncclComm_t comm = nullptr;
+    int nranks = 1;
+
+    int pool_get(cudaEvent_t* out) {
+        if (!event_pool.empty()) {
+            *out = event_pool.back();
+            event_pool.pop_back();
+            return VGPU_CU_OK;
+        }
+        CK(cudaEventCreate(out));
+        return VGPU_CU_OK;
+    }
+};
+
+namespace {
+
+void CUDART_CB slot_done(void* p) {
+    auto* s = static_cast<SlotState*>(p);
+    vgpu_cu_dev* d = s->dev;
+    {
+        std::lock_guard lk(d->cb_mu);
+        d->finished.push_back(s->index);
+    }
+    d->cb_cv.notify_all();
+    void (*fn)(void*, std::uint32_t) = nullptr;
+    void* ctx = nullptr;
+    {
+        std::lock_guard lk(d->notify_mu);
+        fn = d->notify_fn;
+        ctx = d->notify_ctx;
+    }
+    if (fn) fn(ctx, s->index);
+}
+
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.0f;
+    }
+    return ms;
+}
+
+int require_sm100(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        set_err("no CUDA device visible (%s)", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+        return VGPU_CU_ENODEV;
+    }
+    if (device < 0 || device >= n) {
+        set_err("device %d out of range (%d visible)", device, n);
+        return VGPU_CU_ENODEV;
+    }
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        set_err("device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+        return VGPU_CU_ENODEV;
+    }
+    return VGPU_CU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vgpu_cu_last_error(void) { return g_err.c_str(); }
+
+const char* vgpu_cu_strerror(int code) {
+    switch (code) {
+        case VGPU_CU_OK: return "ok";
+        case VGPU_CU_ESIZE: return "size";
+        case VGPU_CU_EPAYLOAD: return "payload";
+        case VGPU_CU_EINTERNAL: return "internal (CUDA)";
+        case VGPU_CU_ENODEV: return "no CUDA device";
+        case VGPU_CU_EINVAL: return "invalid argument";
+        case VGPU_CU_ENCCL: return "NCCL";
+        default: return "unknown";
+    }
+}
+
+int vgpu_cu_device_count(int* n) {
+    if (!n) return VGPU_CU_EINVAL;
+    *n = 0;
+    const cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *n = 0;
+        set_err("%s", cudaGetErrorString(e));
+        return VGPU_CU_ENODEV;
+    }
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_payload(const char* id, std::uint32_t* kernel) {
+    static const char* names[VGPU_CU_K_COUNT] = {"identity", "vector-add", "vector-scale",
+                                                 "nas-ep", "black-scholes", "sgemm"};
+    if (!id || !kernel) return VGPU_CU_EINVAL;
+    for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT; ++k)
+        if (std::strcmp(id, names[k]) == 0) {
+            *kernel = k;
+            return VGPU_CU_OK;
+        }
+    set_err("unknown payload id: %s", id);
+    return VGPU_CU_EPAYLOAD;
+}
+
+int vgpu_cu_output_size(std::uint32_t kernel, const void* in, std::uint64_t in_bytes,
+                        std::uint64_t* out_bytes) {
+    if (!out_bytes) return VGPU_CU_EINVAL;
+    switch (kernel) {
+        case VGPU_CU_K_IDENTITY:
+            *out_bytes = in_bytes;
+            return VGPU_CU_OK;
+        case VGPU_CU_K_VADD:
+            if (in_bytes % 8) {
+                set_err("vector-add: input must hold two equal float32 arrays");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = in_bytes / 2;
+            return VGPU_CU_OK;
+        case VGPU_CU_K_VSCALE:
+            if (in_bytes % 4) {
+                set_err("vector-scale: input must be packed float32");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = in_bytes;
+            return VGPU_CU_OK;
+        case VGPU_CU_K_EP: {
+            if (in_bytes != sizeof(vgpu_ep_params)) {
+                set_err("nas-ep: input must be a %zu-byte parameter record", sizeof(vgpu_ep_params));
+                return VGPU_CU_EPAYLOAD;
+            }
+            if (!in) return VGPU_CU_EINVAL;
+            vgpu_ep_params p;
+            std::memcpy(&p, in, sizeof p);
+            const int rc = ep_check(p);
+            if (rc) return rc;
+            *out_bytes = sizeof(vgpu_ep_result);
+            return VGPU_CU_OK;
+        }
+        case VGPU_CU_K_BS:
+            if (in_bytes % 12) {
+                set_err("black-scholes: input must be S||X||T float32 arrays");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = in_bytes / 12 * 8;
+            return VGPU_CU_OK;
+        case VGPU_CU_K_SGEMM: {
+            const std::uint64_t sq = in_bytes / 8;
+            const std::uint64_t d = isqrt(sq);
+            if (in_bytes % 8 || d * d != sq) {
+                set_err("sgemm: input must be two n x n float32 matrices");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = in_bytes / 2;
+            return VGPU_CU_OK;
+        }
+        default:
+            set_err("unknown kernel %u", kernel);
+            return VGPU_CU_EPAYLOAD;
+    }
+}
+
+int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes,
+                 vgpu_cu_dev** out) {
+    if (!out || max_clients == 0) return VGPU_CU_EINVAL;
+    *out = nullptr;
+    // before the first CUDA call of the process: one hardware queue per stream
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+    int rc = require_sm100(device);
+    if (rc) return rc;
+    CK(cudaSetDevice(device));
+    auto* d = new vgpu_cu_dev();
+    d->device = device;
+    d->max_clients = max_clients;
+    d->slot_bytes = slot_bytes;
+    d->slots.resize(max_clients + 1);
+    const std::uint64_t buf = round_up(std::max<std::uint64_t>(slot_bytes, 256), kAlign);
+    const std::uint64_t per_slot = 2 * buf + round_up(kScratchBytes, kAlign);
+    auto fail = [&](int code) {
+        vgpu_cu_close(d);
+        return code;
+    };
+    cudaError_t e = cudaMalloc(&d->arena, per_slot * max_clients);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(arena)"));
+    e = cudaMemset(d->arena, 0, per_slot * max_clients);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemset(arena)"));
+    for (std::uint32_t i = 1; i <= max_clients; ++i) {
+        SlotState& s = d->slots[i];
+        s.dev = d;
+        s.index = i;
+        std::uint8_t* base = d->arena + per_slot * (i - 1);
+        s.d_in = base;
+        s.d_out = base + buf;
+        s.d_scratch = base + 2 * buf;
+        e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+        for (auto& ev : s.ev) {
+            e = cudaEventCreate(&ev);
+            if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
+        }
+    }
+    e = cudaStreamCreateWithFlags(&d->anchor_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(anchor)"));
+    *out = d;
+    return VGPU_CU_OK;
+}
+
+void vgpu_cu_close(vgpu_cu_dev* d) {
+    if (!d) return;
+    cudaSetDevice(d->device);
+    for (auto& s : d->slots)
+        if (s.stream) cudaStreamSynchronize(s.stream);
+    if (d->anchor_stream) cudaStreamSynchronize(d->anchor_stream);
+    for (auto& s : d->slots) {
+        if (s.reg_base) cudaHostUnregister(s.reg_base);
+        for (auto& ev : s.ev)
+            if (ev) cudaEventDestroy(ev);
+        if (s.stream) cudaStreamDestroy(s.stream);
+    }
+    for (auto& [id, b] : d->batches) {
+        if (b.anchor) d->event_pool.push_back(b.anchor);
+        for (auto ev : b.pooled) d->event_pool.push_back(ev);
+    }
+    for (auto ev : d->event_pool) cudaEventDestroy(ev);
+    if (d->anchor_stream) cudaStreamDestroy(d->anchor_stream);
+    for (void* p : d->pinned) cudaFreeHost(p);
+    if (d->arena) cudaFree(d->arena);
+    if (d->comm && nccl().ok) nccl().comm_destroy(d->comm);
+    cudaGetLastError();
+    delete d;
+}
+
+int vgpu_cu_register_region(vgpu_cu_dev* d, std::uint32_t slot, void* base, std::uint64_t bytes) {
+    if (!d || slot < 1 || slot > d->max_clients || !base) return VGPU_CU_EINVAL;
+    CK(cudaSetDevice(d->device));
+    SlotState& s = d->slots[slot];
+    if (s.reg_base) {
+        cudaHostUnregister(s.reg_base);
+        s.reg_base = nullptr;
+    }
+    if (bytes == 0) return VGPU_CU_OK;
+    CK(cudaHostRegister(base, bytes, cudaHostRegisterPortable));
+    s.reg_base = base;
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_alloc_pinned(vgpu_cu_dev* d, std::uint64_t bytes, void** out) {
+    if (!d || !out) return VGPU_CU_EINVAL;
+    CK(cudaSetDevice(d->device));
+    CK(cudaHostAlloc(out, std::max<std::uint64_t>(bytes, 1), cudaHostAllocPortable));
+    d->pinned.push_back(*out);
+    return VGPU_CU_OK;
+}
+
+void vgpu_cu_free_pinned(vgpu_cu_dev* d, void* p) {
+    if (!d || !p) return;
+    auto it = std::find(d->pinned.begin(), d->pinned.end(), p);
+    if (it == d->pinned.end()) return;
+    d->pinned.erase(it);
+    cudaFreeHost(p);
+}
+
+void vgpu_cu_set_notify(vgpu_cu_dev* d, void (*fn)(void*, std::uint32_t), void* ctx) {
+    if (!d) return;
+    std::lock_guard lk(d->notify_mu);
+    d->notify_fn = fn;
+    d->notify_ctx = ctx;
+}
+
+int vgpu_cu_get_stats(vgpu_cu_dev* d, vgpu_cu_stats* out) {
+    if (!d || !out) return VGPU_CU_EINVAL;
+    out->kernel_launches = d->launches.load();
+    out->tasks = d->tasks.load();
+    out->h2d_bytes = d->h2d_bytes.load();
+    out->d2h_bytes = d->d2h_bytes.load();
+    out->batches = d->nbatches.load();
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, std::uint32_t n,
+                         std::uint64_t* batch_id) {
+    if (!d || (!tasks && n)) return VGPU_CU_EINVAL;
+    if (n == 0) return VGPU_CU_OK;
+    // validate everything before enqueueing anything
+    std::vector<DevJob> jobs(n);
+    for (std::uint32_t i = 0; i < n; ++i) {
+        const vgpu_cu_task& t = tasks[i];
+        if (t.slot < 1 || t.slot > d->max_clients) {
+            set_err("task %u: slot %u out of range", i, t.slot);
+            return VGPU_CU_EINVAL;
+        }
+        if (d->slots[t.slot].busy) {
+            set_err("task %u: slot %u already has a task in flight", i, t.slot);
+            return VGPU_CU_EINVAL;
+        }
+        if (t.kernel >= VGPU_CU_K_COUNT) {
+            set_err("task %u: unknown kernel %u", i, t.kernel);
+            return VGPU_CU_EPAYLOAD;
+        }
+        std::uint64_t need = 0;
+        const int rc = vgpu_cu_output_size(t.kernel, t.h_in, t.in_bytes, &need);
+        if (rc) return rc;
+        if (t.in_bytes > d->slot_bytes || need > d->slot_bytes || t.out_bytes < need) {
+            set_err("task %u: %llu B in / %llu B out exceed the slot (%llu B)", i,
+                    (unsigned long long)t.in_bytes, (unsigned long long)need,
+                    (unsigned long long)d->slot_bytes);
+            return VGPU_CU_ESIZE;
+        }
+        for (std::uint32_t k = 0; k < i; ++k)
+            if (tasks[k].slot == t.slot) {
+                set_err("task %u: slot %u appears twice in one batch", i, t.slot);
+                return VGPU_CU_EINVAL;
+            }
+        SlotState& s = d->slots[t.slot];
+        DevJob& j = jobs[i];
+        j.kernel = t.kernel;
+        j.param = t.param;
+        j.in = s.d_in;
+        j.in_bytes = t.in_bytes;
+        j.out = s.d_out;
+        j.out_bytes = need;
+        j.scratch = s.d_scratch;
+        if (t.kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, t.h_in, sizeof j.ep);
+    }
+    CK(cudaSetDevice(d->device));
+
+    const std::uint64_t bid = d->next_batch++;
+    BatchRec rec;
+    rec.remaining = n;
+    int rc = d->pool_get(&rec.anchor);
+    if (rc) return rc;
+    CK(cudaEventRecord(rec.anchor, d->anchor_stream));
+
+    auto h2d = [&](std::uint32_t i) -> cudaError_t {
+        const vgpu_cu_task& t = tasks[i];
+        SlotState& s = d->slots[t.slot];
+        s.busy = true;
+        s.tag = t.tag;
+        s.batch = bid;
+        s.has_h2d = t.in_bytes > 0;
+        s.has_comp = false;
+        cudaError_t e = cudaEventRecord(s.ev[kEvH2d0], s.stream);
+        if (e == cudaSuccess && t.in_bytes)
+            e = cudaMemcpyAsync(s.d_in, t.h_in, t.in_bytes, cudaMemcpyHostToDevice, s.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(s.ev[kEvH2d1], s.stream);
+        d->h2d_bytes += t.in_bytes;
+        return e;
+    };
+    auto d2h = [&](std::uint32_t i) -> cudaError_t {
+        const vgpu_cu_task& t = tasks[i];
+        SlotState& s = d->slots[t.slot];
+        const std::uint64_t bytes = jobs[i].out_bytes;
+        const std::uint8_t* src = t.kernel == VGPU_CU_K_IDENTITY ? s.d_in : s.d_out;
+        cudaError_t e = cudaEventRecord(s.ev[kEvD2h0], s.stream);
+        if (e == cudaSuccess && bytes)
+            e = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(s.ev[kEvD2h1], s.stream);
+        if (e == cudaSuccess) e = cudaLaunchHostFunc(s.stream, slot_done, &s);
+        d->d2h_bytes += bytes;
+        return e;
+    };
+    auto compute_own = [&](std::uint32_t i) -> cudaError_t {
+        const vgpu_cu_task& t = tasks[i];
+        SlotState& s = d->slots[t.slot];
+        if (t.kernel == VGPU_CU_K_IDENTITY) return cudaSuccess;  // D2H reads d_in
+        s.has_comp = true;
+        s.comp0 = s.ev[kEvC0];
+        s.comp1 = s.ev[kEvC1];
+        std::uint64_t l = 0;
+        cudaError_t e = cudaEventRecord(s.comp0, s.stream);
+        if (e == cudaSuccess) e = launch_jobs(t.kernel, &jobs[i], 1, s.stream, &l);
+        if (e == cudaSuccess) e = cudaEventRecord(s.comp1, s.stream);
+        d->launches += l;
+        return e;
+    };
+
+    cudaError_t e = cudaSuccess;
+    if (style == 1) {  // PS-2: per-stream triples
+        for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) {
+            e = h2d(i);
+            if (e == cudaSuccess) e = compute_own(i);
+            if (e == cudaSuccess) e = d2h(i);
+        }
+    } else {  // PS-1: all sends, one launch per kernel kind, all retrieves
+        for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) e = h2d(i);
+        for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT && e == cudaSuccess; ++k) {
+            std::vector<std::uint32_t> group;
+            for (std::uint32_t i = 0; i < n; ++i)
+                if (tasks[i].kernel == k) group.push_back(i);
+            if (group.empty() || k == VGPU_CU_K_IDENTITY) continue;
+            if (group.size() == 1) {
+                e = compute_own(group[0]);
+                continue;
+            }
+            SlotState& lead = d->slots[tasks[group[0]].slot];
+            cudaEvent_t g0 = nullptr, g1 = nullptr;
+            if ((rc = d->pool_get(&g0)) || (rc = d->pool_get(&g1))) return rc;
+            rec.pooled.push_back(g0);
+            rec.pooled.push_back(g1);
+            for (std::size_t g = 1; g < group.size() && e == cudaSuccess; ++g)
+                e = cudaStreamWaitEvent(lead.stream, d->slots[tasks[group[g]].slot].ev[kEvH2d1], 0);
+            std::vector<DevJob> gj;
+            for (auto i : group) gj.push_back(jobs[i]);
+            std::uint64_t l = 0;
+            if (e == cudaSuccess) e = cudaEventRecord(g0, lead.stream);
+            if (e == cudaSuccess)
+                e = launch_jobs(k, gj.data(), static_cast<std::uint32_t>(gj.size()), lead.stream, &l);
+            if (e == cudaSuccess) e = cudaEventRecord(g1, lead.stream);
+            d->launches += l;
+            for (auto i : group) {
+                SlotState& s = d->slots[tasks[i].slot];
+                s.has_comp = true;
+                s.comp0 = g0;
+                s.comp1 = g1;
+                if (e == cudaSuccess && &s != &lead) e = cudaStreamWaitEvent(s.stream, g1, 0);
+            }
+        }
+        for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) e = d2h(i);
+    }
+    if (e != cudaSuccess) {
+        // drain whatever got enqueued, forget the batch
+        for (std::uint32_t i = 0; i < n; ++i) {
+            SlotState& s = d->slots[tasks[i].slot];
+            cudaStreamSynchronize(s.stream);
+            s.busy = false;
+        }
+        {
+            std::lock_guard lk(d->cb_mu);
+            d->finished.erase(std::remove_if(d->finished.begin(), d->finished.end(),
+                                             [&](std::uint32_t idx) {
+                                                 for (std::uint32_t i = 0; i < n; ++i)
+                                                     if (tasks[i].slot == idx) return true;
+                                                 return false;
+                                             }),
+                              d->finished.end());
+        }
+        d->event_pool.push_back(rec.anchor);
+        for (auto ev : rec.pooled) d->event_pool.push_back(ev);
+        return cuda_fail(e, "vgpu_cu_submit_batch");
+    }
+    d->tasks += n;
+    d->nbatches += 1;
+    d->batches.emplace(bid, std::move(rec));
+    if (batch_id) *batch_id = bid;
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint32_t* n_out) {
+    if (!d || !n_out || (!out && cap)) return VGPU_CU_EINVAL;
+    *n_out = 0;
+    std::vector<std::uint32_t> ready;
+    {
+        std::lock_guard lk(d->cb_mu);
+        const std::size_t take = std::min<std::size_t>(cap, d->finished.size());
+        ready.assign(d->finished.begin(), d->finished.begin() + take);
+        d->finished.erase(d->finished.begin(), d->finished.begin() + take);
+    }
+    if (ready.empty()) return VGPU_CU_OK;
+    cudaSetDevice(d->device);
+    const cudaError_t sticky = cudaPeekAtLastError();
+    for (std::uint32_t idx : ready) {
+        SlotState& s = d->slots[idx];
+        vgpu_cu_done& r = out[(*n_out)++];
+        std::memset(&r, 0, sizeof r);
+        r.tag = s.tag;
+        r.batch = s.batch;
+        r.slot = idx;
+        r.status = sticky == cudaSuccess ? VGPU_CU_OK : VGPU_CU_EINTERNAL;
+        r.h2d_us = s.has_h2d ? 1000.0f * elapsed_ms(s.ev[kEvH2d0], s.ev[kEvH2d1]) : 0.0f;
+        r.comp_us = s.has_comp ? 1000.0f * elapsed_ms(s.comp0, s.comp1) : 0.0f;
+        r.d2h_us = 1000.0f * elapsed_ms(s.ev[kEvD2h0], s.ev[kEvD2h1]);
+        r.span_us = 1000.0f * elapsed_ms(s.ev[kEvH2d0], s.ev[kEvD2h1]);
+        auto it = d->batches.find(s.batch);
+        if (it != d->batches.end()) {
+            BatchRec& b = it->second;
+            b.first = std::min(b.first, elapsed_ms(b.anchor, s.ev[kEvH2d0]));
+            b.last = std::max(b.last, elapsed_ms(b.anchor, s.ev[kEvD2h1]));
+            if (--b.remaining == 0) {
+                r.batch_done = 1;
+                r.batch_span_us = 1000.0f * std::max(0.0f, b.last - b.first);
+                d->event_pool.push_back(b.anchor);
+                for (auto ev : b.pooled) d->event_pool.push_back(ev);
+                d->batches.erase(it);
+            }
+        }
+        s.busy = false;
+    }
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_wait(vgpu_cu_dev* d, std::int64_t timeout_us) {
+    if (!d) return VGPU_CU_EINVAL;
+    std::unique_lock lk(d->cb_mu);
+    d->cb_cv.wait_for(lk, std::chrono::microseconds(timeout_us < 0 ? 0 : timeout_us),
+                      [&] { return !d->finished.empty(); });
+    return VGPU_CU_OK;
+}
+
+// ---- synchronous per-process execution (NativeVgpu, PayloadRegistry::execute) ----
+
+namespace {
+struct ProcCtx {
+    std::mutex mu;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    std::uint8_t* d_in = nullptr;
+    std::uint8_t* d_out = nullptr;
+    std::uint8_t* d_scratch = nullptr;
+    std::uint64_t cap_in = 0, cap_out = 0;
+    std::atomic<std::uint64_t> launches{0};
+};
+ProcCtx& proc() {
+    static ProcCtx c;
+    return c;
+}
+}  // namespace
+
+uint64_t vgpu_cu_execute_launches(void) { return proc().launches.load(); }
+
+int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* in,
+                    std::uint64_t in_bytes, void* out, std::uint64_t out_cap,
+                    std::uint64_t* out_bytes) {
+    if (!out_bytes || (!in && in_bytes)) return VGPU_CU_EINVAL;
+    std::uint64_t need = 0;
+    int rc = vgpu_cu_output_size(kernel, in, in_bytes, &need);
+    if (rc) return rc;
+    if (need > out_cap || (need && !out)) {
+        set_err("output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
+                (unsigned long long)need);
+        return VGPU_CU_ESIZE;
+    }
+    ProcCtx& c = proc();
+    std::lock_guard lk(c.mu);
+    if (c.device != device) {
+        rc = require_sm100(device);
+        if (rc) return rc;
+        CK(cudaSetDevice(device));
+        if (c.stream) cudaStreamDestroy(c.stream);
+        if (c.d_in) cudaFree(c.d_in);
+        if (c.d_out) cudaFree(c.d_out);
+        if (c.d_scratch) cudaFree(c.d_scratch);
+        c.d_in = c.d_out = c.d_scratch = nullptr;
+        c.cap_in = c.cap_out = 0;
+        CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        CK(cudaMalloc(&c.d_scratch, kScratchBytes));
+        CK(cudaMemset(c.d_scratch, 0, kScratchBytes));
+        c.device = device;
+    } else {
+        CK(cudaSetDevice(device));
+    }
+    if (in_bytes > c.cap_in) {
+        if (c.d_in) cudaFree(c.d_in);
+        c.d_in = nullptr;
+        c.cap_in = 0;
+        CK(cudaMalloc(&c.d_in, in_bytes));
+        c.cap_in = in_bytes;
+    }
+    if (need > c.cap_out) {
+        if (c.d_out) cudaFree(c.d_out);
+        c.d_out = nullptr;
+        c.cap_out = 0;
+        CK(cudaMalloc(&c.d_out, need));
+        c.cap_out = need;
+    }
+    DevJob j;
+    j.kernel = kernel;
+    j.param = param;
+    j.in = c.d_in;
+    j.in_bytes = in_bytes;
+    j.out = c.d_out;
+    j.out_bytes = need;
+    j.scratch = c.d_scratch;
+    if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, in, sizeof j.ep);
+    // pageable copies, exactly what an unvirtualized CUDA program does
+    if (in_bytes) CK(cudaMemcpyAsync(c.d_in, in, in_bytes, cudaMemcpyHostToDevice, c.stream));
+    std::uint64_t l = 0;
+    CK(launch_jobs(kernel, &j, 1, c.stream, &l));
+    c.launches += l;
+    if (need) CK(cudaMemcpyAsync(out, c.d_out, need, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    *out_bytes = need;
+    return VGPU_CU_OK;
+}
+
+// ---- device-resident measurement ---------------------------------------------------
+
+int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::uint32_t n_tasks,
+                           const void* const* h_inputs, const std::uint64_t* in_bytes,
+                           std::uint32_t sets, std::uint32_t warmup, std::uint32_t steps,
+                           vgpu_cu_resident_result* res) {
+    if (!res || n_tasks == 0 || !h_inputs || !in_bytes || sets == 0 || steps == 0)
+        return VGPU_CU_EINVAL;
+    std::memset(res, 0, sizeof *res);
+    int rc = require_sm100(device);
+    if (rc) return rc;
+    CK(cudaSetDevice(device));
+    std::vector<std::uint64_t> outb(n_tasks);
+    std::uint64_t per_set = 0;
+    for (std::uint32_t i = 0; i < n_tasks; ++i) {
+        rc = vgpu_cu_output_size(kernel, h_inputs[i], in_bytes[i], &outb[i]);
+        if (rc) return rc;
+        per_set += round_up(in_bytes[i], 256) + round_up(outb[i], 256) + round_up(kScratchBytes, 256);
+    }
+    std::uint8_t* mem = nullptr;
+    CK(cudaMalloc(&mem, per_set * sets));
+    struct Guard {
+        std::uint8_t* p;
+        cudaStream_t s = nullptr;
+        std::vector<cudaEvent_t> evs;
+        ~Guard() {
+            for (auto e : evs) cudaEventDestroy(e);
+            if (s) cudaStreamDestroy(s);
+            cudaFree(p);
+        }
+    } guard{mem};
+    CK(cudaMemset(mem, 0, per_set * sets));
+    std::vector<std::vector<DevJob>> js(sets, std::vector<DevJob>(n_tasks));
+    std::uint8_t* p = mem;
+    for (std::uint32_t s = 0; s < sets; ++s)
+        for (std::uint32_t i = 0; i < n_tasks; ++i) {
+            DevJob& j = js[s][i];
+            j.kernel = kernel;
+            j.param = param;
+            j.in = p;
+            j.in_bytes = in_bytes[i];
+            p += round_up(in_bytes[i], 256);
+            j.out = p;
+            j.out_bytes = outb[i];
+            p += round_up(outb[i], 256);
+            j.scratch = p;
+            p += round_up(kScratchBytes, 256);
+            if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, h_inputs[i], sizeof j.ep);
+            if (in_bytes[i])
+                CK(cudaMemcpy(const_cast<std::uint8_t*>(j.in), h_inputs[i], in_bytes[i],
+                              cudaMemcpyHostToDevice));
+        }
+    CK(cudaStreamCreateWithFlags(&guard.s, cudaStreamNonBlocking));
+    guard.evs.resize(2 * steps + 2);
+    for (auto& e : guard.evs) CK(cudaEventCreate(&e));
+    std::uint64_t l = 0;
+    for (std::uint32_t w = 0; w < warmup; ++w)
+        CK(launch_jobs(kernel, js[w % sets].data(), n_tasks, guard.s, &l));
+    CK(cudaStreamSynchronize(guard.s));
+    l = 0;
+    CK(cudaEventRecord(guard.evs[0], guard.s));
+    for (std::uint32_t t = 0; t < steps; ++t) {
+        CK(cudaEventRecord(guard.evs[2 + 2 * t], guard.s));
+        CK(launch_jobs(kernel, js[(warmup + t) % sets].data(), n_tasks, guard.s, &l));
+        CK(cudaEventRecord(guard.evs[3 + 2 * t], guard.s));
+    }
+    CK(cudaEventRecord(guard.evs[1], guard.s));
+    CK(cudaStreamSynchronize(guard.s));
+    float total = 0.0f;
+    CK(cudaEventElapsedTime(&total, guard.evs[0], guard.evs[1]));
+    double ksum = 0.0;
+    for (std::uint32_t t = 0; t < steps; ++t) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, guard.evs[2 + 2 * t], guard.evs[3 + 2 * t]));
+        ksum += ms;
+    }
+    res->ms_total = total;
+    res->ms_per_step = total / steps;
+    res->launches_per_step = static_cast<std::uint32_t>(l / steps);
+    res->kernel_ms_per_launch = ksum / steps / std::max<std::uint32_t>(1, res->launches_per_step);
+    res->sets = sets;
+    res->resident_bytes = per_set * sets;
+    std::uint64_t bytes = 0;
+    double flops = 0.0;
+    for (std::uint32_t i = 0; i < n_tasks; ++i) job_work(js[0][i], &bytes, &flops);
+    const std::uint32_t lp = std::max<std::uint32_t>(1, res->launches_per_step);
+    res->algo_bytes_per_launch = bytes / lp;
+    res->algo_flops_per_launch = flops / lp;
+    return VGPU_CU_OK;
+}
+
+// ---- multi-GPU final reduction ----------------------------------------------------
+
+int vgpu_cu_nccl_unique_id(void* id_out) {
+    if (!id_out) return VGPU_CU_EINVAL;
+    NcclApi& api = nccl();
+    if (!api.ok) {
+        set_err("libnccl.so.2 not loadable");
+        return VGPU_CU_ENCCL;
+    }
+    ncclUniqueId id;
+    const ncclResult_t r = api.get_unique_id(&id);
+    if (r != ncclSuccess) {
+        set_err("ncclGetUniqueId: %s", api.error_string ? api.error_string(r) : "?");
+        return VGPU_CU_ENCCL;
+    }
+    std::memcpy(id_out, &id, VGPU_CU_NCCL_ID_BYTES);
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_comm_init(vgpu_cu_dev* d, const void* id, int nranks, int rank) {
+    if (!d || !id || nranks < 1 || rank < 0 || rank >= nranks) return VGPU_CU_EINVAL;
+    NcclApi& api = nccl();
+    if (!api.ok) {
+        set_err("libnccl.so.2 not loadable");
+        return VGPU_CU_ENCCL;
+    }
+    CK(cudaSetDevice(d->device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, VGPU_CU_NCCL_ID_BYTES);
+    const ncclResult_t r = api.comm_init_rank(&d->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        set_err("ncclCommInitRank: %s", api.error_string ? api.error_string(r) : "?");
+        d->comm = nullptr;
+        return VGPU_CU_ENCCL;
+    }
+    d->nranks = nranks;
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_reduce_final(vgpu_cu_dev* d, const void* partial, std::uint64_t bytes, void* all_out) {
+    if (!d || !partial || !all_out || bytes == 0) return VGPU_CU_EINVAL;
+    if (!d->comm) {
+        set_err("vgpu_cu_comm_init not called");
+        return VGPU_CU_EINVAL;
+    }
+    CK(cudaSetDevice(d->device));
+    std::uint8_t* buf = nullptr;
+    CK(cudaMalloc(&buf, bytes * (d->nranks + 1)));
+    cudaStream_t s = d->anchor_stream;
+    cudaError_t e = cudaMemcpyAsync(buf, partial, bytes, cudaMemcpyHostToDevice, s);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess)
+        r = nccl().all_gather(buf, buf + bytes, bytes, ncclUint8, d->comm, s);
+    if (e == cudaSuccess && r == ncclSuccess)
+        e = cudaMemcpyAsync(all_out, buf + bytes, bytes * d->nranks, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(buf);
+    if (r != ncclSuccess) {
+        set_err("ncclAllGather: %s", nccl().error_string ? nccl().error_string(r) : "?");
+        return VGPU_CU_ENCCL;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "reduce_final");
+    return VGPU_CU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// vgpu-spmd — one SPMD process of a benchmark run (the forked worker of the
+// reference harness, proj/src/bench/bench.cpp:186-231).
+//
+//   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed
+//             --rounds R [--instance NAME | --native [--device D]]
+//
+// Builds its private input, leases a VGPU (retrying until the daemon is
+// up) — or, with --native, uses its OWN CUDA context through NativeVgpu —
+// prints "READY", waits for one byte on stdin (the start barrier), runs R
+// tasks through the unchanged client API (run_task), checks every result
+// (vecadd: exact elementwise sums; others: identical checksum every round)
+// and prints one JSON line with CLOCK_MONOTONIC timestamps per round.
+#include <malloc.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "vgpu/client.hpp"
+#include "workloads.hpp"
+
+namespace {
+
+std::int64_t now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out) {
+    const std::size_t n = in.size() / 8;
+    if (out.size() != 4 * n) return false;
+    const float* a = reinterpret_cast<const float*>(in.data());
+    const float* b = a + n;
+    const float* o = reinterpret_cast<const float*>(out.data());
+    for (std::size_t i = 0; i < n; ++i)
+        if (o[i] != a[i] + b[i]) return false;
+    return true;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    std::string instance, workload = "vecadd";
+    std::uint32_t worker = 0, workers = 1, rounds = 1;
+    bool native = false;
+    int device = 0;
+    vgpu::wl::Sizes sizes;
+    for (int i = 1; i < argc; ++i) {
+        const std::string a = argv[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= argc) throw std::invalid_argument(a + " needs a value");
+            return argv[++i];
+        };
+        try {
+            if (a == "--instance") instance = val();
+            else if (a == "--worker") worker = std::stoul(val());
+            else if (a == "--workers") workers = std::stoul(val());
+            else if (a == "--workload") workload = val();
+            else if (a == "--rounds") rounds = std::stoul(val());
+            else if (a == "--native") native = true;
+            else if (a == "--device") device = std::stoi(val());
+            else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(val());
+            else if (a == "--ep-m") sizes.ep_m = std::stoul(val());
+            else if (a == "--bs-n") sizes.bs_n = std::stoull(val());
+            else if (a == "--mm-n") sizes.mm_n = std::stoul(val());
+            else throw std::invalid_argument("unknown argument " + a);
+        } catch (const std::exception& e) {
+            std::fprintf(stderr, "vgpu-spmd: %s\n", e.what());
+            return 2;
+        }
+    }
+    // keep large result buffers in the heap between rounds (same for both modes)
+    mallopt(M_MMAP_THRESHOLD, 1 << 30);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+
+    const std::int64_t t_start = now_ns();
+    vgpu::wl::Job job = vgpu::wl::make_job(workload, worker, workers, sizes);
+    std::unique_ptr<vgpu::VgpuHandle> vh;
+    std::unique_ptr<vgpu::NativeVgpu> nh;
+    std::string err;
+    try {
+        if (native) {
+            vgpu::NativeConfig nc;
+            nc.cuda_device = device;
+            nh = std::make_unique<vgpu::NativeVgpu>(nc);
+        } else {
+            for (int attempt = 0;; ++attempt) {
+                try {
+                    vh = std::make_unique<vgpu::VgpuHandle>(vgpu::req(instance));
+                    break;
+                } catch (const vgpu::TransportError&) {
+                    if (attempt > 4000) throw;
+                    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+                }
+            }
+        }
+    } catch (const std::exception& e) {
+        std::printf("{\"worker\": %u, \"ok\": false, \"err\": \"connect: %s\"}\n", worker, e.what());
+        return 3;
+    }
+    std::printf("READY %d\n", static_cast<int>(getpid()));
+    std::fflush(stdout);
+    char go = 0;
+    if (read(0, &go, 1) != 1) return 4;
+
+    std::vector<std::int64_t> t0(rounds), t1(rounds);
+    std::uint64_t first_sum = 0;
+    bool ok = true;
+    const std::int64_t t_go = now_ns();
+    try {
+        for (std::uint32_t r = 0; r < rounds; ++r) {
+            t0[r] = now_ns();
+            const vgpu::Bytes out = native ? nh->run_task(job.input, job.desc)
+                                           : vh->run_task(job.input, job.desc);
+            t1[r] = now_ns();
+            if (out.size() != job.output_bytes) {
+                ok = false;
+                err = "wrong result size";
+            } else if (job.kind == vgpu::wl::Kind::VecAdd) {
+                if (!check_vecadd(job.input, out)) {
+                    ok = false;
+                    err = "vector-add sums differ";
+                }
+            } else {
+                const std::uint64_t h = vgpu::wl::fnv1a(out.data(), out.size());
+                if (r == 0) first_sum = h;
+                if (h != first_sum) {
+                    ok = false;
+                    err = "result changed between rounds";
+                }
+            }
+            if (job.kind == vgpu::wl::Kind::VecAdd && r == 0)
+                first_sum = vgpu::wl::fnv1a(out.data(), out.size());
+        }
+        if (vh) vh->rls();
+    } catch (const std::exception& e) {
+        ok = false;
+        err = e.what();
+    }
+    std::ostringstream os;
+    os << "{\"worker\": " << worker << ", \"ok\": " << (ok ? "true" : "false")
+       << ", \"kind\": " << static_cast<int>(job.kind) << ", \"native\": " << (native ? 1 : 0)
+       << ", \"t_start\": " << t_start << ", \"t_go\": " << t_go << ", \"checksum\": \""
+       << std::hex << first_sum << std::dec << "\", \"in_bytes\": " << job.input.size()
+       << ", \"out_bytes\": " << job.output_bytes << ", \"t0\": [";
+    for (std::uint32_t r = 0; r < rounds; ++r) os << (r ? ", " : "") << t0[r];
+    os << "], \"t1\": [";
+    for (std::uint32_t r = 0; r < rounds; ++r) os << (r ? ", " : "") << t1[r];
+    os << "], \"err\": \"" << err << "\"}";
+    std::printf("%s\n", os.str().c_str());
+    std::fflush(stdout);
+    return ok ? 0 : 5;
+}

@@ -1,0 +1,174 @@
+// Synthetic SPMD workloads of BASELINE.json configs C1-C5.
+//
+// Each worker of an SPMD run builds ONE job: its payload id, a kernel
+// descriptor (the timing triple is the client's declared estimate — the
+// GVM uses it only to pick PS-1/PS-2 and to report the model prediction)
+// and its private input bytes:
+//   vecadd  C1  n = 2^20 fp32 per operand; a[j] = (w+1)*1000 + j%512,
+//               b[j] = (j%512)*0.25 — the reference bench pattern
+//               (proj/src/bench/bench.cpp:34-49), every sum exact in fp32;
+//   ep      C2  NAS EP class A (m = 28) split over the EP workers in equal
+//               contiguous batch ranges (NPB-MPI decomposition);
+//   bs      C3  4 Mi options, S~U[5,30], X~U[1,100], T~U[0.25,10], seed 5347+w;
+//   mm      C4  2048 x 2048 fp32, A,B ~ U[-1,1], seed 1000+w;
+//   mixed   C5  worker w runs kind w % 4 (vecadd, ep, bs, mm).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vgpu/message.hpp"
+#include "vgpu/payload.hpp"
+#include "vgpu_cuda.h"
+
+namespace vgpu::wl {
+
+enum class Kind { VecAdd, Ep, Bs, Mm };
+
+struct Sizes {
+    std::uint64_t vecadd_n = 1ull << 20;
+    std::uint32_t ep_m = 28;
+    std::uint64_t bs_n = 4ull << 20;
+    std::uint32_t mm_n = 2048;
+};
+
+struct Job {
+    Kind kind;
+    KernelDescriptor desc;
+    Bytes input;
+    std::uint64_t output_bytes = 0;
+};
+
+inline Kind kind_of(const std::string& workload, std::uint32_t worker) {
+    if (workload == "vecadd") return Kind::VecAdd;
+    if (workload == "ep") return Kind::Ep;
+    if (workload == "bs") return Kind::Bs;
+    if (workload == "mm") return Kind::Mm;
+    if (workload == "mixed") return static_cast<Kind>(worker % 4);
+    throw std::invalid_argument("unknown workload: " + workload);
+}
+
+inline std::uint64_t xorshift(std::uint64_t& s) {
+    s ^= s >> 12;
+    s ^= s << 25;
+    s ^= s >> 27;
+    return s * 0x2545F4914F6CDD1Dull;
+}
+
+inline float uniform(std::uint64_t& s, float lo, float hi) {
+    const double u = static_cast<double>(xorshift(s) >> 11) * (1.0 / 9007199254740992.0);
+    return static_cast<float>(lo + (hi - lo) * u);
+}
+
+inline std::uint64_t fnv1a(const std::uint8_t* p, std::size_t n) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (std::size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+// declared stage estimates (us): PCIe ~50 GB/s, HBM ~6.5 TB/s, FP32 ~50 TF/s
+inline Micros pcie_us(std::uint64_t bytes) { return bytes / 50'000 + 1; }
+
+inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint32_t workers,
+                    const Sizes& sz = {}) {
+    Job j;
+    j.kind = kind_of(workload, worker);
+    switch (j.kind) {
+        case Kind::VecAdd: {
+            const std::uint64_t n = sz.vecadd_n;
+            std::vector<float> v(2 * n);
+            for (std::uint64_t i = 0; i < n; ++i) {
+                v[i] = static_cast<float>(worker + 1) * 1000.0f + static_cast<float>(i % 512);
+                v[n + i] = static_cast<float>(i % 512) * 0.25f;
+            }
+            j.input.resize(8 * n);
+            std::memcpy(j.input.data(), v.data(), j.input.size());
+            j.desc.payload_id = "vector-add";
+            j.desc.t_data_in = pcie_us(8 * n);
+            j.desc.t_comp = (12 * n) / 6'500'000 + 1;
+            j.desc.t_data_out = pcie_us(4 * n);
+            j.desc.grid_size = static_cast<std::uint32_t>((n + 4095) / 4096);
+            j.output_bytes = 4 * n;
+            break;
+        }
+        case Kind::Ep: {
+            // EP workers share the class: rank among EP workers, count of EP workers
+            std::uint32_t rank = worker, count = workers;
+            if (workload == "mixed") {
+                rank = worker / 4;
+                count = (workers + 2) / 4;  // workers w with w % 4 == 1
+            }
+            const std::uint64_t total = 1ull << (sz.ep_m - 16);
+            const std::uint64_t per = total / count, extra = total % count;
+            vgpu_ep_params p{};
+            p.m = sz.ep_m;
+            p.mk = 16;
+            p.first_batch = rank * per + std::min<std::uint64_t>(rank, extra);
+            p.n_batches = per + (rank < extra ? 1 : 0);
+            j.input.resize(sizeof p);
+            std::memcpy(j.input.data(), &p, sizeof p);
+            j.desc.payload_id = "nas-ep";
+            j.desc.t_data_in = 1;
+            j.desc.t_comp = p.n_batches / 4 + 1;  // ~0.25 us per 2^16-pair batch
+            j.desc.t_data_out = 1;
+            j.desc.grid_size = static_cast<std::uint32_t>(p.n_batches);
+            j.output_bytes = sizeof(vgpu_ep_result);
+            break;
+        }
+        case Kind::Bs: {
+            const std::uint64_t n = sz.bs_n;
+            std::vector<float> v(3 * n);
+            std::uint64_t s = 5347 + worker;
+            for (std::uint64_t i = 0; i < n; ++i) {
+                v[i] = uniform(s, 5.0f, 30.0f);
+                v[n + i] = uniform(s, 1.0f, 100.0f);
+                v[2 * n + i] = uniform(s, 0.25f, 10.0f);
+            }
+            j.input.resize(12 * n);
+            std::memcpy(j.input.data(), v.data(), j.input.size());
+            j.desc.payload_id = "black-scholes";
+            j.desc.t_data_in = pcie_us(12 * n);
+            j.desc.t_comp = (20 * n) / 6'500'000 + 1;
+            j.desc.t_data_out = pcie_us(8 * n);
+            j.desc.grid_size = static_cast<std::uint32_t>((n + 2047) / 2048);
+            j.output_bytes = 8 * n;
+            break;
+        }
+        case Kind::Mm: {
+            const std::uint64_t n = sz.mm_n;
+            std::vector<float> v(2 * n * n);
+            std::uint64_t s = 1000 + worker;
+            for (auto& x : v) x = uniform(s, -1.0f, 1.0f);
+            j.input.resize(8 * n * n);
+            std::memcpy(j.input.data(), v.data(), j.input.size());
+            j.desc.payload_id = "sgemm";
+            j.desc.t_data_in = pcie_us(8 * n * n);
+            j.desc.t_comp = static_cast<Micros>(2.0 * n * n * n / 50e6) + 1;
+            j.desc.t_data_out = pcie_us(4 * n * n);
+            j.desc.grid_size = static_cast<std::uint32_t>((n / 128) * (n / 128));
+            j.output_bytes = 4 * n * n;
+            break;
+        }
+    }
+    return j;
+}
+
+// Largest region any worker of `workload` needs.
+inline std::uint64_t region_bytes(const std::string& workload, const Sizes& sz = {}) {
+    const std::uint64_t va = 8 * sz.vecadd_n, bs = 12 * sz.bs_n,
+                        mm = 8ull * sz.mm_n * sz.mm_n, ep = sizeof(vgpu_ep_result);
+    if (workload == "vecadd") return va;
+    if (workload == "ep") return ep;
+    if (workload == "bs") return bs;
+    if (workload == "mm") return mm;
+    return std::max({va, bs, mm, ep});
+}
+
+}  // namespace vgpu::wl

@@ -1,0 +1,374 @@
+// [gpu] parity of the sm_100a payload kernels against the CPU oracle,
+// through every path a client can reach them: the GVM (loopback and OS
+// transports, PS-1 batched launches and PS-2 triples, both data planes),
+// PayloadRegistry::execute and the NativeVgpu baseline.
+// Bars: bit-exact for vector-add / vector-scale / identity / nas-ep;
+// black-scholes L1-relative <= 1e-6 vs binary64; sgemm relative
+// Frobenius <= 1e-5 vs binary64 accumulation.
+#include <sys/wait.h>
+#include <unistd.h>
+
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "minitest.hpp"
+#include "vgpu/client.hpp"
+#include "vgpu_cuda.h"
+#include "vgpu_oracle.h"
+
+using namespace vgpu;
+using namespace std::chrono_literals;
+
+namespace {
+
+GvmConfig gcfg(std::uint32_t clients, std::uint64_t shm = 16 << 20, Micros window = 2000) {
+    GvmConfig g;
+    g.max_clients = clients;
+    g.barrier_size = clients;
+    g.barrier_window = window;
+    g.per_client_shm_bytes = shm;
+    g.t_init = 100;
+    return g;
+}
+
+KernelDescriptor desc(const std::string& id, bool compute_intensive = true) {
+    KernelDescriptor d;
+    d.payload_id = id;
+    d.t_data_in = compute_intensive ? 20 : 60;
+    d.t_comp = compute_intensive ? 50 : 20;
+    d.t_data_out = compute_intensive ? 20 : 40;
+    return d;
+}
+
+template <class T>
+Bytes pack(const std::vector<T>& v) {
+    Bytes b(v.size() * sizeof(T));
+    if (!b.empty()) std::memcpy(b.data(), v.data(), b.size());
+    return b;
+}
+
+template <class T>
+std::vector<T> unpack(const Bytes& b) {
+    std::vector<T> v(b.size() / sizeof(T));
+    if (!b.empty()) std::memcpy(v.data(), b.data(), b.size());
+    return v;
+}
+
+Bytes vadd_input(std::size_t n, std::uint64_t seed) {
+    std::vector<float> v(2 * n);
+    std::uint64_t s = seed;
+    for (auto& x : v) x = vo_rng_uniform(&s, -1000.f, 1000.f);
+    return pack(v);
+}
+
+Bytes vadd_expect(const Bytes& in) {
+    const std::size_t n = in.size() / 8;
+    std::vector<float> out(n);
+    const float* a = reinterpret_cast<const float*>(in.data());
+    vo_vector_add(out.data(), a, a + n, n);
+    return pack(out);
+}
+
+Bytes ep_input(std::uint32_t m, std::uint64_t first, std::uint64_t count) {
+    vgpu_ep_params p{m, 16, first, count, 0};
+    Bytes b(sizeof p);
+    std::memcpy(b.data(), &p, sizeof p);
+    return b;
+}
+
+Bytes ep_expect(const Bytes& in) {
+    vgpu_ep_params p;
+    std::memcpy(&p, in.data(), sizeof p);
+    vgpu_ep_result r;
+    vo_ep_job(&p, &r);
+    Bytes b(sizeof r);
+    std::memcpy(b.data(), &r, sizeof r);
+    return b;
+}
+
+Bytes bs_input(std::size_t n, std::uint64_t seed) {
+    std::vector<float> v(3 * n);
+    std::uint64_t s = seed;
+    for (std::size_t i = 0; i < n; ++i) {
+        v[i] = vo_rng_uniform(&s, 5.f, 30.f);
+        v[n + i] = vo_rng_uniform(&s, 1.f, 100.f);
+        v[2 * n + i] = vo_rng_uniform(&s, 0.25f, 10.f);
+    }
+    return pack(v);
+}
+
+double bs_l1_error(const Bytes& in, const Bytes& out) {
+    const std::size_t n = in.size() / 12;
+    const float* f = reinterpret_cast<const float*>(in.data());
+    std::vector<double> call(n), put(n);
+    vo_black_scholes(f, f + n, f + 2 * n, n, VGPU_BS_RISKFREE, VGPU_BS_VOLATILITY, call.data(),
+                     put.data());
+    const auto got = unpack<float>(out);
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < n; ++i) {
+        num += std::fabs(call[i] - got[i]) + std::fabs(put[i] - got[n + i]);
+        den += std::fabs(call[i]) + std::fabs(put[i]);
+    }
+    return den > 0 ? num / den : num;
+}
+
+Bytes mm_input(std::size_t n, std::uint64_t seed) {
+    std::vector<float> v(2 * n * n);
+    std::uint64_t s = seed;
+    for (auto& x : v) x = vo_rng_uniform(&s, -1.f, 1.f);
+    return pack(v);
+}
+
+double mm_rel_error(const Bytes& in, const Bytes& out) {
+    const std::size_t n = static_cast<std::size_t>(std::llround(std::sqrt(in.size() / 8.0)));
+    const float* f = reinterpret_cast<const float*>(in.data());
+    std::vector<double> c(n * n);
+    vo_sgemm(f, f + n * n, n, c.data());
+    const auto got = unpack<float>(out);
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < n * n; ++i) {
+        num += (c[i] - got[i]) * (c[i] - got[i]);
+        den += c[i] * c[i];
+    }
+    return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+}  // namespace
+
+TEST_CASE("[gpu] device is a B200-class part") {
+    int n = 0;
+    REQUIRE(vgpu_cu_device_count(&n) == VGPU_CU_OK);
+    REQUIRE(n >= 1);
+}
+
+TEST_CASE("[gpu] reference goldens through PayloadRegistry::execute") {
+    const auto& reg = PayloadRegistry::builtins();
+    const Bytes data{1, 2, 3, 4, 5};
+    CHECK(reg.execute("identity", data) == data);
+    CHECK(unpack<float>(reg.execute("vector-add", pack<float>({1.f, 2.f, 3.f, 4.f}))) ==
+          std::vector<float>({4.f, 6.f}));
+    CHECK(unpack<float>(reg.execute("vector-scale", pack<float>({1.5f}))) ==
+          std::vector<float>({3.0f}));
+    CHECK_THROWS_AS((void)reg.execute("vector-add", Bytes{1, 2, 3}), PayloadError);
+    CHECK_THROWS_AS((void)reg.execute("vector-scale", Bytes{1, 2, 3}), PayloadError);
+    CHECK_THROWS_AS((void)reg.execute("no-such", Bytes{}), PayloadError);
+    // custom factor still lands on the device kernel
+    auto r2 = PayloadRegistry::with_builtins();
+    r2.register_payload("scale-3.25", make_vector_scale(3.25f));
+    REQUIRE(r2.device_kernel("scale-3.25") != nullptr);
+    CHECK(unpack<float>(r2.execute("scale-3.25", pack<float>({2.f}))) == std::vector<float>({6.5f}));
+}
+
+TEST_CASE("[gpu] vector-add / vector-scale bit-exact vs serial oracle (test_payload sizes)") {
+    const auto& reg = PayloadRegistry::builtins();
+    auto scaled = PayloadRegistry::with_builtins();
+    scaled.register_payload("scale-3.25", make_vector_scale(3.25f));
+    for (std::size_t n : {1u, 7u, 1024u, 100003u, 1u << 20}) {
+        const Bytes in = vadd_input(n, 41 + n);
+        CHECK(reg.execute("vector-add", in) == vadd_expect(in));
+        const Bytes a(in.begin(), in.begin() + 4 * n);
+        std::vector<float> want(n);
+        vo_vector_scale(want.data(), reinterpret_cast<const float*>(a.data()), 3.25f, n);
+        CHECK(scaled.execute("scale-3.25", a) == pack(want));
+        vo_vector_scale(want.data(), reinterpret_cast<const float*>(a.data()), 2.0f, n);
+        CHECK(reg.execute("vector-scale", a) == pack(want));
+    }
+    CHECK(reg.execute("vector-add", Bytes{}).empty());
+}
+
+TEST_CASE("[gpu] two-client flow with the real kernels (virtual clock)") {
+    LoopbackHub hub;
+    auto d = GvmDaemon::start_loopback(gcfg(2, 1 << 16, 1'000'000'000), hub);
+    VgpuHandle a = req(hub);
+    VgpuHandle b = req(hub);
+    a.snd(pack<float>({1, 2, 3, 4}));
+    b.snd(pack<float>({10, 20, 30, 40}));
+    std::thread tb([&] { b.str(desc("vector-add")); });
+    a.str(desc("vector-add"));
+    tb.join();
+    CHECK(a.stp());  // virtual clock: done by the time STR is acked
+    CHECK(b.stp());
+    CHECK(unpack<float>(a.rcv()) == std::vector<float>({4, 6}));
+    CHECK(unpack<float>(b.rcv()) == std::vector<float>({40, 60}));
+    const auto m = d->metrics();
+    CHECK(m.batches_flushed == 1);
+    CHECK(m.kernel_launches == 1);  // one batched launch for both clients
+    CHECK(m.batches.at(0).model_makespan_us == 210);
+}
+
+TEST_CASE("[gpu] GVM parity for every payload, PS-1 and PS-2, both data planes") {
+    for (DataPlane plane : {DataPlane::ZeroCopy, DataPlane::Snapshot})
+        for (bool ci : {true, false}) {
+            LoopbackHub hub;
+            auto g = gcfg(4, 16 << 20);
+            g.data_plane = plane;
+            g.clock = ClockMode::Real;
+            auto d = GvmDaemon::start_loopback(g, hub);
+            std::vector<std::string> err(4);
+            std::vector<std::thread> ts;
+            for (int w = 0; w < 4; ++w)
+                ts.emplace_back([&, w] {
+                    try {
+                        VgpuHandle h = req(hub);
+                        for (int rep = 0; rep < 3; ++rep) {
+                            const std::size_t n = rep == 0 ? 100003 : (1u << 18) + 4 * w;
+                            const Bytes in = vadd_input(n, 1000 * w + rep);
+                            if (h.run_task(in, desc("vector-add", ci)) != vadd_expect(in))
+                                err[w] += "vadd ";
+                            const Bytes ep = ep_input(20, 3 * w, 2 + w % 2);
+                            if (h.run_task(ep, desc("nas-ep", ci)) != ep_expect(ep)) err[w] += "ep ";
+                            const Bytes bs = bs_input(4096 + w, 7 + w);
+                            if (bs_l1_error(bs, h.run_task(bs, desc("black-scholes", ci))) > 1e-6)
+                                err[w] += "bs ";
+                            const Bytes mm = mm_input(w == 3 ? 100 : 128, 11 + w);
+                            if (mm_rel_error(mm, h.run_task(mm, desc("sgemm", ci))) > 1e-5)
+                                err[w] += "mm ";
+                            const Bytes id{1, 2, 3, static_cast<std::uint8_t>(w)};
+                            if (h.run_task(id, desc("identity", ci)) != id) err[w] += "id ";
+                        }
+                        h.rls();
+                    } catch (const std::exception& e) {
+                        err[w] += e.what();
+                    }
+                });
+            for (auto& t : ts) t.join();
+            for (int w = 0; w < 4; ++w) {
+                if (!err[w].empty()) MESSAGE("worker " + std::to_string(w) + ": " + err[w]);
+                CHECK(err[w].empty());
+            }
+            const auto m = d->metrics();
+            CHECK(m.device_tasks == 4 * 3 * 5);
+            bool style_ok = true;
+            for (const auto& b : m.batches)
+                style_ok &= b.style == (ci ? ProgrammingStyle::PS1 : ProgrammingStyle::PS2);
+            CHECK(style_ok);
+            bool timed = true;
+            for (const auto& t : m.tasks) timed &= t.pure_gpu_us > 0 || t.end_to_end_us > 0;
+            CHECK(timed);
+        }
+}
+
+TEST_CASE("[gpu] mixed-kernel batch and EP slices fold to the whole class") {
+    LoopbackHub hub;
+    auto d = GvmDaemon::start_loopback(gcfg(5, 4 << 20), hub);
+    std::vector<Bytes> outs(5);
+    std::vector<Bytes> ins = {ep_input(22, 0, 16), ep_input(22, 16, 16), ep_input(22, 32, 32),
+                              vadd_input(5000, 3), mm_input(64, 5)};
+    const char* ids[] = {"nas-ep", "nas-ep", "nas-ep", "vector-add", "sgemm"};
+    std::vector<std::thread> ts;
+    for (int w = 0; w < 5; ++w)
+        ts.emplace_back([&, w] {
+            VgpuHandle h = req(hub);
+            outs[w] = h.run_task(ins[w], desc(ids[w]));
+        });
+    for (auto& t : ts) t.join();
+    CHECK(outs[3] == vadd_expect(ins[3]));
+    CHECK(mm_rel_error(ins[4], outs[4]) <= 1e-5);
+    vgpu_ep_result parts[3], folded, whole;
+    for (int i = 0; i < 3; ++i) {
+        CHECK(outs[i] == ep_expect(ins[i]));
+        std::memcpy(&parts[i], outs[i].data(), sizeof parts[i]);
+    }
+    vo_ep_fold(parts, 3, &folded);
+    vgpu_ep_params p{22, 16, 0, 64, 0};
+    vo_ep_job(&p, &whole);
+    CHECK(folded.pairs == whole.pairs);
+    for (int i = 0; i < 10; ++i) CHECK(folded.q[i] == whole.q[i]);
+    CHECK(std::fabs(folded.sx - whole.sx) <= 1e-9 * std::fabs(whole.sx));
+    CHECK(d->metrics().batches_flushed == 1);
+}
+
+TEST_CASE("[gpu] NAS EP class S on the GPU equals NPB's verification sums") {
+    const Bytes in = ep_input(24, 0, 256);
+    const Bytes out = PayloadRegistry::builtins().execute("nas-ep", in);
+    CHECK(out == ep_expect(in));
+    vgpu_ep_result r;
+    std::memcpy(&r, out.data(), sizeof r);
+    CHECK(r.pairs == 13176389ull);
+    CHECK(std::fabs((r.sx - -3.247834652034740e3) / 3.247834652034740e3) < 1e-8);
+    CHECK(std::fabs((r.sy - -6.958407078382297e3) / 6.958407078382297e3) < 1e-8);
+}
+
+TEST_CASE("[gpu] malformed inputs fail through STP with Payload, slot stays usable after RLS") {
+    LoopbackHub hub;
+    auto d = GvmDaemon::start_loopback(gcfg(1, 1 << 16), hub);
+    const std::pair<const char*, Bytes> bad[] = {
+        {"vector-add", Bytes{1, 2, 3}},
+        {"vector-scale", Bytes{1, 2}},
+        {"black-scholes", Bytes(13)},
+        {"sgemm", Bytes(24)},
+        {"nas-ep", Bytes(31)},
+        {"nas-ep", ep_input(30, 1ull << 14, 1)},
+    };
+    for (const auto& [id, in] : bad) {
+        VgpuHandle h = req(hub);
+        h.snd(in);
+        h.str(desc(id));
+        try {
+            h.stp_wait();
+            FAIL(std::string("accepted malformed ") + id);
+        } catch (const VgpuError& e) {
+            CHECK(e.code() == ErrCode::Payload);
+        }
+        h.rls();
+    }
+    VgpuHandle h = req(hub);
+    CHECK(h.run_task(pack<float>({1, 2, 3, 4}), desc("vector-add")) == pack<float>({4, 6}));
+}
+
+TEST_CASE("[gpu] OS transport: forked SPMD clients through one GVM (real clock)") {
+    GvmConfig g = gcfg(4, 8 << 20, 20000);
+    g.clock = ClockMode::Real;
+    g.instance = "gt" + std::to_string(getpid());
+    unlink_os_instance(g.instance, g.max_clients);
+    std::vector<pid_t> kids;
+    for (std::uint32_t w = 0; w < 4; ++w) {
+        const pid_t pid = fork();
+        if (pid == 0) {
+            for (int attempt = 0; attempt < 2000; ++attempt) {
+                try {
+                    VgpuHandle h = req(g.instance);
+                    for (int rep = 0; rep < 10; ++rep) {
+                        const Bytes in = vadd_input(1u << 20, w * 100 + rep);
+                        if (h.run_task(in, desc("vector-add", false)) != vadd_expect(in)) _exit(3);
+                    }
+                    h.rls();
+                    _exit(0);
+                } catch (const TransportError&) {
+                    usleep(5000);
+                } catch (...) {
+                    _exit(5);
+                }
+            }
+            _exit(6);
+        }
+        kids.push_back(pid);
+    }
+    auto d = GvmDaemon::start_os(g);
+    for (pid_t k : kids) {
+        int st = 0;
+        waitpid(k, &st, 0);
+        CHECK(WIFEXITED(st));
+        CHECK(WEXITSTATUS(st) == 0);
+    }
+    const auto m = d->metrics();
+    CHECK(m.tasks.size() == 40);
+    bool measured = true;
+    for (const auto& t : m.tasks) measured &= t.h2d_us > 0 && t.d2h_us > 0 && t.pure_gpu_us > 0;
+    CHECK(measured);
+    for (const auto& b : m.batches) CHECK(b.measured_makespan_us > 0);
+    d->stop();
+}
+
+TEST_CASE("[gpu] NativeVgpu (own context, pageable copies) matches the GVM") {
+    const Bytes in = vadd_input(123457, 99);
+    NativeVgpu n{NativeConfig{}};
+    CHECK(n.run_task(in, desc("vector-add")) == vadd_expect(in));
+    const Bytes ep = ep_input(20, 5, 3);
+    CHECK(n.run_task(ep, desc("nas-ep")) == ep_expect(ep));
+    const Bytes mm = mm_input(256, 17);
+    CHECK(mm_rel_error(mm, n.run_task(mm, desc("sgemm"))) <= 1e-5);
+    const Bytes bs = bs_input(1 << 16, 23);
+    CHECK(bs_l1_error(bs, n.run_task(bs, desc("black-scholes"))) <= 1e-6);
+}

@@ -1,0 +1,149 @@
+"""[gpu] Parity at BASELINE.json's full sizes, through the C-ABI.
+
+A GVM is started on cuda:0 over the OS transport (vgpu_gvm_start_os) and
+SPMD clients lease VGPUs through vgpu_client_* (each client in its own
+thread; ctypes releases the GIL, the GVM sees independent connections).
+Checks against the oracle (oracle/oracle.py) and committed fixtures:
+  C1 vector-add 4 x 2^20        bit-exact
+  C2 NAS EP class A over 8      bit-exact vs oracle fixture; NPB sums 1e-8
+  C3 Black-Scholes 4Mi options  L1-relative <= 1e-6 vs binary64 oracle
+  C4 SGEMM 2048^2               relative Frobenius <= 1e-5 on 64 sampled rows
+"""
+import json
+import os
+import struct
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1511_07658_b200 import vgpu as V
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _gvm(n, shm, clock=V.ClockMode.Real):
+    inst = f"pt{os.getpid()}_{n}_{shm}"
+    V.unlink_os_instance(inst, n)
+    cfg = V.GvmConfig(instance=inst, max_clients=n, barrier_size=n, per_client_shm_bytes=shm,
+                      barrier_window=20000, clock=clock)
+    return V.GvmDaemon.start_os(cfg), inst
+
+
+def _spmd(inst, inputs, desc):
+    outs = [None] * len(inputs)
+    errs = []
+
+    def worker(i):
+        try:
+            h = V.req(inst)
+            outs[i] = h.run_task(inputs[i], desc)
+            h.rls()
+            h.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(inputs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    return outs
+
+
+def test_c1_vector_add_full_size_bit_exact():
+    n = 1 << 20
+    rng = np.random.default_rng(41)
+    ins, want = [], []
+    for w in range(4):
+        a = rng.uniform(-1000, 1000, n).astype(np.float32)
+        b = rng.uniform(-1000, 1000, n).astype(np.float32)
+        ins.append(a.tobytes() + b.tobytes())
+        want.append(oracle.vector_add(a, b).tobytes())
+    d, inst = _gvm(4, 8 * n)
+    with d:
+        outs = _spmd(inst, ins, V.KernelDescriptor("vector-add", 168, 2, 84))
+        s = d.summary()
+    assert outs == want
+    assert s["device_tasks"] == 4 and s["kernel_launches"] >= 1
+
+
+def test_c2_nas_ep_class_a_over_8_processes():
+    fx = json.load(open(os.path.join(GOLD, "ep_oracle.json")))["28x8"]
+    ins = [oracle.ep_params_bytes(28, 512 * p, 512) for p in range(8)]
+    d, inst = _gvm(8, 4096)
+    with d:
+        outs = _spmd(inst, ins, V.KernelDescriptor("nas-ep", 1, 128, 1))
+    parts = [oracle.ep_from_bytes(o) for o in outs]
+    for p, sxb, syb in zip(parts, fx["parts_sx_bits"], fx["parts_sy_bits"]):
+        assert struct.pack("<d", p.sx).hex() == sxb
+        assert struct.pack("<d", p.sy).hex() == syb
+    f = oracle.ep_fold(parts)
+    assert list(f.q) == fx["q"] and f.pairs == fx["pairs"] == 210832767
+    assert struct.pack("<d", f.sx).hex() == fx["sx_bits"]
+    sxv, syv = oracle.NPB_VERIFY[28]
+    assert abs((f.sx - sxv) / sxv) < 1e-8 and abs((f.sy - syv) / syv) < 1e-8
+
+
+def test_c3_black_scholes_4m_options():
+    n = 4 << 20
+    rng = np.random.default_rng(5347)
+    ins, gold = [], []
+    for w in range(2):
+        S = rng.uniform(5, 30, n).astype(np.float32)
+        X = rng.uniform(1, 100, n).astype(np.float32)
+        T = rng.uniform(0.25, 10, n).astype(np.float32)
+        ins.append(S.tobytes() + X.tobytes() + T.tobytes())
+        gold.append(oracle.black_scholes(S, X, T))
+    d, inst = _gvm(2, 12 * n)
+    with d:
+        outs = _spmd(inst, ins, V.KernelDescriptor("black-scholes", 1000, 13, 670))
+    for out, (call, put) in zip(outs, gold):
+        got = np.frombuffer(out, np.float32).astype(np.float64)
+        ref = np.concatenate([call, put])
+        l1 = np.sum(np.abs(got - ref)) / np.sum(np.abs(ref))
+        assert l1 <= 1e-6, l1
+        assert np.max(np.abs(got - ref)) < 5e-4
+
+
+def test_c4_sgemm_2048_sampled_rows():
+    n = 2048
+    rng = np.random.default_rng(1000)
+    A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    d, inst = _gvm(1, 8 * n * n)
+    with d:
+        (out,) = _spmd(inst, [A.tobytes() + B.tobytes()], V.KernelDescriptor("sgemm", 670, 344, 335))
+    Cm = np.frombuffer(out, np.float32).reshape(n, n)
+    rows = rng.choice(n, 64, replace=False)
+    ref = A[rows].astype(np.float64) @ B.astype(np.float64)
+    err = np.linalg.norm(Cm[rows] - ref) / np.linalg.norm(ref)
+    assert err <= 1e-5, err
+
+
+def test_native_baseline_matches_gvm_bit_exact():
+    n = (1 << 18) + 3
+    rng = np.random.default_rng(7)
+    a = rng.uniform(-1, 1, n).astype(np.float32)
+    b = rng.uniform(-1, 1, n).astype(np.float32)
+    data = a.tobytes() + b.tobytes()
+    native = V.native_run_task(data, V.KernelDescriptor("vector-add"))
+    d, inst = _gvm(1, 8 * n)
+    with d:
+        (virt,) = _spmd(inst, [data], V.KernelDescriptor("vector-add"))
+    assert native == virt == oracle.vector_add(a, b).tobytes()
+
+
+def test_virtual_clock_metrics_match_the_model():
+    n = 1024
+    ins = [np.ones(2 * n, np.float32).tobytes()] * 4
+    d, inst = _gvm(4, 8 * n, clock=V.ClockMode.Virtual)
+    with d:
+        _spmd(inst, ins, V.KernelDescriptor("vector-add", 20, 50, 20))
+        b = d.batches()
+        csv = d.metrics_csv()
+    assert b[0]["model_makespan_us"] == b[0]["measured_makespan_us"] == 210
+    assert csv.startswith("task_id,client_id,queue_wait_us,pure_gpu_us,end_to_end_us")

@@ -1,0 +1,108 @@
+"""Pins the oracle before it is trusted (CPU only).
+
+* vector-add / vector-scale: bit-exact against golden vectors produced by the
+  UNMODIFIED reference library (tests/golden/ref_vector_ops.bin, written by
+  oracle/_ref/ref-golden) and against the reference unit-test goldens
+  (proj/tests/test_payload.cpp:33-37) and the exact-sum bench pattern
+  (proj/src/bench/bench.cpp:34-49).
+* NAS EP: against NPB's published verification sums (epsilon 1e-8) for
+  class S recomputed here, and the committed class S/W/A fixtures.
+* Black-Scholes / SGEMM: parity unpinned by the reference (no arithmetic
+  there); checked for internal consistency (put-call parity, exact small
+  products).
+"""
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _ref_vectors():
+    raw = open(os.path.join(GOLD, "ref_vector_ops.bin"), "rb").read()
+    off, out = 0, []
+    while off < len(raw):
+        (n,) = struct.unpack_from("<Q", raw, off)
+        off += 8
+        arrs = []
+        for _ in range(4):
+            arrs.append(np.frombuffer(raw, np.float32, n, off))
+            off += 4 * n
+        out.append((n, *arrs))
+    return out
+
+
+def test_vector_ops_match_reference_outputs_bit_exact():
+    cases = _ref_vectors()
+    assert [c[0] for c in cases] == [1, 7, 1024, 4099]
+    for n, a, b, add, scale2 in cases:
+        assert oracle.vector_add(a, b).tobytes() == add.tobytes()
+        assert oracle.vector_scale(a, 2.0).tobytes() == scale2.tobytes()
+
+
+def test_reference_unit_goldens():
+    assert oracle.vector_add(np.array([1, 2], np.float32), np.array([3, 4], np.float32)).tolist() == [4, 6]
+    assert oracle.vector_scale(np.array([1.5], np.float32), 2.0).tolist() == [3.0]
+    j = np.arange(1 << 12)
+    for w in range(4):
+        a = ((w + 1) * 1000 + (j % 512)).astype(np.float32)
+        b = ((j % 512) * 0.25).astype(np.float32)
+        exact = (a.astype(np.float64) + b.astype(np.float64))
+        assert np.array_equal(oracle.vector_add(a, b).astype(np.float64), exact)
+
+
+def test_ep_class_s_matches_npb_verification():
+    r = oracle.ep_job(24, 0, 256)
+    sxv, syv = oracle.NPB_VERIFY[24]
+    assert abs((r.sx - sxv) / sxv) < 1e-8
+    assert abs((r.sy - syv) / syv) < 1e-8
+    assert r.pairs == 13176389 == sum(r.q)
+
+
+def test_ep_fixtures_consistent_with_npb_and_oracle():
+    fx = json.load(open(os.path.join(GOLD, "ep_oracle.json")))
+    for m in ("24", "25", "28"):
+        e = fx[m]
+        assert abs((e["sx"] - e["npb_sx"]) / e["npb_sx"]) < 1e-8
+        assert abs((e["sy"] - e["npb_sy"]) / e["npb_sy"]) < 1e-8
+        assert sum(e["q"]) == e["pairs"]
+    r = oracle.ep_job(24, 0, 256)
+    assert struct.pack("<d", r.sx).hex() == fx["24"]["sx_bits"]
+    assert struct.pack("<d", r.sy).hex() == fx["24"]["sy_bits"]
+    assert fx["28"]["pairs"] == 210832767
+    # slices of a class fold to the class counts exactly
+    parts = [oracle.ep_job(24, 64 * p, 64) for p in range(4)]
+    f = oracle.ep_fold(parts)
+    assert list(f.q) == list(r.q) and f.pairs == r.pairs
+    assert abs(f.sx - r.sx) <= 1e-9 * abs(r.sx)
+
+
+def test_ep_rejects_bad_parameters():
+    with pytest.raises(ValueError):
+        oracle.ep_job(24, 200, 100)
+
+
+def test_black_scholes_put_call_parity():
+    rng = np.random.default_rng(5347)
+    n = 4096
+    S = rng.uniform(5, 30, n).astype(np.float32)
+    X = rng.uniform(1, 100, n).astype(np.float32)
+    T = rng.uniform(0.25, 10, n).astype(np.float32)
+    call, put = oracle.black_scholes(S, X, T)
+    # C - P = S - X e^{-rT} holds for the SDK's symmetric CND polynomial
+    lhs = call - put
+    rhs = S.astype(np.float64) - X.astype(np.float64) * np.exp(-0.02 * T.astype(np.float64))
+    assert np.max(np.abs(lhs - rhs)) < 1e-6
+    assert np.all(call >= -1e-9) and np.all(put >= -1e-9)
+
+
+def test_sgemm_oracle_exact_on_small_integers():
+    rng = np.random.default_rng(3)
+    A = rng.integers(-4, 5, (17, 17)).astype(np.float32)
+    B = rng.integers(-4, 5, (17, 17)).astype(np.float32)
+    assert np.array_equal(oracle.sgemm(A, B), A.astype(np.float64) @ B.astype(np.float64))
