@@ -243,7 +243,7 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist):
+                sizes, dist, cold=False):
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
     inst = f"b200bench{os.getpid()}g{dist.local}"
@@ -266,6 +266,8 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         a = [spmd, "--worker", str(gid0 + i), "--workers", str(total_workers), "--workload",
              workload, "--rounds", str(warmup + steps)] + size_args
         a += ["--native", "--device", str(device)] if native else ["--instance", inst]
+        if cold:
+            a.append("--connect-after-go")
         args.append(a)
     try:
         ps = spawn_workers(args, env)
@@ -293,6 +295,17 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         info["tasks"] = tasks
     if native:
         info["cold_ms"] = max((r["t1"][0] - r["t_go"]) * 1e-6 for r in res)
+    # SPMD turnaround of the first task: simultaneous start -> last first-result
+    info["turnaround_ms"] = (max(r["t1"][0] for r in res) - min(r["t_go"] for r in res)) * 1e-6
+    if not native:
+        med = lambda xs: statistics.median(xs) if xs else None
+        info["client_stage_us"] = {k: med([r["stage_ns"][k] * 1e-3 for r in res])
+                                   for k in ("snd", "str", "stp", "rcv")}
+        timed = info["tasks"][-procs * steps:] if info.get("tasks") else []
+        info["device_stage_us"] = {k: med([t[k] for t in timed])
+                                   for k in ("h2d_us", "comp_us", "d2h_us")}
+        info["device_stage_us"]["queue_wait_us"] = med([t["queue_wait_us"] for t in timed])
+        info["device_stage_us"]["pure_gpu_us"] = med([t["pure_gpu_us"] for t in timed])
     return info
 
 
@@ -445,6 +458,21 @@ def main():
                   "cold_turnaround_ms": dist.max(nat["cold_ms"]),
                   "desc": "NativeVgpu: one CUDA context per process, pageable cudaMemcpy, "
                           "time-sliced by the driver, no MPS"}
+    # ---- paper turnaround: P processes start together, each runs one task;
+    # native pays its context creation, the GVM's context already exists ----
+    turnaround = None
+    if not args.no_native:
+        dist.barrier()
+        tv = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, False,
+                         sizes, dist, cold=True)
+        tn = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, True,
+                         sizes, dist, cold=True)
+        v_ms, n_ms = dist.max(tv["turnaround_ms"]), dist.max(tn["turnaround_ms"])
+        turnaround = {"virtualized_ms": v_ms, "native_ms": n_ms, "speedup": n_ms / v_ms,
+                      "procs_per_gpu": procs,
+                      "desc": "paper Figs. 13-22 turnaround: simultaneous start -> last process "
+                              "has its result; virtualized includes REQ, native includes its "
+                              "own CUDA context creation"}
     clock_info = clocks.stop() if clocks else None
 
     # ---- final reduction (multi-GPU only) ----------------------------------------------
@@ -489,7 +517,10 @@ def main():
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": secs * 1e3 / args.steps,
                     "path": "bin/vgpu-spmd x P -> VgpuHandle::run_task -> UDS+shm -> GVM "
-                            "(libvgpu.so) -> per-client CUDA streams"},
+                            "(libvgpu.so) -> per-client CUDA streams",
+                    "client_stage_us": e2e.get("client_stage_us"),
+                    "device_stage_us": e2e.get("device_stage_us")},
+            "turnaround": turnaround,
             "native": native,
             "vs_native": (e2e_value / native["value"]) if native else None,
             "roofline": roof,

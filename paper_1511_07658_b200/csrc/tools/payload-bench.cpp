@@ -11,11 +11,17 @@
 #include "workloads.hpp"
 
 int main(int argc, char** argv) {
+    // payload-bench [device] [kind|all] [tasks|0=1,4,16] [steps]
     int device = argc > 1 ? std::atoi(argv[1]) : 0;
+    const std::string only = argc > 2 ? argv[2] : "all";
+    const std::uint32_t only_tasks = argc > 3 ? std::atoi(argv[3]) : 0;
+    const std::uint32_t steps = argc > 4 ? std::atoi(argv[4]) : 20;
     const char* kinds[] = {"vecadd", "ep", "bs", "mm"};
     const std::uint32_t kernels[] = {VGPU_CU_K_VADD, VGPU_CU_K_EP, VGPU_CU_K_BS, VGPU_CU_K_SGEMM};
     for (int k = 0; k < 4; ++k) {
+        if (only != "all" && only != kinds[k]) continue;
         for (std::uint32_t tasks : {1u, 4u, 16u}) {
+            if (only_tasks && tasks != only_tasks) continue;
             std::vector<vgpu::wl::Job> jobs;
             std::vector<const void*> ptrs;
             std::vector<std::uint64_t> sizes;
@@ -31,7 +37,7 @@ int main(int argc, char** argv) {
                 static_cast<std::uint32_t>(std::min<std::uint64_t>(16, 1 + (512ull << 20) / (set_bytes + 1)));
             vgpu_cu_resident_result r{};
             const int rc = vgpu_cu_resident_bench(device, kernels[k], 2.0f, tasks, ptrs.data(),
-                                                  sizes.data(), sets, 3, 20, &r);
+                                                  sizes.data(), sets, 3, steps, &r);
             if (rc) {
                 std::printf("%-7s tasks=%2u  error %s: %s\n", kinds[k], tasks, vgpu_cu_strerror(rc),
                             vgpu_cu_last_error());

@@ -13,6 +13,7 @@
 #include <malloc.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -49,7 +50,7 @@ bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out) {
 int main(int argc, char** argv) {
     std::string instance, workload = "vecadd";
     std::uint32_t worker = 0, workers = 1, rounds = 1;
-    bool native = false;
+    bool native = false, connect_after_go = false;
     int device = 0;
     vgpu::wl::Sizes sizes;
     for (int i = 1; i < argc; ++i) {
@@ -65,6 +66,7 @@ int main(int argc, char** argv) {
             else if (a == "--workload") workload = val();
             else if (a == "--rounds") rounds = std::stoul(val());
             else if (a == "--native") native = true;
+            else if (a == "--connect-after-go") connect_after_go = true;
             else if (a == "--device") device = std::stoi(val());
             else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(val());
             else if (a == "--ep-m") sizes.ep_m = std::stoul(val());
@@ -85,40 +87,61 @@ int main(int argc, char** argv) {
     std::unique_ptr<vgpu::VgpuHandle> vh;
     std::unique_ptr<vgpu::NativeVgpu> nh;
     std::string err;
-    try {
-        if (native) {
-            vgpu::NativeConfig nc;
-            nc.cuda_device = device;
-            nh = std::make_unique<vgpu::NativeVgpu>(nc);
-        } else {
-            for (int attempt = 0;; ++attempt) {
-                try {
-                    vh = std::make_unique<vgpu::VgpuHandle>(vgpu::req(instance));
-                    break;
-                } catch (const vgpu::TransportError&) {
-                    if (attempt > 4000) throw;
-                    std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    auto connect = [&]() -> bool {
+        try {
+            if (native) {
+                vgpu::NativeConfig nc;
+                nc.cuda_device = device;
+                nh = std::make_unique<vgpu::NativeVgpu>(nc);  // context created at first task
+            } else {
+                for (int attempt = 0;; ++attempt) {
+                    try {
+                        vh = std::make_unique<vgpu::VgpuHandle>(vgpu::req(instance));
+                        break;
+                    } catch (const vgpu::TransportError&) {
+                        if (attempt > 4000) throw;
+                        std::this_thread::sleep_for(std::chrono::milliseconds(5));
+                    }
                 }
             }
+            return true;
+        } catch (const std::exception& e) {
+            std::printf("{\"worker\": %u, \"ok\": false, \"err\": \"connect: %s\"}\n", worker,
+                        e.what());
+            return false;
         }
-    } catch (const std::exception& e) {
-        std::printf("{\"worker\": %u, \"ok\": false, \"err\": \"connect: %s\"}\n", worker, e.what());
-        return 3;
-    }
+    };
+    if (!connect_after_go && !connect()) return 3;
     std::printf("READY %d\n", static_cast<int>(getpid()));
     std::fflush(stdout);
     char go = 0;
     if (read(0, &go, 1) != 1) return 4;
 
     std::vector<std::int64_t> t0(rounds), t1(rounds);
+    std::vector<std::int64_t> st_snd(rounds), st_str(rounds), st_stp(rounds), st_rcv(rounds);
     std::uint64_t first_sum = 0;
     bool ok = true;
     const std::int64_t t_go = now_ns();
+    if (connect_after_go && !connect()) return 3;
     try {
         for (std::uint32_t r = 0; r < rounds; ++r) {
             t0[r] = now_ns();
-            const vgpu::Bytes out = native ? nh->run_task(job.input, job.desc)
-                                           : vh->run_task(job.input, job.desc);
+            vgpu::Bytes out;
+            if (native) {
+                out = nh->run_task(job.input, job.desc);
+            } else {  // run_task, verb by verb so each stage is timed
+                vh->snd(job.input);
+                const std::int64_t a = now_ns();
+                vh->str(job.desc);
+                const std::int64_t b = now_ns();
+                vh->stp_wait();
+                const std::int64_t c = now_ns();
+                out = vh->rcv();
+                st_snd[r] = a - t0[r];
+                st_str[r] = b - a;
+                st_stp[r] = c - b;
+                st_rcv[r] = now_ns() - c;
+            }
             t1[r] = now_ns();
             if (out.size() != job.output_bytes) {
                 ok = false;
@@ -153,7 +176,15 @@ int main(int argc, char** argv) {
     for (std::uint32_t r = 0; r < rounds; ++r) os << (r ? ", " : "") << t0[r];
     os << "], \"t1\": [";
     for (std::uint32_t r = 0; r < rounds; ++r) os << (r ? ", " : "") << t1[r];
-    os << "], \"err\": \"" << err << "\"}";
+    os << "], \"stage_ns\": {";
+    const char* names[] = {"snd", "str", "stp", "rcv"};
+    std::vector<std::int64_t>* stages[] = {&st_snd, &st_str, &st_stp, &st_rcv};
+    for (int k = 0; k < 4; ++k) {
+        std::vector<std::int64_t> v = *stages[k];
+        std::sort(v.begin(), v.end());
+        os << (k ? ", " : "") << "\"" << names[k] << "\": " << (v.empty() ? 0 : v[v.size() / 2]);
+    }
+    os << "}, \"err\": \"" << err << "\"}";
     std::printf("%s\n", os.str().c_str());
     std::fflush(stdout);
     return ok ? 0 : 5;

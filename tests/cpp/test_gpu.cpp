@@ -194,7 +194,7 @@ TEST_CASE("[gpu] two-client flow with the real kernels (virtual clock)") {
     const auto m = d->metrics();
     CHECK(m.batches_flushed == 1);
     CHECK(m.kernel_launches == 1);  // one batched launch for both clients
-    CHECK(m.batches.at(0).model_makespan_us == 210);
+    CHECK(m.batches.at(0).model_makespan_us == 130);  // PS-1 form at N = 2: 2(20+20)+50
 }
 
 TEST_CASE("[gpu] GVM parity for every payload, PS-1 and PS-2, both data planes") {
