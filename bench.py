@@ -243,7 +243,7 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist, cold=False):
+                sizes, dist, cold=False, barrier=0):
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
     inst = f"b200bench{os.getpid()}g{dist.local}"
@@ -254,7 +254,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
     gvm = None
     if not native:
         V.unlink_os_instance(inst, procs)
-        cfg = V.GvmConfig(instance=inst, max_clients=procs, barrier_size=procs,
+        cfg = V.GvmConfig(instance=inst, max_clients=procs, barrier_size=barrier or procs,
                           per_client_shm_bytes=W.region_bytes(workload, sizes),
                           barrier_window=2000, clock=V.ClockMode.Real, cuda_device=device,
                           device_sms=148, device_max_kernels=128, device_slots_per_sm=32)
@@ -309,27 +309,47 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
     return info
 
 
+def _ref_run(ref, workload, procs, rounds, warmup, size_args):
+    run = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds",
+                          str(rounds), "--warmup", str(warmup)] + size_args,
+                         capture_output=True, text=True, timeout=3600)
+    lines = [l for l in run.stdout.strip().splitlines() if l.startswith("{")]
+    if not lines:
+        raise RuntimeError(f"ref-bench failed: {run.stderr[-500:]}")
+    r = json.loads(lines[-1])
+    if not r.get("ok"):
+        raise RuntimeError(f"ref-bench workers failed: {r}")
+    return r
+
+
 def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
-    """The unmodified reference GVM (oracle/_ref/ref-bench) on host cores."""
+    """The unmodified reference GVM (oracle/_ref/ref-bench) on host cores.
+
+    The reference GVM runs every payload sequentially on its dispatcher
+    thread and its client gives up after a 30 s reply timeout
+    (proj/src/client.cpp:17), so the sample shrinks the process count when a
+    full round would not fit; jobs/s is the rate it sustains."""
     ref = os.path.join(REPO, "oracle", "_ref", "ref-bench")
     size_args = ["--vecadd-n", str(sizes.vecadd_n), "--ep-m", str(sizes.ep_m),
                  "--bs-n", str(sizes.bs_n), "--mm-n", str(sizes.mm_n)]
     if not os.path.exists(ref):
         return None
-    # probe one round to size a bounded sample (~budget_s of CPU work)
-    probe = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds", "1",
-                            "--warmup", "0"] + size_args, capture_output=True, text=True,
-                           timeout=1800)
-    one = json.loads(probe.stdout.strip().splitlines()[-1])
-    per_round = max(1e-3, one["seconds"])
-    rounds = max(1, min(200, int(budget_s / per_round)))
-    run = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds",
-                          str(rounds), "--warmup", str(warmup if per_round < budget_s / 4 else 0)]
-                         + size_args, capture_output=True, text=True, timeout=3600)
-    r = json.loads(run.stdout.strip().splitlines()[-1])
+    try:
+        one = _ref_run(ref, workload, 1, 1, 0, size_args)  # probe: one job
+        per_job = max(1e-4, one["seconds"])
+        n = max(1, min(procs, int(20.0 / per_job)))
+        per_round = per_job * n
+        rounds = max(1, min(200, int(budget_s / per_round)))
+        w = warmup if per_round * (rounds + warmup) < 2 * budget_s else 0
+        r = _ref_run(ref, workload, n, rounds, w, size_args)
+    except Exception as e:  # noqa: BLE001 - reported, not fatal for our arm
+        log("reference arm failed:", e)
+        return None
     r["sample"] = (f"reference GVM (oracle/_ref/ref-bench, unmodified libvgpu from /root/reference) "
-                   f"{procs} forked VgpuHandle clients x {rounds} rounds of '{workload}', "
-                   f"virtual clock, OpenMP on all host threads")
+                   f"{n} forked VgpuHandle clients x {rounds} rounds of '{workload}', "
+                   f"virtual clock, OpenMP on all host threads"
+                   + ("" if n == procs else f" (reduced from {procs} processes: one reference "
+                      f"round must fit its 30 s client reply timeout)"))
     return r
 
 
@@ -364,6 +384,21 @@ def final_reduce(V, N, dist, record):
         libs.cuda.vgpu_cu_close(dev)
 
 
+def model_summary(batches):
+    """Paper model (simulate() on the declared triples) vs CUDA-event batch
+    makespans, §6 model validation."""
+    if not batches:
+        return None
+    big = [b for b in batches if b["task_count"] == max(x["task_count"] for x in batches)]
+    mod = statistics.median([b["model_makespan_us"] for b in big])
+    mea = statistics.median([b["measured_makespan_us"] for b in big])
+    return {"batches": len(batches), "tasks_per_batch": big[0]["task_count"],
+            "style": "PS2" if big[-1]["style"] else "PS1",
+            "model_makespan_us_median": mod, "measured_makespan_us_median": mea,
+            "note": "model uses the clients' declared stage estimates (Fermi-style single "
+                    "queue); measured is the B200 batch span from CUDA events"}
+
+
 # ---- main -----------------------------------------------------------------------------
 
 def main():
@@ -377,6 +412,8 @@ def main():
     ap.add_argument("--no-native", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--barrier-size", type=int, default=-1,
+                    help="GVM barrier (tasks per flush); -1 = workload default")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -389,6 +426,7 @@ def main():
     sizes = W.Sizes()
     world = dist.world
     config = {"workload": W.CONFIG_NAME[args.workload], "procs_per_gpu": procs,
+              "barrier_size": procs if args.barrier_size < 0 else args.barrier_size,
               "gpus": world, "global_procs": procs * world, "parallelism": f"gvm-per-gpu x{world}",
               "l2": "value: rotating input sets > 2x L2 between steps; e2e: inputs re-sent from "
                     "host memory every step"}
@@ -438,8 +476,19 @@ def main():
 
     # ---- e2e: virtualized through the GVM ----------------------------------------------
     dist.barrier()
+    # B200 policy: eager dispatch (barrier 1) — per-client hardware queues make
+    # the paper's full barrier pure latency; the barrier-P run is reported too
+    barrier = 1 if args.barrier_size < 0 else args.barrier_size
     e2e = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                      args.warmup, device, False, sizes, dist)
+                      args.warmup, device, False, sizes, dist, barrier=barrier)
+    paper = None
+    if args.barrier_size < 0 and procs > 1:
+        dist.barrier()
+        pb = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                         args.warmup, device, False, sizes, dist, barrier=procs)
+        paper = {"value": procs * world * args.steps / dist.max(pb["seconds"]), "unit": "jobs/s",
+                 "barrier_size": procs, "client_stage_us": pb.get("client_stage_us"),
+                 "device_stage_us": pb.get("device_stage_us"), "batches": pb["batches"]}
     secs = dist.max(e2e["seconds"])
     e2e_value = procs * world * args.steps / secs
     kinds = [W.kind_of(args.workload, gid0 + i) for i in range(procs)]
@@ -450,11 +499,13 @@ def main():
     # ---- native baseline --------------------------------------------------------------
     native = None
     if not args.no_native:
-        dist.barrier()
-        nat = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                          args.warmup, device, True, sizes, dist)
-        nsecs = dist.max(nat["seconds"])
-        native = {"value": procs * world * args.steps / nsecs, "unit": "jobs/s",
+        runs = []
+        for _ in range(2):  # best of two: conservative toward the baseline
+            dist.barrier()
+            nat = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                              args.warmup, device, True, sizes, dist)
+            runs.append(procs * world * args.steps / dist.max(nat["seconds"]))
+        native = {"value": max(runs), "runs": runs, "unit": "jobs/s",
                   "cold_turnaround_ms": dist.max(nat["cold_ms"]),
                   "desc": "NativeVgpu: one CUDA context per process, pageable cudaMemcpy, "
                           "time-sliced by the driver, no MPS"}
@@ -464,7 +515,7 @@ def main():
     if not args.no_native:
         dist.barrier()
         tv = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, False,
-                         sizes, dist, cold=True)
+                         sizes, dist, cold=True, barrier=barrier)
         tn = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, True,
                          sizes, dist, cold=True)
         v_ms, n_ms = dist.max(tv["turnaround_ms"]), dist.max(tn["turnaround_ms"])
@@ -521,6 +572,8 @@ def main():
                     "client_stage_us": e2e.get("client_stage_us"),
                     "device_stage_us": e2e.get("device_stage_us")},
             "turnaround": turnaround,
+            "e2e_paper_barrier": ({k: v for k, v in paper.items() if k != "batches"}
+                                  if paper else None),
             "native": native,
             "vs_native": (e2e_value / native["value"]) if native else None,
             "roofline": roof,
@@ -528,12 +581,7 @@ def main():
             "gpu_launches": launches_value + launches_e2e,
             "clocks": clock_info,
             "final_reduce": reduce_info,
-            "model": {"batches": len(e2e["batches"]),
-                      "model_makespan_us_median": statistics.median(
-                          [b["model_makespan_us"] for b in e2e["batches"]]) if e2e["batches"] else None,
-                      "measured_makespan_us_median": statistics.median(
-                          [b["measured_makespan_us"] for b in e2e["batches"]]) if e2e["batches"] else None,
-                      "style": "PS2" if e2e["batches"] and e2e["batches"][-1]["style"] else "PS1"},
+            "model": model_summary(paper["batches"] if paper else e2e["batches"]),
         }
         print(json.dumps(line), flush=True)
     dist.close()

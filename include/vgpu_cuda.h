@@ -76,17 +76,23 @@ typedef struct vgpu_ep_result {
 #define VGPU_BS_VOLATILITY 0.30f
 
 /* ---- one task of a dispatch batch --------------------------------------- */
+/* task flag: the input already sits in the slot's HBM buffer (uploaded at
+ * SND time with vgpu_cu_upload); the task skips its H2D stage */
+#define VGPU_CU_TASK_INPUT_RESIDENT 1u
+
 typedef struct vgpu_cu_task {
     uint32_t slot;       /* client slot 1..max_clients: stream + HBM buffers */
     uint32_t kernel;     /* vgpu_cu_kernel                                    */
     float param;         /* vector-scale factor                               */
-    uint32_t flags;      /* 0                                                 */
+    uint32_t flags;      /* VGPU_CU_TASK_*                                    */
     const void* h_in;    /* host source (registered region / pinned staging)  */
     uint64_t in_bytes;
     void* h_out;         /* host destination of the result                    */
     uint64_t out_bytes;  /* vgpu_cu_output_size()                             */
     uint64_t tag;        /* echoed in vgpu_cu_done                            */
 } vgpu_cu_task;
+
+enum vgpu_cu_done_kind { VGPU_CU_DONE_TASK = 0, VGPU_CU_DONE_UPLOAD = 1 };
 
 typedef struct vgpu_cu_done {
     uint64_t tag;
@@ -100,6 +106,8 @@ typedef struct vgpu_cu_done {
     float batch_span_us;   /* set on the batch's last completion: first H2D
                               start -> last D2H end over the batch; else 0   */
     uint32_t batch_done;   /* 1 on the batch's last completion               */
+    uint32_t kind;         /* vgpu_cu_done_kind                              */
+    uint32_t reserved;
 } vgpu_cu_done;
 
 typedef struct vgpu_cu_stats {
@@ -132,6 +140,12 @@ int vgpu_cu_payload(const char* id, uint32_t* kernel);
  * PayloadError::MalformedInput). `in` may be NULL except for EP. */
 int vgpu_cu_output_size(uint32_t kernel, const void* in, uint64_t in_bytes,
                         uint64_t* out_bytes);
+
+/* Eager upload (SND time): H2D of `bytes` from h_in into the slot's input
+ * buffer on the slot's stream; poll() reports it as VGPU_CU_DONE_UPLOAD with
+ * `tag`. Once reported, the bytes are captured in HBM (SND snapshot). */
+int vgpu_cu_upload(vgpu_cu_dev* dev, uint32_t slot, const void* h_in, uint64_t bytes,
+                   uint64_t tag);
 
 /* Enqueue a batch. style 0 = PS-1 (all H2D, then compute — one launch per
  * kernel kind over the whole batch's task table — then all D2H), 1 = PS-2

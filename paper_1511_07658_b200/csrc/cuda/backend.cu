@@ -322,21 +322,29 @@ NcclApi& nccl() {
 
 enum { kEvH2d0, kEvH2d1, kEvC0, kEvC1, kEvD2h0, kEvD2h1, kEvCount };
 
-struct SlotState {
+// One stream operation in flight: a task (H2D -> kernel -> D2H) or an eager
+// upload (H2D at SND time). The host callback that closes it hands the
+// record to poll() through the device's finished list.
+struct Op {
     vgpu_cu_dev* dev = nullptr;
+    std::uint32_t slot = 0;
+    std::uint32_t kind = VGPU_CU_DONE_TASK;
+    std::uint64_t tag = 0;
+    std::uint64_t batch = 0;
+    cudaEvent_t ev[kEvCount] = {};
+    bool has_h2d = false, has_comp = false;
+    cudaEvent_t comp0 = nullptr, comp1 = nullptr;
+};
+
+struct SlotState {
     std::uint32_t index = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[kEvCount] = {};
     std::uint8_t* d_in = nullptr;
     std::uint8_t* d_out = nullptr;
     std::uint8_t* d_scratch = nullptr;
     void* reg_base = nullptr;
-    // in flight
-    bool busy = false;
-    std::uint64_t tag = 0;
-    std::uint64_t batch = 0;
-    bool has_h2d = false, has_comp = false;
-    cudaEvent_t comp0 = nullptr, comp1 = nullptr;
+    bool task_busy = false;
+    std::uint32_t ops_in_flight = 0;
 };
 
 struct BatchRec {
@@ -360,7 +368,7 @@ struct vgpu_cu_dev {
 
     std::mutex cb_mu;
     std::condition_variable cb_cv;
-    std::vector<std::uint32_t> finished;
+    std::vector<Op*> finished;
     std::mutex notify_mu;
     void (*notify_fn)(void*, std::uint32_t) = nullptr;
     void* notify_ctx = nullptr;
@@ -379,16 +387,40 @@ struct vgpu_cu_dev {
         CK(cudaEventCreate(out));
         return VGPU_CU_OK;
     }
+
+    int new_op(std::uint32_t slot, std::uint32_t kind, std::uint64_t tag, Op** out) {
+        auto* op = new Op();
+        op->dev = this;
+        op->slot = slot;
+        op->kind = kind;
+        op->tag = tag;
+        for (auto& e : op->ev) {
+            const int rc = pool_get(&e);
+            if (rc) {
+                release_op(op);
+                return rc;
+            }
+        }
+        *out = op;
+        return VGPU_CU_OK;
+    }
+
+    void release_op(Op* op) {
+        for (auto& e : op->ev)
+            if (e) event_pool.push_back(e);
+        delete op;
+    }
 };
 
 namespace {
 
-void CUDART_CB slot_done(void* p) {
-    auto* s = static_cast<SlotState*>(p);
-    vgpu_cu_dev* d = s->dev;
+void CUDART_CB op_done(void* p) {
+    auto* op = static_cast<Op*>(p);
+    vgpu_cu_dev* d = op->dev;
+    const std::uint32_t slot = op->slot;
     {
         std::lock_guard lk(d->cb_mu);
-        d->finished.push_back(s->index);
+        d->finished.push_back(op);
     }
     d->cb_cv.notify_all();
     void (*fn)(void*, std::uint32_t) = nullptr;
@@ -398,7 +430,7 @@ void CUDART_CB slot_done(void* p) {
         fn = d->notify_fn;
         ctx = d->notify_ctx;
     }
-    if (fn) fn(ctx, s->index);
+    if (fn) fn(ctx, slot);
 }
 
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -559,7 +591,6 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemset(arena)"));
     for (std::uint32_t i = 1; i <= max_clients; ++i) {
         SlotState& s = d->slots[i];
-        s.dev = d;
         s.index = i;
         std::uint8_t* base = d->arena + per_slot * (i - 1);
         s.d_in = base;
@@ -567,13 +598,16 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
         s.d_scratch = base + 2 * buf;
         e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
         if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
-        for (auto& ev : s.ev) {
-            e = cudaEventCreate(&ev);
-            if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
-        }
     }
     e = cudaStreamCreateWithFlags(&d->anchor_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(anchor)"));
+    // warm the event pool: 6 events per slot for two ops in flight + batch events
+    for (std::uint32_t i = 0; i < 16 * max_clients + 16; ++i) {
+        cudaEvent_t ev;
+        e = cudaEventCreate(&ev);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
+        d->event_pool.push_back(ev);
+    }
     *out = d;
     return VGPU_CU_OK;
 }
@@ -584,10 +618,13 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
     for (auto& s : d->slots)
         if (s.stream) cudaStreamSynchronize(s.stream);
     if (d->anchor_stream) cudaStreamSynchronize(d->anchor_stream);
+    {
+        std::lock_guard lk(d->cb_mu);
+        for (Op* op : d->finished) d->release_op(op);
+        d->finished.clear();
+    }
     for (auto& s : d->slots) {
         if (s.reg_base) cudaHostUnregister(s.reg_base);
-        for (auto& ev : s.ev)
-            if (ev) cudaEventDestroy(ev);
         if (s.stream) cudaStreamDestroy(s.stream);
     }
     for (auto& [id, b] : d->batches) {
@@ -650,6 +687,39 @@ int vgpu_cu_get_stats(vgpu_cu_dev* d, vgpu_cu_stats* out) {
     return VGPU_CU_OK;
 }
 
+int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::uint64_t bytes,
+                   std::uint64_t tag) {
+    if (!d || slot < 1 || slot > d->max_clients || (!h_in && bytes)) return VGPU_CU_EINVAL;
+    if (bytes > d->slot_bytes) {
+        set_err("upload of %llu B exceeds the slot (%llu B)", (unsigned long long)bytes,
+                (unsigned long long)d->slot_bytes);
+        return VGPU_CU_ESIZE;
+    }
+    if (d->slots[slot].task_busy) {
+        set_err("slot %u has a task in flight", slot);
+        return VGPU_CU_EINVAL;
+    }
+    CK(cudaSetDevice(d->device));
+    SlotState& s = d->slots[slot];
+    Op* op = nullptr;
+    int rc = d->new_op(slot, VGPU_CU_DONE_UPLOAD, tag, &op);
+    if (rc) return rc;
+    op->has_h2d = bytes > 0;
+    cudaError_t e = cudaEventRecord(op->ev[kEvH2d0], s.stream);
+    if (e == cudaSuccess && bytes)
+        e = cudaMemcpyAsync(s.d_in, h_in, bytes, cudaMemcpyHostToDevice, s.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+    if (e == cudaSuccess) e = cudaLaunchHostFunc(s.stream, op_done, op);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(s.stream);
+        d->release_op(op);
+        return cuda_fail(e, "vgpu_cu_upload");
+    }
+    ++s.ops_in_flight;
+    d->h2d_bytes += bytes;
+    return VGPU_CU_OK;
+}
+
 int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, std::uint32_t n,
                          std::uint64_t* batch_id) {
     if (!d || (!tasks && n)) return VGPU_CU_EINVAL;
@@ -662,7 +732,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             set_err("task %u: slot %u out of range", i, t.slot);
             return VGPU_CU_EINVAL;
         }
-        if (d->slots[t.slot].busy) {
+        if (d->slots[t.slot].task_busy) {
             set_err("task %u: slot %u already has a task in flight", i, t.slot);
             return VGPU_CU_EINVAL;
         }
@@ -700,61 +770,80 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
     const std::uint64_t bid = d->next_batch++;
     BatchRec rec;
     rec.remaining = n;
+    std::vector<Op*> ops(n, nullptr);
     int rc = d->pool_get(&rec.anchor);
-    if (rc) return rc;
-    CK(cudaEventRecord(rec.anchor, d->anchor_stream));
+    for (std::uint32_t i = 0; i < n && rc == VGPU_CU_OK; ++i)
+        rc = d->new_op(tasks[i].slot, VGPU_CU_DONE_TASK, tasks[i].tag, &ops[i]);
+    auto drop_ops = [&] {
+        for (Op* op : ops)
+            if (op) d->release_op(op);
+        if (rec.anchor) d->event_pool.push_back(rec.anchor);
+        for (auto ev : rec.pooled) d->event_pool.push_back(ev);
+    };
+    if (rc) {
+        drop_ops();
+        return rc;
+    }
+    for (std::uint32_t i = 0; i < n; ++i) ops[i]->batch = bid;
+    cudaError_t e = cudaEventRecord(rec.anchor, d->anchor_stream);
 
     auto h2d = [&](std::uint32_t i) -> cudaError_t {
         const vgpu_cu_task& t = tasks[i];
         SlotState& s = d->slots[t.slot];
-        s.busy = true;
-        s.tag = t.tag;
-        s.batch = bid;
-        s.has_h2d = t.in_bytes > 0;
-        s.has_comp = false;
-        cudaError_t e = cudaEventRecord(s.ev[kEvH2d0], s.stream);
-        if (e == cudaSuccess && t.in_bytes)
-            e = cudaMemcpyAsync(s.d_in, t.h_in, t.in_bytes, cudaMemcpyHostToDevice, s.stream);
-        if (e == cudaSuccess) e = cudaEventRecord(s.ev[kEvH2d1], s.stream);
-        d->h2d_bytes += t.in_bytes;
-        return e;
+        Op* op = ops[i];
+        const bool resident = (t.flags & VGPU_CU_TASK_INPUT_RESIDENT) != 0;
+        op->has_h2d = t.in_bytes > 0 && !resident;
+        cudaError_t err = cudaEventRecord(op->ev[kEvH2d0], s.stream);
+        if (err == cudaSuccess && op->has_h2d)
+            err = cudaMemcpyAsync(s.d_in, t.h_in, t.in_bytes, cudaMemcpyHostToDevice, s.stream);
+        if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+        if (op->has_h2d) d->h2d_bytes += t.in_bytes;
+        return err;
     };
     auto d2h = [&](std::uint32_t i) -> cudaError_t {
         const vgpu_cu_task& t = tasks[i];
         SlotState& s = d->slots[t.slot];
+        Op* op = ops[i];
         const std::uint64_t bytes = jobs[i].out_bytes;
         const std::uint8_t* src = t.kernel == VGPU_CU_K_IDENTITY ? s.d_in : s.d_out;
-        cudaError_t e = cudaEventRecord(s.ev[kEvD2h0], s.stream);
-        if (e == cudaSuccess && bytes)
-            e = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
-        if (e == cudaSuccess) e = cudaEventRecord(s.ev[kEvD2h1], s.stream);
-        if (e == cudaSuccess) e = cudaLaunchHostFunc(s.stream, slot_done, &s);
+        cudaError_t err = cudaEventRecord(op->ev[kEvD2h0], s.stream);
+        if (err == cudaSuccess && bytes)
+            err = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
+        if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvD2h1], s.stream);
+        if (err == cudaSuccess) err = cudaLaunchHostFunc(s.stream, op_done, op);
+        if (err == cudaSuccess) {
+            ops[i] = nullptr;  // owned by the callback now
+            ++s.ops_in_flight;
+            s.task_busy = true;
+        }
         d->d2h_bytes += bytes;
-        return e;
+        return err;
     };
     auto compute_own = [&](std::uint32_t i) -> cudaError_t {
         const vgpu_cu_task& t = tasks[i];
         SlotState& s = d->slots[t.slot];
+        Op* op = ops[i];
         if (t.kernel == VGPU_CU_K_IDENTITY) return cudaSuccess;  // D2H reads d_in
-        s.has_comp = true;
-        s.comp0 = s.ev[kEvC0];
-        s.comp1 = s.ev[kEvC1];
+        op->has_comp = true;
+        op->comp0 = op->ev[kEvC0];
+        op->comp1 = op->ev[kEvC1];
         std::uint64_t l = 0;
-        cudaError_t e = cudaEventRecord(s.comp0, s.stream);
-        if (e == cudaSuccess) e = launch_jobs(t.kernel, &jobs[i], 1, s.stream, &l);
-        if (e == cudaSuccess) e = cudaEventRecord(s.comp1, s.stream);
+        cudaError_t err = cudaEventRecord(op->comp0, s.stream);
+        if (err == cudaSuccess) err = launch_jobs(t.kernel, &jobs[i], 1, s.stream, &l);
+        if (err == cudaSuccess) err = cudaEventRecord(op->comp1, s.stream);
         d->launches += l;
-        return e;
+        return err;
     };
 
-    cudaError_t e = cudaSuccess;
-    if (style == 1) {  // PS-2: per-stream triples
+    std::vector<std::uint32_t> enqueued;  // tasks whose callback is armed
+    if (e == cudaSuccess && style == 1) {  // PS-2: per-stream triples
         for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) {
             e = h2d(i);
             if (e == cudaSuccess) e = compute_own(i);
             if (e == cudaSuccess) e = d2h(i);
+            if (e == cudaSuccess) enqueued.push_back(i);
         }
-    } else {  // PS-1: all sends, one launch per kernel kind, all retrieves
+    } else if (e == cudaSuccess) {  // PS-1: all sends, one launch per kernel kind, all retrieves
         for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) e = h2d(i);
         for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT && e == cudaSuccess; ++k) {
             std::vector<std::uint32_t> group;
@@ -767,11 +856,14 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             }
             SlotState& lead = d->slots[tasks[group[0]].slot];
             cudaEvent_t g0 = nullptr, g1 = nullptr;
-            if ((rc = d->pool_get(&g0)) || (rc = d->pool_get(&g1))) return rc;
+            if ((rc = d->pool_get(&g0)) || (rc = d->pool_get(&g1))) {
+                e = cudaErrorMemoryAllocation;
+                break;
+            }
             rec.pooled.push_back(g0);
             rec.pooled.push_back(g1);
             for (std::size_t g = 1; g < group.size() && e == cudaSuccess; ++g)
-                e = cudaStreamWaitEvent(lead.stream, d->slots[tasks[group[g]].slot].ev[kEvH2d1], 0);
+                e = cudaStreamWaitEvent(lead.stream, ops[group[g]]->ev[kEvH2d1], 0);
             std::vector<DevJob> gj;
             for (auto i : group) gj.push_back(jobs[i]);
             std::uint64_t l = 0;
@@ -782,33 +874,27 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             d->launches += l;
             for (auto i : group) {
                 SlotState& s = d->slots[tasks[i].slot];
-                s.has_comp = true;
-                s.comp0 = g0;
-                s.comp1 = g1;
+                ops[i]->has_comp = true;
+                ops[i]->comp0 = g0;
+                ops[i]->comp1 = g1;
                 if (e == cudaSuccess && &s != &lead) e = cudaStreamWaitEvent(s.stream, g1, 0);
             }
         }
-        for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) e = d2h(i);
+        for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) {
+            e = d2h(i);
+            if (e == cudaSuccess) enqueued.push_back(i);
+        }
     }
     if (e != cudaSuccess) {
-        // drain whatever got enqueued, forget the batch
-        for (std::uint32_t i = 0; i < n; ++i) {
-            SlotState& s = d->slots[tasks[i].slot];
-            cudaStreamSynchronize(s.stream);
-            s.busy = false;
+        // drain whatever got enqueued; armed callbacks still report, the
+        // daemon fails the batch on the error return and ignores them
+        for (std::uint32_t i = 0; i < n; ++i) cudaStreamSynchronize(d->slots[tasks[i].slot].stream);
+        rec.remaining = static_cast<std::uint32_t>(enqueued.size());
+        if (rec.remaining) {
+            d->batches.emplace(bid, std::move(rec));
+            rec = BatchRec{};
         }
-        {
-            std::lock_guard lk(d->cb_mu);
-            d->finished.erase(std::remove_if(d->finished.begin(), d->finished.end(),
-                                             [&](std::uint32_t idx) {
-                                                 for (std::uint32_t i = 0; i < n; ++i)
-                                                     if (tasks[i].slot == idx) return true;
-                                                 return false;
-                                             }),
-                              d->finished.end());
-        }
-        d->event_pool.push_back(rec.anchor);
-        for (auto ev : rec.pooled) d->event_pool.push_back(ev);
+        drop_ops();
         return cuda_fail(e, "vgpu_cu_submit_batch");
     }
     d->tasks += n;
@@ -821,7 +907,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
 int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint32_t* n_out) {
     if (!d || !n_out || (!out && cap)) return VGPU_CU_EINVAL;
     *n_out = 0;
-    std::vector<std::uint32_t> ready;
+    std::vector<Op*> ready;
     {
         std::lock_guard lk(d->cb_mu);
         const std::size_t take = std::min<std::size_t>(cap, d->finished.size());
@@ -831,23 +917,30 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
     if (ready.empty()) return VGPU_CU_OK;
     cudaSetDevice(d->device);
     const cudaError_t sticky = cudaPeekAtLastError();
-    for (std::uint32_t idx : ready) {
-        SlotState& s = d->slots[idx];
+    for (Op* op : ready) {
+        SlotState& s = d->slots[op->slot];
         vgpu_cu_done& r = out[(*n_out)++];
         std::memset(&r, 0, sizeof r);
-        r.tag = s.tag;
-        r.batch = s.batch;
-        r.slot = idx;
+        r.tag = op->tag;
+        r.batch = op->batch;
+        r.slot = op->slot;
+        r.kind = op->kind;
         r.status = sticky == cudaSuccess ? VGPU_CU_OK : VGPU_CU_EINTERNAL;
-        r.h2d_us = s.has_h2d ? 1000.0f * elapsed_ms(s.ev[kEvH2d0], s.ev[kEvH2d1]) : 0.0f;
-        r.comp_us = s.has_comp ? 1000.0f * elapsed_ms(s.comp0, s.comp1) : 0.0f;
-        r.d2h_us = 1000.0f * elapsed_ms(s.ev[kEvD2h0], s.ev[kEvD2h1]);
-        r.span_us = 1000.0f * elapsed_ms(s.ev[kEvH2d0], s.ev[kEvD2h1]);
-        auto it = d->batches.find(s.batch);
+        r.h2d_us = op->has_h2d ? 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvH2d1]) : 0.0f;
+        if (s.ops_in_flight) --s.ops_in_flight;
+        if (op->kind == VGPU_CU_DONE_UPLOAD) {
+            r.span_us = r.h2d_us;
+            d->release_op(op);
+            continue;
+        }
+        r.comp_us = op->has_comp ? 1000.0f * elapsed_ms(op->comp0, op->comp1) : 0.0f;
+        r.d2h_us = 1000.0f * elapsed_ms(op->ev[kEvD2h0], op->ev[kEvD2h1]);
+        r.span_us = 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvD2h1]);
+        auto it = d->batches.find(op->batch);
         if (it != d->batches.end()) {
             BatchRec& b = it->second;
-            b.first = std::min(b.first, elapsed_ms(b.anchor, s.ev[kEvH2d0]));
-            b.last = std::max(b.last, elapsed_ms(b.anchor, s.ev[kEvD2h1]));
+            b.first = std::min(b.first, elapsed_ms(b.anchor, op->ev[kEvH2d0]));
+            b.last = std::max(b.last, elapsed_ms(b.anchor, op->ev[kEvD2h1]));
             if (--b.remaining == 0) {
                 r.batch_done = 1;
                 r.batch_span_us = 1000.0f * std::max(0.0f, b.last - b.first);
@@ -856,7 +949,8 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
                 d->batches.erase(it);
             }
         }
-        s.busy = false;
+        s.task_busy = false;
+        d->release_op(op);
     }
     return VGPU_CU_OK;
 }
@@ -1008,29 +1102,23 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
                               cudaMemcpyHostToDevice));
         }
     CK(cudaStreamCreateWithFlags(&guard.s, cudaStreamNonBlocking));
-    guard.evs.resize(2 * steps + 2);
+    guard.evs.resize(2);
     for (auto& e : guard.evs) CK(cudaEventCreate(&e));
     std::uint64_t l = 0;
     for (std::uint32_t w = 0; w < warmup; ++w)
         CK(launch_jobs(kernel, js[w % sets].data(), n_tasks, guard.s, &l));
     CK(cudaStreamSynchronize(guard.s));
+    // K back-to-back steps between ONE event pair: the average launch
+    // duration without per-launch event overhead
     l = 0;
     CK(cudaEventRecord(guard.evs[0], guard.s));
-    for (std::uint32_t t = 0; t < steps; ++t) {
-        CK(cudaEventRecord(guard.evs[2 + 2 * t], guard.s));
+    for (std::uint32_t t = 0; t < steps; ++t)
         CK(launch_jobs(kernel, js[(warmup + t) % sets].data(), n_tasks, guard.s, &l));
-        CK(cudaEventRecord(guard.evs[3 + 2 * t], guard.s));
-    }
     CK(cudaEventRecord(guard.evs[1], guard.s));
     CK(cudaStreamSynchronize(guard.s));
     float total = 0.0f;
     CK(cudaEventElapsedTime(&total, guard.evs[0], guard.evs[1]));
-    double ksum = 0.0;
-    for (std::uint32_t t = 0; t < steps; ++t) {
-        float ms = 0.0f;
-        CK(cudaEventElapsedTime(&ms, guard.evs[2 + 2 * t], guard.evs[3 + 2 * t]));
-        ksum += ms;
-    }
+    const double ksum = total;
     res->ms_total = total;
     res->ms_per_step = total / steps;
     res->launches_per_step = static_cast<std::uint32_t>(l / steps);

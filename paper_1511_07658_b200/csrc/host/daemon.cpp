@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <ostream>
@@ -75,7 +76,12 @@ struct Session {
     bool failed = false;
     ErrCode fail_code = ErrCode::Internal;
     std::string fail_detail;
-    bool device_busy = false;    // HBM/stream of this slot still in use
+    bool device_busy = false;    // a task of this slot is on the device
+    std::uint32_t uploads = 0;   // eager SND uploads in flight
+    bool input_resident = false; // the current input already sits in HBM
+    std::uint8_t head[64] = {};  // first bytes of the input (EP parameters)
+    float upload_h2d_us = 0.0f;
+    std::deque<Inbound> backlog; // frames that arrived while an upload ran
 };
 
 struct Pending {
@@ -98,6 +104,7 @@ struct InFlight {
     Clock::time_point arrival_wall;
     Clock::time_point dispatch_wall;
     TaskMetrics vmetrics;  // virtual-clock values, fixed at flush
+    float upload_h2d_us = 0.0f;
 };
 
 struct BatchState {
@@ -130,6 +137,7 @@ struct GvmDaemon::Impl {
     Clock::time_point started = Clock::now();
 
     std::map<std::uint64_t, InFlight> inflight;     // tag -> task
+    std::map<std::uint32_t, std::deque<std::uint64_t>> pending_snd_acks;
     std::map<std::uint64_t, BatchState> batches;     // batch key -> state
     std::uint64_t next_tag = 1;
 
@@ -228,6 +236,15 @@ struct GvmDaemon::Impl {
         if (m.opcode == Opcode::Req) return on_req(m, in.origin);
         Session* s = session(m.client_id);
         if (!s) return;  // no such slot: dropped, as in the reference
+        if (s->uploads > 0) {
+            // per-client order: nothing overtakes the pending SND ACK
+            s->backlog.push_back(in);
+            return;
+        }
+        dispatch(m, s);
+    }
+
+    void dispatch(const Message& m, Session* s) {
         if (!leased(*s)) return nack(m.client_id, m.task_id, ErrCode::NoLease,
                                      "no lease for client");
         switch (m.opcode) {
@@ -245,7 +262,7 @@ struct GvmDaemon::Impl {
         std::uint32_t slot = 0;
         for (std::uint32_t i = 1; i <= cfg.max_clients && slot == 0; ++i) {
             const Session& s = sessions[i - 1];
-            if (!leased(s) && !s.device_busy) slot = i;
+            if (!leased(s) && !s.device_busy && s.uploads == 0) slot = i;
         }
         if (slot == 0) {
             transport->reply_origin(origin, {Opcode::Nack, 0, m.task_id,
@@ -279,6 +296,23 @@ struct GvmDaemon::Impl {
             return nack(m.client_id, m.task_id, ErrCode::Size, "data exceeds leased region");
         s.input_len = *len;
         s.input.clear();
+        s.input_resident = false;
+        std::memcpy(s.head, region.data(), std::min<std::uint64_t>(*len, sizeof s.head));
+        if (dev && cfg.data_plane == DataPlane::ZeroCopy) {
+            // eager upload: the SND snapshot is taken by DMA into the slot's
+            // HBM buffer; the ACK goes out when the copy has landed, so the
+            // client's H2D overlaps the other clients' host work
+            const int rc = vgpu_cu_upload(dev, m.client_id, region.data(), *len,
+                                          (static_cast<std::uint64_t>(m.client_id) << 32) |
+                                              (s.generation & 0xffffffffu));
+            if (rc != VGPU_CU_OK)
+                return nack(m.client_id, m.task_id, ErrCode::Internal,
+                            std::string("upload failed: ") + vgpu_cu_last_error());
+            ++s.uploads;
+            s.phase = Phase::DataIn;
+            pending_snd_acks[m.client_id].push_back(m.task_id);
+            return;
+        }
         if (cfg.data_plane == DataPlane::Snapshot) {
             // reference timing of the region read (daemon.cpp:248)
             if (dev)
@@ -468,7 +502,10 @@ struct GvmDaemon::Impl {
             }
             std::uint64_t out_bytes = 0;
             const std::uint64_t in_len = live ? s->input_len : t.profile.input_bytes;
-            const int rc = vgpu_cu_output_size(dk->kernel, src, in_len, &out_bytes);
+            const std::uint8_t* probe = (live && s->input_resident && in_len <= sizeof s->head)
+                                            ? s->head
+                                            : src;
+            const int rc = vgpu_cu_output_size(dk->kernel, probe, in_len, &out_bytes);
             if (rc != VGPU_CU_OK || !live) {
                 if (live)
                     fail_session(t.client_id, t.generation, ErrCode::Payload,
@@ -500,6 +537,11 @@ struct GvmDaemon::Impl {
             ct.param = dk->param;
             ct.h_in = src;
             ct.in_bytes = in_len;
+            if (s->input_resident) {
+                ct.flags |= VGPU_CU_TASK_INPUT_RESIDENT;
+                if (in_len <= sizeof s->head) ct.h_in = s->head;  // SND-time bytes
+                f.upload_h2d_us = s->upload_h2d_us;
+            }
             if (cfg.data_plane == DataPlane::ZeroCopy) {
                 ct.h_out = transport->region(t.client_id).data();
                 f.out_at = OutAt::Region;
@@ -607,7 +649,7 @@ struct GvmDaemon::Impl {
     // ---- completions ----------------------------------------------------------
 
     void drain_device() {
-        if (!dev || inflight.empty()) return;
+        if (!dev) return;
         vgpu_cu_done done[64];
         for (;;) {
             std::uint32_t n = 0;
@@ -617,6 +659,7 @@ struct GvmDaemon::Impl {
     }
 
     void complete(const vgpu_cu_done& d) {
+        if (d.kind == VGPU_CU_DONE_UPLOAD) return upload_done(d);
         auto it = inflight.find(d.tag);
         if (it == inflight.end()) return;
         const InFlight f = it->second;
@@ -631,7 +674,7 @@ struct GvmDaemon::Impl {
             tm.queue_wait_us = us_between(f.arrival_wall, f.dispatch_wall);
             tm.pure_gpu_us = static_cast<Micros>(d.span_us + 0.5f);
             tm.end_to_end_us = us_between(f.arrival_wall, now);
-            tm.h2d_us = d.h2d_us;
+            tm.h2d_us = d.h2d_us > 0.0f ? d.h2d_us : f.upload_h2d_us;
             tm.comp_us = d.comp_us;
             tm.d2h_us = d.d2h_us;
         }
@@ -661,6 +704,30 @@ struct GvmDaemon::Impl {
                                         ? static_cast<Micros>(d.batch_span_us + 0.5f)
                                         : us_between(bs.dispatch_wall, now);
             record_batch({f.batch_key, bs.style, bs.task_count, bs.model_makespan, measured});
+        }
+    }
+
+    void upload_done(const vgpu_cu_done& d) {
+        Session* s = session(d.slot);
+        if (!s) return;
+        if (s->uploads) --s->uploads;
+        auto& q = pending_snd_acks[d.slot];
+        const std::uint64_t task = q.empty() ? 0 : q.front();
+        if (!q.empty()) q.pop_front();
+        if (!leased(*s)) return;
+        if (d.status != VGPU_CU_OK) {
+            s->phase = Phase::Leased;
+            nack(d.slot, task, ErrCode::Internal, "device upload failed");
+        } else {
+            if (s->uploads == 0) s->input_resident = true;  // the last SND's bytes
+            s->upload_h2d_us = d.h2d_us;
+            ack(d.slot, task);
+        }
+        // replay what the client sent meanwhile, until another upload starts
+        while (s->uploads == 0 && !s->backlog.empty()) {
+            const Inbound in = std::move(s->backlog.front());
+            s->backlog.pop_front();
+            dispatch(in.msg, s);
         }
     }
 

@@ -1,10 +1,17 @@
-set -x
 make -j8 all 2>&1 | tail -1
 timeout 600 ./tests/_bin/vgpu-tests --only-gpu > gpurun_out/gpu_cpp.log 2>&1; echo "cpp rc=$?"
-grep -E "FAIL|minitest" gpurun_out/gpu_cpp.log
+grep -E "FAIL|minitest|note" gpurun_out/gpu_cpp.log
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/pytest_gpu.log
-./paper_1511_07658_b200/bin/payload-bench 0 all 0 20 > gpurun_out/payload_bench.txt 2>&1; cat gpurun_out/payload_bench.txt
-timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "bench rc=$?"
-tail -5 gpurun_out/bench1.err; cat gpurun_out/bench1.json
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:stream_table -s 3 -c 1 -o gpurun_out/prof_vadd -f ./paper_1511_07658_b200/bin/payload-bench 0 vecadd 4 5 > gpurun_out/ncu_vadd.log 2>&1; echo "ncu rc=$?"; tail -3 gpurun_out/ncu_vadd.log
+tail -3 gpurun_out/pytest_gpu.log
+summ() { python - "$1" <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read())
+e=d["e2e"]; p=d.get("e2e_paper_barrier") or {}
+print("value",round(d["value"]),"e2e",round(e["value"],1),"paper",round(p.get("value",0),1),"native",d["native"]["runs"],"vs_native",round(d["vs_native"],3),"turn",round(d["turnaround"]["speedup"],1),"roof",d["roofline"]["frac"],"cpu",d["cpu_baseline"] and d["cpu_baseline"]["value"])
+print(" client",e["client_stage_us"]," device",e["device_stage_us"])
+print(" model",d["model"], "clocks", d["clocks"])
+PY
+}
+for w in vecadd ep bs mm; do
+timeout 900 python bench.py --workload $w --steps 10 --warmup 3 --cpu-budget-s 8 > gpurun_out/b4_$w.json 2> gpurun_out/b4_$w.err; echo "== $w rc=$?"; tail -2 gpurun_out/b4_$w.err; summ gpurun_out/b4_$w.json
+done
