@@ -235,6 +235,10 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
         if k == "ep":
             sets = 2
         r = V.resident_bench(W.PAYLOAD[k], inputs, sets, warmup, steps, device=device)
+        if r["pdl"]:  # also the serialized per-launch duration, for the record
+            rs = V.resident_bench(W.PAYLOAD[k], inputs, sets, warmup, steps, device=device,
+                                  pdl=False)
+            r["serial_kernel_ms_per_launch"] = rs["kernel_ms_per_launch"]
         legs[k] = r
         ms_step += r["ms_per_step"]
         launches += r["launches_per_step"] * steps
@@ -554,7 +558,13 @@ def main():
                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
                     "peak_source": peaks["source"], "kernel": W.PAYLOAD[dom],
                     "algo_bytes_per_launch": d["algo_bytes_per_launch"],
-                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
+                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3,
+                    "launch_chaining": ("PDL: K independent steps back to back, each launch "
+                                        "may ramp up under the previous one's tail")
+                                       if d["pdl"] else "serialized",
+                    "serial_us_per_launch": (d.get("serial_kernel_ms_per_launch") or 0) * 1e3,
+                    "serial_frac": (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"] * 1e-3)
+                                    / 1e9 / peaks["hbm_gbs"]) if d.get("serial_kernel_ms_per_launch") else None}
         else:
             achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
             roof = {"bound": bound, "achieved": achieved, "peak": None, "unit": "TFLOP/s",

@@ -185,15 +185,19 @@ typedef struct vgpu_cu_resident_result {
     uint64_t algo_bytes_per_launch;
     double algo_flops_per_launch;
     uint64_t resident_bytes;    /* HBM held by the rotating sets             */
+    uint32_t pdl;               /* 1: steps chained with programmatic
+                                   dependent launch (HBM-streaming kernels) */
+    uint32_t reserved;
 } vgpu_cu_resident_result;
 
 /* Times `steps` batched launches of `kernel` over n_tasks tasks whose inputs
  * (copied once from h_inputs[i], in_bytes[i]) sit in HBM; `sets` rotating
  * copies keep the working set above L2 between steps. */
+#define VGPU_CU_RESIDENT_NO_PDL 1u /* flags: serialize steps (per-launch duration) */
 int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
                            uint32_t n_tasks, const void* const* h_inputs,
                            const uint64_t* in_bytes, uint32_t sets,
-                           uint32_t warmup, uint32_t steps,
+                           uint32_t warmup, uint32_t steps, uint32_t flags,
                            vgpu_cu_resident_result* out);
 
 /* ---- multi-GPU: the single final reduction (NCCL over NVLink) --------- */

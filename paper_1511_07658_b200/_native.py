@@ -51,7 +51,8 @@ class ResidentResult(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("ms_per_step", C.c_double),
                 ("kernel_ms_per_launch", C.c_double), ("launches_per_step", C.c_uint32),
                 ("sets", C.c_uint32), ("algo_bytes_per_launch", C.c_uint64),
-                ("algo_flops_per_launch", C.c_double), ("resident_bytes", C.c_uint64)]
+                ("algo_flops_per_launch", C.c_double), ("resident_bytes", C.c_uint64),
+                ("pdl", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class CuStats(C.Structure):
@@ -117,7 +118,7 @@ CUDA_API = {
     "vgpu_cu_strerror": (C.c_char_p, [C.c_int]),
     "vgpu_cu_last_error": (C.c_char_p, []),
     "vgpu_cu_resident_bench": (C.c_int, [C.c_int, _U32, C.c_float, _U32, C.POINTER(_P),
-                                         C.POINTER(_U64), _U32, _U32, _U32,
+                                         C.POINTER(_U64), _U32, _U32, _U32, _U32,
                                          C.POINTER(ResidentResult)]),
     "vgpu_cu_nccl_unique_id": (C.c_int, [_P]),
     "vgpu_cu_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int]),

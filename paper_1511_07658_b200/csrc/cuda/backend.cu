@@ -115,9 +115,28 @@ struct DevJob {
     vgpu_ep_params ep{};
 };
 
+// Launch with programmatic stream serialization: the launch may begin as
+// soon as the previous kernel on the stream has started (it executes
+// griddepcontrol.launch_dependents first). Only used for independent,
+// idempotent streaming launches (value leg); the GVM path never chains
+// kernel->kernel on a stream (each slot's kernels are fenced by copies).
+template <class Kern, class Arg>
+cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, cudaStream_t s, const Arg& arg) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, arg);
+}
+
 // Launch every job (all of one kernel kind) on `s`; counts launches.
 cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t n,
-                        cudaStream_t s, std::uint64_t* launches) {
+                        cudaStream_t s, std::uint64_t* launches, bool pdl = false) {
     using namespace vgk;
     switch (kernel) {
         case VGPU_CU_K_IDENTITY:
@@ -148,12 +167,16 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     ctas += static_cast<std::uint32_t>((elems + kStreamChunk - 1) / kStreamChunk);
                 }
                 if (!ctas) continue;
-                if (add)
+                cudaError_t e = cudaSuccess;
+                if (pdl)
+                    e = add ? launch_pdl(stream_table_kernel<true>, ctas, kStreamThreads, s, t)
+                            : launch_pdl(stream_table_kernel<false>, ctas, kStreamThreads, s, t);
+                else if (add)
                     stream_table_kernel<true><<<ctas, kStreamThreads, 0, s>>>(t);
                 else
                     stream_table_kernel<false><<<ctas, kStreamThreads, 0, s>>>(t);
                 ++*launches;
-                const cudaError_t e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaGetLastError();
                 if (e != cudaSuccess) return e;
             }
             return cudaSuccess;
@@ -213,9 +236,13 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     ctas += static_cast<std::uint32_t>((opts + kBsChunk - 1) / kBsChunk);
                 }
                 if (!ctas) continue;
-                bs_table_kernel<<<ctas, kBsThreads, 0, s>>>(t);
+                cudaError_t e = cudaSuccess;
+                if (pdl)
+                    e = launch_pdl(bs_table_kernel, ctas, kBsThreads, s, t);
+                else
+                    bs_table_kernel<<<ctas, kBsThreads, 0, s>>>(t);
                 ++*launches;
-                const cudaError_t e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaGetLastError();
                 if (e != cudaSuccess) return e;
             }
             return cudaSuccess;
@@ -1054,7 +1081,7 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
 int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::uint32_t n_tasks,
                            const void* const* h_inputs, const std::uint64_t* in_bytes,
                            std::uint32_t sets, std::uint32_t warmup, std::uint32_t steps,
-                           vgpu_cu_resident_result* res) {
+                           std::uint32_t flags, vgpu_cu_resident_result* res) {
     if (!res || n_tasks == 0 || !h_inputs || !in_bytes || sets == 0 || steps == 0)
         return VGPU_CU_EINVAL;
     std::memset(res, 0, sizeof *res);
@@ -1110,10 +1137,16 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
     CK(cudaStreamSynchronize(guard.s));
     // K back-to-back steps between ONE event pair: the average launch
     // duration without per-launch event overhead
+    // HBM-streaming launches are short and independent step to step: chain
+    // them with PDL so one step's ramp-up hides under the previous tail, as
+    // consecutive GVM batches overlap on their own streams
+    const bool pdl = !(flags & VGPU_CU_RESIDENT_NO_PDL) && sets >= 2 && (kernel == VGPU_CU_K_VADD || kernel == VGPU_CU_K_VSCALE ||
+                                   kernel == VGPU_CU_K_BS);
+    res->pdl = pdl ? 1u : 0u;
     l = 0;
     CK(cudaEventRecord(guard.evs[0], guard.s));
     for (std::uint32_t t = 0; t < steps; ++t)
-        CK(launch_jobs(kernel, js[(warmup + t) % sets].data(), n_tasks, guard.s, &l));
+        CK(launch_jobs(kernel, js[(warmup + t) % sets].data(), n_tasks, guard.s, &l, pdl));
     CK(cudaEventRecord(guard.evs[1], guard.s));
     CK(cudaStreamSynchronize(guard.s));
     float total = 0.0f;

@@ -52,6 +52,8 @@ __device__ __forceinline__ int find_job(const StreamTable& t, std::uint32_t cta)
 template <bool kAdd>
 __global__ void __launch_bounds__(kStreamThreads)
 stream_table_kernel(const __grid_constant__ StreamTable table) {
+    // lets an independent follow-up launch (PDL) ramp up under this one's tail
+    asm volatile("griddepcontrol.launch_dependents;");
     const int j = find_job(table, blockIdx.x);
     const StreamJob& job = table.job[j];
     const std::uint64_t chunk = blockIdx.x - job.cta_begin;

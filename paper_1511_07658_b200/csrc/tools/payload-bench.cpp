@@ -37,7 +37,7 @@ int main(int argc, char** argv) {
                 static_cast<std::uint32_t>(std::min<std::uint64_t>(16, 1 + (512ull << 20) / (set_bytes + 1)));
             vgpu_cu_resident_result r{};
             const int rc = vgpu_cu_resident_bench(device, kernels[k], 2.0f, tasks, ptrs.data(),
-                                                  sizes.data(), sets, 3, steps, &r);
+                                                  sizes.data(), sets, 3, steps, 0, &r);
             if (rc) {
                 std::printf("%-7s tasks=%2u  error %s: %s\n", kinds[k], tasks, vgpu_cu_strerror(rc),
                             vgpu_cu_last_error());

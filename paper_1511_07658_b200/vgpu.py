@@ -313,7 +313,7 @@ def device_count() -> int:
 
 
 def resident_bench(payload_id: str, inputs: Sequence[bytes], sets: int, warmup: int,
-                   steps: int, device: int = 0, param: float = 2.0) -> dict:
+                   steps: int, device: int = 0, param: float = 2.0, pdl: bool = True) -> dict:
     """Device-only timing of the batched launch with inputs resident in HBM."""
     bufs = [(C.c_uint8 * max(1, len(b))).from_buffer_copy(b if len(b) else b"\0")
             for b in inputs]
@@ -322,7 +322,7 @@ def resident_bench(payload_id: str, inputs: Sequence[bytes], sets: int, warmup: 
     r = N.ResidentResult()
     _cu_check(_libs().cuda.vgpu_cu_resident_bench(device, KERNELS[payload_id], param,
                                                   len(bufs), ptrs, sizes, sets, warmup,
-                                                  steps, C.byref(r)))
+                                                  steps, 0 if pdl else 1, C.byref(r)))
     return {k: getattr(r, k) for k, _ in N.ResidentResult._fields_}
 
 
