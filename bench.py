@@ -357,10 +357,14 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
     return r
 
 
-def final_reduce(V, N, dist, record):
-    """The single cross-GPU collective: NCCL all-gather of per-GPU records,
-    folded on the host in rank order (deterministic)."""
+def final_reduce(N, dist, record):
+    """The single cross-GPU collective: NCCL all-gather of the per-GPU
+    records through vgpu_cu_reduce_final, folded on the host in rank order
+    (paper_1511_07658_b200/reduce.py). At one GPU the communicator has one
+    rank, so the same C path still runs."""
     import ctypes as C
+
+    from paper_1511_07658_b200 import reduce as R
     libs = N.load()
     uid = (C.c_uint8 * 128)()
     if dist.rank == 0:
@@ -375,15 +379,13 @@ def final_reduce(V, N, dist, record):
     try:
         if libs.cuda.vgpu_cu_comm_init(dev, uid, dist.world, dist.rank):
             raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
-        rec = (C.c_double * 4)(*record)
-        allr = (C.c_double * (4 * dist.world))()
+        rec = (C.c_double * R.REC_WIDTH)(*record)
+        allr = (C.c_double * (R.REC_WIDTH * dist.world))()
+        t0 = time.perf_counter()
         if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
             raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
-        folded = [0.0] * 4
-        for r in range(dist.world):
-            for i in range(4):
-                folded[i] = folded[i] + allr[4 * r + i]
-        return folded
+        us = (time.perf_counter() - t0) * 1e6
+        return R.fold_in_rank_order(list(allr), dist.world), us
     finally:
         libs.cuda.vgpu_cu_close(dev)
 
@@ -532,12 +534,17 @@ def main():
 
     # ---- final reduction (multi-GPU only) ----------------------------------------------
     reduce_info = None
-    if world > 1:
-        checks = [int(r["checksum"], 16) & 0xFFFFFFFF for r in e2e["results"]]
-        rec = [float(procs * args.steps), float(sum(checks) % 1000003), e2e["seconds"], ms_step]
-        folded = final_reduce(V, N, dist, rec)
-        reduce_info = {"jobs_all_gpus": folded[0], "collective": "ncclAllGather (NVLink), "
-                       "host fold in rank order"}
+    from paper_1511_07658_b200 import reduce as R
+    record = R.record_from_workers(e2e["results"])
+    try:
+        folded, us = final_reduce(N, dist, record)
+        reduce_info = {"collective": f"ncclAllGather of {R.REC_WIDTH * 8} B per GPU "
+                                     f"({world} rank(s)), host fold in rank order",
+                       "wall_us": us, "jobs_folded": folded[0]}
+        if folded[14] > 0:
+            reduce_info["ep"] = R.ep_verdict(folded, sizes.ep_m)
+    except Exception as e:  # noqa: BLE001 - reported in the line
+        reduce_info = {"error": str(e)[:300], "local_record_jobs": record[0]}
 
     # ---- cpu baseline (rank 0, N = 1) -----------------------------------------------------
     cpu = None

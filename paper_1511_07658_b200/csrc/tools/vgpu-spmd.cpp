@@ -209,7 +209,21 @@ int main(int argc, char** argv) {
         std::sort(v.begin(), v.end());
         os << (k ? ", " : "") << "\"" << names[k] << "\": " << (v.empty() ? 0 : v[v.size() / 2]);
     }
-    os << "}, \"err\": \"" << err << "\"}";
+    os << "}";
+    if (job.kind == vgpu::wl::Kind::Ep && last_out.size() == sizeof(vgpu_ep_result)) {
+        // the job's partial for the final reduction, bit patterns in hex
+        vgpu_ep_result r;
+        std::memcpy(&r, last_out.data(), sizeof r);
+        std::uint64_t bx, by;
+        std::memcpy(&bx, &r.sx, 8);
+        std::memcpy(&by, &r.sy, 8);
+        os << ", \"ep\": {\"sx_bits\": \"" << std::hex << bx << "\", \"sy_bits\": \"" << by
+           << std::dec << "\", \"pairs\": " << r.pairs << ", \"n_batches\": " << r.n_batches
+           << ", \"q\": [";
+        for (int i = 0; i < 10; ++i) os << (i ? ", " : "") << r.q[i];
+        os << "]}";
+    }
+    os << ", \"err\": \"" << err << "\"}";
     std::printf("%s\n", os.str().c_str());
     std::fflush(stdout);
     return ok ? 0 : 5;

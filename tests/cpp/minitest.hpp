@@ -50,10 +50,12 @@ struct Registrar {
 
 inline int run(int argc, char** argv) {
     bool only_gpu = false, exclude_gpu = false;
-    std::vector<std::string> filters;
+    std::vector<std::string> filters, files, skips;
     for (int i = 1; i < argc; ++i) {
         if (!std::strcmp(argv[i], "--only-gpu")) only_gpu = true;
         else if (!std::strcmp(argv[i], "--exclude-gpu")) exclude_gpu = true;
+        else if (!std::strcmp(argv[i], "--file") && i + 1 < argc) files.emplace_back(argv[++i]);
+        else if (!std::strcmp(argv[i], "--skip") && i + 1 < argc) skips.emplace_back(argv[++i]);
         else if (!std::strcmp(argv[i], "--list")) {
             for (auto& c : registry()) std::printf("%s\n", c.name);
             return 0;
@@ -63,6 +65,14 @@ inline int run(int argc, char** argv) {
     for (auto& c : registry()) {
         const bool gpu = std::strstr(c.name, "[gpu]") != nullptr;
         if ((only_gpu && !gpu) || (exclude_gpu && gpu)) continue;
+        if (!files.empty()) {
+            bool hit = false;
+            for (auto& f : files) hit |= std::strstr(c.file, f.c_str()) != nullptr;
+            if (!hit) continue;
+        }
+        bool skipped = false;
+        for (auto& s : skips) skipped |= std::strstr(c.name, s.c_str()) != nullptr;
+        if (skipped) continue;
         if (!filters.empty()) {
             bool hit = false;
             for (auto& f : filters) hit |= std::strstr(c.name, f.c_str()) != nullptr;

@@ -30,3 +30,37 @@ def test_cpp_cpu_suite():
 @pytest.mark.gpu
 def test_cpp_gpu_suite():
     _run("--only-gpu", 900)
+
+
+# ---- drop-in proof: the reference's own unit tests against this library ----
+# tests/_bin/ref-unit-tests is compiled in the build container from the
+# UNMODIFIED /root/reference/proj/tests/test_{message,transport,model,device,
+# daemon,client}.cpp with a doctest shim (oracle/Makefile.ref) and linked to
+# libvgpu.so; the binary travels, the reference sources do not.
+REF_BIN = os.path.join(REPO, "tests", "_bin", "ref-unit-tests")
+# by design: the reference paces real-clock completions with sleeps
+# (daemon.cpp:532-585); on B200 the real clock is the hardware's
+REF_EXPECTED_DIFFERENT = ["real clock paces completion"]
+
+
+def _ref_run(args, timeout):
+    if not os.path.exists(REF_BIN):
+        pytest.skip("ref-unit-tests not built (needs /root/reference at build time)")
+    p = subprocess.run([REF_BIN] + args, cwd=REPO, stdout=subprocess.PIPE,
+                       stderr=subprocess.STDOUT, timeout=timeout, text=True)
+    if p.returncode != 0:
+        pytest.fail(p.stdout[-6000:])
+    assert "0 failed" in p.stdout
+
+
+def test_reference_unit_tests_cpu_suites():
+    _ref_run(["--file", "test_message", "--file", "test_transport", "--file", "test_model",
+              "--file", "test_device"], 300)
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_all_on_b200():
+    args = []
+    for name in REF_EXPECTED_DIFFERENT:
+        args += ["--skip", name]
+    _ref_run(args, 600)
