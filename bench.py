@@ -339,9 +339,11 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
     if not os.path.exists(ref):
         return None
     try:
-        one = _ref_run(ref, workload, 1, 1, 0, size_args)  # probe: one job
-        per_job = max(1e-4, one["seconds"])
-        n = max(1, min(procs, int(20.0 / per_job)))
+        # probe one round: one job, or one job of each kind for the mix
+        n0 = min(procs, 4) if workload == "mixed" else 1
+        one = _ref_run(ref, workload, n0, 1, 0, size_args)
+        per_job = max(1e-4, one["seconds"] / n0)
+        n = n0 if workload == "mixed" else max(1, min(procs, int(20.0 / per_job)))
         per_round = per_job * n
         rounds = max(1, min(200, int(budget_s / per_round)))
         w = warmup if per_round * (rounds + warmup) < 2 * budget_s else 0
@@ -572,10 +574,24 @@ def main():
                     "serial_us_per_launch": (d.get("serial_kernel_ms_per_launch") or 0) * 1e3,
                     "serial_frac": (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"] * 1e-3)
                                     / 1e9 / peaks["hbm_gbs"]) if d.get("serial_kernel_ms_per_launch") else None}
-        else:
+        elif bound == "fp32":
+            # FP32 SIMT peak derived from the part: SMs x 128 lanes x 2 x max SM clock
+            smax = (clock_info or {}).get("sm_max_mhz") or 1965.0
+            peak = 148 * 128 * 2 * smax * 1e6 / 1e12
             achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
-            roof = {"bound": bound, "achieved": achieved, "peak": None, "unit": "TFLOP/s",
+            roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": ncu_traffic(dom), "kernel": W.PAYLOAD[dom],
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock "
+                                   "(no tensor cores: true FP32 SIMT, rel. Frobenius <= 1e-5)",
+                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
+        else:
+            # EP: NPB's own rate unit (uniform random numbers per second); the
+            # FP64-pipe share comes from the committed ncu capture
+            achieved = d["algo_flops_per_launch"] / kernel_s / 1e9
+            roof = {"bound": "fp64", "achieved": achieved, "peak": None, "unit": "G uniforms/s (NPB Mop/s / 1e3)",
                     "frac": None, "traffic": ncu_traffic(dom), "kernel": W.PAYLOAD[dom],
+                    "note": "FP64-pipe bound (log/div/sqrt); see profiles/ for "
+                            "sm__pipe_fp64_cycles_active",
                     "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
         line = {
             "metric": METRIC, "value": value, "unit": "jobs/s", "n_gpus": world,

@@ -98,6 +98,9 @@ public:
     virtual void wake() {}
     // B200: bump the slot's completion doorbell (thread-safe).
     virtual void notify(std::uint32_t /*client_id*/) {}
+    // B200: false once the peer bound to this slot has disconnected (client
+    // death); the GVM then reclaims the slot instead of leaking the lease.
+    virtual bool route_alive(std::uint32_t /*client_id*/) const { return true; }
 };
 
 // ---- in-process loopback --------------------------------------------------

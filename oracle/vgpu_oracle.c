@@ -23,7 +23,7 @@ void vo_vector_scale(float* out, const float* in, float factor, size_t n) {
 
 int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     memset(r, 0, sizeof *r);
-    if (p->mk < 8 || p->mk > 24 || p->m < p->mk || p->m > 40 || p->reserved != 0) return -1;
+    if (p->mk < 8 || p->mk > 20 || p->m < p->mk || p->m > 40 || p->reserved != 0) return -1;
     const uint64_t batches_total = 1ull << (p->m - p->mk);
     if (p->first_batch > batches_total || p->n_batches > batches_total - p->first_batch) return -1;
     const uint64_t per_lane = (1ull << p->mk) / VGPU_EP_LANES;

@@ -77,7 +77,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15
 // ---- payload contracts (host-side validation before launch) ----------------
 
 int ep_check(const vgpu_ep_params& p) {
-    if (p.reserved != 0 || p.mk < 8 || p.mk > 24 || p.m < p.mk || p.m > 40) {
+    if (p.reserved != 0 || p.mk < 8 || p.mk > 20 || p.m < p.mk || p.m > 40) {  // mk <= 20: 12-bit per-lane counters
         set_err("nas-ep: bad class parameters m=%u mk=%u", p.m, p.mk);
         return VGPU_CU_EPAYLOAD;
     }

@@ -265,6 +265,20 @@ struct GvmDaemon::Impl {
             if (!leased(s) && !s.device_busy && s.uploads == 0) slot = i;
         }
         if (slot == 0) {
+            // B200 addition: reclaim leases whose client died without RLS
+            // (the reference keeps them forever); in-flight device work of
+            // the slot must drain first
+            for (std::uint32_t i = 1; i <= cfg.max_clients && slot == 0; ++i) {
+                Session& s = sessions[i - 1];
+                if (leased(s) && !transport->route_alive(i)) {
+                    s.phase = Phase::Released;
+                    s.generation = 0;
+                    s.backlog.clear();
+                    if (!s.device_busy && s.uploads == 0) slot = i;
+                }
+            }
+        }
+        if (slot == 0) {
             transport->reply_origin(origin, {Opcode::Nack, 0, m.task_id,
                                              encode_nack(ErrCode::Full,
                                                          "all client slots leased")});

@@ -276,6 +276,11 @@ public:
         routes_[client_id] = conn_of(origin);
     }
 
+    bool route_alive(std::uint32_t client_id) const override {
+        auto it = routes_.find(client_id);
+        return it != routes_.end() && st_->conn(it->second) != nullptr;
+    }
+
     void send(std::uint32_t client_id, const Message& m) override {
         auto it = routes_.find(client_id);
         if (it == routes_.end()) return;

@@ -525,3 +525,21 @@ TEST_CASE("gvm os: start creates endpoint, regions, doorbell; 8 processes x 100 
     CHECK(d->metrics().tasks.size() == 800);
     d->stop();
 }
+
+TEST_CASE("gvm: a dead client's lease is reclaimed by the next REQ") {
+    LoopbackHub hub;
+    auto d = start(hub, cfg(1, 1));
+    {
+        Raw a(hub);
+        CHECK(a.req().opcode == Opcode::Ack);
+        Raw b(hub);
+        CHECK(code(b.req()) == ErrCode::Full);  // a is alive: no reclaim
+    }  // both connections drop without RLS
+    Raw c(hub);
+    CHECK(c.req().opcode == Opcode::Ack);
+    CHECK(c.lease.client_id == 1);
+    c.snd(pair(1, 2, 3, 4));
+    c.str(1, kCIdesc);
+    CHECK(c.await().opcode == Opcode::Ack);
+    CHECK(c.stp(1).opcode == Opcode::Ack);
+}
