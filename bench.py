@@ -39,6 +39,12 @@ import tempfile
 import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
+# before any CUDA context exists in this process (torch's or the GVM's): one
+# hardware queue per client stream
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# test mode for 1-GPU boxes: every rank drives GPU 0, plumbing over gloo, and
+# the final all-gather goes through torch instead of one NCCL rank per GPU
+SHARED_GPU = os.environ.get("VGPU_BENCH_SHARED_GPU") == "1"
 sys.path.insert(0, REPO)
 
 METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; kernel GB/s vs roofline"
@@ -56,11 +62,12 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = 0 if SHARED_GPU else self.local
         self.torch = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = "nccl" if torch.cuda.is_available() and not SHARED_GPU else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
@@ -250,7 +257,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
                 sizes, dist, cold=False, barrier=0):
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
-    inst = f"b200bench{os.getpid()}g{dist.local}"
+    inst = f"b200bench{os.getpid()}g{dist.rank}"
     env = dict(os.environ)
     env["CUDA_VISIBLE_DEVICES"] = env.get("CUDA_VISIBLE_DEVICES", "")
     if not env["CUDA_VISIBLE_DEVICES"]:
@@ -326,7 +333,7 @@ def _ref_run(ref, workload, procs, rounds, warmup, size_args):
     return r
 
 
-def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
+def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_rounds=200):
     """The unmodified reference GVM (oracle/_ref/ref-bench) on host cores.
 
     The reference GVM runs every payload sequentially on its dispatcher
@@ -345,7 +352,7 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1):
         per_job = max(1e-4, one["seconds"] / n0)
         n = n0 if workload == "mixed" else max(1, min(procs, int(20.0 / per_job)))
         per_round = per_job * n
-        rounds = max(1, min(200, int(budget_s / per_round)))
+        rounds = max(1, min(max_rounds, int(budget_s / per_round)))
         w = warmup if per_round * (rounds + warmup) < 2 * budget_s else 0
         r = _ref_run(ref, workload, n, rounds, w, size_args)
     except Exception as e:  # noqa: BLE001 - reported, not fatal for our arm
@@ -367,6 +374,13 @@ def final_reduce(N, dist, record):
     import ctypes as C
 
     from paper_1511_07658_b200 import reduce as R
+    if SHARED_GPU and dist.world > 1:  # test mode: one GPU cannot host 2 NCCL ranks
+        t = dist.torch.tensor(record, dtype=dist.torch.float64)
+        parts = [dist.torch.zeros_like(t) for _ in range(dist.world)]
+        t0 = time.perf_counter()
+        dist.dist.all_gather(parts, t)
+        us = (time.perf_counter() - t0) * 1e6
+        return R.fold_in_rank_order(dist.torch.cat(parts).tolist(), dist.world), us
     libs = N.load()
     uid = (C.c_uint8 * 128)()
     if dist.rank == 0:
@@ -376,7 +390,7 @@ def final_reduce(N, dist, record):
     uid_bytes = dist.bcast(bytes(uid))
     uid = (C.c_uint8 * 128).from_buffer_copy(uid_bytes)
     dev = C.c_void_p()
-    if libs.cuda.vgpu_cu_open(dist.local, 1, 4096, C.byref(dev)):
+    if libs.cuda.vgpu_cu_open(dist.device, 1, 4096, C.byref(dev)):
         raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
     try:
         if libs.cuda.vgpu_cu_comm_init(dev, uid, dist.world, dist.rank):
@@ -409,7 +423,22 @@ def model_summary(batches):
 
 # ---- main -----------------------------------------------------------------------------
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the real stdout (everything else goes to stderr)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # libraries (NCCL's version banner, CUDA) may write to fd 1: keep the
+    # original stdout for the result line and point fd 1 at stderr
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -441,7 +470,8 @@ def main():
 
     if args.impl == "reference":
         if dist.rank == 0:
-            r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s)
+            r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s,
+                                  warmup=min(args.warmup, 3), max_rounds=args.steps)
             if r is None:
                 line = {"impl": "reference", "unavailable": "oracle/_ref/ref-bench not built "
                         "(needs /root/reference at build time)"}
@@ -456,14 +486,14 @@ def main():
                                          "kind": "reference", "sample": r["sample"]},
                         "e2e": {"value": r["jobs_per_s"], "unit": "jobs/s",
                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-            print(json.dumps(line), flush=True)
+            emit(line)
         dist.close()
         return
 
     N.load()
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
-    device = dist.local
+    device = dist.device
     gid0 = dist.rank * procs
     total_workers = procs * world
     clocks = Clocks(device) if dist.local == 0 or world == 1 else None
@@ -616,7 +646,7 @@ def main():
             "final_reduce": reduce_info,
             "model": model_summary(paper["batches"] if paper else e2e["batches"]),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.close()
 
 

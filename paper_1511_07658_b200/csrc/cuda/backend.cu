@@ -39,6 +39,7 @@
 #include "k_bs.cuh"
 #include "k_ep.cuh"
 #include "k_sgemm.cuh"
+#include "k_sgemm_tc.cuh"
 #include "k_stream.cuh"
 
 namespace {
@@ -112,8 +113,18 @@ struct DevJob {
     std::uint8_t* out = nullptr;
     std::uint64_t out_bytes = 0;
     std::uint8_t* scratch = nullptr;
+    std::uint8_t* ws = nullptr;  // sgemm tensor-core workspace: 2 x in_bytes
     vgpu_ep_params ep{};
 };
+
+// VGPU_SGEMM=simt selects the FP32 SIMT kernel instead of 3xTF32 tcgen05.
+bool sgemm_use_tc() {
+    static const bool tc = [] {
+        const char* e = std::getenv("VGPU_SGEMM");
+        return !(e && std::strcmp(e, "simt") == 0);
+    }();
+    return tc;
+}
 
 // Launch with programmatic stream serialization: the launch may begin as
 // soon as the previous kernel on the stream has started (it executes
@@ -248,6 +259,60 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             return cudaSuccess;
         }
         case VGPU_CU_K_SGEMM: {
+            // tensor-core path (3xTF32, tcgen05) for n % 128 == 0 when a
+            // workspace is present; SIMT FP32 otherwise (or VGPU_SGEMM=simt)
+            bool any_tc = false;
+            for (std::uint32_t i = 0; i < n && !any_tc; ++i) {
+                const std::uint64_t dim = isqrt(jobs[i].in_bytes / 8);
+                any_tc = dim > 0 && dim % kTcBM == 0 && jobs[i].ws != nullptr;
+            }
+            if (any_tc && sgemm_use_tc()) {
+                TcTable tt{};
+                std::uint32_t maxn = 0;
+                std::vector<std::uint32_t> rest;
+                for (std::uint32_t i = 0; i < n; ++i) {
+                    const std::uint32_t dim = static_cast<std::uint32_t>(isqrt(jobs[i].in_bytes / 8));
+                    if (dim == 0) continue;
+                    if (dim % kTcBM != 0 || !jobs[i].ws || tt.njobs == kMaxTcJobs) {
+                        rest.push_back(i);
+                        continue;
+                    }
+                    TcJob& j = tt.job[tt.njobs++];
+                    const std::size_t nn = static_cast<std::size_t>(dim) * dim;
+                    j.A = reinterpret_cast<const float*>(jobs[i].in);
+                    j.B = j.A + nn;
+                    j.C = reinterpret_cast<float*>(jobs[i].out);
+                    float* w = reinterpret_cast<float*>(jobs[i].ws);
+                    j.ahi = w;
+                    j.alo = w + nn;
+                    j.bthi = w + 2 * nn;
+                    j.btlo = w + 3 * nn;
+                    j.n = dim;
+                    maxn = std::max(maxn, dim);
+                }
+                if (tt.njobs) {
+                    static bool attr = [] {
+                        return cudaFuncSetAttribute(tc_gemm_kernel,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kTcSmemBytes) == cudaSuccess;
+                    }();
+                    if (!attr) return cudaErrorInvalidConfiguration;
+                    tc_split_kernel<<<dim3(maxn / 32, maxn / 32, tt.njobs), dim3(32, 8), 0, s>>>(tt);
+                    tc_gemm_kernel<<<dim3(maxn / kTcBN, maxn / kTcBM, tt.njobs), kTcThreads,
+                                     kTcSmemBytes, s>>>(tt);
+                    *launches += 2;
+                    const cudaError_t e = cudaGetLastError();
+                    if (e != cudaSuccess) return e;
+                }
+                if (rest.empty()) return cudaSuccess;
+                std::vector<DevJob> left;
+                for (auto i : rest) {
+                    left.push_back(jobs[i]);
+                    left.back().ws = nullptr;  // SIMT for these
+                }
+                return launch_jobs(kernel, left.data(), static_cast<std::uint32_t>(left.size()), s,
+                                   launches, pdl);
+            }
             GemmTable fast{}, gen{};
             std::uint32_t fast_tiles = 0, gen_tiles = 0;
             auto flush = [&](GemmTable& t, std::uint32_t& tiles, bool is_fast) -> cudaError_t {
@@ -369,6 +434,7 @@ struct SlotState {
     std::uint8_t* d_in = nullptr;
     std::uint8_t* d_out = nullptr;
     std::uint8_t* d_scratch = nullptr;
+    std::uint8_t* d_ws = nullptr;
     void* reg_base = nullptr;
     bool task_busy = false;
     std::uint32_t ops_in_flight = 0;
@@ -607,7 +673,8 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
     d->slot_bytes = slot_bytes;
     d->slots.resize(max_clients + 1);
     const std::uint64_t buf = round_up(std::max<std::uint64_t>(slot_bytes, 256), kAlign);
-    const std::uint64_t per_slot = 2 * buf + round_up(kScratchBytes, kAlign);
+    // in | out | EP scratch | sgemm workspace (hi/lo splits: 2 x input)
+    const std::uint64_t per_slot = 4 * buf + round_up(kScratchBytes, kAlign);
     auto fail = [&](int code) {
         vgpu_cu_close(d);
         return code;
@@ -623,6 +690,7 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
         s.d_in = base;
         s.d_out = base + buf;
         s.d_scratch = base + 2 * buf;
+        s.d_ws = s.d_scratch + round_up(kScratchBytes, kAlign);
         e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
         if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
     }
@@ -790,6 +858,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         j.out = s.d_out;
         j.out_bytes = need;
         j.scratch = s.d_scratch;
+        j.ws = s.d_ws;
         if (t.kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, t.h_in, sizeof j.ep);
     }
     CK(cudaSetDevice(d->device));
@@ -1000,7 +1069,8 @@ struct ProcCtx {
     std::uint8_t* d_in = nullptr;
     std::uint8_t* d_out = nullptr;
     std::uint8_t* d_scratch = nullptr;
-    std::uint64_t cap_in = 0, cap_out = 0;
+    std::uint8_t* d_ws = nullptr;
+    std::uint64_t cap_in = 0, cap_out = 0, cap_ws = 0;
     std::atomic<std::uint64_t> launches{0};
 };
 ProcCtx& proc() {
@@ -1064,6 +1134,16 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     j.out = c.d_out;
     j.out_bytes = need;
     j.scratch = c.d_scratch;
+    if (kernel == VGPU_CU_K_SGEMM) {
+        if (2 * in_bytes > c.cap_ws) {
+            if (c.d_ws) cudaFree(c.d_ws);
+            c.d_ws = nullptr;
+            c.cap_ws = 0;
+            CK(cudaMalloc(&c.d_ws, 2 * in_bytes));
+            c.cap_ws = 2 * in_bytes;
+        }
+        j.ws = c.d_ws;
+    }
     if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, in, sizeof j.ep);
     // pageable copies, exactly what an unvirtualized CUDA program does
     if (in_bytes) CK(cudaMemcpyAsync(c.d_in, in, in_bytes, cudaMemcpyHostToDevice, c.stream));
@@ -1093,7 +1173,8 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
     for (std::uint32_t i = 0; i < n_tasks; ++i) {
         rc = vgpu_cu_output_size(kernel, h_inputs[i], in_bytes[i], &outb[i]);
         if (rc) return rc;
-        per_set += round_up(in_bytes[i], 256) + round_up(outb[i], 256) + round_up(kScratchBytes, 256);
+        per_set += round_up(in_bytes[i], 256) + round_up(outb[i], 256) + round_up(kScratchBytes, 256) +
+                   (kernel == VGPU_CU_K_SGEMM ? round_up(2 * in_bytes[i], 256) : 0);
     }
     std::uint8_t* mem = nullptr;
     CK(cudaMalloc(&mem, per_set * sets));
@@ -1123,6 +1204,10 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
             p += round_up(outb[i], 256);
             j.scratch = p;
             p += round_up(kScratchBytes, 256);
+            if (kernel == VGPU_CU_K_SGEMM) {
+                j.ws = p;
+                p += round_up(2 * in_bytes[i], 256);
+            }
             if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, h_inputs[i], sizeof j.ep);
             if (in_bytes[i])
                 CK(cudaMemcpy(const_cast<std::uint8_t*>(j.in), h_inputs[i], in_bytes[i],

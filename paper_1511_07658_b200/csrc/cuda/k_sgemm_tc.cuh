@@ -1,0 +1,284 @@
+// SGEMM on the 5th-generation tensor cores: 3xTF32 with tcgen05.mma.
+//
+// Precision contract (stated tolerance): every fp32 operand x is
+// split into x_hi = x with its low 13 mantissa bits cleared (exact in TF32)
+// and x_lo = x - x_hi (exact in fp32; the MMA keeps its top 10 mantissa
+// bits). C = A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32 in TMEM.
+// The dropped A_lo B_lo term and the truncation of the lo parts put the
+// error near 2^-21 per product; checked at relative Frobenius <= 1e-5 against
+// the binary64 oracle (the SIMT kernel's bar).
+//
+// Pre-pass (tc_split_kernel): A -> A_hi, A_lo (row-major M x K = K-major);
+// B -> B_hi^T, B_lo^T (N x K, K-major) through a 32x32 shared-memory
+// transpose, so both UMMA operands are K-major.
+//
+// Main kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 128
+// threads, tiles of every task of a batch in one launch (blockIdx.z = task):
+//   * 3-stage cp.async pipeline; each stage holds the four 128 x 32 fp32
+//     operand tiles (A_hi, A_lo, B_hi, B_lo; 16 KiB each) in the canonical
+//     K-major 128-byte-swizzled layout (16-byte chunk c of row r lands at
+//     chunk c ^ (r & 7) inside its 1024-byte 8-row group);
+//   * fence.proxy.async makes the staged bytes visible to the tensor core;
+//     one elected thread issues 4 k-steps x 3 products of
+//     tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=128, K=8) into a
+//     128-column fp32 TMEM accumulator, then tcgen05.commit arrives on the
+//     stage's mbarrier so the stage can be refilled;
+//   * epilogue: each warp drains its 32 TMEM lanes with
+//     tcgen05.ld.32x32b.x32 and stores its rows of C.
+#pragma once
+
+#include <cstdint>
+
+namespace vgk {
+
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;  // BK in fp32 elements (128 bytes)
+constexpr int kTcStages = 3;
+constexpr int kTcThreads = 128;
+constexpr int kTcTileBytes = kTcBM * kTcBK * 4;       // 16 KiB
+constexpr int kTcStageBytes = 4 * kTcTileBytes;       // 64 KiB
+constexpr int kTcSmemBytes = kTcStages * kTcStageBytes + 1024 + 256;
+constexpr int kMaxTcJobs = 64;
+
+struct TcJob {
+    const float* A;   // n x n row-major (split source)
+    const float* B;
+    float* C;
+    float* ahi;       // workspace: n*n each
+    float* alo;
+    float* bthi;      // B^T hi / lo, n x n (row = column of B)
+    float* btlo;
+    std::uint32_t n;
+    std::uint32_t pad;
+};
+
+struct TcTable {
+    TcJob job[kMaxTcJobs];
+    std::uint32_t njobs;
+};
+
+// ---- pre-pass: split + transpose ---------------------------------------------
+
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+    hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    lo = __fsub_rn(x, hi);
+}
+
+// grid (n/32, n/32, jobs), block (32, 8)
+__global__ void __launch_bounds__(256) tc_split_kernel(const __grid_constant__ TcTable table) {
+    const TcJob& job = table.job[blockIdx.z];
+    const int n = static_cast<int>(job.n);
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    if (bx >= n || by >= n) return;
+    __shared__ float tile[32][33];
+    // A: straight split (rows by..by+31, cols bx..bx+31)
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const std::size_t idx = static_cast<std::size_t>(by + r) * n + bx + threadIdx.x;
+        float hi, lo;
+        tf32_split(job.A[idx], hi, lo);
+        job.ahi[idx] = hi;
+        job.alo[idx] = lo;
+    }
+    // B: transpose through shared memory; Bt[c][r] = B[r][c]
+    for (int r = threadIdx.y; r < 32; r += 8)
+        tile[r][threadIdx.x] = job.B[static_cast<std::size_t>(by + r) * n + bx + threadIdx.x];
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const std::size_t idx = static_cast<std::size_t>(bx + r) * n + by + threadIdx.x;
+        float hi, lo;
+        tf32_split(tile[threadIdx.x][r], hi, lo);
+        job.bthi[idx] = hi;
+        job.btlo[idx] = lo;
+    }
+}
+
+// ---- PTX helpers ---------------------------------------------------------------
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async16(std::uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase));
+}
+
+// K-major, 128-byte swizzle, 8-row groups 1024 B apart (CuTe canonical
+// layout Swizzle<3,4,3> o ((8,m),2):((8,SBO),1) in 16-byte units)
+__device__ __forceinline__ std::uint64_t umma_desc_k_sw128(std::uint32_t saddr) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((saddr >> 4) & 0x3FFFu);  // start address
+    d |= static_cast<std::uint64_t>(1u) << 16;                // LBO (unused for SW128 K-major)
+    d |= static_cast<std::uint64_t>(1024u >> 4) << 32;        // SBO: next 8-row group
+    d |= static_cast<std::uint64_t>(1u) << 46;                // version (sm_100)
+    d |= static_cast<std::uint64_t>(2u) << 61;                // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M=128, N=128
+constexpr std::uint32_t kTcIdesc = (1u << 4)          // c_format F32
+                                   | (2u << 7)        // a_format TF32
+                                   | (2u << 10)       // b_format TF32
+                                   | ((kTcBN >> 3) << 17)
+                                   | ((kTcBM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(std::uint32_t tmem_d, std::uint64_t a, std::uint64_t b,
+                                          std::uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kTcIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        smem_u32(bar)));
+}
+
+// ---- main kernel -----------------------------------------------------------------
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ TcTable table) {
+    const TcJob& job = table.job[blockIdx.z];
+    const int n = static_cast<int>(job.n);
+    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
+    if (m0 >= n || n0 >= n) return;
+
+    extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+    std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+        (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kTcStageBytes);
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s <= kTcStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(kTcBN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const std::uint32_t tmem = *tmem_slot;
+
+    const float* srcs[4] = {job.ahi + static_cast<std::size_t>(m0) * n,
+                            job.alo + static_cast<std::size_t>(m0) * n,
+                            job.bthi + static_cast<std::size_t>(n0) * n,
+                            job.btlo + static_cast<std::size_t>(n0) * n};
+    // stage k-block kb into stage s: 4 tiles x 128 rows x 8 chunks, 32 per thread
+    auto load_stage = [&](int kb, int s) {
+        const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int chunk = tid + i * kTcThreads;  // 0..4095
+            const int tile = chunk >> 10;
+            const int r = (chunk >> 3) & 127;
+            const int c = chunk & 7;
+            const float* g = srcs[tile] + static_cast<std::size_t>(r) * n + kb * kTcBK + c * 4;
+            const std::uint32_t d = sbase + tile * kTcTileBytes + (r >> 3) * 1024 + (r & 7) * 128 +
+                                    ((c ^ (r & 7)) << 4);
+            cp_async16(d, g);
+        }
+    };
+
+    const int kblocks = n / kTcBK;
+#pragma unroll
+    for (int s = 0; s < kTcStages - 1; ++s) {
+        if (s < kblocks) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % kTcStages;
+        cp_async_wait<kTcStages - 2>();
+        asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+#pragma unroll
+            for (int k = 0; k < kTcBK / 8; ++k) {
+                const std::uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
+                const std::uint64_t ahi = umma_desc_k_sw128(sbase + 0 * kTcTileBytes + off);
+                const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
+                const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
+                const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
+                const std::uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+                umma_tf32(tmem, ahi, bhi, acc0);
+                umma_tf32(tmem, ahi, blo, 1u);
+                umma_tf32(tmem, alo, bhi, 1u);
+            }
+            umma_commit(&bars[s]);  // stage s free once these MMAs have read it
+        }
+        // refill the stage consumed one iteration ago with k-block kb + S - 1
+        const int next = kb + kTcStages - 1;
+        if (next < kblocks) {
+            const int ns = next % kTcStages;
+            if (kb >= 1) mbar_wait(&bars[ns], ((kb - 1) / kTcStages) & 1);
+            load_stage(next, ns);
+        }
+        cp_async_commit();
+    }
+    // all MMAs done -> accumulator ready
+    if (tid == 0) umma_commit(&bars[kTcStages]);
+    mbar_wait(&bars[kTcStages], 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // epilogue: warp w owns TMEM lanes (= C rows) 32w .. 32w+31
+    const int row = m0 + warp * 32 + (tid & 31);
+    float* crow = job.C + static_cast<std::size_t>(row) * n + n0;
+#pragma unroll
+    for (int cb = 0; cb < kTcBN; cb += 32) {
+        std::uint32_t v[32];
+        const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(warp * 32) << 16) + cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(crow + cb + j) =
+                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcBN));
+}
+
+}  // namespace vgk
