@@ -1,12 +1,12 @@
 // SGEMM on the 5th-generation tensor cores: 3xTF32 with tcgen05.mma.
 //
 // Precision contract (stated tolerance): every fp32 operand x is
-// split into x_hi = x with its low 13 mantissa bits cleared (exact in TF32)
-// and x_lo = x - x_hi (exact in fp32; the MMA keeps its top 10 mantissa
-// bits). C = A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32 in TMEM.
-// The dropped A_lo B_lo term and the truncation of the lo parts put the
-// error near 2^-21 per product; checked at relative Frobenius <= 1e-5 against
-// the binary64 oracle (the SIMT kernel's bar).
+// split into x_hi = x rounded to nearest TF32 and x_lo = x - x_hi (exact in
+// fp32, |x_lo| <= 2^-11 |x|; the MMA keeps its top 10 mantissa bits).
+// C = A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32 in TMEM. The
+// dropped A_lo B_lo term and the lo-part truncation are ~2^-22 per product;
+// checked at relative Frobenius <= 1e-5 against the binary64 oracle (the
+// SIMT kernel's bar). VGPU_SGEMM=simt selects the FP32 SIMT kernel.
 //
 // Pre-pass (tc_split_kernel): A -> A_hi, A_lo (row-major M x K = K-major);
 // B -> B_hi^T, B_lo^T (N x K, K-major) through a 32x32 shared-memory
@@ -58,8 +58,12 @@ struct TcTable {
 
 // ---- pre-pass: split + transpose ---------------------------------------------
 
+// hi = x rounded to nearest TF32 (|lo| <= 2^-11 |x|); lo = x - hi is exact
+// in fp32. Rounding instead of truncating quarters both neglected terms.
 __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-    hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    std::uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
     lo = __fsub_rn(x, hi);
 }
 
