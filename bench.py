@@ -49,6 +49,8 @@ sys.path.insert(0, REPO)
 
 METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; kernel GB/s vs roofline"
 L2_BYTES = 126 << 20
+# arithmetic type each workload's path computes in (EP: binary64 + integer LCG)
+DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f64"}
 
 
 def log(*a):
@@ -172,10 +174,27 @@ def measured_peaks() -> dict:
 
 
 def ncu_traffic(kernel_kind: str):
+    """DRAM bytes (read + write) per launch of the kind's dominant kernel at
+    this bench's shape, from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py)."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
-    return json.load(open(p)).get(kernel_kind)
+        return None, None
+    e = json.load(open(p)).get(kernel_kind)
+    return (e["bytes"], e["source"]) if e else (None, None)
+
+
+def device_peaks(V, device: int) -> dict:
+    """FMA-pipe peaks measured on this GPU now (vgpu_cu_peak_probe), the
+    denominators of the FP64 (EP) and FP32-SIMT (SGEMM) rooflines."""
+    out = {}
+    for k in ("fp64", "fp32"):
+        try:
+            out[k] = V.peak_probe(k, device)
+        except Exception as e:  # noqa: BLE001 - reported as missing
+            log("peak probe", k, "failed:", e)
+            out[k] = None
+    return out
 
 
 def spawn_workers(args_list, env):
@@ -270,8 +289,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
                           barrier_window=2000, clock=V.ClockMode.Real, cuda_device=device,
                           device_sms=148, device_max_kernels=128, device_slots_per_sm=32)
         gvm = V.GvmDaemon.start_os(cfg)
-    size_args = ["--vecadd-n", str(sizes.vecadd_n), "--ep-m", str(sizes.ep_m),
-                 "--bs-n", str(sizes.bs_n), "--mm-n", str(sizes.mm_n)]
+    size_args = sizes.size_args()
     args = []
     for i in range(procs):
         a = [spmd, "--worker", str(gid0 + i), "--workers", str(total_workers), "--workload",
@@ -341,8 +359,7 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_round
     (proj/src/client.cpp:17), so the sample shrinks the process count when a
     full round would not fit; jobs/s is the rate it sustains."""
     ref = os.path.join(REPO, "oracle", "_ref", "ref-bench")
-    size_args = ["--vecadd-n", str(sizes.vecadd_n), "--ep-m", str(sizes.ep_m),
-                 "--bs-n", str(sizes.bs_n), "--mm-n", str(sizes.mm_n)]
+    size_args = sizes.size_args()
     if not os.path.exists(ref):
         return None
     try:
@@ -380,7 +397,8 @@ def final_reduce(N, dist, record):
         t0 = time.perf_counter()
         dist.dist.all_gather(parts, t)
         us = (time.perf_counter() - t0) * 1e6
-        return R.fold_in_rank_order(dist.torch.cat(parts).tolist(), dist.world), us
+        flat = dist.torch.cat(parts).tolist()
+        return R.fold_in_rank_order(flat, dist.world), flat[:R.REC_WIDTH], us
     libs = N.load()
     uid = (C.c_uint8 * 128)()
     if dist.rank == 0:
@@ -401,7 +419,7 @@ def final_reduce(N, dist, record):
         if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
             raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
         us = (time.perf_counter() - t0) * 1e6
-        return R.fold_in_rank_order(list(allr), dist.world), us
+        return R.fold_in_rank_order(list(allr), dist.world), list(allr)[:R.REC_WIDTH], us
     finally:
         libs.cuda.vgpu_cu_close(dev)
 
@@ -420,6 +438,111 @@ def model_summary(batches):
             "note": "model uses the clients' declared stage estimates (Fermi-style single "
                     "queue); measured is the B200 batch span from CUDA events"}
 
+
+
+# ---- rooflines ----------------------------------------------------------------------
+
+KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32"}
+
+
+def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
+    """Roofline of the dominant kernel of one resident leg.
+
+    achieved = ALGORITHMIC work per launch / the launch's average duration
+    (CUDA events on its stream, inside the timed region):
+      vecadd/bs  bytes: 12 B per element / 20 B per option
+      mm         2 n^3 FLOP per task (FP32 SIMT, or 3xTF32 tcgen05 opt-in)
+      ep         IEEE binary64 operations of the restated NPB algorithm:
+                 7 per pair + 32 per accepted pair (W.ep_fp64_ops)
+    peak = MEASURED_PEAKS.json HBM for hbm-bound kernels; the FMA-pipe peak
+    probed on this GPU now for fp64/fp32 (vgpu_cu_peak_probe)."""
+    kernel_s = d["kernel_ms_per_launch"] * 1e-3
+    bound = KIND_BOUND[kind]
+    tkey = "mm_tc" if kind == "mm" and os.environ.get("VGPU_SGEMM") == "tc" else kind
+    traffic, tsrc = ncu_traffic(tkey)
+    r = {"bound": bound, "kernel": W.PAYLOAD[kind], "traffic": traffic,
+         "traffic_source": tsrc, "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3,
+         "launches_per_step": d["launches_per_step"]}
+    if bound == "hbm":
+        hbm = measured_peaks()
+        achieved = d["algo_bytes_per_launch"] / kernel_s / 1e9
+        r.update({"achieved": achieved, "peak": hbm["hbm_gbs"], "unit": "GB/s",
+                  "frac": achieved / hbm["hbm_gbs"], "peak_source": hbm["source"],
+                  "algo_bytes_per_launch": d["algo_bytes_per_launch"],
+                  "launch_chaining": ("PDL: K independent steps back to back, each launch may "
+                                      "ramp up under the previous one's tail") if d["pdl"]
+                                     else "serialized"})
+        if d.get("serial_kernel_ms_per_launch"):
+            r["serial_us_per_launch"] = d["serial_kernel_ms_per_launch"] * 1e3
+            r["serial_frac"] = (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"]
+                                * 1e-3) / 1e9 / hbm["hbm_gbs"])
+        return r
+    if bound == "fp32":
+        peak = peaks.get("fp32")
+        achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
+        r.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                  "frac": achieved / peak if peak else None,
+                  "algo_flops_per_launch": d["algo_flops_per_launch"],
+                  "peak_source": "measured now: FFMA-chain probe (vgpu_cu_peak_probe)",
+                  "precision": ("3xTF32 tcgen05, rel. Frobenius <= 1e-5"
+                                if tkey == "mm_tc" else
+                                "FP32 SIMT, rel. Frobenius <= 1e-5 vs binary64")})
+        return r
+    # EP: NPB's own unit beside the FP64 roofline
+    pairs = d["algo_flops_per_launch"] / 2.0
+    accepted = ep_accepted if ep_accepted else W.EP_ACCEPT_RATE * pairs
+    ops = W.ep_fp64_ops(pairs, accepted)
+    peak = peaks.get("fp64")
+    achieved = ops / kernel_s / 1e12
+    r.update({"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+              "frac": achieved / peak if peak else None,
+              "algo_flops_per_launch": ops, "pairs_per_launch": pairs,
+              "accepted_per_launch": accepted,
+              "npb_mops": 2.0 * pairs / kernel_s / 1e6,
+              "peak_source": "measured now: DFMA-chain probe (vgpu_cu_peak_probe), 2 FLOP/DFMA",
+              "op_count": "IEEE binary64 ops of the restated NPB EP step (each +,-,*,/,sqrt = 1): "
+                          "7 per pair + 23 per accepted pair (table-driven log = 16)"})
+    return r
+
+
+def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
+    """Kernel GB/s (FLOP/s) vs roofline for every BASELINE config kernel at
+    its own config's per-step shape (C1 4 x vecadd, C2 8 x EP slices of
+    class A, C3 16 x Black-Scholes, C4 16 x SGEMM), device-resident. The
+    headline workload's own entry is the line's `roofline`."""
+    shapes = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16}
+    out = {}
+    for kind, procs in shapes.items():
+        if kind == workload:
+            continue
+        try:
+            legs, _, _, dom = leg_value(V, W, kind, procs, 0, procs, steps, warmup, device,
+                                        W.Sizes())
+            r = roofline(W, dom, legs[dom], peaks,
+                         W.EP_CLASS_A_ACCEPTED if kind == "ep" else None)
+            out[kind] = {k: r.get(k) for k in ("bound", "kernel", "achieved", "peak", "unit",
+                                                 "frac", "traffic", "kernel_us_per_launch")}
+            out[kind]["tasks_per_launch"] = procs
+        except Exception as e:  # noqa: BLE001 - reported in the line
+            out[kind] = {"error": str(e)[:200]}
+    return out
+
+
+def leg_overhead_n1(V, N, W, workload, steps, warmup, device, sizes, dist) -> dict:
+    """North-star target 'virtualization overhead under 5% at N=1': ONE SPMD
+    process through the GVM vs the same process non-virtualized (own CUDA
+    context, warm), same job, same steps. overhead = 1 - native/virtualized
+    time per job (negative: the GVM is faster)."""
+    v = leg_workers(V, N, W, workload, 1, 0, 1, steps, warmup, device, False, sizes, dist,
+                    barrier=1)
+    n = leg_workers(V, N, W, workload, 1, 0, 1, steps, warmup, device, True, sizes, dist)
+    v_ms, n_ms = v["seconds"] * 1e3 / steps, n["seconds"] * 1e3 / steps
+    return {"virtualized_ms_per_job": v_ms, "native_warm_ms_per_job": n_ms,
+            "overhead": 1.0 - n_ms / v_ms,
+            "paper_overhead": 1.0 - (v["device_stage_us"]["pure_gpu_us"] or 0) * 1e-3 / v_ms,
+            "client_stage_us": v.get("client_stage_us"), "device_stage_us": v.get("device_stage_us"),
+            "desc": "1 process: GVM e2e vs NativeVgpu warm (own context, pageable copies); "
+                    "paper_overhead = 1 - pure_gpu/turnaround (proj/src/bench/bench.cpp:414-419)"}
 
 # ---- main -----------------------------------------------------------------------------
 
@@ -443,12 +566,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="vecadd", choices=["vecadd", "ep", "bs", "mm", "mixed"])
+    # default: BASELINE.json configs[1] (NAS EP class A, 8 processes per B200)
+    ap.add_argument("--workload", default="ep", choices=["vecadd", "ep", "bs", "mm", "mixed"])
     ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-native", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
+    ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
+    ap.add_argument("--no-kernels", action="store_true",
+                    help="skip the per-kernel roofline summary of the other configs")
     ap.add_argument("--barrier-size", type=int, default=-1,
                     help="GVM barrier (tasks per flush); -1 = workload default")
     args = ap.parse_args()
@@ -460,8 +588,12 @@ def main():
 
     dist = Dist()
     procs = args.procs or W.DEFAULT_PROCS[args.workload]
-    sizes = W.Sizes()
     world = dist.world
+    sizes = W.Sizes.for_world(world)
+    if args.ep_m:
+        sizes.ep_m, sizes.ep_batches = args.ep_m, 0
+    if args.vecadd_n:
+        sizes.vecadd_n = args.vecadd_n
     config = {"workload": W.CONFIG_NAME[args.workload], "procs_per_gpu": procs,
               "barrier_size": procs if args.barrier_size < 0 else args.barrier_size,
               "gpus": world, "global_procs": procs * world, "parallelism": f"gvm-per-gpu x{world}",
@@ -479,7 +611,7 @@ def main():
                 cores = os.cpu_count()
                 line = {"impl": "reference", "metric": METRIC, "value": r["jobs_per_s"],
                         "unit": "jobs/s", "higher_is_better": True, "n_gpus": 0, "steps": r["rounds"],
-                        "warmup": r["warmup"], "ms_per_step": r["ms_per_round"], "dtype": "f32",
+                        "warmup": r["warmup"], "ms_per_step": r["ms_per_round"], "dtype": DTYPE[args.workload],
                         "data": "synthetic", "scaling": "weak", "vs_baseline": None,
                         "config": config,
                         "cpu_baseline": {"value": r["jobs_per_s"], "unit": "jobs/s", "cores": cores,
@@ -562,6 +694,10 @@ def main():
                       "desc": "paper Figs. 13-22 turnaround: simultaneous start -> last process "
                               "has its result; virtualized includes REQ, native includes its "
                               "own CUDA context creation"}
+    overhead = None
+    if not args.no_native and world == 1:
+        overhead = leg_overhead_n1(V, N, W, args.workload if args.workload != "mixed" else "vecadd",
+                                   args.steps, args.warmup, device, sizes, dist)
     clock_info = clocks.stop() if clocks else None
 
     # ---- final reduction (multi-GPU only) ----------------------------------------------
@@ -569,12 +705,12 @@ def main():
     from paper_1511_07658_b200 import reduce as R
     record = R.record_from_workers(e2e["results"])
     try:
-        folded, us = final_reduce(N, dist, record)
+        folded, rank0, us = final_reduce(N, dist, record)
         reduce_info = {"collective": f"ncclAllGather of {R.REC_WIDTH * 8} B per GPU "
                                      f"({world} rank(s)), host fold in rank order",
                        "wall_us": us, "jobs_folded": folded[0]}
         if folded[14] > 0:
-            reduce_info["ep"] = R.ep_verdict(folded, sizes.ep_m)
+            reduce_info["ep"] = R.ep_verdict(folded, sizes.ep_m, sizes.ep_batches, rank0)
     except Exception as e:  # noqa: BLE001 - reported in the line
         reduce_info = {"error": str(e)[:300], "local_record_jobs": record[0]}
 
@@ -587,46 +723,17 @@ def main():
                    "kind": "reference", "sample": r["sample"]}
 
     if dist.rank == 0:
-        d = legs[dom]
-        peaks = measured_peaks()
-        kernel_s = d["kernel_ms_per_launch"] * 1e-3
-        bound = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32"}[dom]
-        if bound == "hbm":
-            achieved = d["algo_bytes_per_launch"] / kernel_s / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
-                    "peak_source": peaks["source"], "kernel": W.PAYLOAD[dom],
-                    "algo_bytes_per_launch": d["algo_bytes_per_launch"],
-                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3,
-                    "launch_chaining": ("PDL: K independent steps back to back, each launch "
-                                        "may ramp up under the previous one's tail")
-                                       if d["pdl"] else "serialized",
-                    "serial_us_per_launch": (d.get("serial_kernel_ms_per_launch") or 0) * 1e3,
-                    "serial_frac": (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"] * 1e-3)
-                                    / 1e9 / peaks["hbm_gbs"]) if d.get("serial_kernel_ms_per_launch") else None}
-        elif bound == "fp32":
-            # FP32 SIMT peak derived from the part: SMs x 128 lanes x 2 x max SM clock
-            smax = (clock_info or {}).get("sm_max_mhz") or 1965.0
-            peak = 148 * 128 * 2 * smax * 1e6 / 1e12
-            achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
-            roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": ncu_traffic(dom), "kernel": W.PAYLOAD[dom],
-                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x max SM clock "
-                                   "(no tensor cores: true FP32 SIMT, rel. Frobenius <= 1e-5)",
-                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
-        else:
-            # EP: NPB's own rate unit (uniform random numbers per second); the
-            # FP64-pipe share comes from the committed ncu capture
-            achieved = d["algo_flops_per_launch"] / kernel_s / 1e9
-            roof = {"bound": "fp64", "achieved": achieved, "peak": None, "unit": "G uniforms/s (NPB Mop/s / 1e3)",
-                    "frac": None, "traffic": ncu_traffic(dom), "kernel": W.PAYLOAD[dom],
-                    "note": "FP64-pipe bound (log/div/sqrt); see profiles/ for "
-                            "sm__pipe_fp64_cycles_active",
-                    "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3}
+        peaks = device_peaks(V, device)
+        accepted = record[13] if record[13] > 0 else None
+        roof = roofline(W, dom, legs[dom], peaks, accepted)
+        kernels = None
+        if not args.no_kernels:
+            kernels = kernel_summary(V, W, args.workload, device, peaks, sizes, args.steps,
+                                     args.warmup)
         line = {
             "metric": METRIC, "value": value, "unit": "jobs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE[args.workload],
             "data": "synthetic", "config": config,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": secs * 1e3 / args.steps,
@@ -640,6 +747,8 @@ def main():
             "native": native,
             "vs_native": (e2e_value / native["value"]) if native else None,
             "roofline": roof,
+            "kernels": kernels,
+            "overhead_n1": overhead,
             "cpu_baseline": cpu,
             "gpu_launches": launches_value + launches_e2e,
             "clocks": clock_info,

@@ -155,6 +155,11 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* dev, int style, const vgpu_cu_task* tasks,
 /* Collect finished tasks (non-blocking). */
 int vgpu_cu_poll(vgpu_cu_dev* dev, vgpu_cu_done* out, uint32_t cap,
                  uint32_t* n_out);
+/* Operations (tasks and uploads) submitted but not yet reported by poll().
+ * poll() detects completion by querying each one's final CUDA event (no
+ * callback latency), so a dispatcher with work pending polls it in a hot
+ * loop; the notify callback still fires for a sleeping dispatcher. */
+int vgpu_cu_pending(vgpu_cu_dev* dev);
 /* Block until at least one task finished or timeout_us passed. */
 int vgpu_cu_wait(vgpu_cu_dev* dev, int64_t timeout_us);
 /* Called (from a CUDA host-callback thread) whenever a task finishes. */
@@ -199,6 +204,13 @@ int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
                            const uint64_t* in_bytes, uint32_t sets,
                            uint32_t warmup, uint32_t steps, uint32_t flags,
                            vgpu_cu_resident_result* out);
+
+/* ---- roofline denominators measured on the device ------------------------ */
+/* Dependent-chain FMA microbenchmark (8 independent chains per thread, a
+ * few waves of 148 x 8 CTAs): the pipe peak the EP (FP64) and SIMT SGEMM
+ * (FP32) rooflines are quoted against, counting 2 FLOP per FMA. */
+enum vgpu_cu_peak_kind { VGPU_CU_PEAK_FP64 = 0, VGPU_CU_PEAK_FP32 = 1 };
+int vgpu_cu_peak_probe(int device, uint32_t kind, double* tflops);
 
 /* ---- multi-GPU: the single final reduction (NCCL over NVLink) --------- */
 #define VGPU_CU_NCCL_ID_BYTES 128

@@ -52,6 +52,7 @@ def lib() -> C.CDLL:
         L.vo_vector_scale.argtypes = [f32p, f32p, C.c_float, C.c_size_t]
         L.vo_ep_job.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
         L.vo_ep_job.restype = C.c_int
+        L.vo_ep_log.argtypes = [f64p, f64p, C.c_size_t]
         L.vo_ep_fold.argtypes = [C.POINTER(EpResult), C.c_size_t, C.POINTER(EpResult)]
         L.vo_black_scholes.argtypes = [f32p, f32p, f32p, C.c_size_t, C.c_double, C.c_double,
                                        f64p, f64p]
@@ -73,6 +74,14 @@ def vector_scale(x: np.ndarray, f: float) -> np.ndarray:
     out = np.empty_like(x)
     lib().vo_vector_scale(out, x, f, x.size)
     return out
+
+
+def ep_log(x: np.ndarray) -> np.ndarray:
+    """vgpu_ep_log, the EP kernel's shared logarithm, on the CPU."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().vo_ep_log(x, y, x.size)
+    return y
 
 
 def ep_params_bytes(m: int, first: int, count: int, mk: int = 16) -> bytes:

@@ -94,6 +94,7 @@ int main(int argc, char** argv) {
         else if (a == "--instance") instance = v;
         else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(v);
         else if (a == "--ep-m") sizes.ep_m = std::stoul(v);
+        else if (a == "--ep-batches") sizes.ep_batches = std::stoull(v);
         else if (a == "--bs-n") sizes.bs_n = std::stoull(v);
         else if (a == "--mm-n") sizes.mm_n = std::stoul(v);
     }

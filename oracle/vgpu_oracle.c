@@ -67,6 +67,10 @@ int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     return 0;
 }
 
+void vo_ep_log(const double* x, double* y, size_t n) {
+    for (size_t i = 0; i < n; ++i) y[i] = vgpu_ep_log(x[i]);
+}
+
 void vo_ep_fold(const vgpu_ep_result* parts, size_t n, vgpu_ep_result* out) {
     memset(out, 0, sizeof *out);
     double sx = 0.0, sy = 0.0;

@@ -39,6 +39,8 @@ void vo_vector_scale(float* out, const float* in, float factor, size_t n);
  * in a binary tree, batches accumulate sequentially in batch order. */
 int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r);
 /* Fold job results in order (the GVM / rank-order host fold). */
+/* vgpu_ep_log (ep_math.h, shared with the kernel) over an array: accuracy tests */
+void vo_ep_log(const double* x, double* y, size_t n);
 void vo_ep_fold(const vgpu_ep_result* parts, size_t n, vgpu_ep_result* out);
 
 void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,

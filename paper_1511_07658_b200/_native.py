@@ -110,6 +110,7 @@ CUDA_API = {
     "vgpu_cu_submit_batch": (C.c_int, [_P, C.c_int, _P, _U32, C.POINTER(_U64)]),
     "vgpu_cu_poll": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_cu_wait": (C.c_int, [_P, _I64]),
+    "vgpu_cu_pending": (C.c_int, [_P]),
     "vgpu_cu_set_notify": (None, [_P, _P, _P]),
     "vgpu_cu_get_stats": (C.c_int, [_P, C.POINTER(CuStats)]),
     "vgpu_cu_execute": (C.c_int, [C.c_int, _U32, C.c_float, _P, _U64, _P, _U64, C.POINTER(_U64)]),
@@ -120,6 +121,7 @@ CUDA_API = {
     "vgpu_cu_resident_bench": (C.c_int, [C.c_int, _U32, C.c_float, _U32, C.POINTER(_P),
                                          C.POINTER(_U64), _U32, _U32, _U32, _U32,
                                          C.POINTER(ResidentResult)]),
+    "vgpu_cu_peak_probe": (C.c_int, [C.c_int, _U32, C.POINTER(C.c_double)]),
     "vgpu_cu_nccl_unique_id": (C.c_int, [_P]),
     "vgpu_cu_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "vgpu_cu_reduce_final": (C.c_int, [_P, _P, _U64, _P]),

@@ -5,19 +5,26 @@
  *   - the 46-bit LCG x <- 5^13 x mod 2^46 is integer arithmetic (exact);
  *   - uniforms are x * 2^-46 (exact in binary64);
  *   - every floating-point operation below is an explicitly rounded IEEE
- *     binary64 op: on the device the __d*_rn intrinsics (never contracted
- *     into FMA), on the host plain operators compiled with
- *     -ffp-contract=off on SSE2 (x86-64 default, no x87);
+ *     binary64 op: on the device the __d*_rn / __fma_rn intrinsics (never
+ *     contracted), on the host plain operators compiled with
+ *     -ffp-contract=off on SSE2 (x86-64 default, no x87) and C99 fma(),
+ *     which is correctly rounded like the device's DFMA;
  *   - log() is ONE implementation compiled for both sides (below), because
  *     glibc and libdevice may differ by an ulp; sqrt and division are
  *     correctly rounded on both sides.
  *
- * vgpu_ep_log is a restatement of the classic fdlibm __ieee754_log
- * algorithm (Sun Microsystems, freely redistributable; < 1 ulp): reduce
- * x = 2^k (1+f) with sqrt(2)/2 < 1+f < sqrt(2), s = f/(2+f), approximate
- * log(1+f) = f - s (f - R(s^2)) with a degree-7 minimax polynomial in s^2,
- * and add k ln2 split into hi/lo parts. Only finite positive normal
- * arguments reach it from EP (0 < t <= 1).
+ * vgpu_ep_log is a table-driven binary64 logarithm written for this
+ * contract (no division, no branches, FMA where it helps): reduce
+ * x = 2^k z with z in [0.6875, 1.375) by integer arithmetic on the bits,
+ * look up c ~ z (256 intervals) with invc = RN(1/c) and -ln(invc) as hi+lo
+ * (ep_log_table.h, scripts/gen_ep_log_table.py, 60-digit decimal), form
+ * r = fma(z, invc, -1) (|r| < 2^-8), and return
+ *   k ln2 + logc + log1p(r),  log1p(r) = r + r^2 (-1/2 + r/3 - ... + r^5/7)
+ * with k ln2_hi + logc_hi summed exactly (Fast2Sum). The two intervals next
+ * to 1 use c = 1, so log stays accurate to the last bits as x -> 1.
+ * tests/test_oracle.py measures it against glibc log (max error <= 1 ulp,
+ * > 99% correctly rounded). Only positive normal arguments reach it from
+ * EP (2^-90 <= t <= 1: LCG states are odd, so x1, x2 != 0).
  *
  * The EP per-pair step follows NPB 3.x EP (ep.f, main loop): x1 = 2u1-1,
  * x2 = 2u2-1, t1 = x1^2 + x2^2; if t1 <= 1: t2 = sqrt(-2 log(t1) / t1),
@@ -35,7 +42,10 @@
 #define EP_FN static inline
 #endif
 
+#include "ep_log_table.h"
+
 #if defined(__CUDA_ARCH__)
+#define EP_FMA(a, b, c) __fma_rn((a), (b), (c))
 #define EP_MUL(a, b) __dmul_rn((a), (b))
 #define EP_ADD(a, b) __dadd_rn((a), (b))
 #define EP_SUB(a, b) __dsub_rn((a), (b))
@@ -43,6 +53,7 @@
 #define EP_SQRT(a) __dsqrt_rn(a)
 #else
 #include <math.h>
+#define EP_FMA(a, b, c) fma((a), (b), (c)) /* C99: correctly rounded */
 #define EP_MUL(a, b) ((a) * (b))
 #define EP_ADD(a, b) ((a) + (b))
 #define EP_SUB(a, b) ((a) - (b))
@@ -91,70 +102,47 @@ EP_FN double ep_uniform(uint64_t x) {
     return EP_MUL((double)(int64_t)x, ep_from_bits(0x3D10000000000000ull)); /* 2^-46 */
 }
 
-EP_FN double vgpu_ep_log(double x) {
-    /* fdlibm constants, given by bit pattern */
-    const double ln2_hi = ep_from_bits(0x3FE62E42FEE00000ull);
-    const double ln2_lo = ep_from_bits(0x3DEA39EF35793C76ull);
-    const double Lg1 = ep_from_bits(0x3FE5555555555593ull);
-    const double Lg2 = ep_from_bits(0x3FD999999997FA04ull);
-    const double Lg3 = ep_from_bits(0x3FD2492494229359ull);
-    const double Lg4 = ep_from_bits(0x3FCC71C51D8E78AFull);
-    const double Lg5 = ep_from_bits(0x3FC7466496CB03DEull);
-    const double Lg6 = ep_from_bits(0x3FC39A09D078C69Full);
-    const double Lg7 = ep_from_bits(0x3FC2F112DF3E5244ull);
-    const double two54 = ep_from_bits(0x4350000000000000ull);
+/* Argument reduction: x = 2^k z, z in [0.6875, 1.375), table index i. */
+EP_FN double ep_log_reduce(double x, int* i, double* kd) {
+    const uint64_t ix = ep_to_bits(x);
+    const uint64_t tmp = ix - VGPU_EP_LOG_OFF;
+    *i = (int)((tmp >> (52 - VGPU_EP_LOG_BITS)) & ((1u << VGPU_EP_LOG_BITS) - 1u));
+    *kd = (double)((int64_t)tmp >> 52);
+    return ep_from_bits(ix - (tmp & 0xFFF0000000000000ull));
+}
 
-    uint64_t bits = ep_to_bits(x);
-    int32_t hx = (int32_t)(bits >> 32);
-    const uint32_t lx = (uint32_t)bits;
-    int32_t k = 0;
-    if (hx < 0x00100000) {
-        if (((hx & 0x7fffffff) | (int32_t)lx) == 0) return ep_from_bits(0xFFF0000000000000ull);
-        if (hx < 0) return ep_from_bits(0x7FF8000000000000ull);
-        k -= 54;
-        x = EP_MUL(x, two54);
-        bits = ep_to_bits(x);
-        hx = (int32_t)(bits >> 32);
-    }
-    if (hx >= 0x7ff00000) return EP_ADD(x, x);
-    k += (hx >> 20) - 1023;
-    hx &= 0x000fffff;
-    const int32_t i0 = (hx + 0x95f64) & 0x100000;
-    /* normalize x or x/2 into [sqrt(2)/2, sqrt(2)) */
-    bits = ((uint64_t)(uint32_t)(hx | (i0 ^ 0x3ff00000)) << 32) | (bits & 0xffffffffull);
-    x = ep_from_bits(bits);
-    k += (i0 >> 20);
-    const double f = EP_SUB(x, 1.0);
-    const double dk = (double)k;
-    if ((0x000fffff & (2 + hx)) < 3) { /* |f| < 2^-20 */
-        if (f == 0.0) {
-            if (k == 0) return 0.0;
-            return EP_ADD(EP_MUL(dk, ln2_hi), EP_MUL(dk, ln2_lo));
-        }
-        const double R = EP_MUL(EP_MUL(f, f), EP_SUB(0.5, EP_MUL(0.33333333333333333, f)));
-        if (k == 0) return EP_SUB(f, R);
-        return EP_SUB(EP_MUL(dk, ln2_hi), EP_SUB(EP_SUB(R, EP_MUL(dk, ln2_lo)), f));
-    }
-    const double s = EP_DIV(f, EP_ADD(2.0, f));
-    const double z = EP_MUL(s, s);
-    int32_t i = hx - 0x6147a;
-    const double w = EP_MUL(z, z);
-    const int32_t j = 0x6b851 - hx;
-    const double t1 = EP_MUL(w, EP_ADD(Lg2, EP_MUL(w, EP_ADD(Lg4, EP_MUL(w, Lg6)))));
-    const double t2 =
-        EP_MUL(z, EP_ADD(Lg1, EP_MUL(w, EP_ADD(Lg3, EP_MUL(w, EP_ADD(Lg5, EP_MUL(w, Lg7)))))));
-    i |= j;
-    const double R = EP_ADD(t2, t1);
-    if (i > 0) {
-        const double hfsq = EP_MUL(EP_MUL(0.5, f), f);
-        if (k == 0) return EP_SUB(f, EP_SUB(hfsq, EP_MUL(s, EP_ADD(hfsq, R))));
-        return EP_SUB(EP_MUL(dk, ln2_hi),
-                      EP_SUB(EP_SUB(hfsq, EP_ADD(EP_MUL(s, EP_ADD(hfsq, R)), EP_MUL(dk, ln2_lo))),
-                             f));
-    }
-    if (k == 0) return EP_SUB(f, EP_MUL(s, EP_SUB(f, R)));
-    return EP_SUB(EP_MUL(dk, ln2_hi),
-                  EP_SUB(EP_SUB(EP_MUL(s, EP_SUB(f, R)), EP_MUL(dk, ln2_lo)), f));
+/* log(2^k z) from the reduced argument and its table entry. */
+EP_FN double ep_log_finish(double z, double kd, double invc, double logc_hi, double logc_lo) {
+    const double ln2_hi = ep_from_bits(0x3FE62E42FEE00000ull); /* 21 trailing zeros: k ln2_hi exact */
+    const double ln2_lo = ep_from_bits(0x3DEA39EF35793C76ull);
+    const double c3 = ep_from_bits(0x3FD5555555555555ull); /*  1/3 */
+    const double c5 = ep_from_bits(0x3FC999999999999Aull); /*  1/5 */
+    const double c6 = ep_from_bits(0xBFC5555555555555ull); /* -1/6 */
+    const double c7 = ep_from_bits(0x3FC2492492492492ull); /*  1/7 */
+    const double r = EP_FMA(z, invc, -1.0);
+    /* k ln2_hi + logc_hi = s + e exactly: |k ln2_hi| >= 0.69 > |logc_hi|, or k = 0 */
+    const double a = EP_MUL(kd, ln2_hi);
+    const double s = EP_ADD(a, logc_hi);
+    const double e = EP_SUB(logc_hi, EP_SUB(s, a));
+    const double r2 = EP_MUL(r, r);
+    double p = EP_FMA(c7, r, c6);
+    p = EP_FMA(p, r, c5);
+    p = EP_FMA(p, r, -0.25);
+    p = EP_FMA(p, r, c3);
+    p = EP_FMA(p, r, -0.5);
+    double lo = EP_FMA(kd, ln2_lo, logc_lo);
+    lo = EP_ADD(lo, e);
+    lo = EP_FMA(r2, p, lo);
+    return EP_ADD(s, EP_ADD(r, lo));
+}
+
+#if !defined(__CUDA_ARCH__) /* host side: the device keeps the table in shared memory */
+EP_FN double vgpu_ep_log(double x) {
+    int i;
+    double kd;
+    const double z = ep_log_reduce(x, &i, &kd);
+    return ep_log_finish(z, kd, ep_from_bits(vgpu_ep_log_tab[i][0]),
+                         ep_from_bits(vgpu_ep_log_tab[i][1]), ep_from_bits(vgpu_ep_log_tab[i][2]));
 }
 
 /* One EP pair from two consecutive LCG states. Returns 1 when accepted and
@@ -174,6 +162,8 @@ EP_FN int vgpu_ep_pair(uint64_t xa, uint64_t xb, double* gx, double* gy, int* an
     *annulus = (int)(a3 > a4 ? a3 : a4);
     return 1;
 }
+
+#endif /* !__CUDA_ARCH__ */
 
 /* LCG state that precedes the first uniform of `batch` (NPB: t1 = s*an^kk,
  * an = a^(2*2^mk)); uniform i (1-based) of the batch is a^i times it. */

@@ -20,8 +20,9 @@ int main(int argc, char** argv) {
     const std::uint32_t kernels[] = {VGPU_CU_K_VADD, VGPU_CU_K_EP, VGPU_CU_K_BS, VGPU_CU_K_SGEMM};
     for (int k = 0; k < 4; ++k) {
         if (only != "all" && only != kinds[k]) continue;
-        for (std::uint32_t tasks : {1u, 4u, 16u}) {
-            if (only_tasks && tasks != only_tasks) continue;
+        const std::vector<std::uint32_t> counts =
+            only_tasks ? std::vector<std::uint32_t>{only_tasks} : std::vector<std::uint32_t>{1, 4, 16};
+        for (std::uint32_t tasks : counts) {
             std::vector<vgpu::wl::Job> jobs;
             std::vector<const void*> ptrs;
             std::vector<std::uint64_t> sizes;

@@ -83,6 +83,7 @@ int main(int argc, char** argv) {
             else if (a == "--device") device = std::stoi(val());
             else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(val());
             else if (a == "--ep-m") sizes.ep_m = std::stoul(val());
+            else if (a == "--ep-batches") sizes.ep_batches = std::stoull(val());
             else if (a == "--bs-n") sizes.bs_n = std::stoull(val());
             else if (a == "--mm-n") sizes.mm_n = std::stoul(val());
             else throw std::invalid_argument("unknown argument " + a);

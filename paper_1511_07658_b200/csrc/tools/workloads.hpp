@@ -32,6 +32,7 @@ enum class Kind { VecAdd, Ep, Bs, Mm };
 struct Sizes {
     std::uint64_t vecadd_n = 1ull << 20;
     std::uint32_t ep_m = 28;
+    std::uint64_t ep_batches = 0;  // batches of the whole run's problem; 0 = 2^(ep_m-16)
     std::uint64_t bs_n = 4ull << 20;
     std::uint32_t mm_n = 2048;
 };
@@ -105,7 +106,7 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
                 rank = worker / 4;
                 count = (workers + 2) / 4;  // workers w with w % 4 == 1
             }
-            const std::uint64_t total = 1ull << (sz.ep_m - 16);
+            const std::uint64_t total = sz.ep_batches ? sz.ep_batches : 1ull << (sz.ep_m - 16);
             const std::uint64_t per = total / count, extra = total % count;
             vgpu_ep_params p{};
             p.m = sz.ep_m;

@@ -326,6 +326,13 @@ def resident_bench(payload_id: str, inputs: Sequence[bytes], sets: int, warmup: 
     return {k: getattr(r, k) for k, _ in N.ResidentResult._fields_}
 
 
+def peak_probe(kind: str, device: int = 0) -> float:
+    """Measured FMA pipe peak in TFLOP/s ("fp64" or "fp32") on `device`."""
+    t = C.c_double()
+    _cu_check(_libs().cuda.vgpu_cu_peak_probe(device, {"fp64": 0, "fp32": 1}[kind], C.byref(t)))
+    return t.value
+
+
 def model_simulate(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int = 1,
                    sms: int = 14, max_kernels: int = 16, slots: int = 8) -> int:
     return _libs().host.vgpu_model_simulate(style, n, t_in, t_comp, t_out, grid, sms,

@@ -28,8 +28,43 @@ CONFIG_NAME = {
 class Sizes:
     vecadd_n: int = 1 << 20
     ep_m: int = 28
+    ep_batches: int = 0  # batches of the whole run's EP problem; 0 = the class, 2^(ep_m-16)
+
+    @staticmethod
+    def for_world(world: int) -> "Sizes":
+        """Weak scaling: every GPU keeps one class-A-sized slice (4096 NPB
+        batches); the run's problem is the first 4096*world batches of the
+        EP sequence with m = 28 + ceil(log2 world) (m = 30, class B, at 4
+        GPUs). Rank 0's slice is always exactly class A."""
+        s = Sizes()
+        if world > 1:
+            s.ep_m = 28 + (world - 1).bit_length()
+            s.ep_batches = 4096 * world
+        return s
+
+    def size_args(self) -> list:
+        return ["--vecadd-n", str(self.vecadd_n), "--ep-m", str(self.ep_m),
+                "--ep-batches", str(self.ep_batches), "--bs-n", str(self.bs_n),
+                "--mm-n", str(self.mm_n)]
     bs_n: int = 4 << 20
     mm_n: int = 2048
+
+
+# NAS EP class A (m = 28): accepted Gaussian pairs (NPB ep.f; pinned by
+# tests/golden/ep_oracle.json and the oracle)
+EP_CLASS_A_ACCEPTED = 210832767
+EP_ACCEPT_RATE = EP_CLASS_A_ACCEPTED / float(1 << 28)
+
+
+def ep_fp64_ops(pairs: float, accepted: float) -> float:
+    """Algorithmic IEEE binary64 operation count of the restated NPB EP step
+    (paper_1511_07658_b200/csrc/common/ep_math.h), each +,-,*,/,sqrt = 1:
+      every pair      x1 = 2u1 - 1, x2 = 2u2 - 1 (4), t = x1^2 + x2^2 (3)  -> 7
+      accepted pair   log t: vgpu_ep_log, 16 (r = fma, Fast2Sum 4, r^2, Horner 5,
+                      low part 3, final 2); -2 log t, / t, sqrt (3);
+                      x1 t2, x2 t2 (2); sx, sy (2)                          -> 23
+    The LCG and the log's argument reduction are integer work, not counted."""
+    return 7.0 * pairs + 23.0 * accepted
 
 
 def kind_of(workload: str, worker: int) -> str:
@@ -38,7 +73,7 @@ def kind_of(workload: str, worker: int) -> str:
 
 def ep_slice(workload: str, worker: int, workers: int, sz: Sizes):
     rank, count = (worker // 4, (workers + 2) // 4) if workload == "mixed" else (worker, workers)
-    total = 1 << (sz.ep_m - 16)
+    total = sz.ep_batches or 1 << (sz.ep_m - 16)
     per, extra = divmod(total, count)
     first = rank * per + min(rank, extra)
     return first, per + (1 if rank < extra else 0)

@@ -73,3 +73,39 @@ def test_two_rank_final_reduce_is_deterministic_and_exact():
     v = R.ep_verdict(a, 24)
     assert v["verified"], v
     assert a[0] == 4.0  # jobs folded
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_weak_scaling_ep_slices(world):
+    """bench.py's N-GPU EP problem: every GPU keeps 4096 batches (one class A)
+    split over its 8 processes, the GPUs tile the first 4096*world batches of
+    the EP sequence, and rank 0's processes cover exactly class A."""
+    from paper_1511_07658_b200 import workloads as W
+    sz = W.Sizes.for_world(world)
+    assert (1 << (sz.ep_m - 16)) >= 4096 * world
+    procs = 8
+    cover = []
+    for g in range(world):
+        mine = [W.ep_slice("ep", g * procs + i, procs * world, sz) for i in range(procs)]
+        assert sum(c for _, c in mine) == 4096
+        assert mine[0][0] == 4096 * g
+        cover += mine
+    nxt = 0
+    for first, count in cover:
+        assert first == nxt and count == 512
+        nxt += count
+    # mixed: 4 EP workers per GPU (worker % 4 == 1), same tiling
+    mixed = [W.ep_slice("mixed", w, 16 * world, sz) for w in range(16 * world) if w % 4 == 1]
+    assert [f for f, _ in mixed] == [1024 * i for i in range(4 * world)]
+
+
+def test_ep_verdict_rank0_class_a():
+    a_sx, a_sy = R.NPB_EP_VERIFY[28]
+    rank0 = R.empty_record()
+    rank0[11], rank0[12], rank0[14] = a_sx, a_sy, 4096
+    folded = R.empty_record()
+    folded[11], folded[12], folded[14] = 2 * a_sx, 2 * a_sy, 8192
+    v = R.ep_verdict(folded, 29, 8192, rank0)
+    assert v["rank0_class_a_verified"] and v["verified"] and "npb_rel_err" not in v
+    rank0[11] *= 1.0 + 1e-6
+    assert not R.ep_verdict(folded, 29, 8192, rank0)["verified"]

@@ -106,3 +106,35 @@ def test_sgemm_oracle_exact_on_small_integers():
     A = rng.integers(-4, 5, (17, 17)).astype(np.float32)
     B = rng.integers(-4, 5, (17, 17)).astype(np.float32)
     assert np.array_equal(oracle.sgemm(A, B), A.astype(np.float64) @ B.astype(np.float64))
+
+
+def test_ep_log_accuracy_against_exact_logarithm():
+    """vgpu_ep_log (the table-driven log shared by the EP kernel and the
+    oracle) against ln computed to 40 digits: at most 1 ulp everywhere EP
+    evaluates it (t in [2^-90, 1]), correctly rounded in > 99% of cases,
+    and exact relative accuracy as t -> 1 (the c = 1 intervals)."""
+    import math
+    from decimal import Decimal, getcontext
+
+    getcontext().prec = 40
+    rng = np.random.default_rng(2024)
+    xs = np.concatenate([
+        rng.uniform(0.0, 1.0, 2000),                               # EP's t is uniform on (0, 1]
+        1.0 - rng.uniform(0.0, 2.0 ** -8, 600),                    # just below 1
+        1.0 - 2.0 ** -rng.uniform(9, 52, 600),                     # 1 - 2^-k
+        2.0 ** -rng.uniform(1, 90, 600),                           # down to EP's smallest t
+        np.array([1.0, 0.5, 0.6875, 0.75, 2.0 ** -90, np.nextafter(1.0, 0.0)]),
+    ])
+    xs = xs[xs > 0]
+    got = oracle.ep_log(xs)
+    errs = []
+    for x, y in zip(xs.tolist(), got.tolist()):
+        exact = Decimal(x).ln()
+        if exact == 0:
+            assert y == 0.0
+            continue
+        ulp = math.ulp(float(exact))
+        errs.append(abs((Decimal(y) - exact) / Decimal(ulp)))
+    errs = np.array([float(e) for e in errs])
+    assert errs.max() <= 1.0, errs.max()
+    assert np.mean(errs <= 0.5) > 0.99, np.mean(errs <= 0.5)
