@@ -14,9 +14,9 @@
  * Conventions: plain C types only; integer status returns (0 = ok, codes 3/5/8
  * deliberately equal vgpu::ErrCode Size/Payload/Internal); no C++ exception
  * crosses the ABI; host pointers handed to submit stay valid until poll()
- * reports the task. submit is called from the GVM dispatcher thread only,
- * poll from the dispatcher too; the notify callback fires on a CUDA-owned
- * thread and must only signal.
+ * reports the task. upload/submit/poll/wait are called from the GVM
+ * dispatcher thread only; completion is detected by event queries in poll()
+ * (no CUDA host callbacks).
  */
 #ifndef VGPU_CUDA_H
 #define VGPU_CUDA_H
@@ -157,14 +157,10 @@ int vgpu_cu_poll(vgpu_cu_dev* dev, vgpu_cu_done* out, uint32_t cap,
                  uint32_t* n_out);
 /* Operations (tasks and uploads) submitted but not yet reported by poll().
  * poll() detects completion by querying each one's final CUDA event (no
- * callback latency), so a dispatcher with work pending polls it in a hot
- * loop; the notify callback still fires for a sleeping dispatcher. */
+ * callback latency), so a dispatcher with work pending polls it. */
 int vgpu_cu_pending(vgpu_cu_dev* dev);
-/* Block until at least one task finished or timeout_us passed. */
+/* Wait (polling events) until an op completed or timeout_us passed. */
 int vgpu_cu_wait(vgpu_cu_dev* dev, int64_t timeout_us);
-/* Called (from a CUDA host-callback thread) whenever a task finishes. */
-void vgpu_cu_set_notify(vgpu_cu_dev* dev, void (*fn)(void* ctx, uint32_t slot),
-                        void* ctx);
 int vgpu_cu_get_stats(vgpu_cu_dev* dev, vgpu_cu_stats* out);
 
 /* Synchronous single task in the CALLING process's own context, pageable

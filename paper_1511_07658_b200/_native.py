@@ -111,7 +111,6 @@ CUDA_API = {
     "vgpu_cu_poll": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_cu_wait": (C.c_int, [_P, _I64]),
     "vgpu_cu_pending": (C.c_int, [_P]),
-    "vgpu_cu_set_notify": (None, [_P, _P, _P]),
     "vgpu_cu_get_stats": (C.c_int, [_P, C.POINTER(CuStats)]),
     "vgpu_cu_execute": (C.c_int, [C.c_int, _U32, C.c_float, _P, _U64, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_execute_launches": (_U64, []),

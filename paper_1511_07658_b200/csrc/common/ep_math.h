@@ -111,37 +111,46 @@ EP_FN double ep_log_reduce(double x, int* i, double* kd) {
     return ep_from_bits(ix - (tmp & 0xFFF0000000000000ull));
 }
 
+/* Constants of ep_log_finish, by value (hex literals = the exact binary64
+ * bits). The kernel keeps them in __constant__ memory so the DFMAs read
+ * them as constant-bank operands. */
+typedef struct vgpu_ep_log_consts {
+    double ln2_hi; /* 21 trailing zero bits: k ln2_hi is exact for |k| < 2^21 */
+    double ln2_lo;
+    double c3, c5, c6, c7; /* 1/3, 1/5, -1/6, 1/7 (c2 = -1/2, c4 = -1/4 are exact) */
+} vgpu_ep_log_consts;
+#define VGPU_EP_LOG_CONSTS_INIT                                                       \
+    {0x1.62e42feep-1, 0x1.a39ef35793c76p-33, 0x1.5555555555555p-2, 0x1.999999999999ap-3, \
+     -0x1.5555555555555p-3, 0x1.2492492492492p-3}
+
 /* log(2^k z) from the reduced argument and its table entry. */
-EP_FN double ep_log_finish(double z, double kd, double invc, double logc_hi, double logc_lo) {
-    const double ln2_hi = ep_from_bits(0x3FE62E42FEE00000ull); /* 21 trailing zeros: k ln2_hi exact */
-    const double ln2_lo = ep_from_bits(0x3DEA39EF35793C76ull);
-    const double c3 = ep_from_bits(0x3FD5555555555555ull); /*  1/3 */
-    const double c5 = ep_from_bits(0x3FC999999999999Aull); /*  1/5 */
-    const double c6 = ep_from_bits(0xBFC5555555555555ull); /* -1/6 */
-    const double c7 = ep_from_bits(0x3FC2492492492492ull); /*  1/7 */
+EP_FN double ep_log_finish(const vgpu_ep_log_consts* K, double z, double kd, double invc,
+                           double logc_hi, double logc_lo) {
     const double r = EP_FMA(z, invc, -1.0);
     /* k ln2_hi + logc_hi = s + e exactly: |k ln2_hi| >= 0.69 > |logc_hi|, or k = 0 */
-    const double a = EP_MUL(kd, ln2_hi);
+    const double a = EP_MUL(kd, K->ln2_hi);
     const double s = EP_ADD(a, logc_hi);
     const double e = EP_SUB(logc_hi, EP_SUB(s, a));
     const double r2 = EP_MUL(r, r);
-    double p = EP_FMA(c7, r, c6);
-    p = EP_FMA(p, r, c5);
+    double p = EP_FMA(K->c7, r, K->c6);
+    p = EP_FMA(p, r, K->c5);
     p = EP_FMA(p, r, -0.25);
-    p = EP_FMA(p, r, c3);
+    p = EP_FMA(p, r, K->c3);
     p = EP_FMA(p, r, -0.5);
-    double lo = EP_FMA(kd, ln2_lo, logc_lo);
+    double lo = EP_FMA(kd, K->ln2_lo, logc_lo);
     lo = EP_ADD(lo, e);
     lo = EP_FMA(r2, p, lo);
     return EP_ADD(s, EP_ADD(r, lo));
 }
 
 #if !defined(__CUDA_ARCH__) /* host side: the device keeps the table in shared memory */
+static const vgpu_ep_log_consts vgpu_ep_log_k = VGPU_EP_LOG_CONSTS_INIT;
+
 EP_FN double vgpu_ep_log(double x) {
     int i;
     double kd;
     const double z = ep_log_reduce(x, &i, &kd);
-    return ep_log_finish(z, kd, ep_from_bits(vgpu_ep_log_tab[i][0]),
+    return ep_log_finish(&vgpu_ep_log_k, z, kd, ep_from_bits(vgpu_ep_log_tab[i][0]),
                          ep_from_bits(vgpu_ep_log_tab[i][1]), ep_from_bits(vgpu_ep_log_tab[i][2]));
 }
 

@@ -15,14 +15,16 @@
 //     parameter space; the lead stream waits on the other tasks' H2D events,
 //     the other streams wait on the launch's end event), then every D2H;
 //     PS-2: per-stream H2D -> kernel -> D2H triples;
-//   * completion: a host function after each task's D2H queues the slot and
-//     rings the daemon's notify callback; poll() turns CUDA events into
+//   * completion: poll() (GVM dispatcher thread) queries each armed op's
+//     final CUDA event — no host callbacks, whose 100-300 us latency on B200
+//     hosts also held the slot's stream — and turns the events into
 //     per-stage times (the paper's t_in / t_comp / t_out) and batch spans.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <thread>
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
@@ -417,8 +419,7 @@ NcclApi& nccl() {
 enum { kEvH2d0, kEvH2d1, kEvC0, kEvC1, kEvD2h0, kEvD2h1, kEvCount };
 
 // One stream operation in flight: a task (H2D -> kernel -> D2H) or an eager
-// upload (H2D at SND time). The host callback that closes it hands the
-// record to poll() through the device's finished list.
+// upload (H2D at SND time). poll() reports it once its final event completed.
 struct Op {
     vgpu_cu_dev* dev = nullptr;
     std::uint32_t slot = 0;
@@ -428,10 +429,6 @@ struct Op {
     cudaEvent_t ev[kEvCount] = {};
     bool has_h2d = false, has_comp = false;
     cudaEvent_t comp0 = nullptr, comp1 = nullptr;
-    // completion is reported ONCE, by whichever sees it first: poll()'s
-    // event query (fast path, dispatcher thread) or the host callback; the
-    // record is released only after its callback ran (events stay owned)
-    bool reported = false;
     cudaEvent_t last() const { return kind == VGPU_CU_DONE_UPLOAD ? ev[kEvH2d1] : ev[kEvD2h1]; }
 };
 
@@ -466,13 +463,9 @@ struct vgpu_cu_dev {
     std::uint64_t next_batch = 1;
     std::vector<void*> pinned;
 
-    std::mutex cb_mu;
-    std::condition_variable cb_cv;
-    std::vector<Op*> finished;        // callbacks ran (callback thread -> poll)
-    std::vector<Op*> outstanding;     // armed, not yet reported (dispatcher thread)
-    std::mutex notify_mu;
-    void (*notify_fn)(void*, std::uint32_t) = nullptr;
-    void* notify_ctx = nullptr;
+    // armed ops in submission order, not yet reported; owned by the
+    // dispatcher thread (submit/upload/poll are only called from it)
+    std::vector<Op*> outstanding;
 
     std::atomic<std::uint64_t> launches{0}, tasks{0}, h2d_bytes{0}, d2h_bytes{0}, nbatches{0};
 
@@ -515,24 +508,6 @@ struct vgpu_cu_dev {
 
 namespace {
 
-void CUDART_CB op_done(void* p) {
-    auto* op = static_cast<Op*>(p);
-    vgpu_cu_dev* d = op->dev;
-    const std::uint32_t slot = op->slot;
-    {
-        std::lock_guard lk(d->cb_mu);
-        d->finished.push_back(op);
-    }
-    d->cb_cv.notify_all();
-    void (*fn)(void*, std::uint32_t) = nullptr;
-    void* ctx = nullptr;
-    {
-        std::lock_guard lk(d->notify_mu);
-        fn = d->notify_fn;
-        ctx = d->notify_ctx;
-    }
-    if (fn) fn(ctx, slot);
-}
 
 float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.0f;
@@ -721,11 +696,8 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
     for (auto& s : d->slots)
         if (s.stream) cudaStreamSynchronize(s.stream);
     if (d->anchor_stream) cudaStreamSynchronize(d->anchor_stream);
-    {
-        std::lock_guard lk(d->cb_mu);
-        for (Op* op : d->finished) d->release_op(op);
-        d->finished.clear();
-    }
+    for (Op* op : d->outstanding) d->release_op(op);
+    d->outstanding.clear();
     for (auto& s : d->slots) {
         if (s.reg_base) cudaHostUnregister(s.reg_base);
         if (s.stream) cudaStreamDestroy(s.stream);
@@ -773,12 +745,6 @@ void vgpu_cu_free_pinned(vgpu_cu_dev* d, void* p) {
     cudaFreeHost(p);
 }
 
-void vgpu_cu_set_notify(vgpu_cu_dev* d, void (*fn)(void*, std::uint32_t), void* ctx) {
-    if (!d) return;
-    std::lock_guard lk(d->notify_mu);
-    d->notify_fn = fn;
-    d->notify_ctx = ctx;
-}
 
 int vgpu_cu_get_stats(vgpu_cu_dev* d, vgpu_cu_stats* out) {
     if (!d || !out) return VGPU_CU_EINVAL;
@@ -812,7 +778,6 @@ int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::ui
     if (e == cudaSuccess && bytes)
         e = cudaMemcpyAsync(s.d_in, h_in, bytes, cudaMemcpyHostToDevice, s.stream);
     if (e == cudaSuccess) e = cudaEventRecord(op->ev[kEvH2d1], s.stream);
-    if (e == cudaSuccess) e = cudaLaunchHostFunc(s.stream, op_done, op);
     if (e != cudaSuccess) {
         cudaStreamSynchronize(s.stream);
         d->release_op(op);
@@ -915,10 +880,9 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         if (err == cudaSuccess && bytes)
             err = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
         if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvD2h1], s.stream);
-        if (err == cudaSuccess) err = cudaLaunchHostFunc(s.stream, op_done, op);
         if (err == cudaSuccess) {
             d->outstanding.push_back(op);
-            ops[i] = nullptr;  // owned by the callback now
+            ops[i] = nullptr;  // owned by outstanding now
             ++s.ops_in_flight;
             s.task_busy = true;
         }
@@ -1022,7 +986,6 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
     r.kind = op->kind;
     r.status = sticky == cudaSuccess ? VGPU_CU_OK : VGPU_CU_EINTERNAL;
     r.h2d_us = op->has_h2d ? 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvH2d1]) : 0.0f;
-    op->reported = true;
     if (s.ops_in_flight) --s.ops_in_flight;
     if (op->kind == VGPU_CU_DONE_UPLOAD) {
         r.span_us = r.h2d_us;
@@ -1052,39 +1015,20 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
 int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint32_t* n_out) {
     if (!d || !n_out || (!out && cap)) return VGPU_CU_EINVAL;
     *n_out = 0;
-    std::vector<Op*> called;
-    {
-        std::lock_guard lk(d->cb_mu);
-        called.swap(d->finished);
-    }
-    if (called.empty() && d->outstanding.empty()) return VGPU_CU_OK;
+    if (d->outstanding.empty()) return VGPU_CU_OK;
     cudaSetDevice(d->device);
     const cudaError_t sticky = cudaPeekAtLastError();
-    // 1. callbacks that ran: report if the fast path has not, then release
-    std::size_t k = 0;
-    for (; k < called.size(); ++k) {
-        Op* op = called[k];
-        if (!op->reported) {
-            if (*n_out == cap) break;
-            report_op(d, op, sticky, out[(*n_out)++]);
-            d->outstanding.erase(std::find(d->outstanding.begin(), d->outstanding.end(), op));
-        }
-        d->release_op(op);
-    }
-    if (k < called.size()) {  // out of room: hand the rest back
-        std::lock_guard lk(d->cb_mu);
-        d->finished.insert(d->finished.begin(), called.begin() + k, called.end());
-        return VGPU_CU_OK;
-    }
-    // 2. fast path: final events already complete (callback not yet run);
-    //    per slot only the oldest op can be done first (stream order)
+    // completion = the op's final event has completed (an event query: no
+    // CUDA host callback, whose latency on B200 hosts is 100-300 us and
+    // which would also hold the slot's stream until it ran)
     for (std::size_t i = 0; i < d->outstanding.size() && *n_out < cap;) {
         Op* op = d->outstanding[i];
         const cudaError_t q = cudaEventQuery(op->last());
         if (q == cudaSuccess) {
             report_op(d, op, sticky, out[(*n_out)++]);
             d->outstanding.erase(d->outstanding.begin() + i);
-            continue;  // released when its callback arrives
+            d->release_op(op);
+            continue;
         }
         if (q != cudaErrorNotReady) cudaGetLastError();
         ++i;
@@ -1099,10 +1043,16 @@ int vgpu_cu_pending(vgpu_cu_dev* d) {
 
 int vgpu_cu_wait(vgpu_cu_dev* d, std::int64_t timeout_us) {
     if (!d) return VGPU_CU_EINVAL;
-    std::unique_lock lk(d->cb_mu);
-    d->cb_cv.wait_for(lk, std::chrono::microseconds(timeout_us < 0 ? 0 : timeout_us),
-                      [&] { return !d->finished.empty(); });
-    return VGPU_CU_OK;
+    const auto deadline = std::chrono::steady_clock::now() +
+                          std::chrono::microseconds(timeout_us < 0 ? 0 : timeout_us);
+    cudaSetDevice(d->device);
+    for (;;) {
+        for (Op* op : d->outstanding)
+            if (cudaEventQuery(op->last()) != cudaErrorNotReady) return VGPU_CU_OK;
+        if (d->outstanding.empty() || std::chrono::steady_clock::now() >= deadline)
+            return VGPU_CU_OK;
+        std::this_thread::sleep_for(std::chrono::microseconds(5));
+    }
 }
 
 // ---- synchronous per-process execution (NativeVgpu, PayloadRegistry::execute) ----

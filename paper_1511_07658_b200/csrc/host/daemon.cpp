@@ -8,12 +8,15 @@
 // dispatcher thread (:413) and pacing completions with sleeps (:532-585),
 // the batch is enqueued on the device backend (include/vgpu_cuda.h) as
 // per-client H2D -> kernel -> D2H work on per-client CUDA streams in the
-// PS-1 / PS-2 order build_work_queue() prescribes, and completions come
-// back from CUDA host callbacks that wake the dispatcher.
+// PS-1 / PS-2 order build_work_queue() prescribes, and the dispatcher
+// detects completions itself by polling the ops' CUDA events (loop()).
 //
-// Threading: one dispatcher thread owns every session (the reference's
-// "handle() effects are serialized", SPEC.md gvm-daemon); the CUDA callback
-// thread only wakes it; metrics are guarded for external snapshots.
+// Threading: one dispatcher thread owns every session and the device handle
+// (the reference's "handle() effects are serialized", SPEC.md gvm-daemon);
+// metrics are guarded for external snapshots.
+#include <sched.h>
+#include <sys/prctl.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -197,17 +200,10 @@ struct GvmDaemon::Impl {
             close_device();
             throw;
         }
-        vgpu_cu_set_notify(
-            dev,
-            [](void* ctx, std::uint32_t) {
-                static_cast<Impl*>(ctx)->transport->wake();
-            },
-            this);
     }
 
     void close_device() {
         if (!dev) return;
-        vgpu_cu_set_notify(dev, nullptr, nullptr);
         for (void* p : staging) vgpu_cu_free_pinned(dev, p);
         staging.clear();
         vgpu_cu_close(dev);  // drains streams and unregisters regions
@@ -673,12 +669,14 @@ struct GvmDaemon::Impl {
 
     // ---- completions ----------------------------------------------------------
 
-    void drain_device() {
-        if (!dev) return;
+    bool drain_device() {
+        if (!dev) return false;
         vgpu_cu_done done[64];
+        bool any = false;
         for (;;) {
             std::uint32_t n = 0;
-            if (vgpu_cu_poll(dev, done, 64, &n) != VGPU_CU_OK || n == 0) return;
+            if (vgpu_cu_poll(dev, done, 64, &n) != VGPU_CU_OK || n == 0) return any;
+            any = true;
             for (std::uint32_t i = 0; i < n; ++i) complete(done[i]);
         }
     }
@@ -758,13 +756,17 @@ struct GvmDaemon::Impl {
 
     // ---- thread --------------------------------------------------------------
 
-    // Hot polling: while device work is pending, or within spin_us of the
-    // last inbound frame (a client's next verb usually follows within tens
-    // of microseconds), the dispatcher polls the socket set and the CUDA
-    // events without sleeping. Completions then cost an event query instead
-    // of a host-callback + eventfd + wake-up chain (~100+ us per verb on
-    // B200 hosts). Idle, it blocks in epoll as before. VGPU_GVM_SPIN_US
-    // (default 200; 0 disables) sets the window.
+    // Completion polling. While device work is pending the dispatcher does
+    // not sleep: it polls the sockets and the ops' CUDA events (yielding the
+    // core now and then), the GVM analogue of the spin-wait a CUDA context
+    // does in cudaStreamSynchronize. It also stays hot for spin_us after the
+    // last frame or completion, since a client's next verb usually follows
+    // within tens of microseconds. Idle, it blocks in epoll with the
+    // reference's 500 us tick. VGPU_GVM_SPIN_US (default 200) sets the
+    // window; VGPU_GVM_SPIN_US=0 also turns off spinning on pending work
+    // (then it naps kPendingNapUs between polls).
+    static constexpr Micros kPendingNapUs = 20;
+
     static Micros spin_window_us() {
         const char* e = std::getenv("VGPU_GVM_SPIN_US");
         return e ? std::strtoll(e, nullptr, 10) : 200;
@@ -773,14 +775,17 @@ struct GvmDaemon::Impl {
     void loop() {
         using std::chrono::microseconds;
         const Micros spin_us = spin_window_us();
-        auto last_frame = Clock::now();
+        prctl(PR_SET_TIMERSLACK, 1000UL, 0, 0, 0);  // naps of kPendingNapUs, not 50 us+
+        auto last_event = Clock::now();
+        std::uint64_t spins = 0;
         while (running.load(std::memory_order_relaxed)) {
             try {
-                drain_device();
+                if (drain_device()) last_event = Clock::now();
+                const bool pending = dev && vgpu_cu_pending(dev) > 0;
                 const bool hot = spin_us > 0 &&
-                                 ((dev && vgpu_cu_pending(dev) > 0) ||
-                                  us_between(last_frame, Clock::now()) < spin_us);
-                microseconds timeout{hot ? 0 : 500};
+                                 (pending || us_between(last_event, Clock::now()) < spin_us);
+                const Micros idle_wait = pending ? kPendingNapUs : 500;
+                microseconds timeout{hot ? 0 : idle_wait};
                 if (!batch.empty()) {
                     const Micros waited = us_between(batch_opened, Clock::now());
                     if (waited >= cfg.barrier_window) {
@@ -788,13 +793,14 @@ struct GvmDaemon::Impl {
                         continue;
                     }
                     timeout = microseconds{
-                        std::min<Micros>(cfg.barrier_window - waited, hot ? 0 : 500)};
+                        std::min<Micros>(cfg.barrier_window - waited, hot ? 0 : idle_wait)};
                 }
                 if (auto in = transport->recv(timeout)) {
                     handle(*in);
-                    last_frame = Clock::now();
+                    last_event = Clock::now();
                 } else if (hot) {
                     cpu_relax();
+                    if ((++spins & 63) == 0) sched_yield();
                 }
                 if (!batch.empty() &&
                     us_between(batch_opened, Clock::now()) >= cfg.barrier_window)
