@@ -21,7 +21,7 @@ CC       ?= gcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
 CXXFLAGS := -O2 -g -std=c++20 -fPIC -Wall -Wextra -pthread -Iinclude
-CFLAGS   := -O2 -g -fPIC -ffp-contract=off -std=c11 -Wall -Wextra
+CFLAGS   := -O2 -g -fPIC -ffp-contract=off -std=c11 -Wall -Wextra -Wno-unknown-pragmas
 
 HOST_SRC := $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJ := $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host/%.o,$(HOST_SRC))

@@ -265,6 +265,11 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
             rs = V.resident_bench(W.PAYLOAD[k], inputs, sets, warmup, steps, device=device,
                                   pdl=False)
             r["serial_kernel_ms_per_launch"] = rs["kernel_ms_per_launch"]
+        if k == "mm" and os.environ.get("VGPU_SGEMM") != "simt":
+            # the tcgen05 GEMM alone, for its tensor-core roofline
+            rm = V.resident_bench(W.PAYLOAD[k], inputs, sets, warmup, steps, device=device,
+                                  main_only=True)
+            r["main_kernel_ms_per_launch"] = rm["kernel_ms_per_launch"]
         legs[k] = r
         ms_step += r["ms_per_step"]
         launches += r["launches_per_step"] * steps
@@ -458,7 +463,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
     probed on this GPU now for fp64/fp32 (vgpu_cu_peak_probe)."""
     kernel_s = d["kernel_ms_per_launch"] * 1e-3
     bound = KIND_BOUND[kind]
-    tkey = "mm_tc" if kind == "mm" and os.environ.get("VGPU_SGEMM") == "tc" else kind
+    tkey = "mm_tc" if kind == "mm" and os.environ.get("VGPU_SGEMM") != "simt" else kind
     traffic, tsrc = ncu_traffic(tkey)
     r = {"bound": bound, "kernel": W.PAYLOAD[kind], "traffic": traffic,
          "traffic_source": tsrc, "kernel_us_per_launch": d["kernel_ms_per_launch"] * 1e3,
@@ -477,6 +482,27 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
             r["serial_frac"] = (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"]
                                 * 1e-3) / 1e9 / hbm["hbm_gbs"])
         return r
+    if bound == "fp32" and d.get("main_kernel_ms_per_launch"):
+        # 3xTF32 on tcgen05: three TF32 MMAs per FP32 product, against the
+        # dense TF32 peak (half the measured BF16 peak on Blackwell)
+        main_s = d["main_kernel_ms_per_launch"] * 1e-3
+        flops = d["algo_flops_per_launch"] * max(1, d["launches_per_step"])  # whole step
+        bf16 = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("bf16_tflops") \
+            if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else None
+        peak = (bf16 or 2250.0) / 2.0
+        achieved = 3.0 * flops / main_s / 1e12
+        r.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                  "frac": achieved / peak, "kernel_us_per_launch": main_s * 1e6,
+                  "fp32_equiv_tflops": flops / main_s / 1e12,
+                  "step_fp32_equiv_tflops": flops / (d["ms_per_step"] * 1e-3) / 1e12,
+                  "algo_flops_per_launch": 3.0 * flops,
+                  "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)"
+                                  if bf16 else "fallback: 2250 / 2 TFLOP/s nominal dense TF32"),
+                  "precision": "3xTF32 tcgen05 (chunked TMEM accumulation): rel. Frobenius "
+                               "4.8e-7 at 2048^2 on B200, bar 1e-5 vs binary64",
+                  "step_kernels": "tc_split_kernel (hi/lo split + B transpose) + tc_gemm_kernel; "
+                                  "achieved/kernel_us are the GEMM's"})
+        return r
     if bound == "fp32":
         peak = peaks.get("fp32")
         achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
@@ -484,9 +510,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                   "frac": achieved / peak if peak else None,
                   "algo_flops_per_launch": d["algo_flops_per_launch"],
                   "peak_source": "measured now: FFMA-chain probe (vgpu_cu_peak_probe)",
-                  "precision": ("3xTF32 tcgen05, rel. Frobenius <= 1e-5"
-                                if tkey == "mm_tc" else
-                                "FP32 SIMT, rel. Frobenius <= 1e-5 vs binary64")})
+                  "precision": "FP32 SIMT (VGPU_SGEMM=simt), rel. Frobenius <= 1e-5 vs binary64"})
         return r
     # EP: NPB's own unit beside the FP64 roofline
     pairs = d["algo_flops_per_launch"] / 2.0
@@ -521,7 +545,8 @@ def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
             r = roofline(W, dom, legs[dom], peaks,
                          W.EP_CLASS_A_ACCEPTED if kind == "ep" else None)
             out[kind] = {k: r.get(k) for k in ("bound", "kernel", "achieved", "peak", "unit",
-                                                 "frac", "traffic", "kernel_us_per_launch")}
+                                                 "frac", "traffic", "kernel_us_per_launch",
+                                                 "fp32_equiv_tflops") if k in r}
             out[kind]["tasks_per_launch"] = procs
         except Exception as e:  # noqa: BLE001 - reported in the line
             out[kind] = {"error": str(e)[:200]}

@@ -195,6 +195,8 @@ typedef struct vgpu_cu_resident_result {
  * (copied once from h_inputs[i], in_bytes[i]) sit in HBM; `sets` rotating
  * copies keep the working set above L2 between steps. */
 #define VGPU_CU_RESIDENT_NO_PDL 1u /* flags: serialize steps (per-launch duration) */
+#define VGPU_CU_RESIDENT_MAIN_ONLY 2u /* flags: SGEMM: time the tcgen05 GEMM alone
+                                         (split pre-pass done before the timed steps) */
 int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
                            uint32_t n_tasks, const void* const* h_inputs,
                            const uint64_t* in_bytes, uint32_t sets,

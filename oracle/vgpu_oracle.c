@@ -5,6 +5,7 @@
 #include "vgpu_oracle.h"
 
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../paper_1511_07658_b200/csrc/common/ep_math.h"
@@ -21,6 +22,43 @@ void vo_vector_scale(float* out, const float* in, float factor, size_t n) {
 
 /* ---- NAS EP (NPB 3.x ep.f main loop, fixed reduction order) ---------- */
 
+/* One NPB batch (2^mk pairs): counts into q, lane sums folded by the fixed
+ * stride-doubling tree into *bsx, *bsy. */
+static void ep_batch(uint64_t b, uint32_t mk, uint64_t per_lane, uint64_t lane_skip,
+                     uint64_t q[10], double* bsx, double* bsy) {
+    double lsx[VGPU_EP_LANES], lsy[VGPU_EP_LANES];
+    uint64_t lane_start = vgpu_ep_batch_seed(b, mk);
+    for (unsigned lane = 0; lane < VGPU_EP_LANES; ++lane) {
+        uint64_t v = lane_start;
+        double sx = 0.0, sy = 0.0;
+        for (uint64_t k = 0; k < per_lane; ++k) {
+            const uint64_t xa = ep_mulmod46(v, VGPU_EP_A);
+            const uint64_t xb = ep_mulmod46(xa, VGPU_EP_A);
+            v = xb;
+            double gx, gy;
+            int l;
+            if (vgpu_ep_pair(xa, xb, &gx, &gy, &l)) {
+                q[l] += 1;
+                sx = sx + gx;
+                sy = sy + gy;
+            }
+        }
+        lsx[lane] = sx;
+        lsy[lane] = sy;
+        lane_start = ep_mulmod46(lane_start, lane_skip);
+    }
+    for (unsigned stride = 1; stride < VGPU_EP_LANES; stride *= 2)
+        for (unsigned i = 0; i < VGPU_EP_LANES; i += 2 * stride) {
+            lsx[i] = lsx[i] + lsx[i + stride];
+            lsy[i] = lsy[i] + lsy[i + stride];
+        }
+    *bsx = lsx[0];
+    *bsy = lsy[0];
+}
+
+/* Batches are independent: with OpenMP (the reference arm, oracle/Makefile.ref)
+ * they run in parallel; the job sums are folded in batch order either way,
+ * so the result bits do not depend on the thread count. */
 int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     memset(r, 0, sizeof *r);
     if (p->mk < 8 || p->mk > 20 || p->m < p->mk || p->m > 40 || p->reserved != 0) return -1;
@@ -28,38 +66,26 @@ int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     if (p->first_batch > batches_total || p->n_batches > batches_total - p->first_batch) return -1;
     const uint64_t per_lane = (1ull << p->mk) / VGPU_EP_LANES;
     const uint64_t lane_skip = ep_powmod46(VGPU_EP_A, 2ull * per_lane);
-    double lsx[VGPU_EP_LANES], lsy[VGPU_EP_LANES];
-    double jsx = 0.0, jsy = 0.0;
-    for (uint64_t b = p->first_batch; b < p->first_batch + p->n_batches; ++b) {
-        const uint64_t seed = vgpu_ep_batch_seed(b, p->mk);
-        uint64_t lane_start = seed;
-        for (unsigned lane = 0; lane < VGPU_EP_LANES; ++lane) {
-            uint64_t v = lane_start;
-            double sx = 0.0, sy = 0.0;
-            for (uint64_t k = 0; k < per_lane; ++k) {
-                const uint64_t xa = ep_mulmod46(v, VGPU_EP_A);
-                const uint64_t xb = ep_mulmod46(xa, VGPU_EP_A);
-                v = xb;
-                double gx, gy;
-                int l;
-                if (vgpu_ep_pair(xa, xb, &gx, &gy, &l)) {
-                    r->q[l] += 1;
-                    sx = sx + gx;
-                    sy = sy + gy;
-                }
-            }
-            lsx[lane] = sx;
-            lsy[lane] = sy;
-            lane_start = ep_mulmod46(lane_start, lane_skip);
-        }
-        for (unsigned stride = 1; stride < VGPU_EP_LANES; stride *= 2)
-            for (unsigned i = 0; i < VGPU_EP_LANES; i += 2 * stride) {
-                lsx[i] = lsx[i] + lsx[i + stride];
-                lsy[i] = lsy[i] + lsy[i + stride];
-            }
-        jsx = jsx + lsx[0];
-        jsy = jsy + lsy[0];
+    const long long nb = (long long)p->n_batches;
+    double* bs = (double*)malloc(sizeof(double) * 2 * (size_t)(nb ? nb : 1));
+    uint64_t* bq = (uint64_t*)calloc(10 * (size_t)(nb ? nb : 1), sizeof(uint64_t));
+    if (!bs || !bq) {
+        free(bs);
+        free(bq);
+        return -1;
     }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long b = 0; b < nb; ++b)
+        ep_batch(p->first_batch + (uint64_t)b, p->mk, per_lane, lane_skip, bq + 10 * b,
+                 bs + 2 * b, bs + 2 * b + 1);
+    double jsx = 0.0, jsy = 0.0;
+    for (long long b = 0; b < nb; ++b) {
+        jsx = jsx + bs[2 * b];
+        jsy = jsy + bs[2 * b + 1];
+        for (int i = 0; i < 10; ++i) r->q[i] += bq[10 * b + i];
+    }
+    free(bs);
+    free(bq);
     r->sx = jsx;
     r->sy = jsy;
     for (int i = 0; i < 10; ++i) r->pairs += r->q[i];
@@ -99,6 +125,7 @@ static double cnd64(double d) {
 
 void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,
                       double R, double V, double* call, double* put) {
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < n; ++i) {
         const double s = S[i], x = X[i], t = T[i];
         const double sqrtT = sqrt(t);
@@ -115,6 +142,7 @@ void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,
 
 void vo_sgemm(const float* A, const float* B, size_t n, double* C) {
     for (size_t i = 0; i < n * n; ++i) C[i] = 0.0;
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < n; ++i)
         for (size_t k = 0; k < n; ++k) {
             const double a = A[i * n + k];

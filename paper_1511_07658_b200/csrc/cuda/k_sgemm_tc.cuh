@@ -3,16 +3,21 @@
 // Precision contract (stated tolerance): every fp32 operand x is
 // split into x_hi = x rounded to nearest TF32 and x_lo = x - x_hi (exact in
 // fp32, |x_lo| <= 2^-11 |x|; the MMA keeps its top 10 mantissa bits).
-// C = A_hi B_hi + A_hi B_lo + A_lo B_hi, accumulated in fp32 in TMEM. The
-// dropped A_lo B_lo term and the lo-part truncation are ~2^-22 per product;
-// checked at relative Frobenius <= 1e-5 against the binary64 oracle (the
-// SIMT kernel's bar). VGPU_SGEMM=simt selects the FP32 SIMT kernel.
+// C = A_hi B_hi + A_hi B_lo + A_lo B_hi. The dropped A_lo B_lo term and the
+// lo-part truncation are ~2^-22 per product. The tensor core's fp32
+// accumulation is NOT round-to-nearest (measured on B200: one TMEM
+// accumulator over K = 2048 gives 1.4e-5 relative Frobenius), so the K loop
+// is cut into chunks of chunk_kb * 32: each chunk accumulates into one of
+// two TMEM accumulators (ping-pong) and the CUDA cores add the finished
+// chunk into registers in IEEE fp32 while the tensor core runs the next
+// chunk. Checked at relative Frobenius <= 1e-5 against the binary64 oracle
+// (the SIMT kernel's bar). VGPU_SGEMM=simt selects the FP32 SIMT kernel.
 //
 // Pre-pass (tc_split_kernel): A -> A_hi, A_lo (row-major M x K = K-major);
 // B -> B_hi^T, B_lo^T (N x K, K-major) through a 32x32 shared-memory
 // transpose, so both UMMA operands are K-major.
 //
-// Main kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 128
+// Main kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 256
 // threads, tiles of every task of a batch in one launch (blockIdx.z = task):
 //   * 3-stage cp.async pipeline; each stage holds the four 128 x 32 fp32
 //     operand tiles (A_hi, A_lo, B_hi, B_lo; 16 KiB each) in the canonical
@@ -23,8 +28,10 @@
 //     tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=128, K=8) into a
 //     128-column fp32 TMEM accumulator, then tcgen05.commit arrives on the
 //     stage's mbarrier so the stage can be refilled;
-//   * epilogue: each warp drains its 32 TMEM lanes with
-//     tcgen05.ld.32x32b.x32 and stores its rows of C.
+//   * chunk drain: warp w reads TMEM lanes 32 (w % 4) .. +31 (= C rows),
+//     columns 64 (w / 4) .. +63 of the finished chunk's accumulator with
+//     tcgen05.ld.32x32b.x32 and adds them into 64 fp32 registers; the
+//     epilogue stores those registers.
 #pragma once
 
 #include <cstdint>
@@ -33,10 +40,11 @@ namespace vgk {
 
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;  // BK in fp32 elements (128 bytes)
 constexpr int kTcStages = 3;
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;
+constexpr int kTcTmemCols = 2 * kTcBN;                 // two accumulators (ping-pong)
 constexpr int kTcTileBytes = kTcBM * kTcBK * 4;       // 16 KiB
 constexpr int kTcStageBytes = 4 * kTcTileBytes;       // 64 KiB
-constexpr int kTcSmemBytes = kTcStages * kTcStageBytes + 1024 + 256;
+constexpr int kTcSmemBytes = kTcStages * kTcStageBytes + 1024 + 256;  // + barriers / TMEM slot
 constexpr int kMaxTcJobs = 64;
 
 struct TcJob {
@@ -54,6 +62,7 @@ struct TcJob {
 struct TcTable {
     TcJob job[kMaxTcJobs];
     std::uint32_t njobs;
+    std::uint32_t chunk_kb;  // k-blocks (of kTcBK) per TMEM accumulation chunk
 };
 
 // ---- pre-pass: split + transpose ---------------------------------------------
@@ -164,6 +173,24 @@ __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
 
 // ---- main kernel -----------------------------------------------------------------
 
+__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, float* out) {
+    std::uint32_t v[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[j] = __uint_as_float(v[j]);
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ TcTable table) {
     const TcJob& job = table.job[blockIdx.z];
     const int n = static_cast<int>(job.n);
@@ -173,18 +200,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     extern __shared__ __align__(1024) std::uint8_t smem_raw[];
     std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
         (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    // bars[0..S-1]: stage free; bars[S], bars[S+1]: accumulator 0/1 chunk done
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kTcStageBytes);
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages + 1);
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0) {
-        for (int s = 0; s <= kTcStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kTcStages + 2; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "n"(kTcBN));
+                     "n"(kTcTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -196,11 +224,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                             job.alo + static_cast<std::size_t>(m0) * n,
                             job.bthi + static_cast<std::size_t>(n0) * n,
                             job.btlo + static_cast<std::size_t>(n0) * n};
-    // stage k-block kb into stage s: 4 tiles x 128 rows x 8 chunks, 32 per thread
+    // stage k-block kb into stage s: 4 tiles x 128 rows x 8 chunks, 16 per thread
     auto load_stage = [&](int kb, int s) {
         const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < (4 * kTcBM * 8) / kTcThreads; ++i) {
             const int chunk = tid + i * kTcThreads;  // 0..4095
             const int tile = chunk >> 10;
             const int r = (chunk >> 3) & 127;
@@ -212,7 +240,29 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         }
     };
 
+    // this thread's share of the tile: TMEM lane quadrant (warp % 4) = 32 C
+    // rows, 64 of the 128 columns (warp / 4)
+    const int quad = warp & 3, half = warp >> 2;
+    float acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0f;
+    auto drain = [&](int chunk) {
+        mbar_wait(&bars[kTcStages + (chunk & 1)], (chunk >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const std::uint32_t base = tmem + (static_cast<std::uint32_t>(quad * 32) << 16) +
+                                   (chunk & 1) * kTcBN + half * 64;
+        float v[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            tmem_ld32(base + h * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
+
     const int kblocks = n / kTcBK;
+    const int ckb = static_cast<int>(table.chunk_kb);
 #pragma unroll
     for (int s = 0; s < kTcStages - 1; ++s) {
         if (s < kblocks) load_stage(s, s);
@@ -220,12 +270,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     }
     for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % kTcStages;
+        const int chunk = kb / ckb;
+        const bool chunk_first = kb % ckb == 0;
+        const bool chunk_last = (kb + 1) % ckb == 0 || kb + 1 == kblocks;
         cp_async_wait<kTcStages - 2>();
         asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy writes -> tensor core
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
             const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+            const std::uint32_t dacc = tmem + (chunk & 1) * kTcBN;
 #pragma unroll
             for (int k = 0; k < kTcBK / 8; ++k) {
                 const std::uint32_t off = k * 32;  // 8 tf32 = 32 bytes along K
@@ -233,12 +287,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
                 const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
                 const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
-                const std::uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-                umma_tf32(tmem, ahi, bhi, acc0);
-                umma_tf32(tmem, ahi, blo, 1u);
-                umma_tf32(tmem, alo, bhi, 1u);
+                // small terms first, then the large one
+                umma_tf32(dacc, ahi, blo, (chunk_first && k == 0) ? 0u : 1u);
+                umma_tf32(dacc, alo, bhi, 1u);
+                umma_tf32(dacc, ahi, bhi, 1u);
             }
             umma_commit(&bars[s]);  // stage s free once these MMAs have read it
+            if (chunk_last) umma_commit(&bars[kTcStages + (chunk & 1)]);  // chunk done
         }
         // refill the stage consumed one iteration ago with k-block kb + S - 1
         const int next = kb + kTcStages - 1;
@@ -248,41 +303,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
             load_stage(next, ns);
         }
         cp_async_commit();
+        // fold the previous chunk while the tensor core runs this one; the
+        // next MMA into that accumulator comes after a later __syncthreads
+        if (chunk_first && chunk > 0) drain(chunk - 1);
     }
-    // all MMAs done -> accumulator ready
-    if (tid == 0) umma_commit(&bars[kTcStages]);
-    mbar_wait(&bars[kTcStages], 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
+    drain((kblocks - 1) / ckb);
 
-    // epilogue: warp w owns TMEM lanes (= C rows) 32w .. 32w+31
-    const int row = m0 + warp * 32 + (tid & 31);
-    float* crow = job.C + static_cast<std::size_t>(row) * n + n0;
+    // epilogue: 64 consecutive columns of one C row per thread
+    const int row = m0 + quad * 32 + (tid & 31);
+    float* crow = job.C + static_cast<std::size_t>(row) * n + n0 + half * 64;
 #pragma unroll
-    for (int cb = 0; cb < kTcBN; cb += 32) {
-        std::uint32_t v[32];
-        const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(warp * 32) << 16) + cb;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(crow + cb + j) =
-                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                            __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-    }
+    for (int j = 0; j < 64; j += 4)
+        *reinterpret_cast<float4*>(crow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcBN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(kTcTmemCols));
 }
 
 }  // namespace vgk

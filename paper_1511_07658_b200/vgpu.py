@@ -313,8 +313,10 @@ def device_count() -> int:
 
 
 def resident_bench(payload_id: str, inputs: Sequence[bytes], sets: int, warmup: int,
-                   steps: int, device: int = 0, param: float = 2.0, pdl: bool = True) -> dict:
-    """Device-only timing of the batched launch with inputs resident in HBM."""
+                   steps: int, device: int = 0, param: float = 2.0, pdl: bool = True,
+                   main_only: bool = False) -> dict:
+    """Device-only timing of the batched launch with inputs resident in HBM.
+    main_only: SGEMM's tcgen05 GEMM alone (pre-pass outside the timed steps)."""
     bufs = [(C.c_uint8 * max(1, len(b))).from_buffer_copy(b if len(b) else b"\0")
             for b in inputs]
     ptrs = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
@@ -322,7 +324,8 @@ def resident_bench(payload_id: str, inputs: Sequence[bytes], sets: int, warmup: 
     r = N.ResidentResult()
     _cu_check(_libs().cuda.vgpu_cu_resident_bench(device, KERNELS[payload_id], param,
                                                   len(bufs), ptrs, sizes, sets, warmup,
-                                                  steps, 0 if pdl else 1, C.byref(r)))
+                                                  steps, (0 if pdl else 1) | (2 if main_only else 0),
+                                                  C.byref(r)))
     return {k: getattr(r, k) for k, _ in N.ResidentResult._fields_}
 
 

@@ -147,3 +147,34 @@ def test_virtual_clock_metrics_match_the_model():
         csv = d.metrics_csv()
     assert b[0]["model_makespan_us"] == b[0]["measured_makespan_us"] == 210
     assert csv.startswith("task_id,client_id,queue_wait_us,pure_gpu_us,end_to_end_us")
+
+
+@pytest.mark.parametrize("path", ["tc", "simt"])
+def test_c4_sgemm_both_paths_within_tolerance(path):
+    """Both SGEMM kernels (3xTF32 tcgen05, the default; FP32 SIMT) against
+    binary64 at 2048^2 and a non-multiple-of-128 size (SIMT fallback), in a
+    fresh process since the path is chosen once per process (VGPU_SGEMM)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np
+from paper_1511_07658_b200 import vgpu as V
+for n in (2048, 200):
+    rng = np.random.default_rng(7 + n)
+    A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    C = np.frombuffer(V.native_run_task(A.tobytes() + B.tobytes(), V.KernelDescriptor("sgemm")),
+                      np.float32).reshape(n, n)
+    rows = rng.choice(n, 48, replace=False)
+    ref = A[rows].astype(np.float64) @ B.astype(np.float64)
+    print(n, np.linalg.norm(C[rows] - ref) / np.linalg.norm(ref))
+'''
+    env = dict(os.environ, VGPU_SGEMM=path)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    for line in out.stdout.split("\n"):
+        if line.strip():
+            n, err = line.split()
+            assert float(err) <= 1e-5, (path, n, err)
