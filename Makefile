@@ -25,7 +25,7 @@ CFLAGS   := -O2 -g -fPIC -ffp-contract=off -std=c11 -Wall -Wextra -Wno-unknown-p
 
 HOST_SRC := $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJ := $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host/%.o,$(HOST_SRC))
-CUDA_HDR := $(wildcard $(CSRC)/cuda/*.cuh) $(CSRC)/common/ep_math.h include/vgpu_cuda.h
+CUDA_HDR := $(wildcard $(CSRC)/cuda/*.cuh) $(wildcard $(CSRC)/common/*.h) include/vgpu_cuda.h
 HDRS     := $(wildcard include/vgpu/*.hpp) include/vgpu_cuda.h include/vgpu_c.h
 TEST_SRC := $(wildcard tests/cpp/*.cpp)
 
@@ -68,7 +68,7 @@ $(TESTBIN)/vgpu-tests: $(TEST_SRC) tests/cpp/minitest.hpp $(LIBDIR)/libvgpu.so o
 
 oracle: oracle/_build/libvgpu_oracle.so
 
-oracle/_build/libvgpu_oracle.so: oracle/vgpu_oracle.c oracle/vgpu_oracle.h $(CSRC)/common/ep_math.h
+oracle/_build/libvgpu_oracle.so: oracle/vgpu_oracle.c oracle/vgpu_oracle.h $(wildcard $(CSRC)/common/*.h)
 	@mkdir -p oracle/_build
 	$(CC) $(CFLAGS) -shared -o $@ oracle/vgpu_oracle.c -lm
 

@@ -525,7 +525,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
               "npb_mops": 2.0 * pairs / kernel_s / 1e6,
               "peak_source": "measured now: DFMA-chain probe (vgpu_cu_peak_probe), 2 FLOP/DFMA",
               "op_count": "IEEE binary64 ops of the restated NPB EP step (each +,-,*,/,sqrt = 1): "
-                          "7 per pair + 23 per accepted pair (table-driven log = 16)"})
+                          "7 per pair + 19 per accepted pair (table-driven log = 12)"})
     return r
 
 

@@ -20,7 +20,7 @@
  * (ep_log_table.h, scripts/gen_ep_log_table.py, 60-digit decimal), form
  * r = fma(z, invc, -1) (|r| < 2^-8), and return
  *   k ln2 + logc + log1p(r),  log1p(r) = r + r^2 (-1/2 + r/3 - ... + r^5/7)
- * with k ln2_hi + logc_hi summed exactly (Fast2Sum). The two intervals next
+ * with k ln2_hi + logc_hi exact (both multiples of 2^-32). The two intervals next
  * to 1 use c = 1, so log stays accurate to the last bits as x -> 1.
  * tests/test_oracle.py measures it against glibc log (max error <= 1 ulp,
  * > 99% correctly rounded). Only positive normal arguments reach it from
@@ -104,11 +104,14 @@ EP_FN double ep_uniform(uint64_t x) {
 
 /* Argument reduction: x = 2^k z, z in [0.6875, 1.375), table index i. */
 EP_FN double ep_log_reduce(double x, int* i, double* kd) {
+    /* the offset's low word is 0: all the work is on the high word */
     const uint64_t ix = ep_to_bits(x);
-    const uint64_t tmp = ix - VGPU_EP_LOG_OFF;
-    *i = (int)((tmp >> (52 - VGPU_EP_LOG_BITS)) & ((1u << VGPU_EP_LOG_BITS) - 1u));
-    *kd = (double)((int64_t)tmp >> 52);
-    return ep_from_bits(ix - (tmp & 0xFFF0000000000000ull));
+    const uint32_t hx = (uint32_t)(ix >> 32);
+    const uint32_t tmp = hx - (uint32_t)(VGPU_EP_LOG_OFF >> 32);
+    *i = (int)((tmp >> (20 - VGPU_EP_LOG_BITS)) & ((1u << VGPU_EP_LOG_BITS) - 1u));
+    *kd = (double)((int32_t)tmp >> 20);
+    const uint32_t zh = hx - (tmp & 0xFFF00000u);
+    return ep_from_bits(((uint64_t)zh << 32) | (ix & 0xFFFFFFFFull));
 }
 
 /* Constants of ep_log_finish, by value (hex literals = the exact binary64
@@ -127,10 +130,8 @@ typedef struct vgpu_ep_log_consts {
 EP_FN double ep_log_finish(const vgpu_ep_log_consts* K, double z, double kd, double invc,
                            double logc_hi, double logc_lo) {
     const double r = EP_FMA(z, invc, -1.0);
-    /* k ln2_hi + logc_hi = s + e exactly: |k ln2_hi| >= 0.69 > |logc_hi|, or k = 0 */
-    const double a = EP_MUL(kd, K->ln2_hi);
-    const double s = EP_ADD(a, logc_hi);
-    const double e = EP_SUB(logc_hi, EP_SUB(s, a));
+    /* ln2_hi and logc_hi are multiples of 2^-32 and |k| <= 1100: exact */
+    const double s = EP_FMA(kd, K->ln2_hi, logc_hi);
     const double r2 = EP_MUL(r, r);
     double p = EP_FMA(K->c7, r, K->c6);
     p = EP_FMA(p, r, K->c5);
@@ -138,7 +139,6 @@ EP_FN double ep_log_finish(const vgpu_ep_log_consts* K, double z, double kd, dou
     p = EP_FMA(p, r, K->c3);
     p = EP_FMA(p, r, -0.5);
     double lo = EP_FMA(kd, K->ln2_lo, logc_lo);
-    lo = EP_ADD(lo, e);
     lo = EP_FMA(r2, p, lo);
     return EP_ADD(s, EP_ADD(r, lo));
 }
@@ -169,6 +169,7 @@ EP_FN int vgpu_ep_pair(uint64_t xa, uint64_t xb, double* gx, double* gy, int* an
     *gx = t3;
     *gy = t4;
     *annulus = (int)(a3 > a4 ? a3 : a4);
+    if (*annulus > 9) *annulus = 9; /* NQ = 10; |t3| < 11.2 for t >= 2^-90, never > 9 in practice */
     return 1;
 }
 
