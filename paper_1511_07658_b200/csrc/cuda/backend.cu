@@ -130,6 +130,16 @@ bool sgemm_use_tc() {
     return tc;
 }
 
+// EP kernel instance (k_ep.cuh template: min blocks per SM, unroll);
+// VGPU_EP_VARIANT selects the alternatives for measurement.
+int ep_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("VGPU_EP_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 // 3xTF32: k-blocks (32 of K) per TMEM accumulation chunk (k_sgemm_tc.cuh);
 // VGPU_SGEMM_CHUNK overrides the default of 2 (K = 64).
 std::uint32_t sgemm_chunk_kb() {
@@ -237,7 +247,14 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     ctas += static_cast<std::uint32_t>(p.n_batches);
                 }
                 if (!ctas) continue;
-                ep_table_kernel<<<ctas, kEpThreads, 0, s>>>(t);
+                switch (ep_variant()) {
+                    case 1: ep_table_kernel<6, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 2: ep_table_kernel<4, 4><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 3: ep_table_kernel<6, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 4: ep_table_kernel<8, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 5: ep_table_kernel<3, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    default: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                }
                 ++*launches;
                 const cudaError_t e = cudaGetLastError();
                 if (e != cudaSuccess) return e;
@@ -884,7 +901,9 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         SlotState& s = d->slots[t.slot];
         Op* op = ops[i];
         const bool resident = (t.flags & VGPU_CU_TASK_INPUT_RESIDENT) != 0;
-        op->has_h2d = t.in_bytes > 0 && !resident;
+        // NAS EP reads its parameter record from the task table (by value):
+        // its input never needs to be in HBM
+        op->has_h2d = t.in_bytes > 0 && !resident && t.kernel != VGPU_CU_K_EP;
         cudaError_t err = cudaEventRecord(op->ev[kEvH2d0], s.stream);
         if (err == cudaSuccess && op->has_h2d)
             err = cudaMemcpyAsync(s.d_in, t.h_in, t.in_bytes, cudaMemcpyHostToDevice, s.stream);

@@ -93,6 +93,7 @@ struct Session {
     bool device_busy = false;    // a task of this slot is on the device
     std::uint32_t uploads = 0;   // eager SND uploads in flight
     bool input_resident = false; // the current input already sits in HBM
+    bool input_inline = false;   // the current input is the <= 64 B snapshot in head
     std::uint8_t head[64] = {};  // first bytes of the input (EP parameters)
     float upload_h2d_us = 0.0f;
     std::deque<Inbound> backlog; // frames that arrived while an upload ran
@@ -318,7 +319,16 @@ struct GvmDaemon::Impl {
         s.input_len = *len;
         s.input.clear();
         s.input_resident = false;
+        s.input_inline = false;
         std::memcpy(s.head, region.data(), std::min<std::uint64_t>(*len, sizeof s.head));
+        if (dev && cfg.data_plane == DataPlane::ZeroCopy && *len <= sizeof s.head) {
+            // tiny inputs (NAS EP's 32-byte parameter record): the host copy
+            // above IS the SND snapshot; ACK now, no DMA round trip (EP
+            // parameters travel to the kernel by value in its task table)
+            s.input_inline = true;
+            s.phase = Phase::DataIn;
+            return ack(m.client_id, m.task_id);
+        }
         if (dev && cfg.data_plane == DataPlane::ZeroCopy) {
             // eager upload: the SND snapshot is taken by DMA into the slot's
             // HBM buffer; the ACK goes out when the copy has landed, so the
@@ -523,9 +533,10 @@ struct GvmDaemon::Impl {
             }
             std::uint64_t out_bytes = 0;
             const std::uint64_t in_len = live ? s->input_len : t.profile.input_bytes;
-            const std::uint8_t* probe = (live && s->input_resident && in_len <= sizeof s->head)
-                                            ? s->head
-                                            : src;
+            const std::uint8_t* probe =
+                (live && (s->input_resident || s->input_inline) && in_len <= sizeof s->head)
+                    ? s->head
+                    : src;
             const int rc = vgpu_cu_output_size(dk->kernel, probe, in_len, &out_bytes);
             if (rc != VGPU_CU_OK || !live) {
                 if (live)
@@ -558,7 +569,9 @@ struct GvmDaemon::Impl {
             ct.param = dk->param;
             ct.h_in = src;
             ct.in_bytes = in_len;
-            if (s->input_resident) {
+            if (s->input_inline) {
+                ct.h_in = s->head;  // SND-time bytes (small pageable H2D, or by value for EP)
+            } else if (s->input_resident) {
                 ct.flags |= VGPU_CU_TASK_INPUT_RESIDENT;
                 if (in_len <= sizeof s->head) ct.h_in = s->head;  // SND-time bytes
                 f.upload_h2d_us = s->upload_h2d_us;

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <thread>
 
+#include <random>
+
 #include "minitest.hpp"
 #include "vgpu/client.hpp"
 
@@ -371,6 +373,26 @@ TEST_CASE("client: run_task, reuse, release") {
     CHECK(f32(out.data(), 0) == 12.f);
     h.rls();
     CHECK(h.phase() == Phase::Released);
+}
+
+TEST_CASE("client: large SND/RCV through the streaming copy, odd sizes and offsets") {
+    // >= 256 KiB payloads take the non-temporal AVX2 copy into the region
+    // (client.cpp stream_copy): unaligned heads and 128-byte tails included
+    LoopbackHub hub;
+    GvmConfig g = cfg(1, 1);
+    g.per_client_shm_bytes = 2 << 20;
+    auto d = start(hub, g);
+    VgpuHandle h = req(hub);
+    std::mt19937 rng(7);
+    for (std::size_t n : {std::size_t{256} << 10, (std::size_t{1} << 20) + 37, (std::size_t{2} << 20) - 5}) {
+        Bytes in(n + 3);
+        for (auto& b : in) b = static_cast<std::uint8_t>(rng());
+        const std::span<const std::uint8_t> view(in.data() + 3, n);  // misaligned source
+        const Bytes out = h.run_task(view, descr(1, 1, 1, "reverse"));
+        REQUIRE(out.size() == n);
+        CHECK(std::equal(out.rbegin(), out.rend(), view.begin()));
+    }
+    h.rls();
 }
 
 TEST_CASE("client: illegal orders fail locally; oversize SND; second SND wins") {
