@@ -278,7 +278,7 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist, cold=False, barrier=0):
+                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False):
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
     inst = f"b200bench{os.getpid()}g{dist.rank}"
@@ -291,8 +291,9 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         V.unlink_os_instance(inst, procs)
         cfg = V.GvmConfig(instance=inst, max_clients=procs, barrier_size=barrier or procs,
                           per_client_shm_bytes=W.region_bytes(workload, sizes),
-                          barrier_window=2000, clock=V.ClockMode.Real, cuda_device=device,
-                          device_sms=148, device_max_kernels=128, device_slots_per_sm=32)
+                          barrier_window=window, clock=V.ClockMode.Real, cuda_device=device,
+                          device_sms=148, device_max_kernels=128, device_slots_per_sm=32,
+                          data_plane=V.DataPlane.Snapshot if snapshot else V.DataPlane.ZeroCopy)
         gvm = V.GvmDaemon.start_os(cfg)
     size_args = sizes.size_args()
     args = []
@@ -427,6 +428,50 @@ def final_reduce(N, dist, record):
         return R.fold_in_rank_order(list(allr), dist.world), list(allr)[:R.REC_WIDTH], us
     finally:
         libs.cuda.vgpu_cu_close(dev)
+
+
+def validate_model(V, N, W, workload, device, sizes, dist, reps=8) -> dict:
+    """SURVEY 8(f)(1): the paper's model on real hardware (PAPER.md:505;
+    proj/src/bench/bench.cpp:341-375 validate_model). Measure one task's
+    stages (t_in, t_comp, t_out) with CUDA events (one SPMD process, the
+    C-config job), then for n = 1..P run batches of n tasks (barrier n,
+    1 s window so batches fill) and compare the measured device batch span
+    (CUDA events) with simulate() fed the measured triple. The GVM runs the
+    Snapshot data plane here, the reference's timing: every task's H2D is
+    part of its batch (the default eager upload moves it to SND time). Two device specs bracket B200: 'concurrent'
+    (the reference's idealized regime, grid 1: kernels of different tasks
+    run side by side) and 'device-filling' (every task's kernel occupies the
+    whole GPU: computes serialize). Deviation rows use the reference's
+    schema (n, model_us, measured_us, deviation_pct)."""
+    procs = W.DEFAULT_PROCS[workload]
+    one = leg_workers(V, N, W, workload, 1, 0, procs, reps, 2, device, False, sizes, dist,
+                      barrier=1, snapshot=True)
+    st = one["device_stage_us"]
+    t_in = max(1, int(round(st["h2d_us"] or 0)))
+    t_comp = max(1, int(round(st["comp_us"] or 0)))
+    t_out = max(1, int(round(st["d2h_us"] or 0)))
+    rows = {"concurrent": [], "device_filling": []}
+    style = None
+    for n in range(1, procs + 1):
+        r = leg_workers(V, N, W, workload, n, 0, procs, reps, 2, device, False, sizes, dist,
+                        barrier=n, window=1_000_000, snapshot=True)
+        full = [b for b in r["batches"] if b["task_count"] == n]
+        if not full:
+            continue
+        measured = statistics.median([b["measured_makespan_us"] for b in full])
+        style = full[-1]["style"]
+        for name, spec in (("concurrent", (1, 148, 128, 32)), ("device_filling", (1, 1, 128, 1))):
+            grid, sms, kern, slots = spec
+            model = V.model_simulate(style, n, t_in, t_comp, t_out, grid, sms, kern, slots)
+            rows[name].append({"n": n, "model_us": model, "measured_us": measured,
+                               "deviation_pct": 100.0 * abs(measured - model) / max(1, model)})
+    out = {"workload": W.CONFIG_NAME[workload], "style": "PS2" if style else "PS1",
+           "task_triple_us": {"t_in": t_in, "t_comp": t_comp, "t_out": t_out},
+           "paper": "PAPER.md:505: EP(M24) 0.42 %, VecMult 4.76 % mean deviation on a C2070"}
+    for name, rs in rows.items():
+        out[name] = {"rows": rs, "mean_deviation_pct":
+                     statistics.mean([x["deviation_pct"] for x in rs]) if rs else None}
+    return out
 
 
 def model_summary(batches):
@@ -598,6 +643,9 @@ def main():
     ap.add_argument("--no-native", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--validate-model", action="store_true",
+                    help="SURVEY 8(f)(1): paper model vs measured batch spans, n = 1..P; "
+                         "prints that report instead of the bench line")
     ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
     ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
     ap.add_argument("--no-kernels", action="store_true",
@@ -651,6 +699,11 @@ def main():
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
     device = dist.device
+    if args.validate_model:
+        if dist.rank == 0:
+            emit(validate_model(V, N, W, args.workload, device, sizes, dist))
+        dist.close()
+        return
     gid0 = dist.rank * procs
     total_workers = procs * world
     clocks = Clocks(device) if dist.local == 0 or world == 1 else None
