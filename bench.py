@@ -474,6 +474,67 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8) -> dict:
     return out
 
 
+def sweep(V, N, W, workload, device, sizes, dist) -> dict:
+    """The paper's turnaround curves (Figs. 13-22; proj/src/bench/bench.cpp:
+    266-339 run_sweep) on B200: for N = 1..P SPMD processes started
+    together, each running one task, the time until the last has its result.
+    Virtualized includes REQ on the already-open GVM; native includes each
+    process creating its own CUDA context (the paper's T_init). Rows use the
+    reference's report schema."""
+    procs = W.DEFAULT_PROCS[workload]
+    rows = []
+    for n in range(1, procs + 1):
+        tv = leg_workers(V, N, W, workload, n, 0, procs, 1, 0, device, False, sizes, dist,
+                         cold=True, barrier=1)
+        tn = leg_workers(V, N, W, workload, n, 0, procs, 1, 0, device, True, sizes, dist,
+                         cold=True)
+        v_us, n_us = tv["turnaround_ms"] * 1e3, tn["turnaround_ms"] * 1e3
+        pg = tv["device_stage_us"]["pure_gpu_us"] or 0.0
+        rows.append({"benchmark": workload, "n": n, "mode": "virtualized", "clock": "real",
+                     "turnaround_us": v_us, "pure_gpu_us": pg,
+                     "overhead_fraction": 1.0 - pg / v_us if v_us else None,
+                     "model_us": None, "deviation_pct": None, "speedup": n_us / v_us})
+        rows.append({"benchmark": workload, "n": n, "mode": "native", "clock": "real",
+                     "turnaround_us": n_us, "pure_gpu_us": None, "overhead_fraction": None,
+                     "model_us": None, "deviation_pct": None, "speedup": 1.0})
+    cols = ["benchmark", "n", "mode", "clock", "turnaround_us", "pure_gpu_us",
+            "overhead_fraction", "model_us", "deviation_pct", "speedup"]
+    csv = ",".join(cols) + "\n" + "\n".join(
+        ",".join("" if r[c] is None else (f"{r[c]:.3f}" if isinstance(r[c], float) else str(r[c]))
+                 for c in cols) for r in rows)
+    return {"report": "sweep", "workload": W.CONFIG_NAME[workload], "rows": rows, "csv": csv}
+
+
+def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
+    """Virtualization overhead across payload sizes (proj/src/bench/
+    bench.cpp:389-423 measure_overhead): one process, vector add of
+    1 KiB .. 64 MiB inputs through the GVM; turnaround per job vs its pure
+    GPU time (CUDA events), overhead = the difference. Reference schema:
+    bytes,turnaround_us,pure_gpu_us,overhead_us,overhead_fraction."""
+    rows = []
+    for nbytes in (1 << 10, 1 << 16, 1 << 20, 16 << 20, 64 << 20):
+        sz = W.Sizes()
+        sz.vecadd_n = nbytes // 8
+        r = leg_workers(V, N, W, "vecadd", 1, 0, 1, steps, warmup, device, False, sz, dist,
+                        barrier=1)
+        t_us = r["seconds"] * 1e6 / steps
+        pg = r["device_stage_us"]["pure_gpu_us"] or 0.0
+        up = r["device_stage_us"]["h2d_us"] or 0.0  # eager upload at SND: device time too
+        gpu = pg + up
+        rows.append({"bytes": nbytes, "turnaround_us": t_us, "pure_gpu_us": gpu,
+                     "overhead_us": max(0.0, t_us - gpu),
+                     "overhead_fraction": max(0.0, t_us - gpu) / t_us})
+    cols = ["bytes", "turnaround_us", "pure_gpu_us", "overhead_us", "overhead_fraction"]
+    csv = ",".join(cols) + "\n" + "\n".join(
+        ",".join(f"{r[c]:.3f}" if isinstance(r[c], float) else str(r[c]) for c in cols)
+        for r in rows)
+    return {"report": "overhead", "rows": rows, "csv": csv,
+            "note": "turnaround = the whole job through the unchanged client API (SND copy into "
+                    "shm, H2D, kernel, D2H, RCV copy out); pure_gpu = upload H2D + task span "
+                    "from CUDA events; the paper's figure is ~20 % at 400 MB on a C2070 "
+                    "(PAPER.md:507)"}
+
+
 def model_summary(batches):
     """Paper model (simulate() on the declared triples) vs CUDA-event batch
     makespans, §6 model validation."""
@@ -646,6 +707,10 @@ def main():
     ap.add_argument("--validate-model", action="store_true",
                     help="SURVEY 8(f)(1): paper model vs measured batch spans, n = 1..P; "
                          "prints that report instead of the bench line")
+    ap.add_argument("--sweep", action="store_true",
+                    help="paper turnaround curves, N = 1..P, virtualized vs native (report)")
+    ap.add_argument("--overhead-curve", action="store_true",
+                    help="virtualization overhead across payload sizes, 1 process (report)")
     ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
     ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
     ap.add_argument("--no-kernels", action="store_true",
@@ -699,9 +764,14 @@ def main():
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
     device = dist.device
-    if args.validate_model:
+    if args.validate_model or args.sweep or args.overhead_curve:
         if dist.rank == 0:
-            emit(validate_model(V, N, W, args.workload, device, sizes, dist))
+            if args.validate_model:
+                emit(validate_model(V, N, W, args.workload, device, sizes, dist))
+            if args.sweep:
+                emit(sweep(V, N, W, args.workload, device, sizes, dist))
+            if args.overhead_curve:
+                emit(overhead_curve(V, N, W, device, dist, args.steps, args.warmup))
         dist.close()
         return
     gid0 = dist.rank * procs
