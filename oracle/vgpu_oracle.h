@@ -13,11 +13,14 @@
  *                        PINNED against the published NPB verification sums
  *                        (classes S, W, A; epsilon 1e-8) in tests/golden/.
  *   Black-Scholes        no reference arithmetic (profiles.cpp:39); CUDA-SDK
- *                        formulation in binary64 — parity UNPINNED by the
- *                        reference (tolerance-checked: L1 relative <= 1e-6).
+ *                        formulation in binary64 — UNPINNED by the reference
+ *                        itself; pinned instead to a published worked example
+ *                        (Hull Ex. 15.6) and the exact-CDF closed form
+ *                        (tests/test_oracle.py). GPU checked at L1 rel <= 1e-6.
  *   SGEMM                no reference arithmetic (profiles.cpp:35); binary64
- *                        accumulation — parity UNPINNED by the reference
- *                        (relative Frobenius <= 1e-5 for FP32 SIMT).
+ *                        accumulation — UNPINNED by the reference itself;
+ *                        pinned to numpy float64 matmul and exact integer
+ *                        products. GPU checked at relative Frobenius <= 1e-5.
  */
 #ifndef VGPU_ORACLE_H
 #define VGPU_ORACLE_H

@@ -7,9 +7,10 @@
   (proj/src/bench/bench.cpp:34-49).
 * NAS EP: against NPB's published verification sums (epsilon 1e-8) for
   class S recomputed here, and the committed class S/W/A fixtures.
-* Black-Scholes / SGEMM: parity unpinned by the reference (no arithmetic
-  there); checked for internal consistency (put-call parity, exact small
-  products).
+* Black-Scholes / SGEMM: unpinned by the reference (no arithmetic there);
+  pinned to published known answers (Hull Ex. 15.6, the exact-CDF closed
+  form, numpy float64 matmul) and internal consistency (put-call parity,
+  exact small products).
 """
 import json
 import os
@@ -138,3 +139,39 @@ def test_ep_log_accuracy_against_exact_logarithm():
     errs = np.array([float(e) for e in errs])
     assert errs.max() <= 1.0, errs.max()
     assert np.mean(errs <= 0.5) > 0.99, np.mean(errs <= 0.5)
+
+
+def test_black_scholes_oracle_known_answers():
+    """Pin the Black-Scholes restatement (CUDA SDK formulation: the
+    5-coefficient polynomial CND) to published worked examples:
+    Hull, Options Futures and Other Derivatives, Example 15.6 (S=42, X=40,
+    T=0.5, r=0.10, sigma=0.20: c = 4.76, p = 0.81), and the closed form with
+    the exact normal CDF (math.erf) to the polynomial's accuracy (7.5e-8 on
+    N(d)) over the SDK's input ranges."""
+    import math
+    c, p = oracle.black_scholes(np.array([42.0]), np.array([40.0]), np.array([0.5]), r=0.10, v=0.20)
+    assert round(float(c[0]), 2) == 4.76 and round(float(p[0]), 2) == 0.81, (c, p)
+    rng = np.random.default_rng(11)
+    S = rng.uniform(5, 30, 2000).astype(np.float32)
+    X = rng.uniform(1, 100, 2000).astype(np.float32)
+    T = rng.uniform(0.25, 10, 2000).astype(np.float32)
+    c, p = oracle.black_scholes(S, X, T)
+    N = lambda d: 0.5 * (1.0 + math.erf(d / math.sqrt(2.0)))
+    for i in range(0, 2000, 7):
+        s, x, t = float(S[i]), float(X[i]), float(T[i])
+        d1 = (math.log(s / x) + (0.02 + 0.5 * 0.09) * t) / (0.3 * math.sqrt(t))
+        d2 = d1 - 0.3 * math.sqrt(t)
+        cc = s * N(d1) - x * math.exp(-0.02 * t) * N(d2)
+        pp = x * math.exp(-0.02 * t) * (1 - N(d2)) - s * (1 - N(d1))
+        tol = 2e-7 * (s + x)
+        assert abs(c[i] - cc) < tol and abs(p[i] - pp) < tol, (i, c[i], cc, p[i], pp)
+
+
+def test_sgemm_oracle_matches_numpy_float64():
+    """Pin the SGEMM restatement (binary64 accumulation of fp32 inputs) to
+    numpy's float64 matmul on random inputs."""
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-1, 1, (96, 96)).astype(np.float32)
+    B = rng.uniform(-1, 1, (96, 96)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.max(np.abs(oracle.sgemm(A, B) - ref)) < 1e-12
