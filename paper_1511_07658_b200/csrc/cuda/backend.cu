@@ -253,6 +253,8 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     case 3: ep_table_kernel<6, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 4: ep_table_kernel<8, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 5: ep_table_kernel<3, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 6: ep_table_kernel<7, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 7: ep_table_kernel<7, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
                     default: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
                 }
                 ++*launches;
