@@ -606,7 +606,8 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                                   if bf16 else "fallback: 2250 / 2 TFLOP/s nominal dense TF32"),
                   "precision": "3xTF32 tcgen05 (chunked TMEM accumulation): rel. Frobenius "
                                "4.8e-7 at 2048^2 on B200, bar 1e-5 vs binary64",
-                  "step_kernels": "tc_split_kernel (hi/lo split + B transpose) + tc_gemm_kernel; "
+                  "step_kernels": "tc_split_kernel (hi/lo split + B transpose) + tc_gemm2_kernel "
+                                  "(CTA pair, tcgen05.mma.cta_group::2, 256x256 tiles); "
                                   "achieved/kernel_us are the GEMM's"})
         return r
     if bound == "fp32":

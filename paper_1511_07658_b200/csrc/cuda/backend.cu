@@ -140,6 +140,17 @@ int ep_variant() {
     return v;
 }
 
+// 3xTF32 on a CTA pair (tcgen05.mma.cta_group::2, 256 x 256 tiles) when
+// every job's n is a multiple of 256 (the default); VGPU_SGEMM=tc forces
+// the 1-CTA 128 x 128 kernel.
+bool sgemm_pair() {
+    static const bool p = [] {
+        const char* e = std::getenv("VGPU_SGEMM");
+        return !(e && std::strcmp(e, "tc") == 0);
+    }();
+    return p;
+}
+
 // 3xTF32: k-blocks (32 of K) per TMEM accumulation chunk (k_sgemm_tc.cuh);
 // VGPU_SGEMM_CHUNK overrides the default of 2 (K = 64).
 std::uint32_t sgemm_chunk_kb() {
@@ -342,8 +353,23 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                         ++*launches;
                     }
                     if (g_sgemm_phases & 2u) {
-                        tc_gemm_kernel<<<dim3(maxn / kTcBN, maxn / kTcBM, tt.njobs), kTcThreads,
-                                         kTcSmemBytes, s>>>(tt);
+                        bool pair = sgemm_pair();
+                        for (std::uint32_t i = 0; i < tt.njobs && pair; ++i)
+                            pair = tt.job[i].n % kTc2BN == 0;
+                        if (pair) {
+                            static bool attr2 = [] {
+                                return cudaFuncSetAttribute(tc_gemm2_kernel,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            kTcSmemBytes) == cudaSuccess;
+                            }();
+                            if (!attr2) return cudaErrorInvalidConfiguration;
+                            const std::uint32_t pn = maxn / kTc2BN;
+                            tc_gemm2_kernel<<<dim3(2 * pn * pn, 1, tt.njobs), kTcThreads, kTcSmemBytes,
+                                              s>>>(tt);
+                        } else {
+                            tc_gemm_kernel<<<dim3(maxn / kTcBN, maxn / kTcBM, tt.njobs), kTcThreads,
+                                             kTcSmemBytes, s>>>(tt);
+                        }
                         ++*launches;
                     }
                     const cudaError_t e = cudaGetLastError();

@@ -322,4 +322,182 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                      "n"(kTcTmemCols));
 }
 
+
+// ---- CTA-pair variant (cta_group::2) ---------------------------------------------
+//
+// Two CTAs of a cluster (the two SMs of a TPC) compute a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8): each CTA stages its
+// own 128 rows of A (hi, lo) and its own 128 columns of B (hi, lo) in the
+// same SW128 K-major layout as above, and the leader CTA's single issuing
+// thread runs the MMA over both CTAs' operands. Per SM that is half the
+// shared-memory operand traffic of the 1-CTA 128 x 128 kernel for the same
+// MMA work (the 1-CTA kernel is shared-memory-bandwidth bound at ~60 % of
+// the TF32 peak). Each CTA's TMEM holds its 128 rows x 256 columns; the
+// same ping-pong chunked accumulation (512 TMEM columns) keeps the FP32
+// accuracy. Synchronisation: one cluster barrier per k-block (both CTAs'
+// stage is in shared memory), tcgen05.commit multicast to both CTAs'
+// mbarriers (stage free / chunk done).
+constexpr int kTc2BN = 256;  // pair tile N (each CTA stages 128 columns)
+constexpr std::uint32_t kTc2Idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    ((kTc2BN >> 3) << 17) | ((256 >> 4) << 24);
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+__device__ __forceinline__ void umma2_tf32(std::uint32_t tmem_d, std::uint64_t a, std::uint64_t b,
+                                           std::uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kTc2Idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma2_commit_both(std::uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(static_cast<unsigned short>(3)));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    tc_gemm2_kernel(const __grid_constant__ TcTable table) {
+    const TcJob& job = table.job[blockIdx.z];
+    const int n = static_cast<int>(job.n);
+    std::uint32_t rank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int pair = blockIdx.x >> 1, pairs_n = n / kTc2BN;
+    const int pm = pair / max(1, pairs_n), pn = pair % max(1, pairs_n);
+    // whole pairs leave together (n % 256 == 0 for every job of this kernel)
+    if (pairs_n == 0 || pm * kTc2BN >= n) return;
+    const int m0 = pm * kTc2BN + static_cast<int>(rank) * kTcBM;   // my A rows = my C rows
+    const int nb = pn * kTc2BN + static_cast<int>(rank) * kTcBM;   // my B columns
+    const int c0 = pn * kTc2BN;                                     // C columns (all 256)
+    const bool leader = rank == 0;
+
+    extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+    std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+        (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    // bars[0..S-1]: stage free; bars[S], bars[S+1]: accumulator 0/1 chunk
+    // done (both multicast by the leader's commits)
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kTcStageBytes);
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < kTcStages + 2; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const std::uint32_t tmem = *tmem_slot;
+
+    const float* srcs[4] = {job.ahi + static_cast<std::size_t>(m0) * n,
+                            job.alo + static_cast<std::size_t>(m0) * n,
+                            job.bthi + static_cast<std::size_t>(nb) * n,
+                            job.btlo + static_cast<std::size_t>(nb) * n};
+    auto load_stage = [&](int kb, int s) {
+        const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+#pragma unroll
+        for (int i = 0; i < (4 * kTcBM * 8) / kTcThreads; ++i) {
+            const int chunk = tid + i * kTcThreads;
+            const int tile = chunk >> 10;
+            const int r = (chunk >> 3) & 127;
+            const int c = chunk & 7;
+            const float* g = srcs[tile] + static_cast<std::size_t>(r) * n + kb * kTcBK + c * 4;
+            const std::uint32_t d = sbase + tile * kTcTileBytes + (r >> 3) * 1024 + (r & 7) * 128 +
+                                    ((c ^ (r & 7)) << 4);
+            cp_async16(d, g);
+        }
+    };
+
+    // warp w: TMEM lanes 32 (w % 4) .. +31 (= my C rows), columns 128 (w / 4) .. +127
+    const int quad = warp & 3, half = warp >> 2;
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+    auto drain = [&](int chunk) {
+        mbar_wait(&bars[kTcStages + (chunk & 1)], (chunk >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const std::uint32_t base = tmem + (static_cast<std::uint32_t>(quad * 32) << 16) +
+                                   (chunk & 1) * kTc2BN + half * 128;
+        float v[32];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            tmem_ld32(base + h * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
+
+    const int kblocks = n / kTcBK;
+    const int ckb = static_cast<int>(table.chunk_kb);
+#pragma unroll
+    for (int s = 0; s < kTcStages - 1; ++s) {
+        if (s < kblocks) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % kTcStages;
+        const int chunk = kb / ckb;
+        const bool chunk_first = kb % ckb == 0;
+        const bool chunk_last = (kb + 1) % ckb == 0 || kb + 1 == kblocks;
+        cp_async_wait<kTcStages - 2>();
+        asm volatile("fence.proxy.async.shared::cta;");
+        // stage s holds k-block kb in BOTH CTAs. (Measured: a per-CTA
+        // __syncthreads plus a remote mbarrier arrive / cluster-scope wait in
+        // the leader is 10 % slower than this cluster barrier.)
+        cluster_sync_all();
+        if (leader && tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+            const std::uint32_t dacc = tmem + (chunk & 1) * kTc2BN;
+#pragma unroll
+            for (int k = 0; k < kTcBK / 8; ++k) {
+                const std::uint32_t off = k * 32;
+                const std::uint64_t ahi = umma_desc_k_sw128(sbase + 0 * kTcTileBytes + off);
+                const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
+                const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
+                const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
+                umma2_tf32(dacc, ahi, blo, (chunk_first && k == 0) ? 0u : 1u);
+                umma2_tf32(dacc, alo, bhi, 1u);
+                umma2_tf32(dacc, ahi, bhi, 1u);
+            }
+            umma2_commit_both(&bars[s]);
+            if (chunk_last) umma2_commit_both(&bars[kTcStages + (chunk & 1)]);
+        }
+        const int next = kb + kTcStages - 1;
+        if (next < kblocks) {
+            const int ns = next % kTcStages;
+            if (kb >= 1) mbar_wait(&bars[ns], ((kb - 1) / kTcStages) & 1);
+            load_stage(next, ns);
+        }
+        cp_async_commit();
+        if (chunk_first && chunk > 0) drain(chunk - 1);
+    }
+    drain((kblocks - 1) / ckb);
+
+    const int row = m0 + quad * 32 + (tid & 31);
+    float* crow = job.C + static_cast<std::size_t>(row) * n + c0 + half * 128;
+#pragma unroll
+    for (int j = 0; j < 128; j += 4)
+        *reinterpret_cast<float4*>(crow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs done with the pair's TMEM
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
 }  // namespace vgk

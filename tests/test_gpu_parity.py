@@ -149,9 +149,10 @@ def test_virtual_clock_metrics_match_the_model():
     assert csv.startswith("task_id,client_id,queue_wait_us,pure_gpu_us,end_to_end_us")
 
 
-@pytest.mark.parametrize("path", ["tc", "simt"])
+@pytest.mark.parametrize("path", ["tc2", "tc", "simt"])
 def test_c4_sgemm_both_paths_within_tolerance(path):
-    """Both SGEMM kernels (3xTF32 tcgen05, the default; FP32 SIMT) against
+    """All SGEMM kernels (3xTF32 tcgen05 on a CTA pair, the default; 3xTF32
+    tcgen05 on one CTA; FP32 SIMT) against
     binary64 at 2048^2 and a non-multiple-of-128 size (SIMT fallback), in a
     fresh process since the path is chosen once per process (VGPU_SGEMM)."""
     import subprocess
