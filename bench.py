@@ -369,15 +369,20 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_round
     if not os.path.exists(ref):
         return None
     try:
-        # probe one round: one job, or one job of each kind for the mix
-        n0 = min(procs, 4) if workload == "mixed" else 1
-        one = _ref_run(ref, workload, n0, 1, 0, size_args)
-        per_job = max(1e-4, one["seconds"] / n0)
-        n = n0 if workload == "mixed" else max(1, min(procs, int(20.0 / per_job)))
-        per_round = per_job * n
+        # probe one full round at the configuration's own shape
+        n = procs
+        one = _ref_run(ref, workload, n, 1, 0, size_args)
+        per_round = max(1e-4, one["seconds"])
+        if per_round > 25.0 and workload != "mixed":
+            # a round must fit the reference client's 30 s reply timeout
+            per_job = per_round / n
+            n = max(1, min(procs, int(20.0 / per_job)))
+            per_round = per_job * n
         rounds = max(1, min(max_rounds, int(budget_s / per_round)))
-        w = warmup if per_round * (rounds + warmup) < 2 * budget_s else 0
-        r = _ref_run(ref, workload, n, rounds, w, size_args)
+        w = warmup if per_round * (rounds + warmup) <= 1.5 * budget_s else 0
+        r = _ref_run(ref, workload, n, rounds, w, size_args) if (rounds > 1 or w) else one
+        if r is one:
+            rounds, w = 1, 0
     except Exception as e:  # noqa: BLE001 - reported, not fatal for our arm
         log("reference arm failed:", e)
         return None
@@ -704,7 +709,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-native", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0,
+                    help="host seconds for the cpu_baseline sample inside our arm")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="host seconds the --impl reference arm may spend on its K steps")
     ap.add_argument("--validate-model", action="store_true",
                     help="SURVEY 8(f)(1): paper model vs measured batch spans, n = 1..P; "
                          "prints that report instead of the bench line")
@@ -741,7 +749,7 @@ def main():
 
     if args.impl == "reference":
         if dist.rank == 0:
-            r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s,
+            r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.ref_budget_s,
                                   warmup=min(args.warmup, 3), max_rounds=args.steps)
             if r is None:
                 line = {"impl": "reference", "unavailable": "oracle/_ref/ref-bench not built "
