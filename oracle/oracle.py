@@ -52,6 +52,8 @@ def lib() -> C.CDLL:
         L.vo_vector_scale.argtypes = [f32p, f32p, C.c_float, C.c_size_t]
         L.vo_ep_job.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
         L.vo_ep_job.restype = C.c_int
+        L.vo_ep_job_lanes.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
+        L.vo_ep_job_lanes.restype = C.c_int
         L.vo_ep_log.argtypes = [f64p, f64p, C.c_size_t]
         L.vo_ep_fold.argtypes = [C.POINTER(EpResult), C.c_size_t, C.POINTER(EpResult)]
         L.vo_black_scholes.argtypes = [f32p, f32p, f32p, C.c_size_t, C.c_double, C.c_double,
@@ -88,9 +90,12 @@ def ep_params_bytes(m: int, first: int, count: int, mk: int = 16) -> bytes:
     return bytes(EpParams(m, mk, first, count, 0))
 
 
-def ep_job(m: int, first: int, count: int, mk: int = 16) -> EpResult:
+def ep_job(m: int, first: int, count: int, mk: int = 16, lanes: bool = False) -> EpResult:
+    """NAS EP job in the kernel's reduction order (lanes=True: the
+    lane-sequential order of the branch-free kernel instance)."""
     r = EpResult()
-    rc = lib().vo_ep_job(C.byref(EpParams(m, mk, first, count, 0)), C.byref(r))
+    fn = lib().vo_ep_job_lanes if lanes else lib().vo_ep_job
+    rc = fn(C.byref(EpParams(m, mk, first, count, 0)), C.byref(r))
     if rc != 0:
         raise ValueError("bad EP parameters")
     return r

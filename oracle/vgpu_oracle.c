@@ -56,10 +56,58 @@ static void ep_batch(uint64_t b, uint32_t mk, uint64_t per_lane, uint64_t lane_s
     *bsy = lsy[0];
 }
 
+/* One NPB batch (2^mk pairs) in the kernel's order (k_ep.cuh): lane l of
+ * 256 owns candidates [l*per_lane, (l+1)*per_lane); warp w = lanes
+ * 32w..32w+31 walks them round by round (round k = candidate k of each of
+ * its lanes, lanes in order) and hands its accepted pairs out in that order,
+ * entry e to lane 32w + e % 32, which adds them sequentially. The 256 lane
+ * sums are then folded by the fixed stride-doubling tree into *bsx, *bsy;
+ * counts go to q. */
+static void ep_batch_compact(uint64_t b, uint32_t mk, uint64_t per_lane, uint64_t lane_skip,
+                     uint64_t q[10], double* bsx, double* bsy) {
+    double lsx[VGPU_EP_LANES], lsy[VGPU_EP_LANES];
+    uint64_t v[VGPU_EP_LANES];
+    uint64_t lane_start = vgpu_ep_batch_seed(b, mk);
+    for (unsigned lane = 0; lane < VGPU_EP_LANES; ++lane) {
+        v[lane] = lane_start;
+        lsx[lane] = 0.0;
+        lsy[lane] = 0.0;
+        lane_start = ep_mulmod46(lane_start, lane_skip);
+    }
+    for (unsigned w = 0; w < VGPU_EP_LANES / 32; ++w) {
+        uint64_t entry = 0;
+        for (uint64_t k = 0; k < per_lane; ++k)
+            for (unsigned L = 0; L < 32; ++L) {
+                const unsigned lane = 32 * w + L;
+                const uint64_t xa = ep_mulmod46(v[lane], VGPU_EP_A);
+                const uint64_t xb = ep_mulmod46(xa, VGPU_EP_A);
+                v[lane] = xb;
+                double gx, gy;
+                int l;
+                if (vgpu_ep_pair(xa, xb, &gx, &gy, &l)) {
+                    const unsigned to = 32 * w + (unsigned)(entry % 32);
+                    ++entry;
+                    q[l] += 1;
+                    lsx[to] = lsx[to] + gx;
+                    lsy[to] = lsy[to] + gy;
+                }
+            }
+    }
+    for (unsigned stride = 1; stride < VGPU_EP_LANES; stride *= 2)
+        for (unsigned i = 0; i < VGPU_EP_LANES; i += 2 * stride) {
+            lsx[i] = lsx[i] + lsx[i + stride];
+            lsy[i] = lsy[i] + lsy[i + stride];
+        }
+    *bsx = lsx[0];
+    *bsy = lsy[0];
+}
+
 /* Batches are independent: with OpenMP (the reference arm, oracle/Makefile.ref)
  * they run in parallel; the job sums are folded in batch order either way,
  * so the result bits do not depend on the thread count. */
-int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
+typedef void (*ep_batch_fn)(uint64_t, uint32_t, uint64_t, uint64_t, uint64_t*, double*, double*);
+
+static int ep_job(const vgpu_ep_params* p, vgpu_ep_result* r, ep_batch_fn batch) {
     memset(r, 0, sizeof *r);
     if (p->mk < 8 || p->mk > 20 || p->m < p->mk || p->m > 40 || p->reserved != 0) return -1;
     const uint64_t batches_total = 1ull << (p->m - p->mk);
@@ -76,7 +124,7 @@ int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     }
 #pragma omp parallel for schedule(dynamic, 1)
     for (long long b = 0; b < nb; ++b)
-        ep_batch(p->first_batch + (uint64_t)b, p->mk, per_lane, lane_skip, bq + 10 * b,
+        batch(p->first_batch + (uint64_t)b, p->mk, per_lane, lane_skip, bq + 10 * b,
                  bs + 2 * b, bs + 2 * b + 1);
     double jsx = 0.0, jsy = 0.0;
     for (long long b = 0; b < nb; ++b) {
@@ -92,6 +140,12 @@ int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) {
     r->n_batches = p->n_batches;
     return 0;
 }
+
+/* the kernel's order (k_ep.cuh default instance: accepted pairs compacted) */
+int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) { return ep_job(p, r, ep_batch_compact); }
+
+/* lane-sequential order (the branch-free instance, VGPU_EP_VARIANT=0..7, 11) */
+int vo_ep_job_lanes(const vgpu_ep_params* p, vgpu_ep_result* r) { return ep_job(p, r, ep_batch); }
 
 void vo_ep_log(const double* x, double* y, size_t n) {
     for (size_t i = 0; i < n; ++i) y[i] = vgpu_ep_log(x[i]);

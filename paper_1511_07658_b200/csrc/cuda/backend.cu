@@ -266,7 +266,10 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     case 5: ep_table_kernel<3, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 6: ep_table_kernel<7, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 7: ep_table_kernel<7, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    default: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 9: ep_table_kernel<3, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 10: ep_table_kernel<2, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 11: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    default: ep_table_kernel<4, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
                 }
                 ++*launches;
                 const cudaError_t e = cudaGetLastError();
