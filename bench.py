@@ -604,6 +604,8 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
         achieved = 3.0 * flops / main_s / 1e12
         r.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                   "frac": achieved / peak, "kernel_us_per_launch": main_s * 1e6,
+                  "spec_dense_tf32_tflops": 1125.0, "frac_of_spec": achieved / 1125.0,
+                  "ncu_tensor_pipe_active": "profiles/r1_ncu_mm_tc2_summary.txt (45 % at 1.76 GHz)",
                   "fp32_equiv_tflops": flops / main_s / 1e12,
                   "step_fp32_equiv_tflops": flops / (d["ms_per_step"] * 1e-3) / 1e12,
                   "algo_flops_per_launch": 3.0 * flops,

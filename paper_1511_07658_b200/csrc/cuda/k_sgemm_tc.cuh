@@ -364,6 +364,30 @@ __device__ __forceinline__ void umma2_commit_both(std::uint64_t* bar) {
         "h"(static_cast<unsigned short>(3)));
 }
 
+// arrive on the mbarrier at the same shared-memory offset in CTA 0 of the
+// cluster (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_leader(std::uint64_t* bar) {
+    asm volatile(
+        "{\n"
+        ".reg .b32 remote;\n"
+        "mapa.shared::cluster.u32 remote, %0, 0;\n"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [remote];\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     tc_gemm2_kernel(const __grid_constant__ TcTable table) {
     const TcJob& job = table.job[blockIdx.z];
@@ -382,14 +406,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     extern __shared__ __align__(1024) std::uint8_t smem_raw[];
     std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
         (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-    // bars[0..S-1]: stage free; bars[S], bars[S+1]: accumulator 0/1 chunk
-    // done (both multicast by the leader's commits)
+    // bars[0..S-1]: stage free, bars[S], bars[S+1]: accumulator 0/1 chunk
+    // done (both multicast by the leader's tcgen05.commit); full[s]: this
+    // CTA's copies of stage s landed (every thread's cp.async arrive);
+    // peer[s] (leader): the peer CTA's copies landed (relayed arrive)
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kTcStageBytes);
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages + 2);
+    std::uint64_t* full = bars + kTcStages + 2;
+    std::uint64_t* peer = full + kTcStages;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(peer + kTcStages);
 
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0) {
         for (int s = 0; s < kTcStages + 2; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], kTcThreads);
+            mbar_init(&peer[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 0) {
@@ -443,49 +475,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     };
 
     const int kblocks = n / kTcBK;
-    const int ckb = static_cast<int>(table.chunk_kb);
+    // >= 2: the copies that feed chunk c+2 are issued after the drain of
+    // chunk c (program order below), which frees its TMEM accumulator
+    const int ckb = max(2, static_cast<int>(table.chunk_kb));
+    // stage s for k-block kb: this thread's 16 copies, tracked by full[s]
+    auto fill = [&](int kb, int s) {
+        load_stage(kb, s);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s]))
+                     : "memory");
+    };
 #pragma unroll
-    for (int s = 0; s < kTcStages - 1; ++s) {
-        if (s < kblocks) load_stage(s, s);
-        cp_async_commit();
-    }
+    for (int s = 0; s < kTcStages - 1; ++s)
+        if (s < kblocks) fill(s, s);
+    // No CTA- or cluster-wide barrier in the loop: mbarriers only. The
+    // leader's thread 0 issues MMA(kb) once both CTAs' copies of k-block kb
+    // landed (own full[s] + the peer's relayed arrive), so MMAs stay queued
+    // ahead of the tensor core while the other threads drain and refill.
     for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % kTcStages;
+        const std::uint32_t ph = (kb / kTcStages) & 1;
         const int chunk = kb / ckb;
         const bool chunk_first = kb % ckb == 0;
         const bool chunk_last = (kb + 1) % ckb == 0 || kb + 1 == kblocks;
-        cp_async_wait<kTcStages - 2>();
-        asm volatile("fence.proxy.async.shared::cta;");
-        // stage s holds k-block kb in BOTH CTAs. (Measured: a per-CTA
-        // __syncthreads plus a remote mbarrier arrive / cluster-scope wait in
-        // the leader is 10 % slower than this cluster barrier.)
-        cluster_sync_all();
-        if (leader && tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
-            const std::uint32_t dacc = tmem + (chunk & 1) * kTc2BN;
+        if (tid == 0) {
+            mbar_wait(&full[s], ph);  // this CTA's stage s (acquire: copies visible)
+            asm volatile("fence.proxy.async.shared::cta;");  // -> tensor core (async proxy)
+            if (leader) {
+                mbar_wait_cluster(&peer[s], ph);  // the peer's stage s
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+                const std::uint32_t dacc = tmem + (chunk & 1) * kTc2BN;
 #pragma unroll
-            for (int k = 0; k < kTcBK / 8; ++k) {
-                const std::uint32_t off = k * 32;
-                const std::uint64_t ahi = umma_desc_k_sw128(sbase + 0 * kTcTileBytes + off);
-                const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
-                const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
-                const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
-                umma2_tf32(dacc, ahi, blo, (chunk_first && k == 0) ? 0u : 1u);
-                umma2_tf32(dacc, alo, bhi, 1u);
-                umma2_tf32(dacc, ahi, bhi, 1u);
+                for (int k = 0; k < kTcBK / 8; ++k) {
+                    const std::uint32_t off = k * 32;
+                    const std::uint64_t ahi = umma_desc_k_sw128(sbase + 0 * kTcTileBytes + off);
+                    const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
+                    const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
+                    const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
+                    umma2_tf32(dacc, ahi, blo, (chunk_first && k == 0) ? 0u : 1u);
+                    umma2_tf32(dacc, alo, bhi, 1u);
+                    umma2_tf32(dacc, ahi, bhi, 1u);
+                }
+                umma2_commit_both(&bars[s]);
+                if (chunk_last) umma2_commit_both(&bars[kTcStages + (chunk & 1)]);
+            } else {
+                mbar_arrive_leader(&peer[s]);  // relay: my stage s is ready
             }
-            umma2_commit_both(&bars[s]);
-            if (chunk_last) umma2_commit_both(&bars[kTcStages + (chunk & 1)]);
         }
+        __syncwarp();
+        // fold the previous chunk while the tensor core runs this one
+        if (chunk_first && chunk > 0) drain(chunk - 1);
+        // refill the stage MMA(kb-1) read with k-block kb + S - 1
         const int next = kb + kTcStages - 1;
         if (next < kblocks) {
             const int ns = next % kTcStages;
             if (kb >= 1) mbar_wait(&bars[ns], ((kb - 1) / kTcStages) & 1);
-            load_stage(next, ns);
+            fill(next, ns);
         }
-        cp_async_commit();
-        if (chunk_first && chunk > 0) drain(chunk - 1);
     }
     drain((kblocks - 1) / ckb);
 

@@ -315,6 +315,15 @@ TEST_CASE("[gpu] malformed inputs fail through STP with Payload, slot stays usab
     }
     VgpuHandle h = req(hub);
     CHECK(h.run_task(pack<float>({1, 2, 3, 4}), desc("vector-add")) == pack<float>({4, 6}));
+    // empty input (n = 0 is valid: no launch) and a 64-byte input, both on
+    // the inline SND path (<= 64 B snapshotted at SND, no DMA round trip)
+    CHECK(h.run_task(Bytes{}, desc("vector-add")).empty());
+    std::vector<float> v(16);
+    for (int i = 0; i < 16; ++i) v[i] = 0.5f * static_cast<float>(i);
+    const Bytes out = h.run_task(pack<float>(v), desc("vector-add"));
+    std::vector<float> want(8);
+    for (int i = 0; i < 8; ++i) want[i] = v[i] + v[8 + i];
+    CHECK(out == pack<float>(want));
 }
 
 TEST_CASE("[gpu] OS transport: forked SPMD clients through one GVM (real clock)") {
