@@ -179,3 +179,36 @@ for n in (2048, 200):
         if line.strip():
             n, err = line.split()
             assert float(err) <= 1e-5, (path, n, err)
+
+
+@pytest.mark.parametrize("sizes", [(512, 256, 768), (512, 384)])
+def test_sgemm_mixed_sizes_in_one_batch(sizes):
+    """One PS-1 batch of SGEMM jobs of different n through the GVM: every
+    n % 256 == 0 takes the CTA-pair kernel (grid sized by the largest job,
+    the smaller jobs' surplus pairs leave together), any n % 256 != 0 sends
+    the batch to the 1-CTA tensor-core kernel. Full-matrix check against
+    binary64 at the FP32 bar."""
+    rng = np.random.default_rng(sum(sizes))
+    mats = [(rng.uniform(-1, 1, (n, n)).astype(np.float32),
+             rng.uniform(-1, 1, (n, n)).astype(np.float32)) for n in sizes]
+    d, inst = _gvm(len(sizes), 8 * max(sizes) ** 2)
+    with d:
+        outs = [None] * len(sizes)
+
+        def worker(i):
+            h = V.req(inst)
+            A, B = mats[i]
+            outs[i] = h.run_task(A.tobytes() + B.tobytes(), V.KernelDescriptor("sgemm", 670, 344, 335))
+            h.rls()
+            h.close()
+
+        ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(sizes))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    for (A, B), out, n in zip(mats, outs, sizes):
+        C = np.frombuffer(out, np.float32).reshape(n, n)
+        ref = A.astype(np.float64) @ B.astype(np.float64)
+        err = np.linalg.norm(C - ref) / np.linalg.norm(ref)
+        assert err <= 1e-5, (n, err)
