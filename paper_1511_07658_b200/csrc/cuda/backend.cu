@@ -352,7 +352,7 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     }();
                     if (!attr) return cudaErrorInvalidConfiguration;
                     if (g_sgemm_phases & 1u) {
-                        tc_split_kernel<<<dim3(maxn / 32, maxn / 32, tt.njobs), dim3(32, 8), 0, s>>>(tt);
+                        tc_split_kernel<<<dim3(maxn / 64, maxn / 64, tt.njobs), 256, 0, s>>>(tt);
                         ++*launches;
                     }
                     if (g_sgemm_phases & 2u) {

@@ -76,31 +76,54 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
     lo = __fsub_rn(x, hi);
 }
 
-// grid (n/32, n/32, jobs), block (32, 8)
+// grid (n/64, n/64, jobs), 256 threads; n % 128 == 0 for this path. A 64x64
+// tile per CTA, 128-bit loads and stores throughout (the pass is HBM-bound:
+// 4 bytes read, 8 written per element of A and of B).
 __global__ void __launch_bounds__(256) tc_split_kernel(const __grid_constant__ TcTable table) {
     const TcJob& job = table.job[blockIdx.z];
     const int n = static_cast<int>(job.n);
-    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    const int bx = blockIdx.x * 64, by = blockIdx.y * 64;
     if (bx >= n || by >= n) return;
-    __shared__ float tile[32][33];
-    // A: straight split (rows by..by+31, cols bx..bx+31)
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const std::size_t idx = static_cast<std::size_t>(by + r) * n + bx + threadIdx.x;
-        float hi, lo;
-        tf32_split(job.A[idx], hi, lo);
-        job.ahi[idx] = hi;
-        job.alo[idx] = lo;
+    const int t = threadIdx.x;
+    const int c4 = (t & 15) * 4;  // 16 threads x 4 columns = 64 columns
+    const int r0 = t >> 4;        // 16 rows per pass, 4 passes
+    // A: straight split, rows by.., cols bx..
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const std::size_t idx = static_cast<std::size_t>(by + r0 + 16 * k) * n + bx + c4;
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(job.A + idx));
+        float4 h, l;
+        tf32_split(v.x, h.x, l.x);
+        tf32_split(v.y, h.y, l.y);
+        tf32_split(v.z, h.z, l.z);
+        tf32_split(v.w, h.w, l.w);
+        *reinterpret_cast<float4*>(job.ahi + idx) = h;
+        *reinterpret_cast<float4*>(job.alo + idx) = l;
     }
     // B: transpose through shared memory; Bt[c][r] = B[r][c]
-    for (int r = threadIdx.y; r < 32; r += 8)
-        tile[r][threadIdx.x] = job.B[static_cast<std::size_t>(by + r) * n + bx + threadIdx.x];
+    __shared__ float tile[64][65];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int r = r0 + 16 * k;
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(
+            job.B + static_cast<std::size_t>(by + r) * n + bx + c4));
+        tile[r][c4] = v.x;
+        tile[r][c4 + 1] = v.y;
+        tile[r][c4 + 2] = v.z;
+        tile[r][c4 + 3] = v.w;
+    }
     __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const std::size_t idx = static_cast<std::size_t>(bx + r) * n + by + threadIdx.x;
-        float hi, lo;
-        tf32_split(tile[threadIdx.x][r], hi, lo);
-        job.bthi[idx] = hi;
-        job.btlo[idx] = lo;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int c = r0 + 16 * k;  // column of B = row of Bt
+        float4 h, l;
+        tf32_split(tile[c4][c], h.x, l.x);
+        tf32_split(tile[c4 + 1][c], h.y, l.y);
+        tf32_split(tile[c4 + 2][c], h.z, l.z);
+        tf32_split(tile[c4 + 3][c], h.w, l.w);
+        const std::size_t idx = static_cast<std::size_t>(bx + c) * n + by + c4;
+        *reinterpret_cast<float4*>(job.bthi + idx) = h;
+        *reinterpret_cast<float4*>(job.btlo + idx) = l;
     }
 }
 
