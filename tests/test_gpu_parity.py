@@ -212,3 +212,34 @@ def test_sgemm_mixed_sizes_in_one_batch(sizes):
         ref = A.astype(np.float64) @ B.astype(np.float64)
         err = np.linalg.norm(C - ref) / np.linalg.norm(ref)
         assert err <= 1e-5, (n, err)
+
+
+@pytest.mark.parametrize("variant", [None, "11"])
+def test_ep_kernel_instances_match_their_oracle_order(variant):
+    """The default EP instance (accepted pairs compacted per warp) and the
+    branch-free instance (VGPU_EP_VARIANT=11, lane-sequential sums) are each
+    bit-exact against the oracle restating their reduction order, in a fresh
+    process (the instance is chosen once per process)."""
+    import subprocess
+    import sys
+    code = r'''
+import os
+from oracle import oracle
+from paper_1511_07658_b200 import vgpu as V
+lanes = os.environ.get("VGPU_EP_VARIANT") == "11"
+for m, first, count in ((24, 0, 256), (28, 1536, 512), (20, 3, 5)):
+    got = oracle.ep_from_bytes(V.native_run_task(oracle.ep_params_bytes(m, first, count),
+                                                 V.KernelDescriptor("nas-ep")))
+    want = oracle.ep_job(m, first, count, lanes=lanes)
+    print(m, first, count, bytes(got) == bytes(want))
+'''
+    env = dict(os.environ)
+    env.pop("VGPU_EP_VARIANT", None)
+    if variant:
+        env["VGPU_EP_VARIANT"] = variant
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l.split() for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 3 and all(l[-1] == "True" for l in lines), out.stdout
