@@ -22,6 +22,10 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
 CXXFLAGS := -O2 -g -std=c++20 -fPIC -Wall -Wextra -pthread -Iinclude
 CFLAGS   := -O2 -g -fPIC -ffp-contract=off -std=c11 -Wall -Wextra -Wno-unknown-pragmas
+# the oracle's batch loops are OpenMP-parallel when the system gcc has libgomp
+# (the image's CC wrapper does not); results do not depend on the thread count
+OCC      := $(shell test -x /usr/bin/gcc && echo /usr/bin/gcc || echo $(CC))
+OMP      := $(shell echo 'int main(void){return 0;}' | $(OCC) -fopenmp -x c - -o /dev/null 2>/dev/null && echo -fopenmp)
 
 HOST_SRC := $(wildcard $(CSRC)/host/*.cpp)
 HOST_OBJ := $(patsubst $(CSRC)/host/%.cpp,$(OBJDIR)/host/%.o,$(HOST_SRC))
@@ -70,7 +74,7 @@ oracle: oracle/_build/libvgpu_oracle.so
 
 oracle/_build/libvgpu_oracle.so: oracle/vgpu_oracle.c oracle/vgpu_oracle.h $(wildcard $(CSRC)/common/*.h)
 	@mkdir -p oracle/_build
-	$(CC) $(CFLAGS) -shared -o $@ oracle/vgpu_oracle.c -lm
+	$(OCC) $(CFLAGS) $(OMP) -shared -o $@ oracle/vgpu_oracle.c -lm
 
 ref:
 	$(MAKE) -f oracle/Makefile.ref

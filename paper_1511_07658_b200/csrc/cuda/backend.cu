@@ -269,6 +269,7 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     case 9: ep_table_kernel<3, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 10: ep_table_kernel<2, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 11: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    case 12: ep_table_kernel<4, 1, true, false><<<ctas, kEpThreads, 0, s>>>(t); break;
                     default: ep_table_kernel<4, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
                 }
                 ++*launches;

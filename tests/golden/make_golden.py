@@ -3,7 +3,7 @@
 ref_vector_ops.bin  written by oracle/_ref/ref-golden, i.e. by the UNMODIFIED
                     reference library's own vector-add / vector-scale
                     payloads (proj/src/payload.cpp) on mt19937(41) inputs.
-ep_oracle.json      the oracle's NAS EP results for classes S, W, A with
+ep_oracle.json      the oracle's NAS EP results for classes S, W, A, B with
                     bit patterns (the GPU must match them exactly) next to
                     NPB's published verification sums (the oracle must match
                     those within NPB's epsilon 1e-8).
@@ -30,7 +30,7 @@ def bits(x: float) -> str:
 def main() -> None:
     subprocess.run([oracle.ref_tool("ref-golden"), HERE], check=True)
     out = {}
-    for m in (24, 25, 28):
+    for m in (24, 25, 28, 30):  # classes S, W, A, B
         r = oracle.ep_job(m, 0, 1 << (m - 16))
         sxv, syv = oracle.NPB_VERIFY[m]
         out[str(m)] = {

@@ -88,6 +88,23 @@ def test_c2_nas_ep_class_a_over_8_processes():
     assert abs((f.sx - sxv) / sxv) < 1e-8 and abs((f.sy - syv) / syv) < 1e-8
 
 
+def test_ep_class_b_bit_exact_through_the_gvm():
+    """NAS EP class B (m = 30: 2^30 pairs, 843,345,606 accepted; every
+    log, division and square root of them) as one job through the GVM:
+    bit-identical to the oracle fixture, and NPB's class B sums."""
+    fx = json.load(open(os.path.join(GOLD, "ep_oracle.json")))["30"]
+    d, inst = _gvm(1, 4096)
+    with d:
+        (out,) = _spmd(inst, [oracle.ep_params_bytes(30, 0, 1 << 14)],
+                       V.KernelDescriptor("nas-ep", 1, 4096, 1))
+    r = oracle.ep_from_bytes(out)
+    assert list(r.q) == fx["q"] and r.pairs == fx["pairs"] == 843345606
+    assert struct.pack("<d", r.sx).hex() == fx["sx_bits"]
+    assert struct.pack("<d", r.sy).hex() == fx["sy_bits"]
+    sxv, syv = oracle.NPB_VERIFY[30]
+    assert abs((r.sx - sxv) / sxv) < 1e-8 and abs((r.sy - syv) / syv) < 1e-8
+
+
 def test_c3_black_scholes_4m_options():
     n = 4 << 20
     rng = np.random.default_rng(5347)

@@ -67,7 +67,7 @@ def test_ep_class_s_matches_npb_verification():
 
 def test_ep_fixtures_consistent_with_npb_and_oracle():
     fx = json.load(open(os.path.join(GOLD, "ep_oracle.json")))
-    for m in ("24", "25", "28"):
+    for m in ("24", "25", "28", "30"):
         e = fx[m]
         assert abs((e["sx"] - e["npb_sx"]) / e["npb_sx"]) < 1e-8
         assert abs((e["sy"] - e["npb_sy"]) / e["npb_sy"]) < 1e-8
