@@ -500,6 +500,11 @@ struct Op {
     cudaEvent_t ev[kEvCount] = {};
     bool has_h2d = false, has_comp = false;
     cudaEvent_t comp0 = nullptr, comp1 = nullptr;
+    cudaEvent_t d2h0 = nullptr;  // D2H start (an alias of comp1 / the input-ready event
+                                 // when nothing separates them on the slot's stream)
+    bool mapped_out = false;     // the kernel wrote the result straight into host memory
+    bool grouped = false;        // launched in a PS-1 group on another stream
+    cudaEvent_t in_ready() const { return has_h2d ? ev[kEvH2d1] : ev[kEvH2d0]; }
     cudaEvent_t last() const { return kind == VGPU_CU_DONE_UPLOAD ? ev[kEvH2d1] : ev[kEvD2h1]; }
 };
 
@@ -511,6 +516,8 @@ struct SlotState {
     std::uint8_t* d_scratch = nullptr;
     std::uint8_t* d_ws = nullptr;
     void* reg_base = nullptr;
+    std::uint8_t* reg_dev = nullptr;  // device alias of the registered region (mapped)
+    std::uint64_t reg_bytes = 0;
     bool task_busy = false;
     std::uint32_t ops_in_flight = 0;
 };
@@ -793,10 +800,17 @@ int vgpu_cu_register_region(vgpu_cu_dev* d, std::uint32_t slot, void* base, std:
     if (s.reg_base) {
         cudaHostUnregister(s.reg_base);
         s.reg_base = nullptr;
+        s.reg_dev = nullptr;
+        s.reg_bytes = 0;
     }
     if (bytes == 0) return VGPU_CU_OK;
-    CK(cudaHostRegister(base, bytes, cudaHostRegisterPortable));
+    CK(cudaHostRegister(base, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
     s.reg_base = base;
+    s.reg_bytes = bytes;
+    void* dev = nullptr;
+    s.reg_dev = cudaHostGetDevicePointer(&dev, base, 0) == cudaSuccess
+                    ? static_cast<std::uint8_t*>(dev)
+                    : (cudaGetLastError(), nullptr);
     return VGPU_CU_OK;
 }
 
@@ -904,7 +918,15 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         j.out_bytes = need;
         j.scratch = s.d_scratch;
         j.ws = s.d_ws;
-        if (t.kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, t.h_in, sizeof j.ep);
+        if (t.kernel == VGPU_CU_K_EP) {
+            std::memcpy(&j.ep, t.h_in, sizeof j.ep);
+            // the 112-byte result goes straight into the client's region
+            // (mapped, written over PCIe by the kernel): no D2H copy
+            const auto* ho = static_cast<const std::uint8_t*>(t.h_out);
+            const auto* rb = static_cast<const std::uint8_t*>(s.reg_base);
+            if (s.reg_dev && ho >= rb && ho + need <= rb + s.reg_bytes)
+                j.out = s.reg_dev + (ho - rb);
+        }
     }
     CK(cudaSetDevice(d->device));
 
@@ -939,17 +961,26 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         cudaError_t err = cudaEventRecord(op->ev[kEvH2d0], s.stream);
         if (err == cudaSuccess && op->has_h2d)
             err = cudaMemcpyAsync(s.d_in, t.h_in, t.in_bytes, cudaMemcpyHostToDevice, s.stream);
-        if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+        if (err == cudaSuccess && op->has_h2d) err = cudaEventRecord(op->ev[kEvH2d1], s.stream);
         if (op->has_h2d) d->h2d_bytes += t.in_bytes;
+        op->mapped_out = jobs[i].out != s.d_out;
         return err;
     };
-    auto d2h = [&](std::uint32_t i) -> cudaError_t {
+    // own: the task's kernel (or its H2D, for identity) is the previous work
+    // on its stream, so the D2H start is that event, not a new one
+    auto d2h = [&](std::uint32_t i, bool own) -> cudaError_t {
         const vgpu_cu_task& t = tasks[i];
         SlotState& s = d->slots[t.slot];
         Op* op = ops[i];
-        const std::uint64_t bytes = jobs[i].out_bytes;
+        const std::uint64_t bytes = op->mapped_out ? 0 : jobs[i].out_bytes;
         const std::uint8_t* src = t.kernel == VGPU_CU_K_IDENTITY ? s.d_in : s.d_out;
-        cudaError_t err = cudaEventRecord(op->ev[kEvD2h0], s.stream);
+        cudaError_t err = cudaSuccess;
+        if (own) {
+            op->d2h0 = op->has_comp ? op->comp1 : op->in_ready();
+        } else {
+            op->d2h0 = op->ev[kEvD2h0];
+            err = cudaEventRecord(op->d2h0, s.stream);
+        }
         if (err == cudaSuccess && bytes)
             err = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
         if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvD2h1], s.stream);
@@ -968,11 +999,10 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         Op* op = ops[i];
         if (t.kernel == VGPU_CU_K_IDENTITY) return cudaSuccess;  // D2H reads d_in
         op->has_comp = true;
-        op->comp0 = op->ev[kEvC0];
+        op->comp0 = op->in_ready();  // nothing between the H2D (or start) and the launch
         op->comp1 = op->ev[kEvC1];
         std::uint64_t l = 0;
-        cudaError_t err = cudaEventRecord(op->comp0, s.stream);
-        if (err == cudaSuccess) err = launch_jobs(t.kernel, &jobs[i], 1, s.stream, &l);
+        cudaError_t err = launch_jobs(t.kernel, &jobs[i], 1, s.stream, &l);
         if (err == cudaSuccess) err = cudaEventRecord(op->comp1, s.stream);
         d->launches += l;
         return err;
@@ -983,7 +1013,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) {
             e = h2d(i);
             if (e == cudaSuccess) e = compute_own(i);
-            if (e == cudaSuccess) e = d2h(i);
+            if (e == cudaSuccess) e = d2h(i, true);
             if (e == cudaSuccess) enqueued.push_back(i);
         }
     } else if (e == cudaSuccess) {  // PS-1: all sends, one launch per kernel kind, all retrieves
@@ -1006,7 +1036,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             rec.pooled.push_back(g0);
             rec.pooled.push_back(g1);
             for (std::size_t g = 1; g < group.size() && e == cudaSuccess; ++g)
-                e = cudaStreamWaitEvent(lead.stream, ops[group[g]]->ev[kEvH2d1], 0);
+                e = cudaStreamWaitEvent(lead.stream, ops[group[g]]->in_ready(), 0);
             std::vector<DevJob> gj;
             for (auto i : group) gj.push_back(jobs[i]);
             std::uint64_t l = 0;
@@ -1018,13 +1048,14 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             for (auto i : group) {
                 SlotState& s = d->slots[tasks[i].slot];
                 ops[i]->has_comp = true;
+                ops[i]->grouped = true;
                 ops[i]->comp0 = g0;
                 ops[i]->comp1 = g1;
                 if (e == cudaSuccess && &s != &lead) e = cudaStreamWaitEvent(s.stream, g1, 0);
             }
         }
         for (std::uint32_t i = 0; i < n && e == cudaSuccess; ++i) {
-            e = d2h(i);
+            e = d2h(i, !ops[i]->grouped);
             if (e == cudaSuccess) enqueued.push_back(i);
         }
     }
@@ -1065,7 +1096,7 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
         return;
     }
     r.comp_us = op->has_comp ? 1000.0f * elapsed_ms(op->comp0, op->comp1) : 0.0f;
-    r.d2h_us = 1000.0f * elapsed_ms(op->ev[kEvD2h0], op->ev[kEvD2h1]);
+    r.d2h_us = 1000.0f * elapsed_ms(op->d2h0 ? op->d2h0 : op->ev[kEvD2h0], op->ev[kEvD2h1]);
     r.span_us = 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvD2h1]);
     auto it = d->batches.find(op->batch);
     if (it != d->batches.end()) {
