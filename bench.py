@@ -605,7 +605,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
         r.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                   "frac": achieved / peak, "kernel_us_per_launch": main_s * 1e6,
                   "spec_dense_tf32_tflops": 1125.0, "frac_of_spec": achieved / 1125.0,
-                  "ncu_tensor_pipe_active": "profiles/r1_ncu_mm_tc2_summary.txt (45 % at 1.76 GHz)",
+                  "ncu_summary": "profiles/r1_ncu_mm_tc2_summary.txt",
                   "fp32_equiv_tflops": flops / main_s / 1e12,
                   "step_fp32_equiv_tflops": flops / (d["ms_per_step"] * 1e-3) / 1e12,
                   "algo_flops_per_launch": 3.0 * flops,
@@ -613,8 +613,8 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                                   if bf16 else "fallback: 2250 / 2 TFLOP/s nominal dense TF32"),
                   "precision": "3xTF32 tcgen05 (chunked TMEM accumulation): rel. Frobenius "
                                "4.8e-7 at 2048^2 on B200, bar 1e-5 vs binary64",
-                  "step_kernels": "tc_split_kernel (hi/lo split + B transpose) + tc_gemm2_kernel "
-                                  "(CTA pair, tcgen05.mma.cta_group::2, 256x256 tiles); "
+                  "step_kernels": "tc_split_kernel (hi/lo split + B transpose) + tc_gemm2_tma_kernel "
+                                  "(CTA pair, tcgen05.mma.cta_group::2, 256x256 tiles, TMA loads); "
                                   "achieved/kernel_us are the GEMM's"})
         return r
     if bound == "fp32":

@@ -20,6 +20,7 @@
 //     hosts also held the slot's stream — and turns the events into
 //     per-stage times (the paper's t_in / t_comp / t_out) and batch spans.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -182,6 +183,72 @@ cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, cudaStream_t s,
 }
 
 // Launch every job (all of one kernel kind) on `s`; counts launches.
+// ---- TMA tensor maps for the CTA-pair SGEMM ----------------------------------------
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link): resolved once, null when the driver lacks it
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// VGPU_SGEMM_TMA=0 keeps the cp.async operand loads of the pair kernel.
+bool sgemm_tma() {
+    static const bool t = [] {
+        const char* e = std::getenv("VGPU_SGEMM_TMA");
+        return !(e && std::strcmp(e, "0") == 0) && tensor_map_encoder() != nullptr;
+    }();
+    return t;
+}
+
+// n x n fp32 row-major matrix as 128-row x 32-float tiles, 128-byte swizzle
+// (the canonical K-major SW128 layout of the UMMA descriptors)
+bool encode_tile_map(CUtensorMap* map, const float* base, std::uint32_t n) {
+    const cuuint64_t dims[2] = {n, n};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * sizeof(float)};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    return tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_tc2_tma(const vgk::TcTable& tt, std::uint32_t maxn, cudaStream_t s) {
+    using namespace vgk;
+    static bool attr = [] {
+        return cudaFuncSetAttribute(tc_gemm2_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kTcSmemBytes) == cudaSuccess;
+    }();
+    if (!attr) return cudaErrorInvalidConfiguration;
+    const std::uint32_t pn = maxn / kTc2BN;
+    for (std::uint32_t b = 0; b < tt.njobs; b += kMaxTc2TmaJobs) {
+        TcTmaTable t{};
+        t.njobs = std::min<std::uint32_t>(kMaxTc2TmaJobs, tt.njobs - b);
+        t.chunk_kb = tt.chunk_kb;
+        for (std::uint32_t i = 0; i < t.njobs; ++i) {
+            const TcJob& j = tt.job[b + i];
+            t.job[i] = j;
+            if (!encode_tile_map(&t.maps[i][0], j.ahi, j.n) || !encode_tile_map(&t.maps[i][1], j.alo, j.n) ||
+                !encode_tile_map(&t.maps[i][2], j.bthi, j.n) || !encode_tile_map(&t.maps[i][3], j.btlo, j.n))
+                return cudaErrorInvalidValue;
+        }
+        tc_gemm2_tma_kernel<<<dim3(2 * pn * pn, 1, t.njobs), kTcThreads, kTcSmemBytes, s>>>(t);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 // SGEMM tensor-core phases launch_jobs issues: 1 = split/transpose pre-pass,
 // 2 = tcgen05 GEMM, 3 = both (the product path). Only the resident
 // measurement (VGPU_CU_RESIDENT_MAIN_ONLY) narrows it, on its own thread.
@@ -357,10 +424,15 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                         ++*launches;
                     }
                     if (g_sgemm_phases & 2u) {
+                        cudaError_t e2 = cudaSuccess;
                         bool pair = sgemm_pair();
                         for (std::uint32_t i = 0; i < tt.njobs && pair; ++i)
                             pair = tt.job[i].n % kTc2BN == 0;
-                        if (pair) {
+                        if (pair && sgemm_tma()) {
+                            e2 = launch_tc2_tma(tt, maxn, s);
+                            if (e2 != cudaSuccess) return e2;
+                            *launches += (tt.njobs + kMaxTc2TmaJobs - 1) / kMaxTc2TmaJobs - 1;
+                        } else if (pair) {
                             static bool attr2 = [] {
                                 return cudaFuncSetAttribute(tc_gemm2_kernel,
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize,

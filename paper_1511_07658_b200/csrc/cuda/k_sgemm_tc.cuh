@@ -34,6 +34,8 @@
 //     epilogue stores those registers.
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 namespace vgk {
@@ -565,6 +567,172 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         *reinterpret_cast<float4*>(crow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
     asm volatile("tcgen05.fence::before_thread_sync;");
     cluster_sync_all();  // both CTAs done with the pair's TMEM
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+
+// ---- CTA pair with TMA operand loads ------------------------------------------------
+//
+// Same pair / chunking / accumulation as tc_gemm2_kernel, but each CTA's
+// thread 0 fetches a stage with four TMA tile loads (cp.async.bulk.tensor,
+// 128 rows x 128 bytes, SWIZZLE_128B: the canonical K-major layout the UMMA
+// descriptors expect) on a 64 KiB expect_tx mbarrier, instead of 256
+// threads issuing 4096 16-byte cp.async copies. The other threads only
+// drain accumulators. Tensor maps (4 per job: A_hi, A_lo, B^T_hi, B^T_lo)
+// travel in the kernel's parameter space.
+constexpr int kMaxTc2TmaJobs = 16;
+
+struct alignas(64) TcTmaTable {
+    CUtensorMap maps[kMaxTc2TmaJobs][4];
+    TcJob job[kMaxTc2TmaJobs];
+    std::uint32_t njobs;
+    std::uint32_t chunk_kb;
+};
+
+__device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    tc_gemm2_tma_kernel(const __grid_constant__ TcTmaTable table) {
+    const TcJob& job = table.job[blockIdx.z];
+    const CUtensorMap* maps = table.maps[blockIdx.z];
+    const int n = static_cast<int>(job.n);
+    std::uint32_t rank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int pair = blockIdx.x >> 1, pairs_n = n / kTc2BN;
+    const int pm = pair / max(1, pairs_n), pn = pair % max(1, pairs_n);
+    if (pairs_n == 0 || pm * kTc2BN >= n) return;
+    const int m0 = pm * kTc2BN + static_cast<int>(rank) * kTcBM;
+    const int nb = pn * kTc2BN + static_cast<int>(rank) * kTcBM;
+    const int c0 = pn * kTc2BN;
+    const bool leader = rank == 0;
+
+    extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+    std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+        (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kTcStageBytes);
+    std::uint64_t* full = bars + kTcStages + 2;
+    std::uint64_t* peer = full + kTcStages;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(peer + kTcStages);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < kTcStages + 2; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&peer[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        for (int t = 0; t < 4; ++t)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&maps[t])));
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const std::uint32_t tmem = *tmem_slot;
+
+    const int quad = warp & 3, half = warp >> 2;
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+    auto drain = [&](int chunk) {
+        mbar_wait(&bars[kTcStages + (chunk & 1)], (chunk >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const std::uint32_t base = tmem + (static_cast<std::uint32_t>(quad * 32) << 16) +
+                                   (chunk & 1) * kTc2BN + half * 128;
+        float v[32];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            tmem_ld32(base + h * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[h * 32 + j] = __fadd_rn(acc[h * 32 + j], v[j]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
+
+    const int kblocks = n / kTcBK;
+    const int ckb = max(2, static_cast<int>(table.chunk_kb));
+    // thread 0: stage s <- k-block kb (A rows m0.., B^T rows nb..), 64 KiB
+    auto fill = [&](int kb, int s) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"(kTcStageBytes)
+                     : "memory");
+        const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+        tma_load_2d(sbase + 0 * kTcTileBytes, &maps[0], kb * kTcBK, m0, &full[s]);
+        tma_load_2d(sbase + 1 * kTcTileBytes, &maps[1], kb * kTcBK, m0, &full[s]);
+        tma_load_2d(sbase + 2 * kTcTileBytes, &maps[2], kb * kTcBK, nb, &full[s]);
+        tma_load_2d(sbase + 3 * kTcTileBytes, &maps[3], kb * kTcBK, nb, &full[s]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < kTcStages - 1; ++s)
+            if (s < kblocks) fill(s, s);
+    for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % kTcStages;
+        const std::uint32_t ph = (kb / kTcStages) & 1;
+        const int chunk = kb / ckb;
+        const bool chunk_first = kb % ckb == 0;
+        const bool chunk_last = (kb + 1) % ckb == 0 || kb + 1 == kblocks;
+        if (tid == 0) {
+            mbar_wait(&full[s], ph);  // TMA bytes of my stage s landed
+            if (leader) {
+                mbar_wait_cluster(&peer[s], ph);  // the peer's stage s
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const std::uint32_t sbase = smem_u32(smem + s * kTcStageBytes);
+                const std::uint32_t dacc = tmem + (chunk & 1) * kTc2BN;
+#pragma unroll
+                for (int k = 0; k < kTcBK / 8; ++k) {
+                    const std::uint32_t off = k * 32;
+                    const std::uint64_t ahi = umma_desc_k_sw128(sbase + 0 * kTcTileBytes + off);
+                    const std::uint64_t alo = umma_desc_k_sw128(sbase + 1 * kTcTileBytes + off);
+                    const std::uint64_t bhi = umma_desc_k_sw128(sbase + 2 * kTcTileBytes + off);
+                    const std::uint64_t blo = umma_desc_k_sw128(sbase + 3 * kTcTileBytes + off);
+                    umma2_tf32(dacc, ahi, blo, (chunk_first && k == 0) ? 0u : 1u);
+                    umma2_tf32(dacc, alo, bhi, 1u);
+                    umma2_tf32(dacc, ahi, bhi, 1u);
+                }
+                umma2_commit_both(&bars[s]);
+                if (chunk_last) umma2_commit_both(&bars[kTcStages + (chunk & 1)]);
+            } else {
+                mbar_arrive_leader(&peer[s]);
+            }
+        }
+        __syncwarp();
+        // all threads: fold the previous chunk while the tensor core runs this one
+        if (chunk_first && chunk > 0) drain(chunk - 1);
+        const int next = kb + kTcStages - 1;
+        if (next < kblocks) {
+            // k-block `next` opens chunk c' whose accumulator chunk c'-2 used:
+            // every thread must be past drain(c'-2) (done at iteration
+            // next - ckb <= kb) before that refill can let the MMA overwrite it
+            if (next % ckb == 0 && next / ckb >= 2) __syncthreads();
+            if (tid == 0) {
+                if (kb >= 1) mbar_wait(&bars[next % kTcStages], ((kb - 1) / kTcStages) & 1);
+                fill(next, next % kTcStages);
+            }
+        }
+    }
+    drain((kblocks - 1) / ckb);
+
+    const int row = m0 + quad * 32 + (tid & 31);
+    float* crow = job.C + static_cast<std::size_t>(row) * n + c0 + half * 128;
+#pragma unroll
+    for (int j = 0; j < 128; j += 4)
+        *reinterpret_cast<float4*>(crow + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
