@@ -144,7 +144,7 @@ static int ep_job(const vgpu_ep_params* p, vgpu_ep_result* r, ep_batch_fn batch)
 /* the kernel's order (k_ep.cuh default instance: accepted pairs compacted) */
 int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r) { return ep_job(p, r, ep_batch_compact); }
 
-/* lane-sequential order (the branch-free instance, VGPU_EP_VARIANT=0..7, 11) */
+/* lane-sequential order (the branch-free instance, VGPU_EP_VARIANT=11) */
 int vo_ep_job_lanes(const vgpu_ep_params* p, vgpu_ep_result* r) { return ep_job(p, r, ep_batch); }
 
 void vo_ep_log(const double* x, double* y, size_t n) {

@@ -42,7 +42,7 @@ void vo_vector_scale(float* out, const float* in, float factor, size_t n);
  * in a binary tree, batches accumulate sequentially in batch order. */
 /* NAS EP job in the kernel's reduction order (accepted pairs compacted per
  * warp); vo_ep_job_lanes: the lane-sequential order of the
- * branch-free kernel instance (VGPU_EP_VARIANT=0..7, 11) */
+ * branch-free kernel instance (VGPU_EP_VARIANT=11) */
 int vo_ep_job(const vgpu_ep_params* p, vgpu_ep_result* r);
 int vo_ep_job_lanes(const vgpu_ep_params* p, vgpu_ep_result* r);
 /* Fold job results in order (the GVM / rank-order host fold). */

@@ -131,8 +131,8 @@ bool sgemm_use_tc() {
     return tc;
 }
 
-// EP kernel instance (k_ep.cuh template: min blocks per SM, unroll);
-// VGPU_EP_VARIANT selects the alternatives for measurement.
+// EP kernel instance (k_ep.cuh template); VGPU_EP_VARIANT=11 / 12 select
+// the measured alternatives.
 int ep_variant() {
     static const int v = [] {
         const char* e = std::getenv("VGPU_EP_VARIANT");
@@ -326,15 +326,9 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 }
                 if (!ctas) continue;
                 switch (ep_variant()) {
-                    case 1: ep_table_kernel<6, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 2: ep_table_kernel<4, 4><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 3: ep_table_kernel<6, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 4: ep_table_kernel<8, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 5: ep_table_kernel<3, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 6: ep_table_kernel<7, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 7: ep_table_kernel<7, 1><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 9: ep_table_kernel<3, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
-                    case 10: ep_table_kernel<2, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
+                    // measured alternatives: the branch-free
+                    // lane-order instance, and compaction with the
+                    // __ddiv_rn / __dsqrt_rn intrinsics
                     case 11: ep_table_kernel<5, 2><<<ctas, kEpThreads, 0, s>>>(t); break;
                     case 12: ep_table_kernel<4, 1, true, false><<<ctas, kEpThreads, 0, s>>>(t); break;
                     default: ep_table_kernel<4, 1, true><<<ctas, kEpThreads, 0, s>>>(t); break;
@@ -559,7 +553,7 @@ NcclApi& nccl() {
 
 // ---- the device handle ----------------------------------------------------------
 
-enum { kEvH2d0, kEvH2d1, kEvC0, kEvC1, kEvD2h0, kEvD2h1, kEvCount };
+enum { kEvH2d0, kEvH2d1, kEvC1, kEvD2h0, kEvD2h1, kEvCount };
 
 // One stream operation in flight: a task (H2D -> kernel -> D2H) or an eager
 // upload (H2D at SND time). poll() reports it once its final event completed.
