@@ -664,8 +664,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     };
 
     const int kblocks = n / kTcBK;
-    const int ckb = max(2, static_cast<int>(table.chunk_kb));
-    // thread 0: stage s <- k-block kb (A rows m0.., B^T rows nb..), 64 KiB
+    // >= 4: a chunk-opening refill (issued right after the MMAs, before
+    // this iteration's drain) then targets an accumulator whose drain ran
+    // two or more iterations earlier; the __syncthreads below covers it
+    const int ckb = max(4, static_cast<int>(table.chunk_kb));
+    // stage s <- k-block kb (A rows m0.., B^T rows nb..), 64 KiB
     auto fill = [&](int kb, int s) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                      "r"(kTcStageBytes)
@@ -710,19 +713,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
         }
         __syncwarp();
-        // all threads: fold the previous chunk while the tensor core runs this one
-        if (chunk_first && chunk > 0) drain(chunk - 1);
+        // refill the stage MMA(kb-1) read with k-block kb + S - 1 (warp 1's
+        // lane 0, so the MMA issue in warp 0 never waits behind it). When
+        // that k-block opens chunk c', chunk c'-2's accumulator must be
+        // drained by every thread first: drain(c'-2) ran at iteration
+        // next - ckb <= kb - 2, and this barrier gathers the CTA.
         const int next = kb + kTcStages - 1;
         if (next < kblocks) {
-            // k-block `next` opens chunk c' whose accumulator chunk c'-2 used:
-            // every thread must be past drain(c'-2) (done at iteration
-            // next - ckb <= kb) before that refill can let the MMA overwrite it
             if (next % ckb == 0 && next / ckb >= 2) __syncthreads();
-            if (tid == 0) {
+            if (tid == 32) {
                 if (kb >= 1) mbar_wait(&bars[next % kTcStages], ((kb - 1) / kTcStages) & 1);
                 fill(next, next % kTcStages);
             }
+            __syncwarp();
         }
+        // all threads: fold the previous chunk while the tensor core runs this one
+        if (chunk_first && chunk > 0) drain(chunk - 1);
     }
     drain((kblocks - 1) / ckb);
 
