@@ -13,11 +13,17 @@
 // chunk. Checked at relative Frobenius <= 1e-5 against the binary64 oracle
 // (the SIMT kernel's bar). VGPU_SGEMM=simt selects the FP32 SIMT kernel.
 //
+// Three GEMM kernels (backend.cu launch_jobs picks one per batch):
+//   tc_gemm2_tma_kernel  default when every n % 256 == 0: CTA pair
+//                        (cta_group::2, 256 x 256 tiles), TMA operand loads
+//   tc_gemm2_kernel      the same pair with cp.async loads (VGPU_SGEMM_TMA=0)
+//   tc_gemm_kernel       one CTA, 128 x 128 tiles (n % 128 == 0; VGPU_SGEMM=tc)
+//
 // Pre-pass (tc_split_kernel): A -> A_hi, A_lo (row-major M x K = K-major);
-// B -> B_hi^T, B_lo^T (N x K, K-major) through a 32x32 shared-memory
+// B -> B_hi^T, B_lo^T (N x K, K-major) through a 64x64 shared-memory
 // transpose, so both UMMA operands are K-major.
 //
-// Main kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 256
+// 1-CTA kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 256
 // threads, tiles of every task of a batch in one launch (blockIdx.z = task):
 //   * 3-stage cp.async pipeline; each stage holds the four 128 x 32 fp32
 //     operand tiles (A_hi, A_lo, B_hi, B_lo; 16 KiB each) in the canonical
