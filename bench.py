@@ -865,7 +865,9 @@ def main():
     record = R.record_from_workers(e2e["results"])
     try:
         folded, rank0, us = final_reduce(N, dist, record)
-        reduce_info = {"collective": f"ncclAllGather of {R.REC_WIDTH * 8} B per GPU "
+        via = ("torch.distributed all_gather over gloo (shared-GPU test mode)"
+               if SHARED_GPU and world > 1 else "ncclAllGather")
+        reduce_info = {"collective": f"{via} of {R.REC_WIDTH * 8} B per GPU "
                                      f"({world} rank(s)), host fold in rank order",
                        "wall_us": us, "jobs_folded": folded[0]}
         if folded[14] > 0:
