@@ -1194,14 +1194,17 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
     for (std::size_t i = 0; i < d->outstanding.size() && *n_out < cap;) {
         Op* op = d->outstanding[i];
         const cudaError_t q = cudaEventQuery(op->last());
-        if (q == cudaSuccess) {
-            report_op(d, op, sticky, out[(*n_out)++]);
-            d->outstanding.erase(d->outstanding.begin() + i);
-            d->release_op(op);
+        if (q == cudaErrorNotReady) {
+            ++i;
             continue;
         }
-        if (q != cudaErrorNotReady) cudaGetLastError();
-        ++i;
+        // done, or the device failed (e.g. a sticky launch/kernel error):
+        // report it either way, with Internal status in the second case,
+        // so the client's STP gets NACK(Internal) instead of waiting forever
+        if (q != cudaSuccess) cudaGetLastError();
+        report_op(d, op, q == cudaSuccess ? sticky : q, out[(*n_out)++]);
+        d->outstanding.erase(d->outstanding.begin() + i);
+        d->release_op(op);
     }
     return VGPU_CU_OK;
 }
