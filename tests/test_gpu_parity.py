@@ -260,3 +260,15 @@ for m, first, count in ((24, 0, 256), (28, 1536, 512), (20, 3, 5)):
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l.split() for l in out.stdout.splitlines() if l.strip()]
     assert len(lines) == 3 and all(l[-1] == "True" for l in lines), out.stdout
+
+
+@pytest.mark.parametrize("mk", [8, 9, 10, 12, 20])
+def test_ep_small_and_large_batches_bit_exact(mk):
+    """EP batches of 2^mk pairs other than NPB's 2^16: 1, 2, 4 and 16 pairs
+    per lane (the compaction kernel's remainder loop and ramp-up path) and
+    4096 per lane, each bit-identical to the oracle."""
+    m = mk + 6  # 64 batches
+    ins = oracle.ep_params_bytes(m, 5, 40, mk=mk)
+    got = oracle.ep_from_bytes(V.native_run_task(ins, V.KernelDescriptor("nas-ep")))
+    want = oracle.ep_job(m, 5, 40, mk=mk)
+    assert bytes(got) == bytes(want), (mk, got.sx, want.sx)
