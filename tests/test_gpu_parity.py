@@ -231,12 +231,14 @@ def test_sgemm_mixed_sizes_in_one_batch(sizes):
         assert err <= 1e-5, (n, err)
 
 
-@pytest.mark.parametrize("variant", [None, "11"])
+@pytest.mark.parametrize("variant", [None, "11", "12"])
 def test_ep_kernel_instances_match_their_oracle_order(variant):
-    """The default EP instance (accepted pairs compacted per warp) and the
-    branch-free instance (VGPU_EP_VARIANT=11, lane-sequential sums) are each
-    bit-exact against the oracle restating their reduction order, in a fresh
-    process (the instance is chosen once per process)."""
+    """The default EP instance (accepted pairs compacted per warp,
+    range-specialised div/sqrt), the branch-free instance (VGPU_EP_VARIANT=11,
+    lane-sequential sums) and compaction with the div/sqrt intrinsics (12)
+    are each bit-exact
+    against the oracle restating their reduction order, in a fresh process
+    (the instance is chosen once per process)."""
     import subprocess
     import sys
     code = r'''
