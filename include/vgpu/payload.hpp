@@ -20,6 +20,8 @@
 //   nas-ep         EpParams (32 B)          -> EpResult (112 B)  (new)
 //   black-scholes  S||X||T, n fp32 each     -> call||put, n fp32 (new)
 //   sgemm          A||B, n*n fp32 each      -> A*B, n*n fp32     (new)
+//   vector-mul     a||b, n fp32 each        -> a*b, n fp32       (new)
+//   nas-cg         CgHeader + CSR matrix    -> CgResult (32 B)   (new)
 #ifndef VGPU_PAYLOAD_HPP
 #define VGPU_PAYLOAD_HPP
 

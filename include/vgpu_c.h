@@ -136,6 +136,16 @@ int vgpu_encode_frame(uint8_t opcode, uint32_t client_id, uint64_t task_id,
 int vgpu_decode_frame(const uint8_t* frame, uint64_t len, uint8_t* opcode,
                       uint32_t* client_id, uint64_t* task_id, uint64_t* payload_len);
 
+/* NPB CG problems for the nas-cg payload (client side, NPB's untimed
+ * makea; include/vgpu/npb_cg.hpp). vgpu_cg_class: class 'S','W','A','B','C'
+ * -> parameters and the published zeta. vgpu_cg_make_input: the nas-cg input
+ * bytes into out (cap bytes); *len = bytes needed (call with out = NULL to
+ * size the buffer). */
+int vgpu_cg_class(char cls, uint32_t* n, uint32_t* nonzer, uint32_t* niter, double* shift,
+                  double* zeta_verify);
+int vgpu_cg_make_input(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
+                       uint64_t cap, uint64_t* len);
+
 const char* vgpu_last_error(void);
 
 #ifdef __cplusplus

@@ -47,7 +47,9 @@ enum vgpu_cu_kernel {
     VGPU_CU_K_EP = 3,        /* "nas-ep"        vgpu_ep_params -> vgpu_ep_result */
     VGPU_CU_K_BS = 4,        /* "black-scholes" S||X||T fp32 -> call||put      */
     VGPU_CU_K_SGEMM = 5,     /* "sgemm"         A||B (n*n fp32) -> A*B         */
-    VGPU_CU_K_COUNT = 6
+    VGPU_CU_K_VMUL = 6,      /* "vector-mul"    a||b fp32 -> a*b               */
+    VGPU_CU_K_CG = 7,        /* "nas-cg"        vgpu_cg_header + CSR -> vgpu_cg_result */
+    VGPU_CU_K_COUNT = 8
 };
 
 /* NAS EP job (input, 32 bytes little-endian). The job computes batches
@@ -70,6 +72,37 @@ typedef struct vgpu_ep_result {
     uint64_t pairs;     /* accepted Gaussian pairs = sum(q) */
     uint64_t n_batches;
 } vgpu_ep_result;
+
+/* NAS CG job (input, little-endian): the timed part of NPB CG — `niter`
+ * outer iterations of `cgitmax` conjugate-gradient steps on the sparse
+ * symmetric matrix the SPMD program built (NPB makea, untimed in NPB
+ * too; vgpu_cg_make_input), starting from x = 1. Layout:
+ *   vgpu_cg_header | rowstr u32[n+1] | colidx u32[nnz] | pad to 8 | a f64[nnz]
+ * rowstr[0] = 0, rowstr[n] = nnz, colidx < n (CSR, zero-based). */
+typedef struct vgpu_cg_header {
+    uint32_t n;
+    uint32_t nnz;
+    uint32_t niter;    /* NPB NITER (15 for classes S..A, 75 for B, C) */
+    uint32_t cgitmax;  /* NPB: 25 */
+    double shift;      /* NPB SHIFT: zeta = shift + 1 / (x . z) */
+} vgpu_cg_header;
+
+/* NAS CG job result (output, 32 bytes): zeta and ||x - A z|| after the last
+ * outer iteration (the values NPB prints and verifies). */
+typedef struct vgpu_cg_result {
+    double zeta;
+    double rnorm;
+    uint32_t niter;
+    uint32_t n;
+    uint64_t nnz;
+} vgpu_cg_result;
+
+/* Bytes of the nas-cg input for a given CSR shape. */
+static inline uint64_t vgpu_cg_input_bytes(uint32_t n, uint32_t nnz) {
+    uint64_t b = sizeof(vgpu_cg_header) + 4ull * (n + 1ull) + 4ull * nnz;
+    b = (b + 7u) & ~7ull;
+    return b + 8ull * nnz;
+}
 
 /* Black-Scholes constants (CUDA SDK formulation). */
 #define VGPU_BS_RISKFREE 0.02f

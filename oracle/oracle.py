@@ -31,6 +31,11 @@ class EpParams(C.Structure):
                 ("n_batches", C.c_uint64), ("reserved", C.c_uint64)]
 
 
+class CgResult(C.Structure):
+    _fields_ = [("zeta", C.c_double), ("rnorm", C.c_double), ("niter", C.c_uint32),
+                ("n", C.c_uint32), ("nnz", C.c_uint64)]
+
+
 class EpResult(C.Structure):
     _fields_ = [("q", C.c_uint64 * 10), ("sx", C.c_double), ("sy", C.c_double),
                 ("pairs", C.c_uint64), ("n_batches", C.c_uint64)]
@@ -50,6 +55,7 @@ def lib() -> C.CDLL:
         f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
         L.vo_vector_add.argtypes = [f32p, f32p, f32p, C.c_size_t]
         L.vo_vector_scale.argtypes = [f32p, f32p, C.c_float, C.c_size_t]
+        L.vo_vector_mul.argtypes = [f32p, f32p, f32p, C.c_size_t]
         L.vo_ep_job.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
         L.vo_ep_job.restype = C.c_int
         L.vo_ep_job_lanes.argtypes = [C.POINTER(EpParams), C.POINTER(EpResult)]
@@ -59,6 +65,11 @@ def lib() -> C.CDLL:
         L.vo_black_scholes.argtypes = [f32p, f32p, f32p, C.c_size_t, C.c_double, C.c_double,
                                        f64p, f64p]
         L.vo_sgemm.argtypes = [f32p, f32p, C.c_size_t, f64p]
+        L.vo_cg_makea.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_void_p,
+                                  C.c_uint64]
+        L.vo_cg_makea.restype = C.c_uint64
+        L.vo_cg_run.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(CgResult)]
+        L.vo_cg_run.restype = C.c_int
         _lib = L
     return _lib
 
@@ -68,6 +79,14 @@ def vector_add(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     b = np.ascontiguousarray(b, np.float32)
     out = np.empty_like(a)
     lib().vo_vector_add(out, a, b, a.size)
+    return out
+
+
+def vector_mul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    out = np.empty_like(a)
+    lib().vo_vector_mul(out, a, b, a.size)
     return out
 
 
@@ -127,6 +146,34 @@ def sgemm(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     Cm = np.empty((n, n), np.float64)
     lib().vo_sgemm(A, B, n, Cm)
     return Cm
+
+
+# NPB CG classes: (n, nonzer, niter, shift, published zeta) — NPB 3.x cg.f
+CG_CLASSES = {
+    "S": (1400, 7, 15, 10.0, 8.5971775078648),
+    "W": (7000, 8, 15, 12.0, 10.362595087124),
+    "A": (14000, 11, 15, 20.0, 17.130235054029),
+    "B": (75000, 13, 75, 60.0, 22.712745482631),
+    "C": (150000, 15, 75, 110.0, 28.973605592845),
+}
+
+
+def cg_makea(n: int, nonzer: int, niter: int, shift: float) -> bytes:
+    need = lib().vo_cg_makea(n, nonzer, niter, shift, None, 0)
+    buf = C.create_string_buffer(need)
+    lib().vo_cg_makea(n, nonzer, niter, shift, buf, need)
+    return buf.raw
+
+
+def cg_run(inp: bytes) -> "CgResult":
+    r = CgResult()
+    if lib().vo_cg_run(inp, len(inp), C.byref(r)):
+        raise ValueError("malformed nas-cg input")
+    return r
+
+
+def cg_from_bytes(b: bytes) -> "CgResult":
+    return CgResult.from_buffer_copy(bytes(b[:C.sizeof(CgResult)]))
 
 
 def ref_tool(name: str) -> str:

@@ -16,6 +16,12 @@ void vo_vector_add(float* out, const float* a, const float* b, size_t n) {
 }
 
 /* reference proj/src/payload_kernels.cpp:24-27 */
+/* vector-mul: the paper's VecMul (profiles.cpp:33 timing profile only), one
+ * IEEE fp32 multiply per element */
+void vo_vector_mul(float* out, const float* a, const float* b, size_t n) {
+    for (size_t i = 0; i < n; ++i) out[i] = a[i] * b[i];
+}
+
 void vo_vector_scale(float* out, const float* in, float factor, size_t n) {
     for (size_t i = 0; i < n; ++i) out[i] = in[i] * factor;
 }
@@ -204,6 +210,190 @@ void vo_sgemm(const float* A, const float* B, size_t n, double* C) {
             double* crow = C + i * n;
             for (size_t j = 0; j < n; ++j) crow[j] += a * (double)brow[j];
         }
+}
+
+/* ---- NAS CG (NPB 3.x cg.f, restated) ------------------------------------ */
+/* No reference arithmetic (proj/src/bench/profiles.cpp:41 is a timing
+ * profile only). makea / sprnvc / vecset / sparse follow NPB 3.x cg.f
+ * literally (positions drawn by rejection from the randlc stream, entries
+ * inserted into per-row sorted lists with duplicates summed on arrival);
+ * vo_cg_run is conj_grad + the outer zeta loop. PINNED: zeta after niter
+ * iterations equals NPB's published verification values for classes S, W,
+ * A within NPB's epsilon 1e-10 (tests/test_oracle.py). */
+
+static uint64_t cg_tran;
+static double cg_randlc(void) {
+    cg_tran = (cg_tran * 1220703125ull) & ((1ull << 46) - 1);
+    return (double)cg_tran * 0x1p-46;
+}
+
+uint64_t vo_cg_makea(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
+                     uint64_t cap) {
+    const double rcond = 0.1;
+    const int w = (int)nonzer + 1;
+    int nn1 = 1;
+    int* arow = malloc(sizeof(int) * n);
+    int* acol = malloc(sizeof(int) * (size_t)n * w);
+    double* aelt = malloc(sizeof(double) * (size_t)n * w);
+    cg_tran = 314159265ull;
+    (void)cg_randlc(); /* zeta = randlc(tran, amult) */
+    do nn1 *= 2; while (nn1 < (int)n);
+    for (int io = 0; io < (int)n; io++) {
+        double v[64];
+        int iv[64], nzv = 0;
+        while (nzv < (int)nonzer) { /* sprnvc */
+            const double vecelt = cg_randlc();
+            const double vecloc = cg_randlc();
+            const int i = (int)(nn1 * vecloc) + 1;
+            int dup = 0;
+            if (i > (int)n) continue;
+            for (int k = 0; k < nzv; k++)
+                if (iv[k] == i) { dup = 1; break; }
+            if (dup) continue;
+            v[nzv] = vecelt;
+            iv[nzv] = i;
+            nzv++;
+        }
+        { /* vecset(.., iouter, 0.5) */
+            int set = 0;
+            for (int k = 0; k < nzv; k++)
+                if (iv[k] == io + 1) { v[k] = 0.5; set = 1; }
+            if (!set) { v[nzv] = 0.5; iv[nzv] = io + 1; nzv++; }
+        }
+        arow[io] = nzv;
+        for (int k = 0; k < nzv; k++) {
+            acol[io * w + k] = iv[k] - 1;
+            aelt[io * w + k] = v[k];
+        }
+    }
+    /* sparse(): preliminary row counts, insertion with duplicate summing */
+    int* rowstr = calloc(n + 1, sizeof(int));
+    for (int i = 0; i < (int)n; i++)
+        for (int z = 0; z < arow[i]; z++) rowstr[acol[i * w + z] + 1] += arow[i];
+    for (int j = 1; j <= (int)n; j++) rowstr[j] += rowstr[j - 1];
+    const int capn = rowstr[n];
+    double* a = malloc(sizeof(double) * (capn ? capn : 1));
+    int* colidx = malloc(sizeof(int) * (capn ? capn : 1));
+    int* nzloc = calloc(n, sizeof(int));
+    for (int k = 0; k < capn; k++) { a[k] = 0.0; colidx[k] = -1; }
+    const double ratio = pow(rcond, 1.0 / (double)n);
+    double size = 1.0;
+    for (int i = 0; i < (int)n; i++) {
+        for (int z = 0; z < arow[i]; z++) {
+            const int j = acol[i * w + z];
+            const double scale = size * aelt[i * w + z];
+            for (int zr = 0; zr < arow[i]; zr++) {
+                const int jcol = acol[i * w + zr];
+                double va = aelt[i * w + zr] * scale;
+                int k;
+                if (jcol == j && j == i) va = va + rcond - shift;
+                for (k = rowstr[j]; k < rowstr[j + 1]; k++) {
+                    if (colidx[k] > jcol) {
+                        for (int kk = rowstr[j + 1] - 2; kk >= k; kk--)
+                            if (colidx[kk] > -1) { a[kk + 1] = a[kk]; colidx[kk + 1] = colidx[kk]; }
+                        colidx[k] = jcol;
+                        a[k] = 0.0;
+                        break;
+                    } else if (colidx[k] == -1) {
+                        colidx[k] = jcol;
+                        break;
+                    } else if (colidx[k] == jcol) {
+                        nzloc[j]++;
+                        break;
+                    }
+                }
+                a[k] = a[k] + va;
+            }
+        }
+        size = size * ratio;
+    }
+    for (int j = 1; j < (int)n; j++) nzloc[j] += nzloc[j - 1];
+    for (int j = 0; j < (int)n; j++) {
+        const int j1 = j > 0 ? rowstr[j] - nzloc[j - 1] : 0;
+        const int j2 = rowstr[j + 1] - nzloc[j];
+        int nza = rowstr[j];
+        for (int k = j1; k < j2; k++) { a[k] = a[nza]; colidx[k] = colidx[nza]; nza++; }
+    }
+    for (int j = 1; j <= (int)n; j++) rowstr[j] -= nzloc[j - 1];
+    const uint32_t nnz = (uint32_t)rowstr[n];
+    const uint64_t need = vgpu_cg_input_bytes(n, nnz);
+    if (out && cap >= need) {
+        vgpu_cg_header h;
+        memset(&h, 0, sizeof h);
+        h.n = n;
+        h.nnz = nnz;
+        h.niter = niter;
+        h.cgitmax = 25;
+        h.shift = shift;
+        memset(out, 0, need);
+        memcpy(out, &h, sizeof h);
+        const uint64_t off_col = sizeof h + 4ull * (n + 1ull);
+        const uint64_t off_a = (off_col + 4ull * nnz + 7u) & ~7ull;
+        for (uint32_t j = 0; j <= n; j++) { const uint32_t v = (uint32_t)rowstr[j]; memcpy(out + sizeof h + 4ull * j, &v, 4); }
+        for (uint32_t k = 0; k < nnz; k++) { const uint32_t c = (uint32_t)colidx[k]; memcpy(out + off_col + 4ull * k, &c, 4); }
+        memcpy(out + off_a, a, 8ull * nnz);
+    }
+    free(arow); free(acol); free(aelt); free(rowstr); free(a); free(colidx); free(nzloc);
+    return need;
+}
+
+int vo_cg_run(const uint8_t* in, uint64_t in_bytes, vgpu_cg_result* res) {
+    vgpu_cg_header h;
+    if (in_bytes < sizeof h) return 1;
+    memcpy(&h, in, sizeof h);
+    if (in_bytes != vgpu_cg_input_bytes(h.n, h.nnz)) return 1;
+    const uint32_t n = h.n;
+    const uint64_t off_col = sizeof h + 4ull * (n + 1ull);
+    const uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
+    const uint32_t* rowstr = (const uint32_t*)(in + sizeof h);
+    const uint32_t* colidx = (const uint32_t*)(in + off_col);
+    const double* a = (const double*)(in + off_a);
+    double* x = malloc(8ull * n); double* z = malloc(8ull * n); double* p = malloc(8ull * n);
+    double* q = malloc(8ull * n); double* r = malloc(8ull * n);
+    double zeta = 0.0, rnorm = 0.0;
+    for (uint32_t j = 0; j < n; j++) x[j] = 1.0;
+    for (uint32_t it = 0; it < h.niter; it++) {
+        /* conj_grad */
+        double rho = 0.0, sum = 0.0, t1 = 0.0, t2 = 0.0;
+        for (uint32_t j = 0; j < n; j++) { q[j] = 0.0; z[j] = 0.0; r[j] = x[j]; p[j] = r[j]; }
+        for (uint32_t j = 0; j < n; j++) rho = rho + r[j] * r[j];
+        for (uint32_t cgit = 0; cgit < h.cgitmax; cgit++) {
+            double d = 0.0, alpha, rho0, beta;
+            for (uint32_t j = 0; j < n; j++) {
+                double s = 0.0;
+                for (uint32_t k = rowstr[j]; k < rowstr[j + 1]; k++) s = s + a[k] * p[colidx[k]];
+                q[j] = s;
+            }
+            for (uint32_t j = 0; j < n; j++) d = d + p[j] * q[j];
+            alpha = rho / d;
+            rho0 = rho;
+            for (uint32_t j = 0; j < n; j++) { z[j] = z[j] + alpha * p[j]; r[j] = r[j] - alpha * q[j]; }
+            rho = 0.0;
+            for (uint32_t j = 0; j < n; j++) rho = rho + r[j] * r[j];
+            beta = rho / rho0;
+            for (uint32_t j = 0; j < n; j++) p[j] = r[j] + beta * p[j];
+        }
+        for (uint32_t j = 0; j < n; j++) {
+            double d = 0.0;
+            for (uint32_t k = rowstr[j]; k < rowstr[j + 1]; k++) d = d + a[k] * z[colidx[k]];
+            r[j] = d;
+        }
+        for (uint32_t j = 0; j < n; j++) { const double d = x[j] - r[j]; sum = sum + d * d; }
+        rnorm = sqrt(sum);
+        /* outer loop: zeta, x = z / ||z|| */
+        for (uint32_t j = 0; j < n; j++) { t1 = t1 + x[j] * z[j]; t2 = t2 + z[j] * z[j]; }
+        t2 = 1.0 / sqrt(t2);
+        zeta = h.shift + 1.0 / t1;
+        for (uint32_t j = 0; j < n; j++) x[j] = t2 * z[j];
+    }
+    memset(res, 0, sizeof *res);
+    res->zeta = zeta;
+    res->rnorm = rnorm;
+    res->niter = h.niter;
+    res->n = n;
+    res->nnz = h.nnz;
+    free(x); free(z); free(p); free(q); free(r);
+    return 0;
 }
 
 /* ---- deterministic generator ---------------------------------------------- */

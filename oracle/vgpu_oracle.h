@@ -17,6 +17,9 @@
  *                        itself; pinned instead to a published worked example
  *                        (Hull Ex. 15.6) and the exact-CDF closed form
  *                        (tests/test_oracle.py). GPU checked at L1 rel <= 1e-6.
+ *   NAS CG               no reference arithmetic (profiles.cpp:41); NPB 3.x cg.f
+ *                        makea + conj_grad — PINNED against NPB's published
+ *                        zeta (classes S, W, A; epsilon 1e-10).
  *   SGEMM                no reference arithmetic (profiles.cpp:35); binary64
  *                        accumulation — UNPINNED by the reference itself;
  *                        pinned to numpy float64 matmul and exact integer
@@ -36,6 +39,7 @@ extern "C" {
 
 void vo_vector_add(float* out, const float* a, const float* b, size_t n);
 void vo_vector_scale(float* out, const float* in, float factor, size_t n);
+void vo_vector_mul(float* out, const float* a, const float* b, size_t n);
 
 /* One EP job with the documented fixed reduction order:
  * 256 lanes per batch, each lane sums its pairs sequentially, lanes combine
@@ -54,6 +58,13 @@ void vo_black_scholes(const float* S, const float* X, const float* T, size_t n,
                       double riskfree, double volatility, double* call, double* put);
 
 void vo_sgemm(const float* A, const float* B, size_t n, double* C);
+
+/* NAS CG: NPB makea into the nas-cg input layout (returns the bytes needed;
+ * writes when out has room) and the timed CG iterations on such an input
+ * (nonzero on a malformed input). */
+uint64_t vo_cg_makea(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
+                     uint64_t cap);
+int vo_cg_run(const uint8_t* in, uint64_t in_bytes, vgpu_cg_result* res);
 
 /* deterministic generators shared by tests and bench (xorshift64*) */
 uint64_t vo_rng_next(uint64_t* state);

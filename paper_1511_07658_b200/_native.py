@@ -158,6 +158,9 @@ HOST_API = {
     "vgpu_encode_frame": (C.c_int, [C.c_uint8, _U32, _U64, _P, _U64, _P, _U64, C.POINTER(_U64)]),
     "vgpu_decode_frame": (C.c_int, [_P, _U64, C.POINTER(C.c_uint8), C.POINTER(_U32),
                                     C.POINTER(_U64), C.POINTER(_U64)]),
+    "vgpu_cg_class": (C.c_int, [C.c_char, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
+                                C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "vgpu_cg_make_input": (C.c_int, [_U32, _U32, _U32, C.c_double, _P, _U64, C.POINTER(_U64)]),
     "vgpu_last_error": (C.c_char_p, []),
 }
 

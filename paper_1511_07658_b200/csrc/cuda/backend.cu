@@ -40,6 +40,7 @@
 
 #include "vgpu_cuda.h"
 #include "k_bs.cuh"
+#include "k_cg.cuh"
 #include "k_ep.cuh"
 #include "k_sgemm.cuh"
 #include "k_sgemm_tc.cuh"
@@ -116,9 +117,21 @@ struct DevJob {
     std::uint8_t* out = nullptr;
     std::uint64_t out_bytes = 0;
     std::uint8_t* scratch = nullptr;
-    std::uint8_t* ws = nullptr;  // sgemm tensor-core workspace: 2 x in_bytes
+    std::uint8_t* ws = nullptr;  // sgemm tensor-core workspace: 2 x in_bytes; nas-cg vectors
     vgpu_ep_params ep{};
+    vgpu_cg_header cg{};
 };
+
+// Device workspace a job needs besides in/out/scratch (0: none).
+std::uint64_t job_ws_bytes(std::uint32_t kernel, const void* h_in, std::uint64_t in_bytes) {
+    if (kernel == VGPU_CU_K_SGEMM) return 2 * in_bytes;
+    if (kernel == VGPU_CU_K_CG && h_in && in_bytes >= sizeof(vgpu_cg_header)) {
+        vgpu_cg_header h;
+        std::memcpy(&h, h_in, sizeof h);
+        return 5ull * 8ull * h.n;  // x, z, p, q, r
+    }
+    return 0;
+}
 
 // 3xTF32 tcgen05 by default (chunked TMEM accumulation: 4.8e-7 relative
 // Frobenius at 2048^2 on B200, below the FP32 SIMT kernel's 8.1e-7);
@@ -249,6 +262,48 @@ cudaError_t launch_tc2_tma(const vgk::TcTable& tt, std::uint32_t maxn, cudaStrea
     return cudaSuccess;
 }
 
+// Largest cluster the CG kernel can run with (16 needs the non-portable
+// attribute and a GPC with 16 free SMs; else 8), 0 when none launches.
+unsigned cg_max_cluster() {
+    static const unsigned c = [] {
+        const int smem = static_cast<int>(8 * vgk::kCgStageMax);
+        for (auto k : {vgk::cg_kernel<true>, vgk::cg_kernel<false>}) {
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+                cudaGetLastError();
+                return 0u;
+            }
+        }
+        for (unsigned cs = vgk::kCgMaxCluster; cs >= 1; cs /= 2) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(cs);
+            cfg.blockDim = dim3(vgk::kCgThreads);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true>, &cfg) == cudaSuccess && nc > 0)
+                return cs;
+            cudaGetLastError();
+        }
+        return 0u;
+    }();
+    return c;
+}
+
+// CTAs per CG job: about 128K nonzeros per CTA (class S: 1, W: 4, A: 16),
+// a power of two up to the launchable maximum
+unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned cmax) {
+    unsigned cs = 1;
+    while (cs < cmax && static_cast<std::uint64_t>(cs) * (1u << 17) < h.nnz) cs *= 2;
+    return cs;
+}
+
 // SGEMM tensor-core phases launch_jobs issues: 1 = split/transpose pre-pass,
 // 2 = tcgen05 GEMM, 3 = both (the product path). Only the resident
 // measurement (VGPU_CU_RESIDENT_MAIN_ONLY) narrows it, on its own thread.
@@ -267,8 +322,9 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 }
             return cudaSuccess;
         case VGPU_CU_K_VADD:
+        case VGPU_CU_K_VMUL:
         case VGPU_CU_K_VSCALE: {
-            const bool add = kernel == VGPU_CU_K_VADD;
+            const bool add = kernel != VGPU_CU_K_VSCALE;  // two operands
             for (std::uint32_t b = 0; b < n; b += kMaxTableJobs) {
                 StreamTable t{};
                 std::uint32_t ctas = 0;
@@ -287,13 +343,13 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 }
                 if (!ctas) continue;
                 cudaError_t e = cudaSuccess;
-                if (pdl)
-                    e = add ? launch_pdl(stream_table_kernel<true>, ctas, kStreamThreads, s, t)
-                            : launch_pdl(stream_table_kernel<false>, ctas, kStreamThreads, s, t);
-                else if (add)
-                    stream_table_kernel<true><<<ctas, kStreamThreads, 0, s>>>(t);
-                else
-                    stream_table_kernel<false><<<ctas, kStreamThreads, 0, s>>>(t);
+                auto go = [&](auto kern) {
+                    if (pdl) e = launch_pdl(kern, ctas, kStreamThreads, s, t);
+                    else kern<<<ctas, kStreamThreads, 0, s>>>(t);
+                };
+                if (kernel == VGPU_CU_K_VADD) go(stream_table_kernel<kOpAdd>);
+                else if (kernel == VGPU_CU_K_VMUL) go(stream_table_kernel<kOpMul>);
+                else go(stream_table_kernel<kOpScale>);
                 ++*launches;
                 if (e == cudaSuccess) e = cudaGetLastError();
                 if (e != cudaSuccess) return e;
@@ -493,6 +549,64 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             if (e != cudaSuccess) return e;
             return flush(gen, gen_tiles, false);
         }
+        case VGPU_CU_K_CG: {
+            // group by (cluster size, p staged in shared memory); one launch
+            // per group of up to kMaxCgJobs clusters
+            const unsigned cmax = cg_max_cluster();
+            if (!cmax) return cudaErrorInvalidConfiguration;
+            std::vector<bool> done(n, false);
+            for (std::uint32_t i = 0; i < n; ++i) {
+                if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
+                const unsigned cs = cg_cluster_for(jobs[i].cg, cmax);
+                const bool stage = jobs[i].cg.n <= kCgStageMax;
+                CgTable t{};
+                std::uint32_t maxn = 0;
+                for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
+                    const vgpu_cg_header& h = jobs[k].cg;
+                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, cmax) != cs ||
+                        (h.n <= kCgStageMax) != stage)
+                        continue;
+                    done[k] = true;
+                    const std::uint8_t* in = jobs[k].in;
+                    CgJob& j = t.job[t.njobs++];
+                    const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
+                    const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
+                    j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
+                    j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
+                    j.a = reinterpret_cast<const double*>(in + off_a);
+                    double* w = reinterpret_cast<double*>(jobs[k].ws);
+                    j.x = w;
+                    j.z = w + h.n;
+                    j.p = w + 2ull * h.n;
+                    j.q = w + 3ull * h.n;
+                    j.r = w + 4ull * h.n;
+                    j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
+                    j.n = h.n;
+                    j.nnz = h.nnz;
+                    j.niter = h.niter;
+                    j.cgitmax = h.cgitmax;
+                    j.shift = h.shift;
+                    maxn = std::max(maxn, h.n);
+                }
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(t.njobs * cs);
+                cfg.blockDim = dim3(kCgThreads);
+                cfg.dynamicSmemBytes = stage ? 8ull * maxn : 0;
+                cfg.stream = s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = cs;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                const cudaError_t e = stage ? cudaLaunchKernelEx(&cfg, cg_kernel<true>, t)
+                                           : cudaLaunchKernelEx(&cfg, cg_kernel<false>, t);
+                ++*launches;
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
         default:
             return cudaErrorInvalidValue;
     }
@@ -513,6 +627,16 @@ void job_work(const DevJob& j, std::uint64_t* bytes, double* flops) {
             const double d = static_cast<double>(isqrt(j.in_bytes / 8));
             *bytes += j.in_bytes + j.in_bytes / 2;
             *flops += 2.0 * d * d * d;
+            break;
+        }
+        case VGPU_CU_K_VMUL: *bytes += j.in_bytes + j.in_bytes / 2; *flops += j.in_bytes / 8.0; break;
+        case VGPU_CU_K_CG: {
+            // per SpMV the matrix streams once: a (8 B) + colidx (4 B) per
+            // nonzero + rowstr (4 B per row); cgitmax + 1 SpMVs per outer
+            // iteration. Flops: 2 per nonzero per SpMV + 10 per row per step.
+            const double spmv = static_cast<double>(j.cg.niter) * (j.cg.cgitmax + 1.0);
+            *bytes += static_cast<std::uint64_t>(spmv * (12.0 * j.cg.nnz + 4.0 * j.cg.n));
+            *flops += spmv * 2.0 * j.cg.nnz + 10.0 * j.cg.niter * j.cg.cgitmax * j.cg.n;
             break;
         }
         default: break;
@@ -599,6 +723,7 @@ struct vgpu_cu_dev {
     int device = 0;
     std::uint32_t max_clients = 0;
     std::uint64_t slot_bytes = 0;
+    std::uint64_t buf_bytes = 0;  // per-slot buffer (slot_bytes rounded); ws = 2 x buf
     std::uint8_t* arena = nullptr;
     std::vector<SlotState> slots;  // [0] unused
     cudaStream_t anchor_stream = nullptr;
@@ -716,8 +841,8 @@ int vgpu_cu_device_count(int* n) {
 }
 
 int vgpu_cu_payload(const char* id, std::uint32_t* kernel) {
-    static const char* names[VGPU_CU_K_COUNT] = {"identity", "vector-add", "vector-scale",
-                                                 "nas-ep", "black-scholes", "sgemm"};
+    static const char* names[VGPU_CU_K_COUNT] = {"identity", "vector-add", "vector-scale", "nas-ep",
+                                                 "black-scholes", "sgemm", "vector-mul", "nas-cg"};
     if (!id || !kernel) return VGPU_CU_EINVAL;
     for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT; ++k)
         if (std::strcmp(id, names[k]) == 0) {
@@ -742,6 +867,37 @@ int vgpu_cu_output_size(std::uint32_t kernel, const void* in, std::uint64_t in_b
             }
             *out_bytes = in_bytes / 2;
             return VGPU_CU_OK;
+        case VGPU_CU_K_VMUL:
+            if (in_bytes % 8) {
+                set_err("vector-mul: input must hold two equal float32 arrays");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = in_bytes / 2;
+            return VGPU_CU_OK;
+        case VGPU_CU_K_CG: {
+            if (in_bytes < sizeof(vgpu_cg_header)) {
+                set_err("nas-cg: input shorter than its %zu-byte header", sizeof(vgpu_cg_header));
+                return VGPU_CU_EPAYLOAD;
+            }
+            if (!in) return VGPU_CU_EINVAL;
+            vgpu_cg_header h;
+            std::memcpy(&h, in, sizeof h);
+            if (h.n == 0 || h.nnz == 0 || in_bytes != vgpu_cg_input_bytes(h.n, h.nnz)) {
+                set_err("nas-cg: %llu bytes do not match a CSR matrix of n=%u, nnz=%u",
+                        (unsigned long long)in_bytes, h.n, h.nnz);
+                return VGPU_CU_EPAYLOAD;
+            }
+            std::uint32_t first = 0, last = 0;
+            const auto* rs = static_cast<const std::uint8_t*>(in) + sizeof h;
+            std::memcpy(&first, rs, 4);
+            std::memcpy(&last, rs + 4ull * h.n, 4);
+            if (first != 0 || last != h.nnz || h.niter > 100000 || h.cgitmax > 10000) {
+                set_err("nas-cg: rowstr must run 0..nnz; niter <= 1e5, cgitmax <= 1e4");
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = sizeof(vgpu_cg_result);
+            return VGPU_CU_OK;
+        }
         case VGPU_CU_K_VSCALE:
             if (in_bytes % 4) {
                 set_err("vector-scale: input must be packed float32");
@@ -800,6 +956,7 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
     d->slot_bytes = slot_bytes;
     d->slots.resize(max_clients + 1);
     const std::uint64_t buf = round_up(std::max<std::uint64_t>(slot_bytes, 256), kAlign);
+    d->buf_bytes = buf;
     // in | out | EP scratch | sgemm workspace (hi/lo splits: 2 x input)
     const std::uint64_t per_slot = 4 * buf + round_up(kScratchBytes, kAlign);
     auto fail = [&](int code) {
@@ -984,6 +1141,13 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         j.out_bytes = need;
         j.scratch = s.d_scratch;
         j.ws = s.d_ws;
+        if (t.kernel == VGPU_CU_K_CG) {
+            std::memcpy(&j.cg, t.h_in, sizeof j.cg);
+            if (job_ws_bytes(t.kernel, t.h_in, t.in_bytes) > 2 * d->buf_bytes) {
+                set_err("task %u: nas-cg vectors (%u rows) exceed the slot workspace", i, j.cg.n);
+                return VGPU_CU_ESIZE;
+            }
+        }
         if (t.kernel == VGPU_CU_K_EP) {
             std::memcpy(&j.ep, t.h_in, sizeof j.ep);
             // the 112-byte result goes straight into the client's region
@@ -1303,17 +1467,18 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     j.out = c.d_out;
     j.out_bytes = need;
     j.scratch = c.d_scratch;
-    if (kernel == VGPU_CU_K_SGEMM) {
-        if (2 * in_bytes > c.cap_ws) {
+    if (const std::uint64_t wsb = job_ws_bytes(kernel, in, in_bytes)) {
+        if (wsb > c.cap_ws) {
             if (c.d_ws) cudaFree(c.d_ws);
             c.d_ws = nullptr;
             c.cap_ws = 0;
-            CK(cudaMalloc(&c.d_ws, 2 * in_bytes));
-            c.cap_ws = 2 * in_bytes;
+            CK(cudaMalloc(&c.d_ws, wsb));
+            c.cap_ws = wsb;
         }
         j.ws = c.d_ws;
     }
     if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, in, sizeof j.ep);
+    if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, in, sizeof j.cg);
     // pageable copies, exactly what an unvirtualized CUDA program does
     if (in_bytes) CK(cudaMemcpyAsync(c.d_in, in, in_bytes, cudaMemcpyHostToDevice, c.stream));
     std::uint64_t l = 0;
@@ -1343,7 +1508,7 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
         rc = vgpu_cu_output_size(kernel, h_inputs[i], in_bytes[i], &outb[i]);
         if (rc) return rc;
         per_set += round_up(in_bytes[i], 256) + round_up(outb[i], 256) + round_up(kScratchBytes, 256) +
-                   (kernel == VGPU_CU_K_SGEMM ? round_up(2 * in_bytes[i], 256) : 0);
+                   round_up(job_ws_bytes(kernel, h_inputs[i], in_bytes[i]), 256);
     }
     std::uint8_t* mem = nullptr;
     CK(cudaMalloc(&mem, per_set * sets));
@@ -1373,11 +1538,12 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
             p += round_up(outb[i], 256);
             j.scratch = p;
             p += round_up(kScratchBytes, 256);
-            if (kernel == VGPU_CU_K_SGEMM) {
+            if (const std::uint64_t wsb = job_ws_bytes(kernel, h_inputs[i], in_bytes[i])) {
                 j.ws = p;
-                p += round_up(2 * in_bytes[i], 256);
+                p += round_up(wsb, 256);
             }
             if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, h_inputs[i], sizeof j.ep);
+            if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, h_inputs[i], sizeof j.cg);
             if (in_bytes[i])
                 CK(cudaMemcpy(const_cast<std::uint8_t*>(j.in), h_inputs[i], in_bytes[i],
                               cudaMemcpyHostToDevice));
@@ -1406,7 +1572,7 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
     // HBM-streaming launches are short and independent step to step: chain
     // them with PDL so one step's ramp-up hides under the previous tail, as
     // consecutive GVM batches overlap on their own streams
-    const bool pdl = !(flags & VGPU_CU_RESIDENT_NO_PDL) && sets >= 2 && (kernel == VGPU_CU_K_VADD || kernel == VGPU_CU_K_VSCALE ||
+    const bool pdl = !(flags & VGPU_CU_RESIDENT_NO_PDL) && sets >= 2 && (kernel == VGPU_CU_K_VADD || kernel == VGPU_CU_K_VSCALE || kernel == VGPU_CU_K_VMUL ||
                                    kernel == VGPU_CU_K_BS);
     res->pdl = pdl ? 1u : 0u;
     l = 0;

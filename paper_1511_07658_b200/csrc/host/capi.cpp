@@ -9,6 +9,7 @@
 #include "vgpu/daemon.hpp"
 #include "vgpu/device.hpp"
 #include "vgpu/model.hpp"
+#include "vgpu/npb_cg.hpp"
 #include "vgpu_c.h"
 
 using namespace vgpu;
@@ -317,6 +318,31 @@ uint64_t vgpu_model_no_vt(uint32_t n, uint64_t t_init, uint64_t t_ctx, uint64_t 
         t_err = e.what();
         return 0;
     }
+}
+
+int vgpu_cg_class(char cls, uint32_t* n, uint32_t* nonzer, uint32_t* niter, double* shift,
+                  double* zeta_verify) {
+    if (!n || !nonzer || !niter || !shift || !zeta_verify) return VGPU_E_INVALID;
+    return guarded([&] {
+        const npb::CgClass c = npb::cg_class(cls);
+        *n = c.n;
+        *nonzer = c.nonzer;
+        *niter = c.niter;
+        *shift = c.shift;
+        *zeta_verify = c.zeta_verify;
+    });
+}
+
+int vgpu_cg_make_input(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
+                       uint64_t cap, uint64_t* len) {
+    if (!len) return VGPU_E_INVALID;
+    return guarded([&] {
+        const std::vector<std::uint8_t> b = npb::make_cg_input(n, nonzer, niter, shift);
+        *len = b.size();
+        if (!out) return;
+        if (cap < b.size()) throw std::invalid_argument("vgpu_cg_make_input: buffer too small");
+        std::memcpy(out, b.data(), b.size());
+    });
 }
 
 int vgpu_encode_frame(uint8_t opcode, uint32_t client_id, uint64_t task_id, const uint8_t* payload,

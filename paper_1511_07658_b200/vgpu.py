@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import struct
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -285,7 +286,7 @@ def native_run_task(data, task: KernelDescriptor, cuda_device: int = 0,
 # ---- device-level helpers (vgpu_cuda.h) ----------------------------------------
 
 KERNELS = {"identity": 0, "vector-add": 1, "vector-scale": 2, "nas-ep": 3,
-           "black-scholes": 4, "sgemm": 5}
+           "black-scholes": 4, "sgemm": 5, "vector-mul": 6, "nas-cg": 7}
 
 
 def _cu_check(rc: int) -> None:
@@ -340,3 +341,47 @@ def model_simulate(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid:
                    sms: int = 14, max_kernels: int = 16, slots: int = 8) -> int:
     return _libs().host.vgpu_model_simulate(style, n, t_in, t_comp, t_out, grid, sms,
                                             max_kernels, slots)
+
+
+# ---- NPB CG problems (client side of the nas-cg payload) ----------------------
+
+CG_HEADER = struct.Struct("<IIIId")   # vgpu_cg_header: n, nnz, niter, cgitmax, shift
+CG_RESULT = struct.Struct("<ddIIQ")   # vgpu_cg_result: zeta, rnorm, niter, n, nnz
+
+
+@dataclass
+class CgClass:
+    n: int
+    nonzer: int
+    niter: int
+    shift: float
+    zeta_verify: float
+
+
+def cg_class(cls: str) -> CgClass:
+    """NPB CG class parameters and the published zeta (S, W, A, B, C)."""
+    n, nz, it = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    sh, zv = C.c_double(), C.c_double()
+    _check(_libs().host.vgpu_cg_class(cls.encode()[:1], C.byref(n), C.byref(nz), C.byref(it),
+                                      C.byref(sh), C.byref(zv)))
+    return CgClass(n.value, nz.value, it.value, sh.value, zv.value)
+
+
+def cg_make_input(n: int, nonzer: int, niter: int, shift: float) -> bytes:
+    """The nas-cg input for an NPB-shaped problem (NPB makea, untimed in NPB)."""
+    lib = _libs().host
+    need = C.c_uint64()
+    _check(lib.vgpu_cg_make_input(n, nonzer, niter, shift, None, 0, C.byref(need)))
+    buf = (C.c_uint8 * need.value)()
+    _check(lib.vgpu_cg_make_input(n, nonzer, niter, shift, buf, need.value, C.byref(need)))
+    return bytes(buf)
+
+
+def cg_input_for_class(cls: str, niter: Optional[int] = None) -> bytes:
+    c = cg_class(cls)
+    return cg_make_input(c.n, c.nonzer, c.niter if niter is None else niter, c.shift)
+
+
+def cg_result(out: bytes) -> tuple:
+    """(zeta, rnorm, niter, n, nnz) from a nas-cg result."""
+    return CG_RESULT.unpack(bytes(out[:CG_RESULT.size]))

@@ -300,6 +300,9 @@ TEST_CASE("[gpu] malformed inputs fail through STP with Payload, slot stays usab
         {"sgemm", Bytes(24)},
         {"nas-ep", Bytes(31)},
         {"nas-ep", ep_input(30, 1ull << 14, 1)},
+        {"vector-mul", Bytes{1, 2, 3}},
+        {"nas-cg", Bytes(23)},
+        {"nas-cg", Bytes(64)},  // header says n = 0
     };
     for (const auto& [id, in] : bad) {
         VgpuHandle h = req(hub);

@@ -16,7 +16,8 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared(header):
     text = open(os.path.join(REPO, "include", header)).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(vgpu_[a-z0-9_]+)\s*\(", text)))
+    inline = set(re.findall(r"static\s+inline\s+[\w\s\*]+?\b(vgpu_[a-z0-9_]+)\s*\(", text))
+    return sorted(set(re.findall(r"\b(vgpu_[a-z0-9_]+)\s*\(", text)) - inline)
 
 
 @pytest.mark.parametrize("header,lib", [("vgpu_cuda.h", "cuda"), ("vgpu_c.h", "host")])

@@ -7,6 +7,10 @@
   (proj/src/bench/bench.cpp:34-49).
 * NAS EP: against NPB's published verification sums (epsilon 1e-8) for
   class S recomputed here, and the committed class S/W/A fixtures.
+* NAS CG: NPB makea + conj_grad against NPB's published zeta (epsilon
+  1e-10) for classes S, W and A; the product's client-side builder
+  (vgpu_cg_make_input) produces the oracle's matrix byte for byte.
+* vector-mul: numpy float32 multiply (IEEE, bit-exact).
 * Black-Scholes / SGEMM: unpinned by the reference (no arithmetic there);
   pinned to published known answers (Hull Ex. 15.6, the exact-CDF closed
   form, numpy float64 matmul) and internal consistency (put-call parity,
@@ -175,3 +179,37 @@ def test_sgemm_oracle_matches_numpy_float64():
     B = rng.uniform(-1, 1, (96, 96)).astype(np.float32)
     ref = A.astype(np.float64) @ B.astype(np.float64)
     assert np.max(np.abs(oracle.sgemm(A, B) - ref)) < 1e-12
+
+
+@pytest.mark.parametrize("cls", ["S", "W", "A"])
+def test_cg_oracle_matches_npb_published_zeta(cls):
+    n, nonzer, niter, shift, zeta = oracle.CG_CLASSES[cls]
+    inp = oracle.cg_makea(n, nonzer, niter, shift)
+    r = oracle.cg_run(inp)
+    assert abs(r.zeta - zeta) / zeta <= 1e-10, (cls, r.zeta)
+    assert r.rnorm < 1e-12 and r.niter == niter and r.n == n
+
+
+@pytest.mark.parametrize("cls", ["S", "W", "A"])
+def test_cg_client_builder_matches_oracle_makea_bytes(cls):
+    from paper_1511_07658_b200 import vgpu as V
+    n, nonzer, niter, shift, zeta = oracle.CG_CLASSES[cls]
+    c = V.cg_class(cls)
+    assert (c.n, c.nonzer, c.niter, c.shift, c.zeta_verify) == (n, nonzer, niter, shift, zeta)
+    assert V.cg_input_for_class(cls) == oracle.cg_makea(n, nonzer, niter, shift)
+
+
+def test_cg_oracle_rejects_malformed_input_and_builder_rejects_bad_class():
+    from paper_1511_07658_b200 import vgpu as V
+    inp = oracle.cg_makea(1400, 7, 1, 10.0)
+    with pytest.raises(ValueError):
+        oracle.cg_run(inp[:-8])
+    with pytest.raises(ValueError):
+        V.cg_class("Q")
+
+
+def test_vector_mul_oracle_is_ieee_float32():
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1e3, 1e3, 4097).astype(np.float32)
+    b = rng.uniform(-1e3, 1e3, 4097).astype(np.float32)
+    assert oracle.vector_mul(a, b).tobytes() == (a * b).tobytes()
