@@ -266,8 +266,9 @@ cudaError_t launch_tc2_tma(const vgk::TcTable& tt, std::uint32_t maxn, cudaStrea
 // attribute and a GPC with 16 free SMs; else 8), 0 when none launches.
 unsigned cg_max_cluster() {
     static const unsigned c = [] {
-        const int smem = static_cast<int>(8 * vgk::kCgStageMax);
-        for (auto k : {vgk::cg_kernel<true>, vgk::cg_kernel<false>}) {
+        const int smem = static_cast<int>(vgk::kCgSmemBytes);
+        for (auto k : {vgk::cg_kernel<true, 8>, vgk::cg_kernel<true, 16>, vgk::cg_kernel<true, 32>,
+                       vgk::cg_kernel<false, 8>, vgk::cg_kernel<false, 16>, vgk::cg_kernel<false, 32>}) {
             if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
                 cudaGetLastError();
@@ -287,7 +288,7 @@ unsigned cg_max_cluster() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true>, &cfg) == cudaSuccess && nc > 0)
+            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true, 32>, &cfg) == cudaSuccess && nc > 0)
                 return cs;
             cudaGetLastError();
         }
@@ -296,12 +297,40 @@ unsigned cg_max_cluster() {
     return c;
 }
 
-// CTAs per CG job: about 128K nonzeros per CTA (class S: 1, W: 4, A: 16),
-// a power of two up to the launchable maximum
-unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned cmax) {
+// CTAs per CG job, a power of two up to the launchable maximum: the batch's
+// fair share of the SMs (`fair`), at least one CTA per ~128K nonzeros, at
+// most one per 64 rows. The SpMV is latency-bound per SM, so a job runs as
+// wide as the batch leaves room for.
+unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned cmax, unsigned fair) {
     unsigned cs = 1;
     while (cs < cmax && static_cast<std::uint64_t>(cs) * (1u << 17) < h.nnz) cs *= 2;
+    while (cs < cmax && cs * 2 <= fair) cs *= 2;
+    while (cs > 1 && static_cast<std::uint64_t>(cs) * 64 > h.n) cs /= 2;
     return cs;
+}
+
+// SpMV lanes per row for a job (k_cg.cuh cg_segment); VGPU_CG_SEG=8|16|32
+// forces one (measurement)
+unsigned cg_seg_for(const vgpu_cg_header& h) {
+    static const unsigned force = [] {
+        const char* e = std::getenv("VGPU_CG_SEG");
+        const unsigned v = e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+        return v == 8 || v == 16 || v == 32 ? v : 0u;
+    }();
+    return force ? force : vgk::cg_segment(h.n, h.nnz);
+}
+
+unsigned device_sms() {
+    static const unsigned n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            v = 148;
+        }
+        return static_cast<unsigned>(v);
+    }();
+    return n;
 }
 
 // SGEMM tensor-core phases launch_jobs issues: 1 = split/transpose pre-pass,
@@ -554,17 +583,21 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             // per group of up to kMaxCgJobs clusters
             const unsigned cmax = cg_max_cluster();
             if (!cmax) return cudaErrorInvalidConfiguration;
+            unsigned ncg = 0;
+            for (std::uint32_t i = 0; i < n; ++i) ncg += jobs[i].ws && jobs[i].cg.n ? 1u : 0u;
+            const unsigned fair = ncg ? std::max(1u, device_sms() / ncg) : 1u;
             std::vector<bool> done(n, false);
             for (std::uint32_t i = 0; i < n; ++i) {
                 if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
-                const unsigned cs = cg_cluster_for(jobs[i].cg, cmax);
+                const unsigned cs = cg_cluster_for(jobs[i].cg, cmax, fair);
                 const bool stage = jobs[i].cg.n <= kCgStageMax;
+                const unsigned seg = cg_seg_for(jobs[i].cg);
                 CgTable t{};
                 std::uint32_t maxn = 0;
                 for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
                     const vgpu_cg_header& h = jobs[k].cg;
-                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, cmax) != cs ||
-                        (h.n <= kCgStageMax) != stage)
+                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, cmax, fair) != cs ||
+                        (h.n <= kCgStageMax) != stage || cg_seg_for(h) != seg)
                         continue;
                     done[k] = true;
                     const std::uint8_t* in = jobs[k].in;
@@ -588,10 +621,17 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     j.shift = h.shift;
                     maxn = std::max(maxn, h.n);
                 }
+                // p staged (n doubles), then the largest rowstr slice if it fits
+                std::uint32_t maxrows = 0;
+                for (std::uint32_t k = 0; k < t.njobs; ++k)
+                    maxrows = std::max(maxrows, (t.job[k].n + cs - 1) / cs + 2);
+                t.stage_n = stage ? maxn : 0;
+                const std::uint64_t base = 8ull * t.stage_n;
+                t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3(t.njobs * cs);
                 cfg.blockDim = dim3(kCgThreads);
-                cfg.dynamicSmemBytes = stage ? 8ull * maxn : 0;
+                cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
                 cfg.stream = s;
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
@@ -600,8 +640,15 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 at[0].val.clusterDim.z = 1;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                const cudaError_t e = stage ? cudaLaunchKernelEx(&cfg, cg_kernel<true>, t)
-                                           : cudaLaunchKernelEx(&cfg, cg_kernel<false>, t);
+                cudaError_t e;
+                if (stage)
+                    e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_kernel<true, 32>, t)
+                        : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_kernel<true, 16>, t)
+                                    : cudaLaunchKernelEx(&cfg, cg_kernel<true, 8>, t);
+                else
+                    e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_kernel<false, 32>, t)
+                        : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_kernel<false, 16>, t)
+                                    : cudaLaunchKernelEx(&cfg, cg_kernel<false, 8>, t);
                 ++*launches;
                 if (e != cudaSuccess) return e;
             }

@@ -33,6 +33,7 @@ constexpr int kCgThreads = 1024;
 constexpr int kCgMaxCluster = 16;     // CTAs per job at most (non-portable size)
 constexpr int kMaxCgJobs = 16;
 constexpr std::uint32_t kCgStageMax = 24576;  // rows whose p fits in shared memory (192 KiB)
+constexpr std::uint32_t kCgSmemBytes = 224 * 1024;  // dynamic shared memory cap per CTA
 
 struct CgJob {
     const std::uint32_t* rowstr;
@@ -51,6 +52,8 @@ struct CgJob {
 struct CgTable {
     CgJob job[kMaxCgJobs];
     std::uint32_t njobs;
+    std::uint32_t stage_n;     // doubles of staged p at the start of dynamic smem
+    std::uint32_t srow_words;  // room for a rowstr slice after it (u32 words)
 };
 
 __device__ __forceinline__ double cg_warp_sum(double v) {
@@ -65,9 +68,12 @@ struct CgReduce {
     double total[3];
 };
 
-// Sum W per-thread values over the whole cluster: warp tree, warps in
-// order, CTAs in rank order (warp 0 of every CTA computes the same bits).
-// The cluster barrier inside also orders every global write before it.
+// Sum W per-thread values over the whole cluster with one fixed tree:
+// lanes -> warps (shuffle tree), warps -> CTA (warp 0, shuffle tree over the
+// 32 warp partials), CTAs -> cluster (warp 0 of every CTA reads all partials
+// over DSMEM and runs the same tree), so every CTA holds the same bits and
+// results repeat run to run. The cluster barrier inside also orders every
+// global write before it.
 template <int W>
 __device__ __forceinline__ void cg_cluster_sum(double (&v)[W], CgReduce& red, unsigned& parity,
                                                cgx::cluster_group& cluster, unsigned csize) {
@@ -78,27 +84,22 @@ __device__ __forceinline__ void cg_cluster_sum(double (&v)[W], CgReduce& red, un
         if (lane == 0) red.warp[warp][w] = s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            double s = 0.0;
-#pragma unroll
-            for (int k = 0; k < kCgThreads / 32; ++k) s += red.warp[k][w];
-            red.slot[parity][w] = s;
+            const double s = cg_warp_sum(red.warp[lane][w]);
+            if (lane == 0) red.slot[parity][w] = s;
         }
     }
     cluster.sync();
     if (warp == 0) {
-        // lane c fetches CTA c's partials (one DSMEM round trip), lane 0
-        // adds them in rank order
-        double part[W];
         const double* src = lane < csize ? cluster.map_shared_rank(&red.slot[parity][0], lane) : nullptr;
+        double part[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) part[w] = src ? src[w] : 0.0;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            double s = 0.0;
-            for (unsigned c = 0; c < csize; ++c) s += __shfl_sync(0xffffffffu, part[w], c);
+            const double s = cg_warp_sum(part[w]);
             if (lane == 0) red.total[w] = s;
         }
     }
@@ -108,27 +109,72 @@ __device__ __forceinline__ void cg_cluster_sum(double (&v)[W], CgReduce& red, un
     parity ^= 1u;
 }
 
-// y[row] = sum_k a[k] * v[colidx[k]] for this CTA's rows, one warp per row;
-// lane 0 of the owning warp gets the row sum. Calls f(row, sum) on lane 0.
-template <typename Gather, typename F>
-__device__ __forceinline__ void cg_spmv(const CgJob& job, std::uint32_t r0, std::uint32_t r1,
-                                        Gather gather, F f) {
+// y[row] = sum_k a[k] * v[colidx[k]] for this CTA's rows. A row belongs to
+// a segment of `seg` lanes (8, 16 or 32 by the job's nonzeros per row), so a
+// warp works on 32 / seg rows at once; each lane issues up to kCgChains
+// predicated loads of (colidx, a) at once, which covers a whole NPB row in
+// one memory round trip (the SpMV is bound by memory latency x parallelism
+// per SM, not by bandwidth). Row bounds come from shared memory (rs: this
+// CTA's rowstr slice). The sum order is fixed by (seg, lane), so results
+// are deterministic. f(row, sum) runs on the segment's first lane.
+constexpr unsigned kCgChains = 4;
+
+struct CgMatrix {  // the hot fields of a job, in registers
+    const std::uint32_t* __restrict__ colidx;
+    const double* __restrict__ a;
+    std::uint32_t nm1;  // n - 1: column clamp
+};
+
+template <unsigned seg, typename Gather, typename F>
+__device__ __forceinline__ void cg_spmv(const CgMatrix& m, const std::uint32_t* rs, std::uint32_t r0,
+                                        std::uint32_t r1, Gather gather, F f) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (std::uint32_t row = r0 + warp; row < r1; row += kCgThreads / 32) {
-        const std::uint32_t k0 = __ldg(job.rowstr + row), k1 = __ldg(job.rowstr + row + 1);
-        double s = 0.0;
-        for (std::uint32_t k = k0 + lane; k < k1; k += 32) {
-            const std::uint32_t c = min(__ldg(job.colidx + k), job.n - 1);  // malformed input stays in bounds
-            s = fma(__ldg(job.a + k), gather(c), s);
+    const unsigned sl = lane & (seg - 1);
+    constexpr unsigned per_warp = 32 / seg;
+    const std::uint32_t nm1 = m.nm1;
+    const std::uint32_t* __restrict__ colidx = m.colidx;
+    const double* __restrict__ a = m.a;
+    for (std::uint32_t row0 = r0 + warp * per_warp; row0 < r1; row0 += (kCgThreads / 32) * per_warp) {
+        const std::uint32_t row = row0 + lane / seg;
+        double acc[kCgChains];
+#pragma unroll
+        for (unsigned c = 0; c < kCgChains; ++c) acc[c] = 0.0;
+        if (row < r1) {
+            const std::uint32_t k1 = rs[row - r0 + 1];
+            for (std::uint32_t k = rs[row - r0] + sl; k < k1; k += kCgChains * seg) {
+                std::uint32_t col[kCgChains];
+                double av[kCgChains];
+#pragma unroll
+                for (unsigned c = 0; c < kCgChains; ++c) {
+                    const std::uint32_t kk = k + c * seg;
+                    const bool in = kk < k1;
+                    // malformed column indices are clamped into bounds
+                    col[c] = in ? min(__ldg(colidx + kk), nm1) : 0u;
+                    av[c] = in ? __ldg(a + kk) : 0.0;
+                }
+#pragma unroll
+                for (unsigned c = 0; c < kCgChains; ++c) acc[c] = fma(av[c], gather(col[c]), acc[c]);
+            }
         }
-        s = cg_warp_sum(s);
-        if (lane == 0) f(row, s);
+        double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+        for (unsigned o = seg / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, seg);
+        if (sl == 0 && row < r1) f(row, s);
     }
 }
 
-template <bool kStage>
+// Lanes per row segment for a job (measured on B200: S, W and A all run
+// best at 16 with four chains per lane).
+__host__ __device__ __forceinline__ unsigned cg_segment(std::uint32_t n, std::uint32_t nnz) {
+    const std::uint32_t per_row = nnz / (n ? n : 1);
+    return per_row >= 256 ? 32u : per_row >= 40 ? 16u : 8u;
+}
+
+template <bool kStage, unsigned kSeg>
 __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant__ CgTable table) {
-    extern __shared__ double ps[];  // staged p (kStage)
+    // dynamic shared memory: staged p (kStage: n doubles), then this CTA's
+    // rowstr slice when it fits (table.srow_words)
+    extern __shared__ double ps[];
     __shared__ CgReduce red;
     cgx::cluster_group cluster = cgx::this_cluster();
     const unsigned csize = cluster.num_blocks();
@@ -138,15 +184,39 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     const std::uint32_t r0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * rank) / csize);
     const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (rank + 1)) / csize);
     unsigned parity = 0;
+    const CgMatrix mat{job.colidx, job.a, n - 1};
+    std::uint32_t* const srow = reinterpret_cast<std::uint32_t*>(ps + (kStage ? table.stage_n : 0));
+    const bool rs_smem = r1 - r0 + 1 <= table.srow_words;
+    if (rs_smem)
+        for (std::uint32_t i = threadIdx.x; i <= r1 - r0; i += kCgThreads) srow[i] = __ldg(job.rowstr + r0 + i);
+    const std::uint32_t* const rs = rs_smem ? srow : job.rowstr + r0;
+    __syncthreads();
     double* const x = job.x;
     double* const z = job.z;
     double* const p = job.p;
     double* const q = job.q;
     double* const r = job.r;
 
+    // whole p into shared memory: 16-byte loads, two in flight per thread
     auto stage_p = [&]() {
         if constexpr (kStage) {
-            for (std::uint32_t i = threadIdx.x; i < n; i += kCgThreads) ps[i] = __ldcg(p + i);
+            const double2* p2 = reinterpret_cast<const double2*>(p);
+            double2* s2 = reinterpret_cast<double2*>(ps);
+            const std::uint32_t n2 = n / 2;
+            for (std::uint32_t i0 = threadIdx.x; i0 < n2; i0 += 2 * kCgThreads) {
+                double2 t[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const std::uint32_t i = i0 + u * kCgThreads;
+                    if (i < n2) t[u] = __ldcg(p2 + i);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const std::uint32_t i = i0 + u * kCgThreads;
+                    if (i < n2) s2[i] = t[u];
+                }
+            }
+            if ((n & 1u) && threadIdx.x == 0) ps[n - 1] = __ldcg(p + n - 1);
             __syncthreads();
         }
     };
@@ -157,7 +227,8 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
 
     for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = 1.0;
     double zeta = 0.0, rnorm = 0.0;
-    for (std::uint32_t it = 0; it < job.niter; ++it) {
+    const std::uint32_t niter = job.niter, cgitmax = job.cgitmax;
+    for (std::uint32_t it = 0; it < niter; ++it) {
         // conj_grad: q = z = 0, r = p = x, rho = r . r
         double v1[1] = {0.0};
         for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) {
@@ -170,12 +241,12 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
         cg_cluster_sum(v1, red, parity, cluster, csize);  // also publishes p
         double rho = v1[0];
         stage_p();
-        for (std::uint32_t cgit = 0; cgit < job.cgitmax; ++cgit) {
+        for (std::uint32_t cgit = 0; cgit < cgitmax; ++cgit) {
             // q = A p, d = p . q
             double d[1] = {0.0};
-            cg_spmv(job, r0, r1, gather_p, [&](std::uint32_t row, double s) {
+            cg_spmv<kSeg>(mat, rs, r0, r1, gather_p, [&](std::uint32_t row, double s) {
                 q[row] = s;
-                d[0] = fma(p[row], s, d[0]);
+                d[0] = fma(gather_p(row), s, d[0]);
             });
             cg_cluster_sum(d, red, parity, cluster, csize);
             const double alpha = rho / d[0];
@@ -198,7 +269,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
         }
         // ||x - A z||, x . z, z . z (z complete: written before the last barriers)
         double s3[3] = {0.0, 0.0, 0.0};
-        cg_spmv(job, r0, r1, [&](std::uint32_t c) { return __ldcg(z + c); },
+        cg_spmv<kSeg>(mat, rs, r0, r1, [&](std::uint32_t c) { return __ldcg(z + c); },
                 [&](std::uint32_t row, double s) {
                     const double xi = x[row], zi = z[row];
                     const double e = xi - s;
