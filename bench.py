@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """bench.py — aggregate SPMD jobs/s through the B200 GVM (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vecadd|ep|bs|mm|mixed]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vecadd|ep|bs|mm|mixed|cg|vmul]
                     [--procs P] [--impl ours|reference]
 
 One "step" = one SPMD round: each of the P processes sharing a GPU runs one
@@ -50,7 +50,8 @@ sys.path.insert(0, REPO)
 METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; kernel GB/s vs roofline"
 L2_BYTES = 126 << 20
 # arithmetic type each workload's path computes in (EP: binary64 + integer LCG)
-DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f64"}
+DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f64", "cg": "f64",
+         "vmul": "f32"}
 
 
 def log(*a):
@@ -558,7 +559,7 @@ def model_summary(batches):
 
 # ---- rooflines ----------------------------------------------------------------------
 
-KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32"}
+KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32", "cg": "hbm", "vmul": "hbm"}
 
 
 def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
@@ -567,6 +568,9 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
     achieved = ALGORITHMIC work per launch / the launch's average duration
     (CUDA events on its stream, inside the timed region):
       vecadd/bs  bytes: 12 B per element / 20 B per option
+      vmul       12 B per element
+      cg         12 B per nonzero + 4 B per row per SpMV, 26 SpMVs per
+                 outer iteration (the matrix streams once per SpMV)
       mm         2 n^3 FLOP per task (FP32 SIMT, or 3xTF32 tcgen05 opt-in)
       ep         IEEE binary64 operations of the restated NPB algorithm:
                  7 per pair + 32 per accepted pair (W.ep_fp64_ops)
@@ -706,7 +710,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     # default: BASELINE.json configs[1] (NAS EP class A, 8 processes per B200)
-    ap.add_argument("--workload", default="ep", choices=["vecadd", "ep", "bs", "mm", "mixed"])
+    ap.add_argument("--workload", default="ep",
+                    choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul"])
     ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-native", action="store_true")

@@ -79,9 +79,43 @@ vgpu::Bytes mm_payload(vgpu::ByteView in) {
     return out;
 }
 
+vgpu::Bytes cg_payload(vgpu::ByteView in) {
+    vgpu_cg_result r;
+    if (vo_cg_run(in.data(), in.size(), &r) != 0)
+        throw vgpu::PayloadError(vgpu::PayloadError::Kind::MalformedInput, "nas-cg input");
+    vgpu::Bytes out(sizeof r);
+    std::memcpy(out.data(), &r, sizeof r);
+    return out;
+}
+
+vgpu::Bytes vmul_payload(vgpu::ByteView in) {
+    if (in.size() % 8)
+        throw vgpu::PayloadError(vgpu::PayloadError::Kind::MalformedInput, "vector-mul input");
+    const std::size_t n = in.size() / 8;
+    const float* f = reinterpret_cast<const float*>(in.data());
+    vgpu::Bytes out(4 * n);
+    vo_vector_mul(reinterpret_cast<float*>(out.data()), f, f + n, n);
+    return out;
+}
+
+// the CG program's makea: the oracle's NPB restatement
+vgpu::Bytes cg_makea(char cls) {
+    static const struct { char c; std::uint32_t n, nonzer, niter; double shift; } kClasses[] = {
+        {'S', 1400, 7, 15, 10.0}, {'W', 7000, 8, 15, 12.0}, {'A', 14000, 11, 15, 20.0},
+        {'B', 75000, 13, 75, 60.0}, {'C', 150000, 15, 75, 110.0}};
+    for (const auto& k : kClasses)
+        if (k.c == cls) {
+            vgpu::Bytes b(vo_cg_makea(k.n, k.nonzer, k.niter, k.shift, nullptr, 0));
+            vo_cg_makea(k.n, k.nonzer, k.niter, k.shift, b.data(), b.size());
+            return b;
+        }
+    throw std::invalid_argument("unknown NPB CG class");
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+    vgpu::wl::cg_builder() = cg_makea;
     std::string workload = "vecadd", instance = "refbench" + std::to_string(getpid());
     std::uint32_t procs = 4, rounds = 3, warmup = 1;
     vgpu::wl::Sizes sizes;
@@ -97,6 +131,7 @@ int main(int argc, char** argv) {
         else if (a == "--ep-batches") sizes.ep_batches = std::stoull(v);
         else if (a == "--bs-n") sizes.bs_n = std::stoull(v);
         else if (a == "--mm-n") sizes.mm_n = std::stoul(v);
+        else if (a == "--cg-class") sizes.cg_class = v[0];
     }
     const std::uint32_t total = warmup + rounds;
     // per-worker timestamps live in a shared anonymous mapping
@@ -155,6 +190,8 @@ int main(int argc, char** argv) {
     reg.register_payload("nas-ep", ep_payload);
     reg.register_payload("black-scholes", bs_payload);
     reg.register_payload("sgemm", mm_payload);
+    reg.register_payload("nas-cg", cg_payload);
+    reg.register_payload("vector-mul", vmul_payload);
     vgpu::GvmConfig g;
     g.instance = instance;
     g.max_clients = procs;

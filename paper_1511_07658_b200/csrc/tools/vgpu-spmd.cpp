@@ -1,7 +1,7 @@
 // vgpu-spmd — one SPMD process of a benchmark run (the forked worker of the
 // reference harness, proj/src/bench/bench.cpp:186-231).
 //
-//   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed
+//   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul
 //             --rounds R [--instance NAME | --native [--device D]]
 //
 // Builds its private input, leases a VGPU (retrying until the daemon is
@@ -14,6 +14,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include <vector>
 
 #include "vgpu/client.hpp"
+#include "vgpu/npb_cg.hpp"
 #include "workloads.hpp"
 
 namespace {
@@ -36,15 +38,17 @@ std::int64_t now_ns() {
 
 // stride 1 checks every element; inside the timed loop a sparse stride keeps
 // the check cheap and identical for both modes; the full check runs after.
-bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out, std::size_t stride) {
+// (vector-mul: mul = true, out = a * b)
+bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out, std::size_t stride, bool mul = false) {
     const std::size_t n = in.size() / 8;
     if (out.size() != 4 * n) return false;
     const float* a = reinterpret_cast<const float*>(in.data());
     const float* b = a + n;
     const float* o = reinterpret_cast<const float*>(out.data());
+    auto want = [&](std::size_t i) { return mul ? a[i] * b[i] : a[i] + b[i]; };
     for (std::size_t i = 0; i < n; i += stride)
-        if (o[i] != a[i] + b[i]) return false;
-    return n == 0 || o[n - 1] == a[n - 1] + b[n - 1];
+        if (o[i] != want(i)) return false;
+    return n == 0 || o[n - 1] == want(n - 1);
 }
 
 std::uint64_t sample_hash(const vgpu::Bytes& out, std::size_t stride) {
@@ -86,6 +90,7 @@ int main(int argc, char** argv) {
             else if (a == "--ep-batches") sizes.ep_batches = std::stoull(val());
             else if (a == "--bs-n") sizes.bs_n = std::stoull(val());
             else if (a == "--mm-n") sizes.mm_n = std::stoul(val());
+            else if (a == "--cg-class") sizes.cg_class = val()[0];
             else throw std::invalid_argument("unknown argument " + a);
         } catch (const std::exception& e) {
             std::fprintf(stderr, "vgpu-spmd: %s\n", e.what());
@@ -96,6 +101,11 @@ int main(int argc, char** argv) {
     mallopt(M_MMAP_THRESHOLD, 1 << 30);
     mallopt(M_TRIM_THRESHOLD, 1 << 30);
 
+    // NPB CG workers build their matrix with the product's makea
+    vgpu::wl::cg_builder() = [](char cls) {
+        const vgpu::npb::CgClass c = vgpu::npb::cg_class(cls);
+        return vgpu::npb::make_cg_input(c.n, c.nonzer, c.niter, c.shift);
+    };
     const std::int64_t t_start = now_ns();
     vgpu::wl::Job job = vgpu::wl::make_job(workload, worker, workers, sizes);
     std::unique_ptr<vgpu::VgpuHandle> vh;
@@ -162,10 +172,10 @@ int main(int argc, char** argv) {
             if (out.size() != job.output_bytes) {
                 ok = false;
                 err = "wrong result size";
-            } else if (job.kind == vgpu::wl::Kind::VecAdd) {
-                if (!check_vecadd(job.input, out, kStride)) {
+            } else if (job.kind == vgpu::wl::Kind::VecAdd || job.kind == vgpu::wl::Kind::VecMul) {
+                if (!check_vecadd(job.input, out, kStride, job.kind == vgpu::wl::Kind::VecMul)) {
                     ok = false;
-                    err = "vector-add sums differ";
+                    err = "vector-add/mul results differ";
                 }
             } else {
                 const std::uint64_t h = sample_hash(out, kStride);
@@ -180,7 +190,8 @@ int main(int argc, char** argv) {
         }
         if (vh) vh->rls();
         // full checks outside the timed loop
-        if (ok && job.kind == vgpu::wl::Kind::VecAdd && !check_vecadd(job.input, last_out, 1)) {
+        if (ok && (job.kind == vgpu::wl::Kind::VecAdd || job.kind == vgpu::wl::Kind::VecMul) &&
+            !check_vecadd(job.input, last_out, 1, job.kind == vgpu::wl::Kind::VecMul)) {
             ok = false;
             err = "vector-add sums differ (full check)";
         }
@@ -211,6 +222,21 @@ int main(int argc, char** argv) {
         os << (k ? ", " : "") << "\"" << names[k] << "\": " << (v.empty() ? 0 : v[v.size() / 2]);
     }
     os << "}";
+    if (job.kind == vgpu::wl::Kind::Cg && last_out.size() == sizeof(vgpu_cg_result)) {
+        // NPB's own verification: zeta within 1e-10 of the published value
+        vgpu_cg_result r;
+        std::memcpy(&r, last_out.data(), sizeof r);
+        const double want = vgpu::npb::cg_class(sizes.cg_class).zeta_verify;
+        const bool verified = std::fabs(r.zeta - want) / want <= 1e-10;
+        char buf[160];
+        std::snprintf(buf, sizeof buf, ", \"cg\": {\"zeta\": %.15g, \"rnorm\": %.6g, \"verified\": %s}",
+                      r.zeta, r.rnorm, verified ? "true" : "false");
+        os << buf;
+        if (!verified && ok) {
+            ok = false;
+            err = "nas-cg zeta differs from NPB's";
+        }
+    }
     if (job.kind == vgpu::wl::Kind::Ep && last_out.size() == sizeof(vgpu_ep_result)) {
         // the job's partial for the final reduction, bit patterns in hex
         vgpu_ep_result r;

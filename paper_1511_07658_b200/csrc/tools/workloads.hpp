@@ -11,7 +11,14 @@
 //               contiguous batch ranges (NPB-MPI decomposition);
 //   bs      C3  4 Mi options, S~U[5,30], X~U[1,100], T~U[0.25,10], seed 5347+w;
 //   mm      C4  2048 x 2048 fp32, A,B ~ U[-1,1], seed 1000+w;
-//   mixed   C5  worker w runs kind w % 4 (vecadd, ep, bs, mm).
+//   mixed   C5  worker w runs kind w % 4 (vecadd, ep, bs, mm);
+// and the paper's remaining payloads (not BASELINE
+// configs):
+//   cg      NAS CG, every worker runs the whole NPB class (default A): the
+//           program builds its matrix with NPB's makea (untimed in NPB) —
+//           through cg_builder(), which the program sets (vgpu-spmd: the
+//           product's vgpu::npb::make_cg_input; ref-bench: the oracle's);
+//   vmul    VecMul, vecadd's shapes and values, payload vector-mul.
 #pragma once
 
 #include <cmath>
@@ -27,7 +34,7 @@
 
 namespace vgpu::wl {
 
-enum class Kind { VecAdd, Ep, Bs, Mm };
+enum class Kind { VecAdd, Ep, Bs, Mm, Cg, VecMul };
 
 struct Sizes {
     std::uint64_t vecadd_n = 1ull << 20;
@@ -35,7 +42,31 @@ struct Sizes {
     std::uint64_t ep_batches = 0;  // batches of the whole run's problem; 0 = 2^(ep_m-16)
     std::uint64_t bs_n = 4ull << 20;
     std::uint32_t mm_n = 2048;
+    char cg_class = 'A';
 };
+
+// NPB CG shapes (cg.f): rows, nonzeros per generated vector
+struct CgShape {
+    std::uint32_t n, nonzer;
+};
+
+inline CgShape cg_shape(char cls) {
+    switch (cls) {
+        case 'S': return {1400, 7};
+        case 'W': return {7000, 8};
+        case 'A': return {14000, 11};
+        case 'B': return {75000, 13};
+        case 'C': return {150000, 15};
+        default: throw std::invalid_argument(std::string("unknown NPB CG class ") + cls);
+    }
+}
+
+// The program's NPB makea: nas-cg input bytes for a class
+using CgBuilder = Bytes (*)(char cls);
+inline CgBuilder& cg_builder() {
+    static CgBuilder b = nullptr;
+    return b;
+}
 
 struct Job {
     Kind kind;
@@ -49,6 +80,8 @@ inline Kind kind_of(const std::string& workload, std::uint32_t worker) {
     if (workload == "ep") return Kind::Ep;
     if (workload == "bs") return Kind::Bs;
     if (workload == "mm") return Kind::Mm;
+    if (workload == "cg") return Kind::Cg;
+    if (workload == "vmul") return Kind::VecMul;
     if (workload == "mixed") return static_cast<Kind>(worker % 4);
     throw std::invalid_argument("unknown workload: " + workload);
 }
@@ -82,6 +115,7 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
     Job j;
     j.kind = kind_of(workload, worker);
     switch (j.kind) {
+        case Kind::VecMul:
         case Kind::VecAdd: {
             const std::uint64_t n = sz.vecadd_n;
             std::vector<float> v(2 * n);
@@ -91,7 +125,7 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
             }
             j.input.resize(8 * n);
             std::memcpy(j.input.data(), v.data(), j.input.size());
-            j.desc.payload_id = "vector-add";
+            j.desc.payload_id = j.kind == Kind::VecAdd ? "vector-add" : "vector-mul";
             j.desc.t_data_in = pcie_us(8 * n);
             j.desc.t_comp = (12 * n) / 6'500'000 + 1;
             j.desc.t_data_out = pcie_us(4 * n);
@@ -142,6 +176,20 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
             j.output_bytes = 8 * n;
             break;
         }
+        case Kind::Cg: {
+            if (!cg_builder()) throw std::logic_error("cg workload: no NPB makea set (cg_builder)");
+            j.input = cg_builder()(sz.cg_class);
+            vgpu_cg_header h;
+            std::memcpy(&h, j.input.data(), sizeof h);
+            j.desc.payload_id = "nas-cg";
+            j.desc.t_data_in = pcie_us(j.input.size());
+            // niter x 26 SpMVs of 12 B per nonzero at ~2 TB/s
+            j.desc.t_comp = static_cast<Micros>(h.niter * 26.0 * 12.0 * h.nnz / 2e6) + 1;
+            j.desc.t_data_out = 1;
+            j.desc.grid_size = 16;
+            j.output_bytes = sizeof(vgpu_cg_result);
+            break;
+        }
         case Kind::Mm: {
             const std::uint64_t n = sz.mm_n;
             std::vector<float> v(2 * n * n);
@@ -169,6 +217,11 @@ inline std::uint64_t region_bytes(const std::string& workload, const Sizes& sz =
     if (workload == "ep") return ep;
     if (workload == "bs") return bs;
     if (workload == "mm") return mm;
+    if (workload == "vmul") return va;
+    if (workload == "cg") {  // upper bound: nnz <= n (nonzer + 1)^2
+        const CgShape c = cg_shape(sz.cg_class);
+        return vgpu_cg_input_bytes(c.n, c.n * (c.nonzer + 1) * (c.nonzer + 1));
+    }
     return std::max({va, bs, mm, ep});
 }
 

@@ -1,4 +1,5 @@
-"""BASELINE.json configs C1-C5 as job lists (mirror of csrc/tools/workloads.hpp).
+"""BASELINE.json configs C1-C5 (+ the paper's CG and VecMul) as job lists
+(mirror of csrc/tools/workloads.hpp).
 
 Used by bench.py's device-resident leg; the SPMD workers (bin/vgpu-spmd)
 build the same shapes natively. vecadd and EP inputs are bit-identical to
@@ -12,16 +13,23 @@ import numpy as np
 
 from ._native import EpParams
 
-PAYLOAD = {"vecadd": "vector-add", "ep": "nas-ep", "bs": "black-scholes", "mm": "sgemm"}
-KINDS = ("vecadd", "ep", "bs", "mm")
-DEFAULT_PROCS = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "mixed": 16}
+PAYLOAD = {"vecadd": "vector-add", "ep": "nas-ep", "bs": "black-scholes", "mm": "sgemm",
+           "cg": "nas-cg", "vmul": "vector-mul"}
+KINDS = ("vecadd", "ep", "bs", "mm")  # the kinds `mixed` cycles through (C5)
+DEFAULT_PROCS = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "mixed": 16, "cg": 8, "vmul": 4}
 CONFIG_NAME = {
     "vecadd": "C1 vector addition, 1M floats per process",
     "ep": "C2 NAS EP class A split over the processes",
     "bs": "C3 Black-Scholes 4M options per process",
     "mm": "C4 FP32 matrix multiply 2048x2048 per process",
     "mixed": "C5 mixed: workers cycle vecadd/ep/bs/mm",
+    "cg": "NAS CG class A per process (paper workload, not a BASELINE config)",
+    "vmul": "VecMul 1M floats per process (paper workload, not a BASELINE config)",
 }
+
+# NPB CG shapes (n, nonzer) for the region bound (mirror of workloads.hpp)
+CG_SHAPES = {"S": (1400, 7), "W": (7000, 8), "A": (14000, 11), "B": (75000, 13), "C": (150000, 15)}
+_cg_cache = {}
 
 
 @dataclass
@@ -45,9 +53,10 @@ class Sizes:
     def size_args(self) -> list:
         return ["--vecadd-n", str(self.vecadd_n), "--ep-m", str(self.ep_m),
                 "--ep-batches", str(self.ep_batches), "--bs-n", str(self.bs_n),
-                "--mm-n", str(self.mm_n)]
+                "--mm-n", str(self.mm_n), "--cg-class", self.cg_class]
     bs_n: int = 4 << 20
     mm_n: int = 2048
+    cg_class: str = "A"
 
 
 # NAS EP class A (m = 28): accepted Gaussian pairs (NPB ep.f; pinned by
@@ -79,9 +88,20 @@ def ep_slice(workload: str, worker: int, workers: int, sz: Sizes):
     return first, per + (1 if rank < extra else 0)
 
 
+def cg_input(cls: str) -> bytes:
+    """The CG program's matrix (NPB makea through the product's client-side
+    builder, vgpu_cg_make_input); the same for every worker, built once."""
+    if cls not in _cg_cache:
+        from .vgpu import cg_input_for_class
+        _cg_cache[cls] = cg_input_for_class(cls)
+    return _cg_cache[cls]
+
+
 def job_input(workload: str, worker: int, workers: int, sz: Sizes = Sizes()) -> bytes:
     k = kind_of(workload, worker)
-    if k == "vecadd":
+    if k == "cg":
+        return cg_input(sz.cg_class)
+    if k in ("vecadd", "vmul"):
         j = np.arange(sz.vecadd_n)
         a = ((worker + 1) * 1000.0 + (j % 512)).astype(np.float32)
         b = ((j % 512) * 0.25).astype(np.float32)
@@ -101,12 +121,22 @@ def job_input(workload: str, worker: int, workers: int, sz: Sizes = Sizes()) -> 
 
 def output_bytes(kind: str, sz: Sizes = Sizes()) -> int:
     return {"vecadd": 4 * sz.vecadd_n, "ep": 112, "bs": 8 * sz.bs_n,
-            "mm": 4 * sz.mm_n * sz.mm_n}[kind]
+            "mm": 4 * sz.mm_n * sz.mm_n, "cg": 32, "vmul": 4 * sz.vecadd_n}[kind]
+
+
+def cg_input_bound(cls: str) -> int:
+    """nas-cg input bytes upper bound (nnz <= n (nonzer + 1)^2)."""
+    n, nz = CG_SHAPES[cls]
+    nnz = n * (nz + 1) ** 2
+    b = 24 + 4 * (n + 1) + 4 * nnz
+    return ((b + 7) & ~7) + 8 * nnz
 
 
 def input_bytes(kind: str, sz: Sizes = Sizes()) -> int:
+    if kind == "cg":
+        return cg_input_bound(sz.cg_class)
     return {"vecadd": 8 * sz.vecadd_n, "ep": 32, "bs": 12 * sz.bs_n,
-            "mm": 8 * sz.mm_n * sz.mm_n}[kind]
+            "mm": 8 * sz.mm_n * sz.mm_n, "vmul": 8 * sz.vecadd_n}[kind]
 
 
 def region_bytes(workload: str, sz: Sizes = Sizes()) -> int:
