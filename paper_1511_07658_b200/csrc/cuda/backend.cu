@@ -262,20 +262,26 @@ cudaError_t launch_tc2_tma(const vgk::TcTable& tt, std::uint32_t maxn, cudaStrea
     return cudaSuccess;
 }
 
-// Largest cluster the CG kernel can run with (16 needs the non-portable
-// attribute and a GPC with 16 free SMs; else 8), 0 when none launches.
-unsigned cg_max_cluster() {
-    static const unsigned c = [] {
+// Co-resident clusters of the CG kernel per cluster size 1..16 (above 8
+// needs the non-portable attribute; a cluster lives in one GPC, so at 16
+// CTAs only ~7 fit on a B200). All zero when the kernel cannot launch.
+struct CgOccupancy {
+    int active[vgk::kCgMaxCluster + 1] = {};  // index: cluster size
+};
+
+const CgOccupancy& cg_occupancy() {
+    static const CgOccupancy occ = [] {
+        CgOccupancy o;
         const int smem = static_cast<int>(vgk::kCgSmemBytes);
         for (auto k : {vgk::cg_kernel<true, 8>, vgk::cg_kernel<true, 16>, vgk::cg_kernel<true, 32>,
                        vgk::cg_kernel<false, 8>, vgk::cg_kernel<false, 16>, vgk::cg_kernel<false, 32>}) {
             if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
                 cudaGetLastError();
-                return 0u;
+                return o;
             }
         }
-        for (unsigned cs = vgk::kCgMaxCluster; cs >= 1; cs /= 2) {
+        for (unsigned cs = 1; cs <= vgk::kCgMaxCluster; ++cs) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(cs);
             cfg.blockDim = dim3(vgk::kCgThreads);
@@ -288,24 +294,34 @@ unsigned cg_max_cluster() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true, 32>, &cfg) == cudaSuccess && nc > 0)
-                return cs;
-            cudaGetLastError();
+            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true, 32>, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                nc = 0;
+            }
+            o.active[cs] = nc;
         }
-        return 0u;
+        if (std::getenv("VGPU_CG_VERBOSE")) {
+            std::fprintf(stderr, "nas-cg co-resident clusters by size:");
+            for (unsigned cs = 1; cs <= vgk::kCgMaxCluster; ++cs) std::fprintf(stderr, " %u:%d", cs, o.active[cs]);
+            std::fprintf(stderr, "\n");
+        }
+        return o;
     }();
-    return c;
+    return occ;
 }
 
-// CTAs per CG job, a power of two up to the launchable maximum: the batch's
-// fair share of the SMs (`fair`), at least one CTA per ~128K nonzeros, at
-// most one per 64 rows. The SpMV is latency-bound per SM, so a job runs as
-// wide as the batch leaves room for.
-unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned cmax, unsigned fair) {
-    unsigned cs = 1;
-    while (cs < cmax && static_cast<std::uint64_t>(cs) * (1u << 17) < h.nnz) cs *= 2;
-    while (cs < cmax && cs * 2 <= fair) cs *= 2;
-    while (cs > 1 && static_cast<std::uint64_t>(cs) * 64 > h.n) cs /= 2;
+// CTAs per CG job: the widest cluster at which all `jobs` clusters of the
+// batch are co-resident (the SpMV is latency-bound per SM, so a job runs as
+// wide as the batch leaves room for, but a second wave would double the
+// step), at most one CTA per 64 rows. 0: cannot launch.
+unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned jobs) {
+    const CgOccupancy& o = cg_occupancy();
+    unsigned cs = vgk::kCgMaxCluster;
+    while (cs > 1 && (o.active[cs] < static_cast<int>(jobs) || 64ull * cs > h.n)) --cs;
+    if (o.active[cs] <= 0) {  // nothing fits all jobs at once: the widest that launches
+        for (cs = vgk::kCgMaxCluster; cs >= 1 && o.active[cs] <= 0; --cs) {
+        }
+    }
     return cs;
 }
 
@@ -318,19 +334,6 @@ unsigned cg_seg_for(const vgpu_cg_header& h) {
         return v == 8 || v == 16 || v == 32 ? v : 0u;
     }();
     return force ? force : vgk::cg_segment(h.n, h.nnz);
-}
-
-unsigned device_sms() {
-    static const unsigned n = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-            cudaGetLastError();
-            v = 148;
-        }
-        return static_cast<unsigned>(v);
-    }();
-    return n;
 }
 
 // SGEMM tensor-core phases launch_jobs issues: 1 = split/transpose pre-pass,
@@ -581,22 +584,20 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
         case VGPU_CU_K_CG: {
             // group by (cluster size, p staged in shared memory); one launch
             // per group of up to kMaxCgJobs clusters
-            const unsigned cmax = cg_max_cluster();
-            if (!cmax) return cudaErrorInvalidConfiguration;
             unsigned ncg = 0;
             for (std::uint32_t i = 0; i < n; ++i) ncg += jobs[i].ws && jobs[i].cg.n ? 1u : 0u;
-            const unsigned fair = ncg ? std::max(1u, device_sms() / ncg) : 1u;
             std::vector<bool> done(n, false);
             for (std::uint32_t i = 0; i < n; ++i) {
                 if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
-                const unsigned cs = cg_cluster_for(jobs[i].cg, cmax, fair);
+                const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);
+                if (!cs) return cudaErrorInvalidConfiguration;
                 const bool stage = jobs[i].cg.n <= kCgStageMax;
                 const unsigned seg = cg_seg_for(jobs[i].cg);
                 CgTable t{};
                 std::uint32_t maxn = 0;
                 for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
                     const vgpu_cg_header& h = jobs[k].cg;
-                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, cmax, fair) != cs ||
+                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, ncg) != cs ||
                         (h.n <= kCgStageMax) != stage || cg_seg_for(h) != seg)
                         continue;
                     done[k] = true;
