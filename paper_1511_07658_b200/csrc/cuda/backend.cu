@@ -273,8 +273,10 @@ const CgOccupancy& cg_occupancy() {
     static const CgOccupancy occ = [] {
         CgOccupancy o;
         const int smem = static_cast<int>(vgk::kCgSmemBytes);
-        for (auto k : {vgk::cg_kernel<true, 8>, vgk::cg_kernel<true, 16>, vgk::cg_kernel<true, 32>,
-                       vgk::cg_kernel<false, 8>, vgk::cg_kernel<false, 16>, vgk::cg_kernel<false, 32>}) {
+        using namespace vgk;
+        for (auto k : {cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>, cg_kernel<kCgGlobal, 32>,
+                       cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>, cg_kernel<kCgStaged, 32>,
+                       cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>, cg_kernel<kCgResident, 32>}) {
             if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
                 cudaGetLastError();
@@ -294,7 +296,7 @@ const CgOccupancy& cg_occupancy() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<true, 32>, &cfg) != cudaSuccess) {
+            if (cudaOccupancyMaxActiveClusters(&nc, vgk::cg_kernel<vgk::kCgResident, 32>, &cfg) != cudaSuccess) {
                 cudaGetLastError();
                 nc = 0;
             }
@@ -582,23 +584,37 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             return flush(gen, gen_tiles, false);
         }
         case VGPU_CU_K_CG: {
-            // group by (cluster size, p staged in shared memory); one launch
-            // per group of up to kMaxCgJobs clusters
+            // group by (cluster size, vector placement, row segment); one
+            // launch per group of up to kMaxCgJobs clusters
             unsigned ncg = 0;
             for (std::uint32_t i = 0; i < n; ++i) ncg += jobs[i].ws && jobs[i].cg.n ? 1u : 0u;
+            // placement: everything in shared memory if p + 4 own slices +
+            // the rowstr slice fit, else p alone, else HBM
+            // (VGPU_CG_MODE=0|1 caps it: HBM / staged p, for measurement and tests)
+            static const int mode_cap = [] {
+                const char* e = std::getenv("VGPU_CG_MODE");
+                return e && *e >= '0' && *e <= '2' ? *e - '0' : 2;
+            }();
+            auto mode_for = [&](const vgpu_cg_header& h, unsigned cs) {
+                const std::uint64_t rows = (h.n + cs - 1) / cs + 2;
+                int m = kCgGlobal;
+                if (8ull * h.n + 32ull * rows + 4ull * rows <= kCgSmemBytes) m = kCgResident;
+                else if (h.n <= kCgStageMax) m = kCgStaged;
+                return std::min(m, mode_cap);
+            };
             std::vector<bool> done(n, false);
             for (std::uint32_t i = 0; i < n; ++i) {
                 if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
                 const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);
                 if (!cs) return cudaErrorInvalidConfiguration;
-                const bool stage = jobs[i].cg.n <= kCgStageMax;
+                const int mode = mode_for(jobs[i].cg, cs);
                 const unsigned seg = cg_seg_for(jobs[i].cg);
                 CgTable t{};
-                std::uint32_t maxn = 0;
+                std::uint32_t maxn = 0, maxrows = 0;
                 for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
                     const vgpu_cg_header& h = jobs[k].cg;
                     if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, ncg) != cs ||
-                        (h.n <= kCgStageMax) != stage || cg_seg_for(h) != seg)
+                        mode_for(h, cs) != mode || cg_seg_for(h) != seg)
                         continue;
                     done[k] = true;
                     const std::uint8_t* in = jobs[k].in;
@@ -621,13 +637,12 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                     j.cgitmax = h.cgitmax;
                     j.shift = h.shift;
                     maxn = std::max(maxn, h.n);
+                    maxrows = std::max(maxrows, (h.n + cs - 1) / cs + 2);
                 }
-                // p staged (n doubles), then the largest rowstr slice if it fits
-                std::uint32_t maxrows = 0;
-                for (std::uint32_t k = 0; k < t.njobs; ++k)
-                    maxrows = std::max(maxrows, (t.job[k].n + cs - 1) / cs + 2);
-                t.stage_n = stage ? maxn : 0;
-                const std::uint64_t base = 8ull * t.stage_n;
+                // p (n doubles) | own x z r q slices | rowstr slice if it fits
+                t.stage_n = mode != kCgGlobal ? maxn : 0;
+                t.own_rows = mode == kCgResident ? maxrows : 0;
+                const std::uint64_t base = 8ull * t.stage_n + 32ull * t.own_rows;
                 t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3(t.njobs * cs);
@@ -641,15 +656,18 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 at[0].val.clusterDim.z = 1;
                 cfg.attrs = at;
                 cfg.numAttrs = 1;
-                cudaError_t e;
-                if (stage)
-                    e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_kernel<true, 32>, t)
-                        : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_kernel<true, 16>, t)
-                                    : cudaLaunchKernelEx(&cfg, cg_kernel<true, 8>, t);
-                else
-                    e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_kernel<false, 32>, t)
-                        : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_kernel<false, 16>, t)
-                                    : cudaLaunchKernelEx(&cfg, cg_kernel<false, 8>, t);
+                auto go = [&](auto k8, auto k16, auto k32) {
+                    return seg == 32 ? cudaLaunchKernelEx(&cfg, k32, t)
+                           : seg == 16 ? cudaLaunchKernelEx(&cfg, k16, t)
+                                       : cudaLaunchKernelEx(&cfg, k8, t);
+                };
+                const cudaError_t e =
+                    mode == kCgResident ? go(cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>,
+                                             cg_kernel<kCgResident, 32>)
+                    : mode == kCgStaged ? go(cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>,
+                                             cg_kernel<kCgStaged, 32>)
+                                        : go(cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>,
+                                             cg_kernel<kCgGlobal, 32>);
                 ++*launches;
                 if (e != cudaSuccess) return e;
             }

@@ -53,7 +53,8 @@ struct CgTable {
     CgJob job[kMaxCgJobs];
     std::uint32_t njobs;
     std::uint32_t stage_n;     // doubles of staged p at the start of dynamic smem
-    std::uint32_t srow_words;  // room for a rowstr slice after it (u32 words)
+    std::uint32_t own_rows;    // kCgResident: doubles per own vector slice after it
+    std::uint32_t srow_words;  // room for a rowstr slice after them (u32 words)
 };
 
 __device__ __forceinline__ double cg_warp_sum(double v) {
@@ -170,10 +171,22 @@ __host__ __device__ __forceinline__ unsigned cg_segment(std::uint32_t n, std::ui
     return per_row >= 256 ? 32u : per_row >= 40 ? 16u : 8u;
 }
 
-template <bool kStage, unsigned kSeg>
+// Vector placement (kMode, chosen per launch on the host by what fits in
+// shared memory):
+//   kCgGlobal    all vectors in the job's HBM workspace; p gathered via L2
+//   kCgStaged    p re-staged into shared memory after every update
+//   kCgResident  everything in shared memory: this CTA's x, z, r, q slices,
+//                the whole p; each CTA PUSHES its new p slice into every
+//                peer's copy over DSMEM (st.shared::cluster) and the cluster
+//                barrier that NPB's dependences need anyway publishes it, so
+//                no staging pass and no HBM round trip for vectors at all
+//                (classes S..A at the widths the batch allows).
+enum CgMode { kCgGlobal = 0, kCgStaged = 1, kCgResident = 2 };
+
+template <int kMode, unsigned kSeg>
 __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant__ CgTable table) {
-    // dynamic shared memory: staged p (kStage: n doubles), then this CTA's
-    // rowstr slice when it fits (table.srow_words)
+    // dynamic shared memory: p (stage_n doubles) | x z r q slices (own_rows
+    // doubles each, kCgResident) | this CTA's rowstr slice (srow_words)
     extern __shared__ double ps[];
     __shared__ CgReduce red;
     cgx::cluster_group cluster = cgx::this_cluster();
@@ -185,22 +198,27 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (rank + 1)) / csize);
     unsigned parity = 0;
     const CgMatrix mat{job.colidx, job.a, n - 1};
-    std::uint32_t* const srow = reinterpret_cast<std::uint32_t*>(ps + (kStage ? table.stage_n : 0));
+    constexpr bool kStage = kMode != kCgGlobal;
+    constexpr bool kRes = kMode == kCgResident;
+    const std::uint32_t own = kRes ? table.own_rows : 0;
+    double* const own0 = ps + (kStage ? table.stage_n : 0);
+    std::uint32_t* const srow = reinterpret_cast<std::uint32_t*>(own0 + 4ull * own);
     const bool rs_smem = r1 - r0 + 1 <= table.srow_words;
     if (rs_smem)
         for (std::uint32_t i = threadIdx.x; i <= r1 - r0; i += kCgThreads) srow[i] = __ldg(job.rowstr + r0 + i);
     const std::uint32_t* const rs = rs_smem ? srow : job.rowstr + r0;
     __syncthreads();
-    double* const x = job.x;
-    double* const z = job.z;
-    double* const p = job.p;
-    double* const q = job.q;
-    double* const r = job.r;
+    // vector element of global row i: own slices rebased to r0 when resident
+    double* const x = kRes ? own0 - r0 : job.x;
+    double* const z = kRes ? own0 + own - r0 : job.z;
+    double* const r = kRes ? own0 + 2ull * own - r0 : job.r;
+    double* const q = kRes ? own0 + 3ull * own - r0 : job.q;
+    double* const p = kRes ? ps : job.p;  // own rows of p (resident: the local full copy)
 
     // whole p into shared memory: 16-byte loads, two in flight per thread
     auto stage_p = [&]() {
-        if constexpr (kStage) {
-            const double2* p2 = reinterpret_cast<const double2*>(p);
+        if constexpr (kMode == kCgStaged) {
+            const double2* p2 = reinterpret_cast<const double2*>(job.p);
             double2* s2 = reinterpret_cast<double2*>(ps);
             const std::uint32_t n2 = n / 2;
             for (std::uint32_t i0 = threadIdx.x; i0 < n2; i0 += 2 * kCgThreads) {
@@ -216,13 +234,21 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
                     if (i < n2) s2[i] = t[u];
                 }
             }
-            if ((n & 1u) && threadIdx.x == 0) ps[n - 1] = __ldcg(p + n - 1);
+            if ((n & 1u) && threadIdx.x == 0) ps[n - 1] = __ldcg(job.p + n - 1);
             __syncthreads();
         }
     };
     auto gather_p = [&](std::uint32_t c) -> double {
         if constexpr (kStage) return ps[c];
-        else return __ldcg(p + c);
+        else return __ldcg(job.p + c);
+    };
+    // resident: element i of the full vector in every CTA's copy (own too)
+    auto push = [&](std::uint32_t i, double v) {
+        if constexpr (kRes) {
+            for (unsigned c = 0; c < csize; ++c) cluster.map_shared_rank(ps, c)[i] = v;
+        } else {
+            p[i] = v;
+        }
     };
 
     for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = 1.0;
@@ -235,7 +261,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
             const double xi = x[i];
             z[i] = 0.0;
             r[i] = xi;
-            p[i] = xi;
+            push(i, xi);
             v1[0] = fma(xi, xi, v1[0]);
         }
         cg_cluster_sum(v1, red, parity, cluster, csize);  // also publishes p
@@ -263,20 +289,29 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
             cg_cluster_sum(rr, red, parity, cluster, csize);
             rho = rr[0];
             const double beta = rho / rho0;
-            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) p[i] = fma(beta, p[i], r[i]);
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, fma(beta, p[i], r[i]));
             cluster.sync();  // p complete before anyone gathers it
             stage_p();
         }
-        // ||x - A z||, x . z, z . z (z complete: written before the last barriers)
+        // ||x - A z||, x . z, z . z: the residual SpMV gathers z — resident:
+        // pushed into every CTA's (now unused) p copy; else from HBM
+        if constexpr (kRes) {
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, z[i]);
+            cluster.sync();
+        }
         double s3[3] = {0.0, 0.0, 0.0};
-        cg_spmv<kSeg>(mat, rs, r0, r1, [&](std::uint32_t c) { return __ldcg(z + c); },
-                [&](std::uint32_t row, double s) {
-                    const double xi = x[row], zi = z[row];
-                    const double e = xi - s;
-                    s3[0] = fma(e, e, s3[0]);
-                    s3[1] = fma(xi, zi, s3[1]);
-                    s3[2] = fma(zi, zi, s3[2]);
-                });
+        cg_spmv<kSeg>(mat, rs, r0, r1,
+                      [&](std::uint32_t c) {
+                          if constexpr (kRes) return ps[c];
+                          else return __ldcg(job.z + c);
+                      },
+                      [&](std::uint32_t row, double s) {
+                          const double xi = x[row], zi = z[row];
+                          const double e = xi - s;
+                          s3[0] = fma(e, e, s3[0]);
+                          s3[1] = fma(xi, zi, s3[1]);
+                          s3[2] = fma(zi, zi, s3[2]);
+                      });
         cg_cluster_sum(s3, red, parity, cluster, csize);
         rnorm = sqrt(s3[0]);
         zeta = job.shift + 1.0 / s3[1];

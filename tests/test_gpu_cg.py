@@ -130,3 +130,47 @@ def test_vector_mul_bit_exact(n):
     with d:
         outs = _spmd(inst, ins, V.KernelDescriptor("vector-mul", 168, 2, 84))
     assert outs == want
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_nas_cg_every_vector_placement(mode):
+    """Each placement of the CG vectors (VGPU_CG_MODE: 0 HBM, 1 p staged in
+    shared memory, 2 everything in shared memory with DSMEM pushes) meets
+    NPB's verification and the oracle, in a fresh process (the cap is read
+    once per process). Classes S and W in one batch, and a class S alone
+    (widest cluster)."""
+    import subprocess
+    import sys
+    code = r'''
+import threading
+from oracle import oracle
+from paper_1511_07658_b200 import vgpu as V
+for classes in (["S", "W"], ["S"]):
+    ins = [V.cg_input_for_class(c) for c in classes]
+    outs = [V.native_run_task(i, V.KernelDescriptor("nas-cg")) for i in ins] if len(classes) == 1 else None
+    if outs is None:
+        inst = "cgm%d" % len(classes)
+        V.unlink_os_instance(inst, len(classes))
+        cfg = V.GvmConfig(instance=inst, max_clients=len(classes), barrier_size=len(classes),
+                          per_client_shm_bytes=8 << 20, barrier_window=20000, clock=V.ClockMode.Real)
+        outs = [None] * len(classes)
+        with V.GvmDaemon.start_os(cfg):
+            def w(k):
+                h = V.req(inst)
+                outs[k] = h.run_task(ins[k], V.KernelDescriptor("nas-cg"))
+                h.rls(); h.close()
+            ts = [threading.Thread(target=w, args=(k,)) for k in range(len(classes))]
+            [t.start() for t in ts]; [t.join() for t in ts]
+    for c, i, o in zip(classes, ins, outs):
+        zeta = V.cg_result(o)[0]
+        ref = oracle.cg_run(i).zeta
+        want = V.cg_class(c).zeta_verify
+        print(c, abs(zeta - want) / want <= 1e-10 and abs(zeta - ref) / ref <= 1e-12)
+'''
+    env = dict(os.environ, VGPU_CG_MODE=mode)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l.split() for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 3 and all(l[-1] == "True" for l in lines), out.stdout
