@@ -118,7 +118,6 @@ __device__ __forceinline__ void cg_cluster_sum(double (&v)[W], CgReduce& red, un
 // per SM, not by bandwidth). Row bounds come from shared memory (rs: this
 // CTA's rowstr slice). The sum order is fixed by (seg, lane), so results
 // are deterministic. f(row, sum) runs on the segment's first lane.
-constexpr unsigned kCgChains = 4;
 
 struct CgMatrix {  // the hot fields of a job, in registers
     const std::uint32_t* __restrict__ colidx;
@@ -126,7 +125,7 @@ struct CgMatrix {  // the hot fields of a job, in registers
     std::uint32_t nm1;  // n - 1: column clamp
 };
 
-template <unsigned seg, typename Gather, typename F>
+template <unsigned seg, unsigned kCgChains, typename Gather, typename F>
 __device__ __forceinline__ void cg_spmv(const CgMatrix& m, const std::uint32_t* rs, std::uint32_t r0,
                                         std::uint32_t r1, Gather gather, F f) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,7 +156,12 @@ __device__ __forceinline__ void cg_spmv(const CgMatrix& m, const std::uint32_t* 
                 for (unsigned c = 0; c < kCgChains; ++c) acc[c] = fma(av[c], gather(col[c]), acc[c]);
             }
         }
-        double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        // fixed pairwise order over the chains
+#pragma unroll
+        for (unsigned w = kCgChains / 2; w > 0; w /= 2)
+#pragma unroll
+            for (unsigned c = 0; c < w; ++c) acc[c] += acc[c + w];
+        double s = acc[0];
 #pragma unroll
         for (unsigned o = seg / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, seg);
         if (sl == 0 && row < r1) f(row, s);
@@ -200,6 +204,9 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     const CgMatrix mat{job.colidx, job.a, n - 1};
     constexpr bool kStage = kMode != kCgGlobal;
     constexpr bool kRes = kMode == kCgResident;
+    // load chains per lane (measured on B200: 4 beats 8 at every class,
+    // even where 8 fit the 64-register budget without spilling)
+    constexpr unsigned kChains = 4;
     const std::uint32_t own = kRes ? table.own_rows : 0;
     double* const own0 = ps + (kStage ? table.stage_n : 0);
     std::uint32_t* const srow = reinterpret_cast<std::uint32_t*>(own0 + 4ull * own);
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
         for (std::uint32_t cgit = 0; cgit < cgitmax; ++cgit) {
             // q = A p, d = p . q
             double d[1] = {0.0};
-            cg_spmv<kSeg>(mat, rs, r0, r1, gather_p, [&](std::uint32_t row, double s) {
+            cg_spmv<kSeg, kChains>(mat, rs, r0, r1, gather_p, [&](std::uint32_t row, double s) {
                 q[row] = s;
                 d[0] = fma(gather_p(row), s, d[0]);
             });
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
             cluster.sync();
         }
         double s3[3] = {0.0, 0.0, 0.0};
-        cg_spmv<kSeg>(mat, rs, r0, r1,
+        cg_spmv<kSeg, kChains>(mat, rs, r0, r1,
                       [&](std::uint32_t c) {
                           if constexpr (kRes) return ps[c];
                           else return __ldcg(job.z + c);
