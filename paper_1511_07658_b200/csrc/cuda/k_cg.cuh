@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     if (rs_smem)
         for (std::uint32_t i = threadIdx.x; i <= r1 - r0; i += kCgThreads) srow[i] = __ldg(job.rowstr + r0 + i);
     const std::uint32_t* const rs = rs_smem ? srow : job.rowstr + r0;
-    __syncthreads();
+    // every CTA of the cluster must be running before anyone writes into its
+    // shared memory (the first p push below); also orders the srow loads
+    cluster.sync();
     // vector element of global row i: own slices rebased to r0 when resident
     double* const x = kRes ? own0 - r0 : job.x;
     double* const z = kRes ? own0 + own - r0 : job.z;
