@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """bench.py — aggregate SPMD jobs/s through the B200 GVM (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vecadd|ep|bs|mm|mixed|cg|vmul]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vecadd|ep|bs|mm|mixed|cg|vmul|es]
                     [--procs P] [--impl ours|reference]
 
 One "step" = one SPMD round: each of the P processes sharing a GPU runs one
@@ -51,7 +51,7 @@ METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; ker
 L2_BYTES = 126 << 20
 # arithmetic type each workload's path computes in (EP: binary64 + integer LCG)
 DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f64", "cg": "f64",
-         "vmul": "f32"}
+         "vmul": "f32", "es": "f32"}
 
 
 def log(*a):
@@ -559,7 +559,8 @@ def model_summary(batches):
 
 # ---- rooflines ----------------------------------------------------------------------
 
-KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32", "cg": "hbm", "vmul": "hbm"}
+KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32", "cg": "hbm", "vmul": "hbm",
+              "es": "rsqrt"}
 
 
 def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
@@ -571,6 +572,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
       vmul       12 B per element
       cg         12 B per nonzero + 4 B per row per SpMV, 26 SpMVs per
                  outer iteration (the matrix streams once per SpMV)
+      es         atom-lattice-point interactions (one MUFU rsqrt each)
       mm         2 n^3 FLOP per task (FP32 SIMT, or 3xTF32 tcgen05 opt-in)
       ep         IEEE binary64 operations of the restated NPB algorithm:
                  7 per pair + 32 per accepted pair (W.ep_fp64_ops)
@@ -596,6 +598,16 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
             r["serial_us_per_launch"] = d["serial_kernel_ms_per_launch"] * 1e3
             r["serial_frac"] = (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"]
                                 * 1e-3) / 1e9 / hbm["hbm_gbs"])
+        return r
+    if bound == "rsqrt":
+        # electrostatics: one MUFU reciprocal square root per atom-point;
+        # peak = SMs x 16 MUFU lanes per clock x the SM clock under load
+        sms, mhz = peaks.get("sms") or 148, peaks.get("sm_mhz") or 1965.0
+        peak = sms * 16 * mhz * 1e6 / 1e12
+        achieved = d["algo_flops_per_launch"] / kernel_s / 1e12
+        r.update({"achieved": achieved, "peak": peak, "unit": "T rsqrt/s",
+                  "frac": achieved / peak, "algo_interactions_per_launch": d["algo_flops_per_launch"],
+                  "peak_source": "SMs x 16 MUFU.RSQ per clock x max SM clock (no probe)"})
         return r
     if bound == "fp32" and d.get("main_kernel_ms_per_launch"):
         # 3xTF32 on tcgen05: three TF32 MMAs per FP32 product, against the
@@ -711,7 +723,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     # default: BASELINE.json configs[1] (NAS EP class A, 8 processes per B200)
     ap.add_argument("--workload", default="ep",
-                    choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul"])
+                    choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul", "es"])
     ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-native", action="store_true")

@@ -22,6 +22,7 @@
 //   sgemm          A||B, n*n fp32 each      -> A*B, n*n fp32     (new)
 //   vector-mul     a||b, n fp32 each        -> a*b, n fp32       (new)
 //   nas-cg         CgHeader + CSR matrix    -> CgResult (32 B)   (new)
+//   electrostatics EsHeader + atoms (x,y,z,q) -> lattice potential fp32 (new)
 #ifndef VGPU_PAYLOAD_HPP
 #define VGPU_PAYLOAD_HPP
 

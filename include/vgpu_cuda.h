@@ -49,7 +49,8 @@ enum vgpu_cu_kernel {
     VGPU_CU_K_SGEMM = 5,     /* "sgemm"         A||B (n*n fp32) -> A*B         */
     VGPU_CU_K_VMUL = 6,      /* "vector-mul"    a||b fp32 -> a*b               */
     VGPU_CU_K_CG = 7,        /* "nas-cg"        vgpu_cg_header + CSR -> vgpu_cg_result */
-    VGPU_CU_K_COUNT = 8
+    VGPU_CU_K_ES = 8,        /* "electrostatics" vgpu_es_header + atoms -> lattice potential */
+    VGPU_CU_K_COUNT = 9
 };
 
 /* NAS EP job (input, 32 bytes little-endian). The job computes batches
@@ -103,6 +104,17 @@ static inline uint64_t vgpu_cg_input_bytes(uint32_t n, uint32_t nnz) {
     b = (b + 7u) & ~7ull;
     return b + 8ull * nnz;
 }
+
+/* Electrostatics job (VMD direct Coulomb summation, the paper's ES):
+ * input = vgpu_es_header | float atoms[natoms][4] (x, y, z, q); output =
+ * float V[nz][ny][nx], V(p) = sum_i q_i / |p - a_i| at p = (x, y, z) * spacing.
+ * Atoms must not sit on lattice points (r = 0). */
+typedef struct vgpu_es_header {
+    uint32_t natoms;
+    uint32_t nx, ny, nz;
+    float spacing;
+    uint32_t reserved[3]; /* must be 0 */
+} vgpu_es_header;
 
 /* Black-Scholes constants (CUDA SDK formulation). */
 #define VGPU_BS_RISKFREE 0.02f

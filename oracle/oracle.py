@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         L.vo_cg_makea.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_void_p,
                                   C.c_uint64]
         L.vo_cg_makea.restype = C.c_uint64
+        L.vo_es.argtypes = [C.c_char_p, C.c_uint64, f64p]
+        L.vo_es.restype = C.c_int
         L.vo_cg_run.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(CgResult)]
         L.vo_cg_run.restype = C.c_int
         _lib = L
@@ -174,6 +176,15 @@ def cg_run(inp: bytes) -> "CgResult":
 
 def cg_from_bytes(b: bytes) -> "CgResult":
     return CgResult.from_buffer_copy(bytes(b[:C.sizeof(CgResult)]))
+
+
+def es(inp: bytes) -> np.ndarray:
+    """binary64 lattice potential [nz, ny, nx] of an electrostatics input."""
+    natoms, nx, ny, nz = np.frombuffer(inp[:16], np.uint32)
+    out = np.empty(int(nx) * int(ny) * int(nz), np.float64)
+    if lib().vo_es(inp, len(inp), out):
+        raise ValueError("malformed electrostatics input")
+    return out.reshape(int(nz), int(ny), int(nx))
 
 
 def ref_tool(name: str) -> str:

@@ -98,6 +98,21 @@ vgpu::Bytes vmul_payload(vgpu::ByteView in) {
     return out;
 }
 
+vgpu::Bytes es_payload(vgpu::ByteView in) {
+    if (in.size() < sizeof(vgpu_es_header))
+        throw vgpu::PayloadError(vgpu::PayloadError::Kind::MalformedInput, "electrostatics input");
+    vgpu_es_header h;
+    std::memcpy(&h, in.data(), sizeof h);
+    const std::size_t pts = static_cast<std::size_t>(h.nx) * h.ny * h.nz;
+    std::vector<double> v(pts);
+    if (vo_es(in.data(), in.size(), v.data()) != 0)
+        throw vgpu::PayloadError(vgpu::PayloadError::Kind::MalformedInput, "electrostatics input");
+    vgpu::Bytes out(4 * pts);
+    float* o = reinterpret_cast<float*>(out.data());
+    for (std::size_t i = 0; i < pts; ++i) o[i] = static_cast<float>(v[i]);
+    return out;
+}
+
 // the CG program's makea: the oracle's NPB restatement
 vgpu::Bytes cg_makea(char cls) {
     static const struct { char c; std::uint32_t n, nonzer, niter; double shift; } kClasses[] = {
@@ -132,6 +147,7 @@ int main(int argc, char** argv) {
         else if (a == "--bs-n") sizes.bs_n = std::stoull(v);
         else if (a == "--mm-n") sizes.mm_n = std::stoul(v);
         else if (a == "--cg-class") sizes.cg_class = v[0];
+        else if (a == "--es-atoms") sizes.es_atoms = std::stoul(v);
     }
     const std::uint32_t total = warmup + rounds;
     // per-worker timestamps live in a shared anonymous mapping
@@ -192,6 +208,7 @@ int main(int argc, char** argv) {
     reg.register_payload("sgemm", mm_payload);
     reg.register_payload("nas-cg", cg_payload);
     reg.register_payload("vector-mul", vmul_payload);
+    reg.register_payload("electrostatics", es_payload);
     vgpu::GvmConfig g;
     g.instance = instance;
     g.max_clients = procs;

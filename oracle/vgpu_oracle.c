@@ -396,6 +396,34 @@ int vo_cg_run(const uint8_t* in, uint64_t in_bytes, vgpu_cg_result* res) {
     return 0;
 }
 
+/* ---- Electrostatics (direct Coulomb summation, binary64) ------------------ */
+/* No reference arithmetic (proj/src/bench/profiles.cpp:43 is a timing
+ * profile only): V(p) = sum_i q_i / |p - a_i| over the lattice
+ * p = (x, y, z) * spacing, summed in binary64 in atom order. UNPINNED by
+ * the reference; pinned to the closed form for a single charge and to
+ * superposition (tests/test_oracle.py). */
+int vo_es(const uint8_t* in, uint64_t in_bytes, double* out) {
+    vgpu_es_header h;
+    if (in_bytes < sizeof h) return 1;
+    memcpy(&h, in, sizeof h);
+    if (in_bytes != sizeof h + 16ull * h.natoms) return 1;
+    const float* at = (const float*)(in + sizeof h);
+    const int64_t pts = (int64_t)h.nx * h.ny * h.nz;
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < pts; ++p) {
+        const double px = (double)(p % h.nx) * h.spacing;
+        const double py = (double)((p / h.nx) % h.ny) * h.spacing;
+        const double pz = (double)(p / ((int64_t)h.nx * h.ny)) * h.spacing;
+        double v = 0.0;
+        for (uint32_t i = 0; i < h.natoms; ++i) {
+            const double dx = px - at[4 * i], dy = py - at[4 * i + 1], dz = pz - at[4 * i + 2];
+            v += at[4 * i + 3] / sqrt(dx * dx + dy * dy + dz * dz);
+        }
+        out[p] = v;
+    }
+    return 0;
+}
+
 /* ---- deterministic generator ---------------------------------------------- */
 
 uint64_t vo_rng_next(uint64_t* s) {

@@ -20,6 +20,9 @@
  *   NAS CG               no reference arithmetic (profiles.cpp:41); NPB 3.x cg.f
  *                        makea + conj_grad — PINNED against NPB's published
  *                        zeta (classes S, W, A; epsilon 1e-10).
+ *   Electrostatics       no reference arithmetic (profiles.cpp:43); binary64
+ *                        direct Coulomb sum — UNPINNED by the reference; pinned
+ *                        to the single-charge closed form and superposition.
  *   SGEMM                no reference arithmetic (profiles.cpp:35); binary64
  *                        accumulation — UNPINNED by the reference itself;
  *                        pinned to numpy float64 matmul and exact integer
@@ -65,6 +68,10 @@ void vo_sgemm(const float* A, const float* B, size_t n, double* C);
 uint64_t vo_cg_makea(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
                      uint64_t cap);
 int vo_cg_run(const uint8_t* in, uint64_t in_bytes, vgpu_cg_result* res);
+
+/* Electrostatics: binary64 lattice potential of an "electrostatics" input
+ * (out: nx*ny*nz doubles); nonzero on a malformed input. */
+int vo_es(const uint8_t* in, uint64_t in_bytes, double* out);
 
 /* deterministic generators shared by tests and bench (xorshift64*) */
 uint64_t vo_rng_next(uint64_t* state);

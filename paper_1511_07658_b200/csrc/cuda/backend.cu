@@ -42,6 +42,7 @@
 #include "k_bs.cuh"
 #include "k_cg.cuh"
 #include "k_ep.cuh"
+#include "k_es.cuh"
 #include "k_sgemm.cuh"
 #include "k_sgemm_tc.cuh"
 #include "k_stream.cuh"
@@ -120,6 +121,7 @@ struct DevJob {
     std::uint8_t* ws = nullptr;  // sgemm tensor-core workspace: 2 x in_bytes; nas-cg vectors
     vgpu_ep_params ep{};
     vgpu_cg_header cg{};
+    vgpu_es_header es{};
 };
 
 // Device workspace a job needs besides in/out/scratch (0: none).
@@ -583,6 +585,34 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             if (e != cudaSuccess) return e;
             return flush(gen, gen_tiles, false);
         }
+        case VGPU_CU_K_ES: {
+            for (std::uint32_t b = 0; b < n; b += kMaxEsJobs) {
+                EsTable t{};
+                std::uint32_t ctas = 0;
+                for (std::uint32_t i = b; i < std::min(n, b + kMaxEsJobs); ++i) {
+                    const vgpu_es_header& h = jobs[i].es;
+                    if (!h.nx || !h.ny || !h.nz) continue;
+                    EsJob& j = t.job[t.njobs++];
+                    j.atoms = reinterpret_cast<const float4*>(jobs[i].in + sizeof(vgpu_es_header));
+                    j.out = reinterpret_cast<float*>(jobs[i].out);
+                    j.natoms = h.natoms;
+                    j.nx = h.nx;
+                    j.ny = h.ny;
+                    j.nz = h.nz;
+                    j.h = h.spacing;
+                    j.bx = (h.nx + kEsTx * kEsPts - 1) / (kEsTx * kEsPts);
+                    j.by = (h.ny + kEsTy - 1) / kEsTy;
+                    j.cta_begin = ctas;
+                    ctas += j.bx * j.by * h.nz;
+                }
+                if (!ctas) continue;
+                es_table_kernel<<<ctas, kEsThreads, 0, s>>>(t);
+                ++*launches;
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
         case VGPU_CU_K_CG: {
             // group by (cluster size, vector placement, row segment); one
             // launch per group of up to kMaxCgJobs clusters
@@ -696,6 +726,13 @@ void job_work(const DevJob& j, std::uint64_t* bytes, double* flops) {
             break;
         }
         case VGPU_CU_K_VMUL: *bytes += j.in_bytes + j.in_bytes / 2; *flops += j.in_bytes / 8.0; break;
+        case VGPU_CU_K_ES: {
+            // flops field: atom-lattice-point interactions (one rsqrt each)
+            const double pts = static_cast<double>(j.es.nx) * j.es.ny * j.es.nz;
+            *bytes += j.in_bytes + static_cast<std::uint64_t>(4.0 * pts);
+            *flops += pts * j.es.natoms;
+            break;
+        }
         case VGPU_CU_K_CG: {
             // per SpMV the matrix streams once: a (8 B) + colidx (4 B) per
             // nonzero + rowstr (4 B per row); cgitmax + 1 SpMVs per outer
@@ -907,8 +944,9 @@ int vgpu_cu_device_count(int* n) {
 }
 
 int vgpu_cu_payload(const char* id, std::uint32_t* kernel) {
-    static const char* names[VGPU_CU_K_COUNT] = {"identity", "vector-add", "vector-scale", "nas-ep",
-                                                 "black-scholes", "sgemm", "vector-mul", "nas-cg"};
+    static const char* names[VGPU_CU_K_COUNT] = {"identity",      "vector-add", "vector-scale",
+                                                 "nas-ep",        "black-scholes", "sgemm",
+                                                 "vector-mul",    "nas-cg",     "electrostatics"};
     if (!id || !kernel) return VGPU_CU_EINVAL;
     for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT; ++k)
         if (std::strcmp(id, names[k]) == 0) {
@@ -962,6 +1000,24 @@ int vgpu_cu_output_size(std::uint32_t kernel, const void* in, std::uint64_t in_b
                 return VGPU_CU_EPAYLOAD;
             }
             *out_bytes = sizeof(vgpu_cg_result);
+            return VGPU_CU_OK;
+        }
+        case VGPU_CU_K_ES: {
+            if (in_bytes < sizeof(vgpu_es_header)) {
+                set_err("electrostatics: input shorter than its %zu-byte header", sizeof(vgpu_es_header));
+                return VGPU_CU_EPAYLOAD;
+            }
+            if (!in) return VGPU_CU_EINVAL;
+            vgpu_es_header h;
+            std::memcpy(&h, in, sizeof h);
+            const std::uint64_t pts = static_cast<std::uint64_t>(h.nx) * h.ny * h.nz;
+            if (in_bytes != sizeof h + 16ull * h.natoms || pts == 0 || pts > (1ull << 30) ||
+                h.nz > 65535 || !(h.spacing > 0.0f) || h.reserved[0] || h.reserved[1] || h.reserved[2]) {
+                set_err("electrostatics: %llu bytes do not match a header + %u atoms, or bad lattice",
+                        (unsigned long long)in_bytes, h.natoms);
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = 4 * pts;
             return VGPU_CU_OK;
         }
         case VGPU_CU_K_VSCALE:
@@ -1207,6 +1263,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         j.out_bytes = need;
         j.scratch = s.d_scratch;
         j.ws = s.d_ws;
+        if (t.kernel == VGPU_CU_K_ES) std::memcpy(&j.es, t.h_in, sizeof j.es);
         if (t.kernel == VGPU_CU_K_CG) {
             std::memcpy(&j.cg, t.h_in, sizeof j.cg);
             if (job_ws_bytes(t.kernel, t.h_in, t.in_bytes) > 2 * d->buf_bytes) {
@@ -1545,6 +1602,7 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     }
     if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, in, sizeof j.ep);
     if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, in, sizeof j.cg);
+    if (kernel == VGPU_CU_K_ES) std::memcpy(&j.es, in, sizeof j.es);
     // pageable copies, exactly what an unvirtualized CUDA program does
     if (in_bytes) CK(cudaMemcpyAsync(c.d_in, in, in_bytes, cudaMemcpyHostToDevice, c.stream));
     std::uint64_t l = 0;
@@ -1610,6 +1668,7 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
             }
             if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, h_inputs[i], sizeof j.ep);
             if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, h_inputs[i], sizeof j.cg);
+            if (kernel == VGPU_CU_K_ES) std::memcpy(&j.es, h_inputs[i], sizeof j.es);
             if (in_bytes[i])
                 CK(cudaMemcpy(const_cast<std::uint8_t*>(j.in), h_inputs[i], in_bytes[i],
                               cudaMemcpyHostToDevice));

@@ -20,7 +20,7 @@ int default_device() {
 }
 
 const char* kBuiltinIds[VGPU_CU_K_COUNT] = {
-    "identity", "vector-add", "vector-scale", "nas-ep", "black-scholes", "sgemm", "vector-mul", "nas-cg"};
+    "identity", "vector-add", "vector-scale", "nas-ep", "black-scholes", "sgemm", "vector-mul", "nas-cg", "electrostatics"};
 
 }  // namespace
 

@@ -91,6 +91,7 @@ int main(int argc, char** argv) {
             else if (a == "--bs-n") sizes.bs_n = std::stoull(val());
             else if (a == "--mm-n") sizes.mm_n = std::stoul(val());
             else if (a == "--cg-class") sizes.cg_class = val()[0];
+            else if (a == "--es-atoms") sizes.es_atoms = std::stoul(val());
             else throw std::invalid_argument("unknown argument " + a);
         } catch (const std::exception& e) {
             std::fprintf(stderr, "vgpu-spmd: %s\n", e.what());

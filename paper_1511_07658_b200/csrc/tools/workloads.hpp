@@ -18,7 +18,10 @@
 //           program builds its matrix with NPB's makea (untimed in NPB) —
 //           through cg_builder(), which the program sets (vgpu-spmd: the
 //           product's vgpu::npb::make_cg_input; ref-bench: the oracle's);
-//   vmul    VecMul, vecadd's shapes and values, payload vector-mul.
+//   vmul    VecMul, vecadd's shapes and values, payload vector-mul;
+//   es      Electrostatics (VMD direct Coulomb summation): 100K atoms,
+//           64 x 64 lattice x 25 slices (the paper's "100K atoms / 25
+//           iterations"), atoms ~ U(box), q ~ U[-1,1], seed 777+w.
 #pragma once
 
 #include <cmath>
@@ -34,7 +37,7 @@
 
 namespace vgpu::wl {
 
-enum class Kind { VecAdd, Ep, Bs, Mm, Cg, VecMul };
+enum class Kind { VecAdd, Ep, Bs, Mm, Cg, VecMul, Es };
 
 struct Sizes {
     std::uint64_t vecadd_n = 1ull << 20;
@@ -43,6 +46,9 @@ struct Sizes {
     std::uint64_t bs_n = 4ull << 20;
     std::uint32_t mm_n = 2048;
     char cg_class = 'A';
+    std::uint32_t es_atoms = 100000;
+    std::uint32_t es_nx = 64, es_ny = 64, es_nz = 25;
+    float es_h = 0.5f;
 };
 
 // NPB CG shapes (cg.f): rows, nonzeros per generated vector
@@ -82,6 +88,7 @@ inline Kind kind_of(const std::string& workload, std::uint32_t worker) {
     if (workload == "mm") return Kind::Mm;
     if (workload == "cg") return Kind::Cg;
     if (workload == "vmul") return Kind::VecMul;
+    if (workload == "es") return Kind::Es;
     if (workload == "mixed") return static_cast<Kind>(worker % 4);
     throw std::invalid_argument("unknown workload: " + workload);
 }
@@ -176,6 +183,33 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
             j.output_bytes = 8 * n;
             break;
         }
+        case Kind::Es: {
+            vgpu_es_header h{};
+            h.natoms = sz.es_atoms;
+            h.nx = sz.es_nx;
+            h.ny = sz.es_ny;
+            h.nz = sz.es_nz;
+            h.spacing = sz.es_h;
+            std::vector<float> at(4ull * h.natoms);
+            std::uint64_t s = 777 + worker;
+            for (std::uint32_t i = 0; i < h.natoms; ++i) {
+                at[4 * i] = uniform(s, 0.0f, h.nx * h.spacing);
+                at[4 * i + 1] = uniform(s, 0.0f, h.ny * h.spacing);
+                at[4 * i + 2] = uniform(s, 0.0f, h.nz * h.spacing);
+                at[4 * i + 3] = uniform(s, -1.0f, 1.0f);
+            }
+            j.input.resize(sizeof h + 16ull * h.natoms);
+            std::memcpy(j.input.data(), &h, sizeof h);
+            std::memcpy(j.input.data() + sizeof h, at.data(), 16ull * h.natoms);
+            const std::uint64_t pts = static_cast<std::uint64_t>(h.nx) * h.ny * h.nz;
+            j.desc.payload_id = "electrostatics";
+            j.desc.t_data_in = pcie_us(j.input.size());
+            j.desc.t_comp = static_cast<Micros>(pts * h.natoms / 4.6e6) + 1;  // ~4.6e12 rsqrt/s
+            j.desc.t_data_out = pcie_us(4 * pts);
+            j.desc.grid_size = static_cast<std::uint32_t>((h.nx + 63) / 64 * ((h.ny + 7) / 8) * h.nz);
+            j.output_bytes = 4 * pts;
+            break;
+        }
         case Kind::Cg: {
             if (!cg_builder()) throw std::logic_error("cg workload: no NPB makea set (cg_builder)");
             j.input = cg_builder()(sz.cg_class);
@@ -218,6 +252,9 @@ inline std::uint64_t region_bytes(const std::string& workload, const Sizes& sz =
     if (workload == "bs") return bs;
     if (workload == "mm") return mm;
     if (workload == "vmul") return va;
+    if (workload == "es")
+        return std::max<std::uint64_t>(sizeof(vgpu_es_header) + 16ull * sz.es_atoms,
+                                       4ull * sz.es_nx * sz.es_ny * sz.es_nz);
     if (workload == "cg") {  // upper bound: nnz <= n (nonzer + 1)^2
         const CgShape c = cg_shape(sz.cg_class);
         return vgpu_cg_input_bytes(c.n, c.n * (c.nonzer + 1) * (c.nonzer + 1));

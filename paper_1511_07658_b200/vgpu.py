@@ -286,7 +286,8 @@ def native_run_task(data, task: KernelDescriptor, cuda_device: int = 0,
 # ---- device-level helpers (vgpu_cuda.h) ----------------------------------------
 
 KERNELS = {"identity": 0, "vector-add": 1, "vector-scale": 2, "nas-ep": 3,
-           "black-scholes": 4, "sgemm": 5, "vector-mul": 6, "nas-cg": 7}
+           "black-scholes": 4, "sgemm": 5, "vector-mul": 6, "nas-cg": 7,
+           "electrostatics": 8}
 
 
 def _cu_check(rc: int) -> None:
@@ -385,3 +386,15 @@ def cg_input_for_class(cls: str, niter: Optional[int] = None) -> bytes:
 def cg_result(out: bytes) -> tuple:
     """(zeta, rnorm, niter, n, nnz) from a nas-cg result."""
     return CG_RESULT.unpack(bytes(out[:CG_RESULT.size]))
+
+
+# ---- electrostatics inputs ------------------------------------------------------
+
+ES_HEADER = struct.Struct("<IIIIfIII")  # vgpu_es_header
+
+
+def es_input(atoms, nx: int, ny: int, nz: int, spacing: float) -> bytes:
+    """electrostatics input: header + float32 atoms [natoms, 4] (x, y, z, q)."""
+    import numpy as np
+    a = np.ascontiguousarray(atoms, np.float32).reshape(-1, 4)
+    return ES_HEADER.pack(a.shape[0], nx, ny, nz, spacing, 0, 0, 0) + a.tobytes()

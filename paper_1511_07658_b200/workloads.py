@@ -14,9 +14,10 @@ import numpy as np
 from ._native import EpParams
 
 PAYLOAD = {"vecadd": "vector-add", "ep": "nas-ep", "bs": "black-scholes", "mm": "sgemm",
-           "cg": "nas-cg", "vmul": "vector-mul"}
+           "cg": "nas-cg", "vmul": "vector-mul", "es": "electrostatics"}
 KINDS = ("vecadd", "ep", "bs", "mm")  # the kinds `mixed` cycles through (C5)
-DEFAULT_PROCS = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "mixed": 16, "cg": 8, "vmul": 4}
+DEFAULT_PROCS = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "mixed": 16, "cg": 8, "vmul": 4,
+                 "es": 8}
 CONFIG_NAME = {
     "vecadd": "C1 vector addition, 1M floats per process",
     "ep": "C2 NAS EP class A split over the processes",
@@ -25,6 +26,7 @@ CONFIG_NAME = {
     "mixed": "C5 mixed: workers cycle vecadd/ep/bs/mm",
     "cg": "NAS CG class A per process (paper workload, not a BASELINE config)",
     "vmul": "VecMul 1M floats per process (paper workload, not a BASELINE config)",
+    "es": "Electrostatics 100K atoms x 64x64x25 lattice per process (paper workload, not a BASELINE config)",
 }
 
 # NPB CG shapes (n, nonzer) for the region bound (mirror of workloads.hpp)
@@ -53,10 +55,14 @@ class Sizes:
     def size_args(self) -> list:
         return ["--vecadd-n", str(self.vecadd_n), "--ep-m", str(self.ep_m),
                 "--ep-batches", str(self.ep_batches), "--bs-n", str(self.bs_n),
-                "--mm-n", str(self.mm_n), "--cg-class", self.cg_class]
+                "--mm-n", str(self.mm_n), "--cg-class", self.cg_class,
+                "--es-atoms", str(self.es_atoms)]
     bs_n: int = 4 << 20
     mm_n: int = 2048
     cg_class: str = "A"
+    es_atoms: int = 100000
+    es_lattice: tuple = (64, 64, 25)
+    es_h: float = 0.5
 
 
 # NAS EP class A (m = 28): accepted Gaussian pairs (NPB ep.f; pinned by
@@ -101,6 +107,8 @@ def job_input(workload: str, worker: int, workers: int, sz: Sizes = Sizes()) -> 
     k = kind_of(workload, worker)
     if k == "cg":
         return cg_input(sz.cg_class)
+    if k == "es":
+        return es_input_native(worker, sz)
     if k in ("vecadd", "vmul"):
         j = np.arange(sz.vecadd_n)
         a = ((worker + 1) * 1000.0 + (j % 512)).astype(np.float32)
@@ -119,9 +127,23 @@ def job_input(workload: str, worker: int, workers: int, sz: Sizes = Sizes()) -> 
     return rng.uniform(-1, 1, 2 * n * n).astype(np.float32).tobytes()
 
 
+def es_input_native(worker: int, sz: Sizes) -> bytes:
+    """An ES job of the configured size (numpy values: like BS/MM, the
+    kernel's cost does not depend on them)."""
+    from .vgpu import es_input
+    nx, ny, nz = sz.es_lattice
+    h = sz.es_h
+    rng = np.random.default_rng(777 + worker)
+    n = sz.es_atoms
+    at = np.stack([rng.uniform(0, nx * h, n), rng.uniform(0, ny * h, n),
+                   rng.uniform(0, nz * h, n), rng.uniform(-1, 1, n)], axis=1).astype(np.float32)
+    return es_input(at, nx, ny, nz, h)
+
+
 def output_bytes(kind: str, sz: Sizes = Sizes()) -> int:
     return {"vecadd": 4 * sz.vecadd_n, "ep": 112, "bs": 8 * sz.bs_n,
-            "mm": 4 * sz.mm_n * sz.mm_n, "cg": 32, "vmul": 4 * sz.vecadd_n}[kind]
+            "mm": 4 * sz.mm_n * sz.mm_n, "cg": 32, "vmul": 4 * sz.vecadd_n,
+            "es": 4 * sz.es_lattice[0] * sz.es_lattice[1] * sz.es_lattice[2]}[kind]
 
 
 def cg_input_bound(cls: str) -> int:
@@ -136,7 +158,8 @@ def input_bytes(kind: str, sz: Sizes = Sizes()) -> int:
     if kind == "cg":
         return cg_input_bound(sz.cg_class)
     return {"vecadd": 8 * sz.vecadd_n, "ep": 32, "bs": 12 * sz.bs_n,
-            "mm": 8 * sz.mm_n * sz.mm_n, "vmul": 8 * sz.vecadd_n}[kind]
+            "mm": 8 * sz.mm_n * sz.mm_n, "vmul": 8 * sz.vecadd_n,
+            "es": 32 + 16 * sz.es_atoms}[kind]
 
 
 def region_bytes(workload: str, sz: Sizes = Sizes()) -> int:

@@ -174,3 +174,42 @@ for classes in (["S", "W"], ["S"]):
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l.split() for l in out.stdout.splitlines() if l.strip()]
     assert len(lines) == 3 and all(l[-1] == "True" for l in lines), out.stdout
+
+
+def _es_atoms(seed, natoms, nx, ny, nz, h):
+    rng = np.random.default_rng(seed)
+    at = np.empty((natoms, 4), np.float32)
+    at[:, 0] = rng.uniform(0, nx * h, natoms)
+    at[:, 1] = rng.uniform(0, ny * h, natoms)
+    at[:, 2] = rng.uniform(0, nz * h, natoms)
+    at[:, 3] = rng.uniform(-1, 1, natoms)
+    return at
+
+
+def test_electrostatics_ragged_lattices_vs_binary64_oracle():
+    """Direct Coulomb summation (the paper's ES) on lattices that do not
+    divide the CTA tile (x: 64 points, y: 8 rows), three clients in one batch:
+    L1-relative <= 1e-6 against the binary64 oracle."""
+    shapes = [(2000, 70, 33, 5, 0.5), (513, 1, 1, 1, 0.25), (4096, 64, 64, 3, 0.3)]
+    ins = [V.es_input(_es_atoms(i, *s), *s[1:]) for i, s in enumerate(shapes)]
+    d, inst = _gvm(3, max(len(b) for b in ins) + (1 << 16))
+    with d:
+        outs = _spmd(inst, ins, V.KernelDescriptor("electrostatics", 20, 30000, 20, 288))
+    for s, inp, out in zip(shapes, ins, outs):
+        got = np.frombuffer(out, np.float32).reshape(s[3], s[2], s[1]).astype(np.float64)
+        ref = oracle.es(inp)
+        err = np.abs(got - ref).sum() / np.abs(ref).sum()
+        assert err <= 1e-6, (s, err)
+
+
+def test_electrostatics_paper_size_100k_atoms():
+    """The paper's ES size: 100K atoms, 25 lattice slices (64 x 64 each)."""
+    at = _es_atoms(11, 100000, 64, 64, 25, 0.5)
+    inp = V.es_input(at, 64, 64, 25, 0.5)
+    out = V.native_run_task(inp, V.KernelDescriptor("electrostatics"))
+    got = np.frombuffer(out, np.float32).reshape(25, 64, 64).astype(np.float64)
+    ref = oracle.es(inp)
+    err = np.abs(got - ref).sum() / np.abs(ref).sum()
+    assert err <= 1e-6, err
+    with pytest.raises(Exception):
+        V.native_run_task(inp[:-4], V.KernelDescriptor("electrostatics"))

@@ -213,3 +213,22 @@ def test_vector_mul_oracle_is_ieee_float32():
     a = rng.uniform(-1e3, 1e3, 4097).astype(np.float32)
     b = rng.uniform(-1e3, 1e3, 4097).astype(np.float32)
     assert oracle.vector_mul(a, b).tobytes() == (a * b).tobytes()
+
+
+def test_es_oracle_single_charge_closed_form_and_superposition():
+    from paper_1511_07658_b200 import vgpu as V
+    inp = V.es_input([[0.25, 0.5, 0.75, 2.0]], 4, 3, 2, 0.5)
+    z, y, x = np.meshgrid(np.arange(2) * 0.5, np.arange(3) * 0.5, np.arange(4) * 0.5, indexing="ij")
+    want = 2.0 / np.sqrt((x - 0.25) ** 2 + (y - 0.5) ** 2 + (z - 0.75) ** 2)
+    assert np.abs(oracle.es(inp) - want).max() <= 1e-15 * np.abs(want).max()
+    rng = np.random.default_rng(5)
+    a = rng.uniform(0.1, 3.9, (50, 4)).astype(np.float32)
+    b = rng.uniform(0.1, 3.9, (70, 4)).astype(np.float32)
+    a[:, 3] -= 2.0
+    b[:, 3] -= 2.0
+    va = oracle.es(V.es_input(a, 9, 7, 3, 0.45))
+    vb = oracle.es(V.es_input(b, 9, 7, 3, 0.45))
+    vab = oracle.es(V.es_input(np.concatenate([a, b]), 9, 7, 3, 0.45))
+    assert np.allclose(vab, va + vb, rtol=1e-12, atol=1e-12)
+    with pytest.raises(ValueError):
+        oracle.es(V.es_input(a, 9, 7, 3, 0.45)[:-4])
