@@ -6,18 +6,19 @@
 // oracle/vgpu_oracle.c (vo_cg_run) and pinned there to NPB's published zeta
 // values for classes S, W and A.
 //
-// B200 design: one thread-block CLUSTER per job (1..16 CTAs by matrix size,
-// one CTA per SM: class S takes 1, W 4, A 16). Each CTA owns a contiguous
-// slice of rows; its vector slices (x, z, r, q, p) live in the job's HBM
-// workspace, the whole direction vector p is
-// re-staged into shared memory after every update when it fits (n <= 24K,
-// classes S..A), so the SpMV gathers p from shared memory and only the
-// matrix streams from L2/HBM (12 B per nonzero: a f64 + colidx u32).
-// Dot products reduce warp -> CTA (fixed order) -> cluster: every CTA reads
-// the cluster's partials over DSMEM in rank order, so all CTAs hold the same
-// bits and the result is deterministic run to run. Three cluster barriers
-// per CG step (p . q, r . r, the p update), as NPB's data dependences need.
-// SpMV: one warp per row, lanes stride the row, shuffle-tree sum.
+// B200 design: one thread-block CLUSTER per job, one 1024-thread CTA per SM;
+// the host picks the widest cluster (up to 16) at which the whole batch is
+// co-resident (backend.cu cg_cluster_for). Each CTA owns a contiguous slice
+// of rows. Vectors live in shared memory when they fit (classes S..A: the
+// CTA's x, z, r, q slices and the whole p, new p slices PUSHED into every
+// peer's copy over DSMEM), else p alone is staged there, else all stay in
+// the job's HBM workspace (CgMode below); only the matrix streams from
+// L2/HBM (12 B per nonzero: a f64 + colidx u32). Dot products reduce warp
+// -> CTA -> cluster by one fixed shuffle tree over DSMEM partials in rank
+// order, so all CTAs hold the same bits and the result repeats run to run.
+// Three cluster barriers per CG step (p . q, r . r, the p update), as NPB's
+// data dependences need. SpMV: row segments of 8/16/32 lanes, predicated
+// load chains per lane, shuffle-tree sum (cg_spmv).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -112,10 +113,9 @@ __device__ __forceinline__ void cg_cluster_sum(double (&v)[W], CgReduce& red, un
 
 // y[row] = sum_k a[k] * v[colidx[k]] for this CTA's rows. A row belongs to
 // a segment of `seg` lanes (8, 16 or 32 by the job's nonzeros per row), so a
-// warp works on 32 / seg rows at once; each lane issues up to kCgChains
-// predicated loads of (colidx, a) at once, which covers a whole NPB row in
-// one memory round trip (the SpMV is bound by memory latency x parallelism
-// per SM, not by bandwidth). Row bounds come from shared memory (rs: this
+// warp works on 32 / seg rows at once; each lane issues kCgChains predicated
+// loads of (colidx, a) at once (the SpMV is bound by memory latency x
+// parallelism per SM, not by bandwidth). Row bounds come from shared memory (rs: this
 // CTA's rowstr slice). The sum order is fixed by (seg, lane), so results
 // are deterministic. f(row, sum) runs on the segment's first lane.
 
