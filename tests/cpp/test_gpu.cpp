@@ -14,6 +14,7 @@
 
 #include "minitest.hpp"
 #include "vgpu/client.hpp"
+#include "vgpu/npb_cg.hpp"
 #include "vgpu_cuda.h"
 #include "vgpu_oracle.h"
 
@@ -290,6 +291,50 @@ TEST_CASE("[gpu] NAS EP class S on the GPU equals NPB's verification sums") {
     CHECK(std::fabs((r.sy - -6.958407078382297e3) / 6.958407078382297e3) < 1e-8);
 }
 
+TEST_CASE("[gpu] NAS CG class S through the C++ API meets NPB's verification") {
+    const npb::CgClass c = npb::cg_class('S');
+    const Bytes in = npb::make_cg_input(c.n, c.nonzer, c.niter, c.shift);
+    const Bytes out = PayloadRegistry::builtins().execute("nas-cg", in);
+    REQUIRE(out.size() == sizeof(vgpu_cg_result));
+    vgpu_cg_result r;
+    std::memcpy(&r, out.data(), sizeof r);
+    CHECK(std::fabs(r.zeta - c.zeta_verify) / c.zeta_verify <= 1e-10);
+    vgpu_cg_result o;
+    REQUIRE(vo_cg_run(in.data(), in.size(), &o) == 0);
+    CHECK(std::fabs(r.zeta - o.zeta) / o.zeta <= 1e-12);
+    CHECK(r.nnz == o.nnz);
+    // the oracle's NPB makea builds the same bytes
+    Bytes ref(vo_cg_makea(c.n, c.nonzer, c.niter, c.shift, nullptr, 0));
+    vo_cg_makea(c.n, c.nonzer, c.niter, c.shift, ref.data(), ref.size());
+    CHECK(ref == in);
+}
+
+TEST_CASE("[gpu] vector-mul and electrostatics through the C++ API") {
+    std::vector<float> v(2 * 1001);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = 0.25f * static_cast<float>(i % 97) - 7.0f;
+    Bytes out = PayloadRegistry::builtins().execute("vector-mul", pack<float>(v));
+    std::vector<float> want(1001);
+    vo_vector_mul(want.data(), v.data(), v.data() + 1001, 1001);
+    CHECK(out == pack<float>(want));
+    // one charge: V = q / r exactly up to rsqrt.approx
+    vgpu_es_header h{};
+    h.natoms = 1;
+    h.nx = 5;
+    h.ny = 3;
+    h.nz = 2;
+    h.spacing = 0.5f;
+    Bytes in(sizeof h + 16);
+    const float atom[4] = {0.3f, 0.4f, 0.1f, -2.0f};
+    std::memcpy(in.data(), &h, sizeof h);
+    std::memcpy(in.data() + sizeof h, atom, 16);
+    out = PayloadRegistry::builtins().execute("electrostatics", in);
+    REQUIRE(out.size() == 4u * 30u);
+    std::vector<double> ref(30);
+    REQUIRE(vo_es(in.data(), in.size(), ref.data()) == 0);
+    const float* got = reinterpret_cast<const float*>(out.data());
+    for (int i = 0; i < 30; ++i) CHECK(std::fabs(got[i] - ref[i]) <= 1e-6 * std::fabs(ref[i]));
+}
+
 TEST_CASE("[gpu] malformed inputs fail through STP with Payload, slot stays usable after RLS") {
     LoopbackHub hub;
     auto d = GvmDaemon::start_loopback(gcfg(1, 1 << 16), hub);
@@ -303,6 +348,8 @@ TEST_CASE("[gpu] malformed inputs fail through STP with Payload, slot stays usab
         {"vector-mul", Bytes{1, 2, 3}},
         {"nas-cg", Bytes(23)},
         {"nas-cg", Bytes(64)},  // header says n = 0
+        {"electrostatics", Bytes(31)},
+        {"electrostatics", Bytes(48)},  // header says 0 x 0 x 0, spacing 0
     };
     for (const auto& [id, in] : bad) {
         VgpuHandle h = req(hub);
