@@ -511,6 +511,30 @@ def sweep(V, N, W, workload, device, sizes, dist) -> dict:
     return {"report": "sweep", "workload": W.CONFIG_NAME[workload], "rows": rows, "csv": csv}
 
 
+def speedup(V, N, W, device, dist, procs=8) -> dict:
+    """The paper's speedup summary (Fig. "sp": seven
+    benchmarks at 8 SPMD processes, 1.4x-7.4x on its 2015 GPU) on B200:
+    per workload, 8 processes started together, each running one job;
+    speedup = native turnaround (each process creates its own CUDA context,
+    pageable copies) / virtualized turnaround (REQ on the open GVM). Same
+    definitions as --sweep, at N = 8 only, over every workload built."""
+    rows = []
+    for wl in ("ep", "vecadd", "mm", "bs", "cg", "es", "vmul"):
+        sz = W.Sizes()
+        try:
+            tv = leg_workers(V, N, W, wl, procs, 0, procs, 1, 0, device, False, sz, dist,
+                             cold=True, barrier=procs)
+            tn = leg_workers(V, N, W, wl, procs, 0, procs, 1, 0, device, True, sz, dist, cold=True)
+            v_ms, n_ms = tv["turnaround_ms"], tn["turnaround_ms"]
+            rows.append({"benchmark": wl, "workload": W.CONFIG_NAME[wl], "n": procs,
+                         "virtualized_ms": v_ms, "native_ms": n_ms, "speedup": n_ms / v_ms})
+        except Exception as e:  # noqa: BLE001 - reported in the row
+            rows.append({"benchmark": wl, "error": str(e)[:200]})
+    return {"report": "speedup", "procs": procs, "rows": rows,
+            "paper": "8 processes, 7 benchmarks (EP M30, VecAdd, MM, MG, BS, CG, ES): 1.4x-7.4x "
+                     "(PAPER.md:513); here MG is not built and VecMul is added"}
+
+
 def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
     """Virtualization overhead across payload sizes (proj/src/bench/
     bench.cpp:389-423 measure_overhead): one process, vector add of
@@ -737,6 +761,9 @@ def main():
                          "prints that report instead of the bench line")
     ap.add_argument("--sweep", action="store_true",
                     help="paper turnaround curves, N = 1..P, virtualized vs native (report)")
+    ap.add_argument("--speedup", action="store_true",
+                    help="paper speedup summary: every workload at 8 processes, turnaround "
+                         "native / virtualized (report)")
     ap.add_argument("--overhead-curve", action="store_true",
                     help="virtualization overhead across payload sizes, 1 process (report)")
     ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
@@ -792,8 +819,10 @@ def main():
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
     device = dist.device
-    if args.validate_model or args.sweep or args.overhead_curve:
+    if args.validate_model or args.sweep or args.overhead_curve or args.speedup:
         if dist.rank == 0:
+            if args.speedup:
+                emit(speedup(V, N, W, device, dist))
             if args.validate_model:
                 emit(validate_model(V, N, W, args.workload, device, sizes, dist))
             if args.sweep:
