@@ -84,3 +84,45 @@ def test_ep_op_count_and_sizes(W):
     s = W.Sizes.for_world(8)
     assert s.ep_m == 31 and s.ep_batches == 8 * 4096
     assert "--ep-batches" in s.size_args()
+
+
+def test_paper_workload_shapes(W):
+    """cg / es / vmul jobs: sizes agree with the C-ABI validation and the
+    region bound covers the real input."""
+    from paper_1511_07658_b200 import vgpu as V
+    sz = W.Sizes()
+    sz.cg_class = "S"
+    cg = W.job_input("cg", 0, 8, sz)
+    assert len(cg) <= W.input_bytes("cg", sz) <= W.region_bytes("cg", sz)
+    assert V.output_size("nas-cg", cg) == W.output_bytes("cg", sz) == 32
+    es = W.job_input("es", 3, 8, sz)
+    assert len(es) == W.input_bytes("es", sz) == 32 + 16 * sz.es_atoms
+    assert V.output_size("electrostatics", es) == W.output_bytes("es", sz) == 4 * 64 * 64 * 25
+    vm = W.job_input("vmul", 1, 4, sz)
+    assert V.output_size("vector-mul", vm) == W.output_bytes("vmul", sz) == len(vm) // 2
+    assert "--cg-class" in sz.size_args() and "--es-atoms" in sz.size_args()
+
+
+def test_rsqrt_and_cg_rooflines(bench, W):
+    r = bench.roofline(W, "es", _leg(10.0, flops=4.0e10), {})
+    assert r["bound"] == "rsqrt" and r["unit"] == "T rsqrt/s"
+    assert r["achieved"] == pytest.approx(4.0, rel=1e-9)
+    assert r["peak"] == pytest.approx(148 * 16 * 1965e6 / 1e12)
+    r = bench.roofline(W, "cg", _leg(2.0, bytes_=10 ** 10), {})
+    assert r["bound"] == "hbm" and r["achieved"] == pytest.approx(5000.0)
+
+
+@pytest.mark.parametrize("workload,extra", [("cg", ["--cg-class", "S"]), ("es", ["--es-atoms", "300"]),
+                                            ("vmul", ["--vecadd-n", "4096"])])
+def test_reference_arm_runs_the_paper_workloads(workload, extra):
+    """The unmodified reference GVM (oracle/_ref/ref-bench) runs the new
+    payloads through its own register_payload path on host cores."""
+    import json
+    import subprocess
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref-bench")
+    if not os.path.exists(ref):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    out = subprocess.run([ref, "--workload", workload, "--procs", "2", "--rounds", "1",
+                          "--warmup", "0"] + extra, capture_output=True, text=True, timeout=300)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["ok"] and d["jobs_per_s"] > 0
