@@ -680,6 +680,23 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
               "peak_source": "measured now: DFMA-chain probe (vgpu_cu_peak_probe), 2 FLOP/DFMA",
               "op_count": "IEEE binary64 ops of the restated NPB EP step (each +,-,*,/,sqrt = 1): "
                           "7 per pair + 19 per accepted pair (table-driven log = 12)"})
+    # the pipe view of the same kernel from its committed ncu capture: the
+    # op count above is algorithmic; the hardware also runs the log's
+    # reduction, the Newton steps of div/sqrt and the compaction
+    summ = os.path.join(REPO, "profiles", "r1_ncu_ep_summary_v6.txt")
+    if os.path.exists(summ):
+        vals = {}
+        for line in open(summ):
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                                                "smsp__issue_active.avg.pct_of_peak_sustained_active"):
+                vals[parts[0]] = float(parts[-1])
+        if vals:
+            r["ncu_pipes"] = {"fp64_pipe_active_pct": vals.get("sm__pipe_fp64_cycles_active.avg."
+                                                               "pct_of_peak_sustained_active"),
+                              "issue_active_pct": vals.get("smsp__issue_active.avg."
+                                                           "pct_of_peak_sustained_active"),
+                              "source": "profiles/r1_ncu_ep_summary_v6.txt (ncu --set full)"}
     return r
 
 
