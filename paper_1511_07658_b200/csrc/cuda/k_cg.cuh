@@ -123,6 +123,7 @@ struct CgMatrix {  // the hot fields of a job, in registers
     const std::uint32_t* __restrict__ colidx;
     const double* __restrict__ a;
     std::uint32_t nm1;  // n - 1: column clamp
+    std::uint32_t nnz;  // row-bound clamp
 };
 
 template <unsigned seg, unsigned kCgChains, typename Gather, typename F>
@@ -140,7 +141,9 @@ __device__ __forceinline__ void cg_spmv(const CgMatrix& m, const std::uint32_t* 
 #pragma unroll
         for (unsigned c = 0; c < kCgChains; ++c) acc[c] = 0.0;
         if (row < r1) {
-            const std::uint32_t k1 = rs[row - r0 + 1];
+            // a malformed rowstr (only its ends are checked on the host)
+            // cannot send the loads outside the matrix
+            const std::uint32_t k1 = min(rs[row - r0 + 1], m.nnz);
             for (std::uint32_t k = rs[row - r0] + sl; k < k1; k += kCgChains * seg) {
                 std::uint32_t col[kCgChains];
                 double av[kCgChains];
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     const std::uint32_t r0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * rank) / csize);
     const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (rank + 1)) / csize);
     unsigned parity = 0;
-    const CgMatrix mat{job.colidx, job.a, n - 1};
+    const CgMatrix mat{job.colidx, job.a, n - 1, job.nnz};
     constexpr bool kStage = kMode != kCgGlobal;
     constexpr bool kRes = kMode == kCgResident;
     // load chains per lane (measured on B200: 4 beats 8 at every class,

@@ -215,3 +215,21 @@ def test_electrostatics_paper_size_100k_atoms():
     assert err <= 1e-5, err
     with pytest.raises(Exception):
         V.native_run_task(inp[:-4], V.KernelDescriptor("electrostatics"))
+
+
+def test_nas_cg_malformed_interior_rowstr_stays_in_bounds():
+    """Only rowstr's ends are validated on the host; interior entries beyond
+    nnz and column indices beyond n are clamped in the kernel, so a bad
+    client gets a (meaningless) result instead of a device fault that would
+    take the shared GVM context down. The next job still verifies."""
+    good = V.cg_input_for_class("S", niter=1)
+    n, nnz = V.CG_HEADER.unpack(good[:24])[:2]
+    bad = bytearray(good)
+    rs = np.frombuffer(bad, np.uint32, n + 1, 24)
+    rs[n // 2] = 0xFFFFFFF0
+    col = np.frombuffer(bad, np.uint32, nnz, 24 + 4 * (n + 1))
+    col[:100] = 0xFFFFFFFF
+    V.native_run_task(bytes(bad), V.KernelDescriptor("nas-cg"))
+    out = V.native_run_task(V.cg_input_for_class("S"), V.KernelDescriptor("nas-cg"))
+    zeta = V.cg_result(out)[0]
+    assert abs(zeta - V.cg_class("S").zeta_verify) / V.cg_class("S").zeta_verify <= 1e-10
