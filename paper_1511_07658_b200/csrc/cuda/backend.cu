@@ -130,7 +130,8 @@ std::uint64_t job_ws_bytes(std::uint32_t kernel, const void* h_in, std::uint64_t
     if (kernel == VGPU_CU_K_CG && h_in && in_bytes >= sizeof(vgpu_cg_header)) {
         vgpu_cg_header h;
         std::memcpy(&h, h_in, sizeof h);
-        return 5ull * 8ull * h.n;  // x, z, p, q, r
+        // x, z, p, q, r, then the grid variant's barrier and partials
+        return ((5ull * 8ull * h.n + 255) & ~255ull) + sizeof(vgk::CgGridSync);
     }
     return 0;
 }
@@ -320,6 +321,12 @@ const CgOccupancy& cg_occupancy() {
 // step), at most one CTA per 64 rows. 0: cannot launch.
 unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned jobs) {
     const CgOccupancy& o = cg_occupancy();
+    static const unsigned force = [] {  // VGPU_CG_CLUSTER=k: measurement only
+        const char* e = std::getenv("VGPU_CG_CLUSTER");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 1 && v <= vgk::kCgMaxCluster ? static_cast<unsigned>(v) : 0u;
+    }();
+    if (force && o.active[force] > 0) return force;
     unsigned cs = vgk::kCgMaxCluster;
     while (cs > 1 && (o.active[cs] < static_cast<int>(jobs) || 64ull * cs > h.n)) --cs;
     if (o.active[cs] <= 0) {  // nothing fits all jobs at once: the widest that launches
@@ -327,6 +334,26 @@ unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned jobs) {
         }
     }
     return cs;
+}
+
+// SMs of the current device; the grid CG kernels' shared-memory opt-in
+unsigned cg_sms() {
+    static const unsigned n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return 0u;
+        }
+        const int smem = static_cast<int>(vgk::kCgSmemBytes);
+        for (auto k : {vgk::cg_grid_kernel<8>, vgk::cg_grid_kernel<16>, vgk::cg_grid_kernel<32>})
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+                cudaGetLastError();
+                return 0u;
+            }
+        return static_cast<unsigned>(v);
+    }();
+    return n;
 }
 
 // SpMV lanes per row for a job (k_cg.cuh cg_segment); VGPU_CG_SEG=8|16|32
@@ -633,6 +660,87 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 return std::min(m, mode_cap);
             };
             std::vector<bool> done(n, false);
+            // grid variant: every job an equal share of all SMs (plain CTAs,
+            // co-resident launch) when that is at least twice the cluster
+            // width (measured: its global barriers and L2 staging cost about
+            // what 1.8x the SMs gains — class A x 8: 24.5 ms grid at 18 CTAs
+            // vs 22.5 ms clusters of 10; one class-A job: 10.5 vs 14.7 ms),
+            // for jobs whose p fits in shared memory; VGPU_CG_GRID=0 disables
+            // it, =1 takes it whenever it is wider
+            static const int grid_env = [] {
+                const char* e = std::getenv("VGPU_CG_GRID");
+                return e && (*e == '0' || *e == '1') ? *e - '0' : -1;
+            }();
+            const bool grid_ok = grid_env != 0;
+            const unsigned grid_factor = grid_env == 1 ? 1u : 2u;
+            const unsigned per_job = ncg ? std::min<unsigned>(kCgMaxGridCtas, cg_sms() / ncg) : 0;
+            if (grid_ok && per_job > 1) {
+                std::vector<std::uint32_t> gi;
+                for (std::uint32_t i = 0; i < n; ++i) {
+                    const vgpu_cg_header& h = jobs[i].cg;
+                    if (!jobs[i].ws || h.n == 0 || h.n > kCgStageMax) continue;
+                    if (per_job < grid_factor * cg_cluster_for(h, ncg) || per_job <= cg_cluster_for(h, ncg) ||
+                        64ull * per_job > h.n)
+                        continue;
+                    gi.push_back(i);
+                }
+                for (std::size_t g0 = 0; g0 < gi.size(); g0 += kMaxCgJobs) {
+                    CgGridTable t{};
+                    std::uint32_t maxn = 0, maxrows = 0;
+                    const unsigned seg = cg_seg_for(jobs[gi[g0]].cg);
+                    for (std::size_t g = g0; g < std::min(gi.size(), g0 + kMaxCgJobs); ++g) {
+                        const std::uint32_t k = gi[g];
+                        const vgpu_cg_header& h = jobs[k].cg;
+                        if (cg_seg_for(h) != seg) continue;
+                        done[k] = true;
+                        const std::uint8_t* in = jobs[k].in;
+                        CgJob& j = t.job[t.njobs];
+                        const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
+                        const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
+                        j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
+                        j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
+                        j.a = reinterpret_cast<const double*>(in + off_a);
+                        double* w = reinterpret_cast<double*>(jobs[k].ws);
+                        j.x = w;
+                        j.z = w + h.n;
+                        j.p = w + 2ull * h.n;
+                        j.q = w + 3ull * h.n;
+                        j.r = w + 4ull * h.n;
+                        j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
+                        j.n = h.n;
+                        j.nnz = h.nnz;
+                        j.niter = h.niter;
+                        j.cgitmax = h.cgitmax;
+                        j.shift = h.shift;
+                        t.sync[t.njobs] = reinterpret_cast<CgGridSync*>(
+                            jobs[k].ws + ((5ull * 8ull * h.n + 255) & ~255ull));
+                        const cudaError_t e = cudaMemsetAsync(t.sync[t.njobs], 0, sizeof(CgGridSync), s);
+                        if (e != cudaSuccess) return e;
+                        ++t.njobs;
+                        maxn = std::max(maxn, h.n);
+                        maxrows = std::max(maxrows, (h.n + per_job - 1) / per_job + 2);
+                    }
+                    if (!t.njobs) continue;
+                    t.ctas_per_job = per_job;
+                    const std::uint64_t base = 8ull * maxn;
+                    t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
+                    cudaLaunchConfig_t cfg{};
+                    cfg.gridDim = dim3(t.njobs * per_job);
+                    cfg.blockDim = dim3(kCgThreads);
+                    cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
+                    cfg.stream = s;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeCooperative;  // the job's CTAs spin on each other
+                    at[0].val.cooperative = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    const cudaError_t e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<32>, t)
+                                          : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<16>, t)
+                                                      : cudaLaunchKernelEx(&cfg, cg_grid_kernel<8>, t);
+                    ++*launches;
+                    if (e != cudaSuccess) return e;
+                }
+            }
             for (std::uint32_t i = 0; i < n; ++i) {
                 if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
                 const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);

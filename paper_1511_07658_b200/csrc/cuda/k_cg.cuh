@@ -33,6 +33,7 @@ namespace cgx = cooperative_groups;
 constexpr int kCgThreads = 1024;
 constexpr int kCgMaxCluster = 16;     // CTAs per job at most (non-portable size)
 constexpr int kMaxCgJobs = 16;
+constexpr int kCgMaxGridCtas = 32;  // CTAs per job in the grid variant (warp-0 reduction)
 constexpr std::uint32_t kCgStageMax = 24576;  // rows whose p fits in shared memory (192 KiB)
 constexpr std::uint32_t kCgSmemBytes = 224 * 1024;  // dynamic shared memory cap per CTA
 
@@ -341,6 +342,201 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     }
     // no CTA may exit while a peer can still read its shared memory
     cluster.sync();
+}
+
+
+// ---- grid variant: a job spans plain CTAs on any SMs ------------------------
+// Clusters live inside one GPC (16-CTA clusters: 7 co-resident on a B200),
+// so a batch of 8 class-A jobs gets only 80 SMs as clusters. The grid
+// variant gives each job an equal share of ALL SMs (one 1024-thread CTA per
+// SM, the launch co-resident by construction: cooperative launch) and
+// replaces the cluster barrier and DSMEM with a global-memory barrier and
+// partials in L2; p is re-staged into shared memory from L2 after every
+// update (n <= kCgStageMax). Same arithmetic, same fixed reduction trees
+// (CTA partials summed in CTA order), so results are deterministic too.
+
+struct CgGridSync {            // per job, zeroed before every launch
+    unsigned count;
+    unsigned gen;
+    unsigned pad[2];
+    double part[2][kCgMaxGridCtas][4];  // [parity][cta][value]
+};
+
+struct CgGridTable {
+    CgJob job[kMaxCgJobs];
+    CgGridSync* sync[kMaxCgJobs];
+    std::uint32_t njobs;
+    std::uint32_t ctas_per_job;
+    std::uint32_t srow_words;
+};
+
+__device__ __forceinline__ unsigned cg_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// barrier over the job's CTAs (generation counting); orders global memory
+__device__ __forceinline__ void cg_grid_barrier(CgGridSync* sy, unsigned nctas, unsigned& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = gen;
+        __threadfence();
+        if (atomicAdd(&sy->count, 1u) == nctas - 1) {
+            sy->count = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&sy->gen), "r"(g + 1) : "memory");
+        } else {
+            while (cg_ld_acquire(&sy->gen) == g) {
+            }
+        }
+    }
+    gen += 1;
+    __syncthreads();
+}
+
+template <int W>
+__device__ __forceinline__ void cg_grid_sum(double (&v)[W], CgReduce& red, unsigned& parity, CgGridSync* sy,
+                                            unsigned cta, unsigned nctas, unsigned& gen) {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const double s = cg_warp_sum(v[w]);
+        if (lane == 0) red.warp[warp][w] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const double s = cg_warp_sum(red.warp[lane][w]);
+            if (lane == 0) sy->part[parity][cta][w] = s;
+        }
+    }
+    cg_grid_barrier(sy, nctas, gen);
+    if (warp == 0) {
+        double part[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[w] = lane < nctas ? __ldcg(&sy->part[parity][lane][w]) : 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const double s = cg_warp_sum(part[w]);
+            if (lane == 0) red.total[w] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = red.total[w];
+    parity ^= 1u;
+}
+
+template <unsigned kSeg>
+__global__ void __launch_bounds__(kCgThreads, 1) cg_grid_kernel(const __grid_constant__ CgGridTable table) {
+    extern __shared__ double ps[];  // p (n doubles) | rowstr slice
+    __shared__ CgReduce red;
+    const unsigned nctas = table.ctas_per_job;
+    const unsigned jid = blockIdx.x / nctas, cta = blockIdx.x % nctas;
+    const CgJob& job = table.job[jid];
+    CgGridSync* const sy = table.sync[jid];
+    const std::uint32_t n = job.n;
+    const std::uint32_t r0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * cta) / nctas);
+    const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (cta + 1)) / nctas);
+    unsigned parity = 0, gen = 0;
+    const CgMatrix mat{job.colidx, job.a, n - 1, job.nnz};
+    std::uint32_t* const srow = reinterpret_cast<std::uint32_t*>(ps + n);
+    const bool rs_smem = r1 - r0 + 1 <= table.srow_words;
+    if (rs_smem)
+        for (std::uint32_t i = threadIdx.x; i <= r1 - r0; i += kCgThreads) srow[i] = __ldg(job.rowstr + r0 + i);
+    const std::uint32_t* const rs = rs_smem ? srow : job.rowstr + r0;
+    __syncthreads();
+    double* const x = job.x;
+    double* const z = job.z;
+    double* const p = job.p;
+    double* const q = job.q;
+    double* const r = job.r;
+    auto stage = [&](const double* src) {
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        double2* d2 = reinterpret_cast<double2*>(ps);
+        const std::uint32_t n2 = n / 2;
+        for (std::uint32_t i0 = threadIdx.x; i0 < n2; i0 += 2 * kCgThreads) {
+            double2 t[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const std::uint32_t i = i0 + u * kCgThreads;
+                if (i < n2) t[u] = __ldcg(s2 + i);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const std::uint32_t i = i0 + u * kCgThreads;
+                if (i < n2) d2[i] = t[u];
+            }
+        }
+        if ((n & 1u) && threadIdx.x == 0) ps[n - 1] = __ldcg(src + n - 1);
+        __syncthreads();
+    };
+    auto gather = [&](std::uint32_t c) -> double { return ps[c]; };
+
+    for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = 1.0;
+    double zeta = 0.0, rnorm = 0.0;
+    const std::uint32_t niter = job.niter, cgitmax = job.cgitmax;
+    for (std::uint32_t it = 0; it < niter; ++it) {
+        double v1[1] = {0.0};
+        for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) {
+            const double xi = x[i];
+            z[i] = 0.0;
+            r[i] = xi;
+            p[i] = xi;
+            v1[0] = fma(xi, xi, v1[0]);
+        }
+        cg_grid_sum(v1, red, parity, sy, cta, nctas, gen);  // also publishes p
+        double rho = v1[0];
+        stage(p);
+        for (std::uint32_t cgit = 0; cgit < cgitmax; ++cgit) {
+            double d[1] = {0.0};
+            cg_spmv<kSeg, 4>(mat, rs, r0, r1, gather, [&](std::uint32_t row, double s) {
+                q[row] = s;
+                d[0] = fma(ps[row], s, d[0]);
+            });
+            cg_grid_sum(d, red, parity, sy, cta, nctas, gen);
+            const double alpha = rho / d[0];
+            const double rho0 = rho;
+            double rr[1] = {0.0};
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) {
+                z[i] = fma(alpha, ps[i], z[i]);
+                const double ri = fma(-alpha, q[i], r[i]);
+                r[i] = ri;
+                rr[0] = fma(ri, ri, rr[0]);
+            }
+            cg_grid_sum(rr, red, parity, sy, cta, nctas, gen);
+            rho = rr[0];
+            const double beta = rho / rho0;
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) p[i] = fma(beta, ps[i], r[i]);
+            cg_grid_barrier(sy, nctas, gen);  // p complete before anyone stages it
+            stage(p);
+        }
+        stage(z);  // the residual gathers z (complete since the last barriers)
+        double s3[3] = {0.0, 0.0, 0.0};
+        cg_spmv<kSeg, 4>(mat, rs, r0, r1, gather, [&](std::uint32_t row, double s) {
+            const double xi = x[row], zi = z[row];
+            const double e = xi - s;
+            s3[0] = fma(e, e, s3[0]);
+            s3[1] = fma(xi, zi, s3[1]);
+            s3[2] = fma(zi, zi, s3[2]);
+        });
+        cg_grid_sum(s3, red, parity, sy, cta, nctas, gen);
+        rnorm = sqrt(s3[0]);
+        zeta = job.shift + 1.0 / s3[1];
+        const double scale = 1.0 / sqrt(s3[2]);
+        for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = scale * z[i];
+    }
+    if (cta == 0 && threadIdx.x == 0) {
+        vgpu_cg_result res;
+        res.zeta = zeta;
+        res.rnorm = rnorm;
+        res.niter = job.niter;
+        res.n = n;
+        res.nnz = job.nnz;
+        *job.out = res;
+    }
 }
 
 }  // namespace vgk

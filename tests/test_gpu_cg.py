@@ -132,13 +132,14 @@ def test_vector_mul_bit_exact(n):
     assert outs == want
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "grid"])
 def test_nas_cg_every_vector_placement(mode):
-    """Each placement of the CG vectors (VGPU_CG_MODE: 0 HBM, 1 p staged in
-    shared memory, 2 everything in shared memory with DSMEM pushes) meets
-    NPB's verification and the oracle, in a fresh process (the cap is read
-    once per process). Classes S and W in one batch, and a class S alone
-    (widest cluster)."""
+    """Each placement of the CG vectors (cluster kernel, VGPU_CG_GRID=0 and
+    VGPU_CG_MODE: 0 HBM, 1 p staged in shared memory, 2 everything in shared
+    memory with DSMEM pushes; and the grid kernel, VGPU_CG_GRID=1: plain
+    co-resident CTAs with a global-memory barrier) meets NPB's verification
+    and the oracle, in a fresh process (the switches are read once per
+    process). Classes S and W in one batch, and a class S alone."""
     import subprocess
     import sys
     code = r'''
@@ -167,7 +168,8 @@ for classes in (["S", "W"], ["S"]):
         want = V.cg_class(c).zeta_verify
         print(c, abs(zeta - want) / want <= 1e-10 and abs(zeta - ref) / ref <= 1e-12)
 '''
-    env = dict(os.environ, VGPU_CG_MODE=mode)
+    env = dict(os.environ, VGPU_CG_GRID="1") if mode == "grid" else \
+        dict(os.environ, VGPU_CG_MODE=mode, VGPU_CG_GRID="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=600)
