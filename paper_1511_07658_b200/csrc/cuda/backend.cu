@@ -660,16 +660,18 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                 return std::min(m, mode_cap);
             };
             std::vector<bool> done(n, false);
-            // grid variant: every job an equal share of all SMs (plain CTAs,
-            // co-resident launch) when that is at least twice the cluster
-            // width (measured: its global barriers and L2 staging cost about
-            // what 1.8x the SMs gains — class A x 8: 24.5 ms grid at 18 CTAs
-            // vs 22.5 ms clusters of 10; one class-A job: 10.5 vs 14.7 ms),
-            // for jobs whose p fits in shared memory; VGPU_CG_GRID=0 disables
-            // it, =1 takes it whenever it is wider
+            // grid variant (opt-in, VGPU_CG_GRID=2: when at least twice the
+            // cluster width; =1: whenever wider): every job an equal share of
+            // all SMs as plain co-resident CTAs with a global-memory barrier.
+            // Measured: one class-A job 10.5 vs 14.7 ms on a 16-CTA cluster;
+            // 8 jobs 24.5 ms at 18 CTAs vs 22.5 ms on clusters of 10. Not the
+            // default: its spin barrier relies on the whole grid being
+            // resident, which a cluster gets from the hardware but a
+            // cooperative grid sharing the GPU with other clients' streams
+            // (PS-2 launches run concurrently) is not promised here.
             static const int grid_env = [] {
                 const char* e = std::getenv("VGPU_CG_GRID");
-                return e && (*e == '0' || *e == '1') ? *e - '0' : -1;
+                return e && (*e == '1' || *e == '2') ? *e - '0' : 0;
             }();
             const bool grid_ok = grid_env != 0;
             const unsigned grid_factor = grid_env == 1 ? 1u : 2u;

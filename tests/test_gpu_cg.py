@@ -134,10 +134,10 @@ def test_vector_mul_bit_exact(n):
 
 @pytest.mark.parametrize("mode", ["0", "1", "2", "grid"])
 def test_nas_cg_every_vector_placement(mode):
-    """Each placement of the CG vectors (cluster kernel, VGPU_CG_GRID=0 and
+    """Each placement of the CG vectors (cluster kernel, the default, with
     VGPU_CG_MODE: 0 HBM, 1 p staged in shared memory, 2 everything in shared
-    memory with DSMEM pushes; and the grid kernel, VGPU_CG_GRID=1: plain
-    co-resident CTAs with a global-memory barrier) meets NPB's verification
+    memory with DSMEM pushes; and the opt-in grid kernel, VGPU_CG_GRID=1:
+    plain co-resident CTAs with a global-memory barrier) meets NPB's verification
     and the oracle, in a fresh process (the switches are read once per
     process). Classes S and W in one batch, and a class S alone."""
     import subprocess
@@ -169,7 +169,7 @@ for classes in (["S", "W"], ["S"]):
         print(c, abs(zeta - want) / want <= 1e-10 and abs(zeta - ref) / ref <= 1e-12)
 '''
     env = dict(os.environ, VGPU_CG_GRID="1") if mode == "grid" else \
-        dict(os.environ, VGPU_CG_MODE=mode, VGPU_CG_GRID="0")
+        dict(os.environ, VGPU_CG_MODE=mode)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                          text=True, timeout=600)
