@@ -235,3 +235,65 @@ def test_nas_cg_malformed_interior_rowstr_stays_in_bounds():
     out = V.native_run_task(V.cg_input_for_class("S"), V.KernelDescriptor("nas-cg"))
     zeta = V.cg_result(out)[0]
     assert abs(zeta - V.cg_class("S").zeta_verify) / V.cg_class("S").zeta_verify <= 1e-10
+
+
+@pytest.mark.parametrize("style", ["ps1", "ps2"])
+def test_every_payload_kind_in_one_gvm_batch(style):
+    """Seven clients, seven payload kinds (vector-add, vector-mul, nas-ep,
+    black-scholes, sgemm, nas-cg, electrostatics) in one barrier batch: the
+    PS-1 launch grouping (one launch per kind, compute-intensive descriptors)
+    and PS-2 (per-stream triples, I/O-intensive descriptors) both give every
+    client its own oracle answer."""
+    rng = np.random.default_rng(21)
+    n = 4099
+    a = rng.uniform(-10, 10, n).astype(np.float32)
+    b = rng.uniform(-10, 10, n).astype(np.float32)
+    S = rng.uniform(5, 30, 1000).astype(np.float32)
+    X = rng.uniform(1, 100, 1000).astype(np.float32)
+    T = rng.uniform(0.25, 10, 1000).astype(np.float32)
+    A = rng.uniform(-1, 1, (128, 128)).astype(np.float32)
+    B = rng.uniform(-1, 1, (128, 128)).astype(np.float32)
+    cg = V.cg_input_for_class("S", niter=2)
+    es = V.es_input(_es_atoms(4, 700, 20, 9, 3, 0.5), 20, 9, 3, 0.5)
+    jobs = [("vector-add", a.tobytes() + b.tobytes()), ("vector-mul", a.tobytes() + b.tobytes()),
+            ("nas-ep", oracle.ep_params_bytes(20, 1, 6)),
+            ("black-scholes", S.tobytes() + X.tobytes() + T.tobytes()),
+            ("sgemm", A.tobytes() + B.tobytes()), ("nas-cg", cg), ("electrostatics", es)]
+    # the reference's batch_style: PS-1 for a compute-intensive majority,
+    # PS-2 for an I/O-intensive one (proj/src/model.cpp:38-41)
+    t = (10, 500000, 10) if style == "ps1" else (5000, 10, 5000)
+    d, inst = _gvm(len(jobs), max(len(j[1]) for j in jobs) + (1 << 16))
+    outs = [None] * len(jobs)
+    errs = []
+
+    def worker(i):
+        try:
+            h = V.req(inst)
+            outs[i] = h.run_task(jobs[i][1], V.KernelDescriptor(jobs[i][0], *t))
+            h.rls()
+            h.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    with d:
+        ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(jobs))]
+        [x.start() for x in ts]
+        [x.join() for x in ts]
+        batches = d.batches()
+    assert not errs, errs
+    assert batches and all(bt["task_count"] == len(jobs) for bt in batches), batches
+    assert {bt["style"] for bt in batches} == {0 if style == "ps1" else 1}, batches
+    assert outs[0] == oracle.vector_add(a, b).tobytes()
+    assert outs[1] == oracle.vector_mul(a, b).tobytes()
+    assert bytes(oracle.ep_from_bytes(outs[2])) == bytes(oracle.ep_job(20, 1, 6))
+    call, put = oracle.black_scholes(S, X, T)
+    got = np.frombuffer(outs[3], np.float32)
+    assert np.abs(got[:1000] - call).sum() / np.abs(call).sum() <= 1e-6
+    C = np.frombuffer(outs[4], np.float32).reshape(128, 128)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.linalg.norm(C - ref) / np.linalg.norm(ref) <= 1e-5
+    zeta = V.cg_result(outs[5])[0]
+    assert abs(zeta - oracle.cg_run(cg).zeta) / abs(oracle.cg_run(cg).zeta) <= 1e-12
+    vg = np.frombuffer(outs[6], np.float32).astype(np.float64)
+    ve = oracle.es(es).ravel()
+    assert np.abs(vg - ve).sum() / np.abs(ve).sum() <= 1e-5
