@@ -599,7 +599,8 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
       es         atom-lattice-point interactions (one MUFU rsqrt each)
       mm         2 n^3 FLOP per task (FP32 SIMT, or 3xTF32 tcgen05 opt-in)
       ep         IEEE binary64 operations of the restated NPB algorithm:
-                 7 per pair + 32 per accepted pair (W.ep_fp64_ops)
+                 binary64 FLOPs (FMA = 2, as the peak counts them): 7 per
+                 pair + 28 per accepted pair (W.ep_fp64_ops)
     peak = MEASURED_PEAKS.json HBM for hbm-bound kernels; the FMA-pipe peak
     probed on this GPU now for fp64/fp32 (vgpu_cu_peak_probe)."""
     kernel_s = d["kernel_ms_per_launch"] * 1e-3
@@ -678,8 +679,9 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
               "accepted_per_launch": accepted,
               "npb_mops": 2.0 * pairs / kernel_s / 1e6,
               "peak_source": "measured now: DFMA-chain probe (vgpu_cu_peak_probe), 2 FLOP/DFMA",
-              "op_count": "IEEE binary64 ops of the restated NPB EP step (each +,-,*,/,sqrt = 1): "
-                          "7 per pair + 19 per accepted pair (table-driven log = 12)"})
+              "op_count": "binary64 FLOPs of the restated NPB EP step, FMA = 2 as in the peak, "
+                          "+,-,*,/,sqrt = 1: 7 per pair + 28 per accepted pair (table-driven log = "
+                          "21: 9 FMAs + 3 other ops)"})
     # the pipe view of the same kernel from its committed ncu capture: the
     # op count above is algorithmic; the hardware also runs the log's
     # reduction, the Newton steps of div/sqrt and the compaction

@@ -72,14 +72,17 @@ EP_ACCEPT_RATE = EP_CLASS_A_ACCEPTED / float(1 << 28)
 
 
 def ep_fp64_ops(pairs: float, accepted: float) -> float:
-    """Algorithmic IEEE binary64 operation count of the restated NPB EP step
-    (paper_1511_07658_b200/csrc/common/ep_math.h), each +,-,*,/,sqrt = 1:
+    """Algorithmic binary64 FLOPs of the restated NPB EP step
+    (paper_1511_07658_b200/csrc/common/ep_math.h), counted as the FP64 peak
+    counts them: an FMA = 2, every other +,-,*,/,sqrt = 1:
       every pair      x1 = 2u1 - 1, x2 = 2u2 - 1 (4), t = x1^2 + x2^2 (3)  -> 7
-      accepted pair   log t: vgpu_ep_log, 12 (r = fma, k ln2_hi + logc_hi = 1
-                      exact fma, r^2, Horner 5, low part 2, final 2);
-                      -2 log t, / t, sqrt (3); x1 t2, x2 t2 (2); sx, sy (2) -> 19
-    The LCG and the log's argument reduction are integer work, not counted."""
-    return 7.0 * pairs + 19.0 * accepted
+      accepted pair   log t (vgpu_ep_log): 7 FMAs (r = z/c - 1, k ln2_hi +
+                      logc_hi, 5 Horner steps) + 2 FMAs (low part) = 18, r^2
+                      and the final 2 additions = 3 -> 21; -2 log t, / t,
+                      sqrt (3); x1 t2, x2 t2 (2); sx, sy (2)                  -> 28
+    The LCG and the log's argument reduction are integer work, not counted.
+    (Until the end of round 1 every op counted 1, FMAs included: 7 + 19.)"""
+    return 7.0 * pairs + 28.0 * accepted
 
 
 def kind_of(workload: str, worker: int) -> str:

@@ -40,7 +40,7 @@ def test_hbm_roofline_is_bytes_over_time(bench, W):
 def test_fp64_roofline_counts_restated_ep_ops(bench, W):
     pairs, acc = float(1 << 28), float(W.EP_CLASS_A_ACCEPTED)
     r = bench.roofline(W, "ep", _leg(1.0, flops=2 * pairs), {"fp64": 34.0}, acc)
-    ops = 7 * pairs + 19 * acc
+    ops = 7 * pairs + 28 * acc
     assert r["algo_flops_per_launch"] == pytest.approx(ops)
     assert r["achieved"] == pytest.approx(ops / 1e-3 / 1e12)
     assert r["frac"] == pytest.approx(r["achieved"] / 34.0)
@@ -79,7 +79,7 @@ def test_model_summary_takes_the_full_batches(bench):
 
 
 def test_ep_op_count_and_sizes(W):
-    assert W.ep_fp64_ops(10, 4) == 7 * 10 + 19 * 4
+    assert W.ep_fp64_ops(10, 4) == 7 * 10 + 28 * 4
     assert W.EP_ACCEPT_RATE == pytest.approx(0.7854, abs=1e-3)  # pi / 4
     s = W.Sizes.for_world(8)
     assert s.ep_m == 31 and s.ep_batches == 8 * 4096
