@@ -705,9 +705,11 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
 def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
     """Kernel GB/s (FLOP/s) vs roofline for every BASELINE config kernel at
     its own config's per-step shape (C1 4 x vecadd, C2 8 x EP slices of
-    class A, C3 16 x Black-Scholes, C4 16 x SGEMM), device-resident. The
-    headline workload's own entry is the line's `roofline`."""
-    shapes = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16}
+    class A, C3 16 x Black-Scholes, C4 16 x SGEMM) and the paper's extra
+    workloads (8 x NAS CG class A, 8 x electrostatics, 4 x vector-mul),
+    device-resident. The headline workload's own entry is the line's
+    `roofline`."""
+    shapes = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "cg": 8, "es": 8, "vmul": 4}
     out = {}
     for kind, procs in shapes.items():
         if kind == workload:
