@@ -1,5 +1,8 @@
 """electrostatics kernel variants (VGPU_ES_VARIANT) at the bench shape:
-8 jobs x 100K atoms x 64x64x25, device-resident, and accuracy vs binary64."""
+8 jobs x 100K atoms x 64x64x25, device-resident, and accuracy vs binary64.
+The variants (FMA-pipe rsqrt offload, 8 points per thread) were measured
+with this script and removed afterwards (electrostatics row);
+today every variant number runs the kept kernel."""
 import os, subprocess, sys
 code = r'''
 import numpy as np
