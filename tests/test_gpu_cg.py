@@ -19,11 +19,11 @@ from paper_1511_07658_b200 import vgpu as V
 pytestmark = pytest.mark.gpu
 
 
-def _gvm(n, shm):
+def _gvm(n, shm, window=20000):
     inst = f"cg{os.getpid()}_{n}_{shm}"
     V.unlink_os_instance(inst, n)
     cfg = V.GvmConfig(instance=inst, max_clients=n, barrier_size=n, per_client_shm_bytes=shm,
-                      barrier_window=20000, clock=V.ClockMode.Real)
+                      barrier_window=window, clock=V.ClockMode.Real)
     return V.GvmDaemon.start_os(cfg), inst
 
 
@@ -262,7 +262,8 @@ def test_every_payload_kind_in_one_gvm_batch(style):
     # the reference's batch_style: PS-1 for a compute-intensive majority,
     # PS-2 for an I/O-intensive one (proj/src/model.cpp:38-41)
     t = (10, 500000, 10) if style == "ps1" else (5000, 10, 5000)
-    d, inst = _gvm(len(jobs), max(len(j[1]) for j in jobs) + (1 << 16))
+    # a long barrier window: the batch flushes when all seven have arrived
+    d, inst = _gvm(len(jobs), max(len(j[1]) for j in jobs) + (1 << 16), window=10_000_000)
     outs = [None] * len(jobs)
     errs = []
 
