@@ -372,6 +372,183 @@ unsigned cg_seg_for(const vgpu_cg_header& h) {
 // measurement (VGPU_CU_RESIDENT_MAIN_ONLY) narrows it, on its own thread.
 thread_local unsigned g_sgemm_phases = 3;
 
+// NAS CG jobs (k_cg.cuh): cluster kernels grouped by (width, vector
+// placement, row segment), or the opt-in grid kernel. Counts launches.
+cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::uint64_t* launches) {
+    using namespace vgk;
+    // group by (cluster size, vector placement, row segment); one
+    // launch per group of up to kMaxCgJobs clusters
+    unsigned ncg = 0;
+    for (std::uint32_t i = 0; i < n; ++i) ncg += jobs[i].ws && jobs[i].cg.n ? 1u : 0u;
+    // placement: everything in shared memory if p + 4 own slices +
+    // the rowstr slice fit, else p alone, else HBM
+    // (VGPU_CG_MODE=0|1 caps it: HBM / staged p, for measurement and tests)
+    static const int mode_cap = [] {
+        const char* e = std::getenv("VGPU_CG_MODE");
+        return e && *e >= '0' && *e <= '2' ? *e - '0' : 2;
+    }();
+    auto mode_for = [&](const vgpu_cg_header& h, unsigned cs) {
+        const std::uint64_t rows = (h.n + cs - 1) / cs + 2;
+        int m = kCgGlobal;
+        if (8ull * h.n + 32ull * rows + 4ull * rows <= kCgSmemBytes) m = kCgResident;
+        else if (h.n <= kCgStageMax) m = kCgStaged;
+        return std::min(m, mode_cap);
+    };
+    std::vector<bool> done(n, false);
+    // grid variant (opt-in, VGPU_CG_GRID=2: when at least twice the
+    // cluster width; =1: whenever wider): every job an equal share of
+    // all SMs as plain co-resident CTAs with a global-memory barrier.
+    // Measured: one class-A job 10.5 vs 14.7 ms on a 16-CTA cluster;
+    // 8 jobs 24.5 ms at 18 CTAs vs 22.5 ms on clusters of 10. Not the
+    // default: its spin barrier relies on the whole grid being
+    // resident, which a cluster gets from the hardware but a
+    // cooperative grid sharing the GPU with other clients' streams
+    // (PS-2 launches run concurrently) is not promised here.
+    static const int grid_env = [] {
+        const char* e = std::getenv("VGPU_CG_GRID");
+        return e && (*e == '1' || *e == '2') ? *e - '0' : 0;
+    }();
+    const bool grid_ok = grid_env != 0;
+    const unsigned grid_factor = grid_env == 1 ? 1u : 2u;
+    const unsigned per_job = ncg ? std::min<unsigned>(kCgMaxGridCtas, cg_sms() / ncg) : 0;
+    if (grid_ok && per_job > 1) {
+        std::vector<std::uint32_t> gi;
+        for (std::uint32_t i = 0; i < n; ++i) {
+            const vgpu_cg_header& h = jobs[i].cg;
+            if (!jobs[i].ws || h.n == 0 || h.n > kCgStageMax) continue;
+            if (per_job < grid_factor * cg_cluster_for(h, ncg) || per_job <= cg_cluster_for(h, ncg) ||
+                64ull * per_job > h.n)
+                continue;
+            gi.push_back(i);
+        }
+        for (std::size_t g0 = 0; g0 < gi.size(); g0 += kMaxCgJobs) {
+            CgGridTable t{};
+            std::uint32_t maxn = 0, maxrows = 0;
+            const unsigned seg = cg_seg_for(jobs[gi[g0]].cg);
+            for (std::size_t g = g0; g < std::min(gi.size(), g0 + kMaxCgJobs); ++g) {
+                const std::uint32_t k = gi[g];
+                const vgpu_cg_header& h = jobs[k].cg;
+                if (cg_seg_for(h) != seg) continue;
+                done[k] = true;
+                const std::uint8_t* in = jobs[k].in;
+                CgJob& j = t.job[t.njobs];
+                const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
+                const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
+                j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
+                j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
+                j.a = reinterpret_cast<const double*>(in + off_a);
+                double* w = reinterpret_cast<double*>(jobs[k].ws);
+                j.x = w;
+                j.z = w + h.n;
+                j.p = w + 2ull * h.n;
+                j.q = w + 3ull * h.n;
+                j.r = w + 4ull * h.n;
+                j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
+                j.n = h.n;
+                j.nnz = h.nnz;
+                j.niter = h.niter;
+                j.cgitmax = h.cgitmax;
+                j.shift = h.shift;
+                t.sync[t.njobs] = reinterpret_cast<CgGridSync*>(
+                    jobs[k].ws + ((5ull * 8ull * h.n + 255) & ~255ull));
+                const cudaError_t e = cudaMemsetAsync(t.sync[t.njobs], 0, sizeof(CgGridSync), s);
+                if (e != cudaSuccess) return e;
+                ++t.njobs;
+                maxn = std::max(maxn, h.n);
+                maxrows = std::max(maxrows, (h.n + per_job - 1) / per_job + 2);
+            }
+            if (!t.njobs) continue;
+            t.ctas_per_job = per_job;
+            const std::uint64_t base = 8ull * maxn;
+            t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(t.njobs * per_job);
+            cfg.blockDim = dim3(kCgThreads);
+            cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;  // the job's CTAs spin on each other
+            at[0].val.cooperative = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            const cudaError_t e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<32>, t)
+                                  : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<16>, t)
+                                              : cudaLaunchKernelEx(&cfg, cg_grid_kernel<8>, t);
+            ++*launches;
+            if (e != cudaSuccess) return e;
+        }
+    }
+    for (std::uint32_t i = 0; i < n; ++i) {
+        if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
+        const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);
+        if (!cs) return cudaErrorInvalidConfiguration;
+        const int mode = mode_for(jobs[i].cg, cs);
+        const unsigned seg = cg_seg_for(jobs[i].cg);
+        CgTable t{};
+        std::uint32_t maxn = 0, maxrows = 0;
+        for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
+            const vgpu_cg_header& h = jobs[k].cg;
+            if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, ncg) != cs ||
+                mode_for(h, cs) != mode || cg_seg_for(h) != seg)
+                continue;
+            done[k] = true;
+            const std::uint8_t* in = jobs[k].in;
+            CgJob& j = t.job[t.njobs++];
+            const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
+            const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
+            j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
+            j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
+            j.a = reinterpret_cast<const double*>(in + off_a);
+            double* w = reinterpret_cast<double*>(jobs[k].ws);
+            j.x = w;
+            j.z = w + h.n;
+            j.p = w + 2ull * h.n;
+            j.q = w + 3ull * h.n;
+            j.r = w + 4ull * h.n;
+            j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
+            j.n = h.n;
+            j.nnz = h.nnz;
+            j.niter = h.niter;
+            j.cgitmax = h.cgitmax;
+            j.shift = h.shift;
+            maxn = std::max(maxn, h.n);
+            maxrows = std::max(maxrows, (h.n + cs - 1) / cs + 2);
+        }
+        // p (n doubles) | own x z r q slices | rowstr slice if it fits
+        t.stage_n = mode != kCgGlobal ? maxn : 0;
+        t.own_rows = mode == kCgResident ? maxrows : 0;
+        const std::uint64_t base = 8ull * t.stage_n + 32ull * t.own_rows;
+        t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(t.njobs * cs);
+        cfg.blockDim = dim3(kCgThreads);
+        cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        auto go = [&](auto k8, auto k16, auto k32) {
+            return seg == 32 ? cudaLaunchKernelEx(&cfg, k32, t)
+                   : seg == 16 ? cudaLaunchKernelEx(&cfg, k16, t)
+                               : cudaLaunchKernelEx(&cfg, k8, t);
+        };
+        const cudaError_t e =
+            mode == kCgResident ? go(cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>,
+                                     cg_kernel<kCgResident, 32>)
+            : mode == kCgStaged ? go(cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>,
+                                     cg_kernel<kCgStaged, 32>)
+                                : go(cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>,
+                                     cg_kernel<kCgGlobal, 32>);
+        ++*launches;
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t n,
                         cudaStream_t s, std::uint64_t* launches, bool pdl = false) {
     using namespace vgk;
@@ -640,179 +817,8 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
             }
             return cudaSuccess;
         }
-        case VGPU_CU_K_CG: {
-            // group by (cluster size, vector placement, row segment); one
-            // launch per group of up to kMaxCgJobs clusters
-            unsigned ncg = 0;
-            for (std::uint32_t i = 0; i < n; ++i) ncg += jobs[i].ws && jobs[i].cg.n ? 1u : 0u;
-            // placement: everything in shared memory if p + 4 own slices +
-            // the rowstr slice fit, else p alone, else HBM
-            // (VGPU_CG_MODE=0|1 caps it: HBM / staged p, for measurement and tests)
-            static const int mode_cap = [] {
-                const char* e = std::getenv("VGPU_CG_MODE");
-                return e && *e >= '0' && *e <= '2' ? *e - '0' : 2;
-            }();
-            auto mode_for = [&](const vgpu_cg_header& h, unsigned cs) {
-                const std::uint64_t rows = (h.n + cs - 1) / cs + 2;
-                int m = kCgGlobal;
-                if (8ull * h.n + 32ull * rows + 4ull * rows <= kCgSmemBytes) m = kCgResident;
-                else if (h.n <= kCgStageMax) m = kCgStaged;
-                return std::min(m, mode_cap);
-            };
-            std::vector<bool> done(n, false);
-            // grid variant (opt-in, VGPU_CG_GRID=2: when at least twice the
-            // cluster width; =1: whenever wider): every job an equal share of
-            // all SMs as plain co-resident CTAs with a global-memory barrier.
-            // Measured: one class-A job 10.5 vs 14.7 ms on a 16-CTA cluster;
-            // 8 jobs 24.5 ms at 18 CTAs vs 22.5 ms on clusters of 10. Not the
-            // default: its spin barrier relies on the whole grid being
-            // resident, which a cluster gets from the hardware but a
-            // cooperative grid sharing the GPU with other clients' streams
-            // (PS-2 launches run concurrently) is not promised here.
-            static const int grid_env = [] {
-                const char* e = std::getenv("VGPU_CG_GRID");
-                return e && (*e == '1' || *e == '2') ? *e - '0' : 0;
-            }();
-            const bool grid_ok = grid_env != 0;
-            const unsigned grid_factor = grid_env == 1 ? 1u : 2u;
-            const unsigned per_job = ncg ? std::min<unsigned>(kCgMaxGridCtas, cg_sms() / ncg) : 0;
-            if (grid_ok && per_job > 1) {
-                std::vector<std::uint32_t> gi;
-                for (std::uint32_t i = 0; i < n; ++i) {
-                    const vgpu_cg_header& h = jobs[i].cg;
-                    if (!jobs[i].ws || h.n == 0 || h.n > kCgStageMax) continue;
-                    if (per_job < grid_factor * cg_cluster_for(h, ncg) || per_job <= cg_cluster_for(h, ncg) ||
-                        64ull * per_job > h.n)
-                        continue;
-                    gi.push_back(i);
-                }
-                for (std::size_t g0 = 0; g0 < gi.size(); g0 += kMaxCgJobs) {
-                    CgGridTable t{};
-                    std::uint32_t maxn = 0, maxrows = 0;
-                    const unsigned seg = cg_seg_for(jobs[gi[g0]].cg);
-                    for (std::size_t g = g0; g < std::min(gi.size(), g0 + kMaxCgJobs); ++g) {
-                        const std::uint32_t k = gi[g];
-                        const vgpu_cg_header& h = jobs[k].cg;
-                        if (cg_seg_for(h) != seg) continue;
-                        done[k] = true;
-                        const std::uint8_t* in = jobs[k].in;
-                        CgJob& j = t.job[t.njobs];
-                        const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
-                        const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
-                        j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
-                        j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
-                        j.a = reinterpret_cast<const double*>(in + off_a);
-                        double* w = reinterpret_cast<double*>(jobs[k].ws);
-                        j.x = w;
-                        j.z = w + h.n;
-                        j.p = w + 2ull * h.n;
-                        j.q = w + 3ull * h.n;
-                        j.r = w + 4ull * h.n;
-                        j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
-                        j.n = h.n;
-                        j.nnz = h.nnz;
-                        j.niter = h.niter;
-                        j.cgitmax = h.cgitmax;
-                        j.shift = h.shift;
-                        t.sync[t.njobs] = reinterpret_cast<CgGridSync*>(
-                            jobs[k].ws + ((5ull * 8ull * h.n + 255) & ~255ull));
-                        const cudaError_t e = cudaMemsetAsync(t.sync[t.njobs], 0, sizeof(CgGridSync), s);
-                        if (e != cudaSuccess) return e;
-                        ++t.njobs;
-                        maxn = std::max(maxn, h.n);
-                        maxrows = std::max(maxrows, (h.n + per_job - 1) / per_job + 2);
-                    }
-                    if (!t.njobs) continue;
-                    t.ctas_per_job = per_job;
-                    const std::uint64_t base = 8ull * maxn;
-                    t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
-                    cudaLaunchConfig_t cfg{};
-                    cfg.gridDim = dim3(t.njobs * per_job);
-                    cfg.blockDim = dim3(kCgThreads);
-                    cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
-                    cfg.stream = s;
-                    cudaLaunchAttribute at[1];
-                    at[0].id = cudaLaunchAttributeCooperative;  // the job's CTAs spin on each other
-                    at[0].val.cooperative = 1;
-                    cfg.attrs = at;
-                    cfg.numAttrs = 1;
-                    const cudaError_t e = seg == 32   ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<32>, t)
-                                          : seg == 16 ? cudaLaunchKernelEx(&cfg, cg_grid_kernel<16>, t)
-                                                      : cudaLaunchKernelEx(&cfg, cg_grid_kernel<8>, t);
-                    ++*launches;
-                    if (e != cudaSuccess) return e;
-                }
-            }
-            for (std::uint32_t i = 0; i < n; ++i) {
-                if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
-                const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);
-                if (!cs) return cudaErrorInvalidConfiguration;
-                const int mode = mode_for(jobs[i].cg, cs);
-                const unsigned seg = cg_seg_for(jobs[i].cg);
-                CgTable t{};
-                std::uint32_t maxn = 0, maxrows = 0;
-                for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
-                    const vgpu_cg_header& h = jobs[k].cg;
-                    if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, ncg) != cs ||
-                        mode_for(h, cs) != mode || cg_seg_for(h) != seg)
-                        continue;
-                    done[k] = true;
-                    const std::uint8_t* in = jobs[k].in;
-                    CgJob& j = t.job[t.njobs++];
-                    const std::uint64_t off_col = sizeof(vgpu_cg_header) + 4ull * (h.n + 1ull);
-                    const std::uint64_t off_a = (off_col + 4ull * h.nnz + 7u) & ~7ull;
-                    j.rowstr = reinterpret_cast<const std::uint32_t*>(in + sizeof(vgpu_cg_header));
-                    j.colidx = reinterpret_cast<const std::uint32_t*>(in + off_col);
-                    j.a = reinterpret_cast<const double*>(in + off_a);
-                    double* w = reinterpret_cast<double*>(jobs[k].ws);
-                    j.x = w;
-                    j.z = w + h.n;
-                    j.p = w + 2ull * h.n;
-                    j.q = w + 3ull * h.n;
-                    j.r = w + 4ull * h.n;
-                    j.out = reinterpret_cast<vgpu_cg_result*>(jobs[k].out);
-                    j.n = h.n;
-                    j.nnz = h.nnz;
-                    j.niter = h.niter;
-                    j.cgitmax = h.cgitmax;
-                    j.shift = h.shift;
-                    maxn = std::max(maxn, h.n);
-                    maxrows = std::max(maxrows, (h.n + cs - 1) / cs + 2);
-                }
-                // p (n doubles) | own x z r q slices | rowstr slice if it fits
-                t.stage_n = mode != kCgGlobal ? maxn : 0;
-                t.own_rows = mode == kCgResident ? maxrows : 0;
-                const std::uint64_t base = 8ull * t.stage_n + 32ull * t.own_rows;
-                t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
-                cudaLaunchConfig_t cfg{};
-                cfg.gridDim = dim3(t.njobs * cs);
-                cfg.blockDim = dim3(kCgThreads);
-                cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
-                cfg.stream = s;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributeClusterDimension;
-                at[0].val.clusterDim.x = cs;
-                at[0].val.clusterDim.y = 1;
-                at[0].val.clusterDim.z = 1;
-                cfg.attrs = at;
-                cfg.numAttrs = 1;
-                auto go = [&](auto k8, auto k16, auto k32) {
-                    return seg == 32 ? cudaLaunchKernelEx(&cfg, k32, t)
-                           : seg == 16 ? cudaLaunchKernelEx(&cfg, k16, t)
-                                       : cudaLaunchKernelEx(&cfg, k8, t);
-                };
-                const cudaError_t e =
-                    mode == kCgResident ? go(cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>,
-                                             cg_kernel<kCgResident, 32>)
-                    : mode == kCgStaged ? go(cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>,
-                                             cg_kernel<kCgStaged, 32>)
-                                        : go(cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>,
-                                             cg_kernel<kCgGlobal, 32>);
-                ++*launches;
-                if (e != cudaSuccess) return e;
-            }
-            return cudaSuccess;
-        }
+        case VGPU_CU_K_CG:
+            return launch_cg(jobs, n, s, launches);
         default:
             return cudaErrorInvalidValue;
     }
