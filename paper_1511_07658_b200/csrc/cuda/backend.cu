@@ -198,7 +198,6 @@ cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, cudaStream_t s,
     return cudaLaunchKernelEx(&cfg, kern, arg);
 }
 
-// Launch every job (all of one kernel kind) on `s`; counts launches.
 // ---- TMA tensor maps for the CTA-pair SGEMM ----------------------------------------
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
@@ -549,6 +548,7 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
     return cudaSuccess;
 }
 
+// Launch every job (all of one kernel kind) on `s`; counts launches.
 cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t n,
                         cudaStream_t s, std::uint64_t* launches, bool pdl = false) {
     using namespace vgk;
