@@ -436,7 +436,7 @@ def final_reduce(N, dist, record):
         libs.cuda.vgpu_cu_close(dev)
 
 
-def validate_model(V, N, W, workload, device, sizes, dist, reps=8) -> dict:
+def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> dict:
     """SURVEY 8(f)(1): the paper's model on real hardware (PAPER.md:505;
     proj/src/bench/bench.cpp:341-375 validate_model). Measure one task's
     stages (t_in, t_comp, t_out) with CUDA events (one SPMD process, the
@@ -449,7 +449,7 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8) -> dict:
     run side by side) and 'device-filling' (every task's kernel occupies the
     whole GPU: computes serialize). Deviation rows use the reference's
     schema (n, model_us, measured_us, deviation_pct)."""
-    procs = W.DEFAULT_PROCS[workload]
+    procs = procs or W.DEFAULT_PROCS[workload]
     one = leg_workers(V, N, W, workload, 1, 0, procs, reps, 2, device, False, sizes, dist,
                       barrier=1, snapshot=True)
     st = one["device_stage_us"]
@@ -480,14 +480,14 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8) -> dict:
     return out
 
 
-def sweep(V, N, W, workload, device, sizes, dist) -> dict:
+def sweep(V, N, W, workload, device, sizes, dist, procs=0) -> dict:
     """The paper's turnaround curves (Figs. 13-22; proj/src/bench/bench.cpp:
     266-339 run_sweep) on B200: for N = 1..P SPMD processes started
     together, each running one task, the time until the last has its result.
     Virtualized includes REQ on the already-open GVM; native includes each
     process creating its own CUDA context (the paper's T_init). Rows use the
     reference's report schema."""
-    procs = W.DEFAULT_PROCS[workload]
+    procs = procs or W.DEFAULT_PROCS[workload]
     rows = []
     for n in range(1, procs + 1):
         tv = leg_workers(V, N, W, workload, n, 0, procs, 1, 0, device, False, sizes, dist,
@@ -845,9 +845,9 @@ def main():
             if args.speedup:
                 emit(speedup(V, N, W, device, dist))
             if args.validate_model:
-                emit(validate_model(V, N, W, args.workload, device, sizes, dist))
+                emit(validate_model(V, N, W, args.workload, device, sizes, dist, procs=args.procs))
             if args.sweep:
-                emit(sweep(V, N, W, args.workload, device, sizes, dist))
+                emit(sweep(V, N, W, args.workload, device, sizes, dist, procs=args.procs))
             if args.overhead_curve:
                 emit(overhead_curve(V, N, W, device, dist, args.steps, args.warmup))
         dist.close()

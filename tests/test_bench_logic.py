@@ -126,3 +126,17 @@ def test_reference_arm_runs_the_paper_workloads(workload, extra):
                           "--warmup", "0"] + extra, capture_output=True, text=True, timeout=300)
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["ok"] and d["jobs_per_s"] > 0
+
+
+def test_vgpu_bench_cli_takes_the_reference_flags():
+    """scripts/vgpu_bench.py: the reference's vgpu-bench command line
+    (proj/tools/vgpu_bench.cpp:30-75) maps onto bench.py's reports; MG and
+    unknown profiles are refused with status 2 before any GPU work."""
+    import importlib.util as U
+    spec = U.spec_from_file_location("vgpu_bench", os.path.join(ROOT, "scripts", "vgpu_bench.py"))
+    vb = U.module_from_spec(spec)
+    spec.loader.exec_module(vb)
+    assert vb.main(["sweep", "--profile", "MG", "--mode", "native", "--clock", "real"]) == 2
+    assert vb.main(["validate", "--profile", "NOPE"]) == 2
+    assert set(vb.PROFILES.values()) <= {"ep", "vecadd", "vmul", "mm", "bs", "cg", "es"}
+    assert vb.rows_to_csv([{"n": 1, "a": 2}, {"n": 2, "b": 3}]).splitlines()[0] == "n,a,b"
