@@ -72,7 +72,11 @@ def main(argv=None) -> int:
         sys.stderr.write(out.stderr[-2000:])
         return out.returncode
     report = json.loads(out.stdout.strip().splitlines()[-1])
-    text = report.get("csv") or rows_to_csv(report.get("rows", []))
+    rows = report.get("rows")
+    if rows is None:  # validate: one row set per device model
+        rows = [{"model": name, **r} for name in ("concurrent", "device_filling")
+                for r in report.get(name, {}).get("rows", [])]
+    text = report.get("csv") or rows_to_csv(rows)
     if a.out:
         with open(a.out, "w") as fh:
             fh.write(text)
