@@ -685,7 +685,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
     # the pipe view of the same kernel from its committed ncu capture: the
     # op count above is algorithmic; the hardware also runs the log's
     # reduction, the Newton steps of div/sqrt and the compaction
-    summ = os.path.join(REPO, "profiles", "r1_ncu_ep_summary_v6.txt")
+    summ = os.path.join(REPO, "profiles", "r1_ncu_ep_summary_v7.txt")
     if os.path.exists(summ):
         vals = {}
         for line in open(summ):
@@ -698,7 +698,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                                                                "pct_of_peak_sustained_active"),
                               "issue_active_pct": vals.get("smsp__issue_active.avg."
                                                            "pct_of_peak_sustained_active"),
-                              "source": "profiles/r1_ncu_ep_summary_v6.txt (ncu --set full)"}
+                              "source": "profiles/r1_ncu_ep_summary_v7.txt (ncu --set full)"}
     return r
 
 
