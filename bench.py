@@ -233,7 +233,11 @@ def collect(procs, timeout=1800.0):
         lines = [l for l in so.decode().splitlines() if l.startswith("{")]
         if not lines:
             raise RuntimeError(f"worker produced no result (rc={p.returncode}): {se.decode()[-2000:]}")
-        out.append(json.loads(lines[-1]))
+        r = json.loads(lines[-1])
+        if p.returncode != 0:  # a failed verification must never count as jobs/s
+            r["ok"] = False
+            r["err"] = f"rc={p.returncode}: {r.get('err', '')}"
+        out.append(r)
     return out
 
 

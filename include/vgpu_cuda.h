@@ -185,6 +185,13 @@ int vgpu_cu_payload(const char* id, uint32_t* kernel);
  * PayloadError::MalformedInput). `in` may be NULL except for EP. */
 int vgpu_cu_output_size(uint32_t kernel, const void* in, uint64_t in_bytes,
                         uint64_t* out_bytes);
+/* Per-task preflight against THIS device's slots: vgpu_cu_output_size plus
+ * the slot limits submit enforces (input, result and device workspace must
+ * fit the slot). The GVM runs it per task before a batch is submitted, so a
+ * task that cannot run fails alone (VGPU_CU_EPAYLOAD / VGPU_CU_ESIZE) and
+ * never takes its co-batched clients down with a failed submit. */
+int vgpu_cu_task_check(vgpu_cu_dev* dev, uint32_t kernel, const void* in, uint64_t in_bytes,
+                       uint64_t* out_bytes);
 
 /* Eager upload (SND time): H2D of `bytes` from h_in into the slot's input
  * buffer on the slot's stream; poll() reports it as VGPU_CU_DONE_UPLOAD with

@@ -60,7 +60,13 @@ void set_err(const char* fmt, ...) {
     g_err = buf;
 }
 
+// Every failing CUDA call is reported through here, which also consumes the
+// error: a one-off API error (bad argument, allocation failure) must not
+// linger in the runtime's last-error slot and fail unrelated later work.
+// Sticky device faults are not cleared by this; they surface again on the
+// ops' event queries (vgpu_cu_poll) and are handled by vgpu_cu_recover.
 int cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();
     set_err("%s: %s", what, cudaGetErrorString(e));
     return VGPU_CU_EINTERNAL;
 }
@@ -1179,6 +1185,29 @@ int vgpu_cu_output_size(std::uint32_t kernel, const void* in, std::uint64_t in_b
     }
 }
 
+int vgpu_cu_task_check(vgpu_cu_dev* d, std::uint32_t kernel, const void* in,
+                       std::uint64_t in_bytes, std::uint64_t* out_bytes) {
+    if (!d || !out_bytes) return VGPU_CU_EINVAL;
+    std::uint64_t need = 0;
+    const int rc = vgpu_cu_output_size(kernel, in, in_bytes, &need);
+    if (rc) return rc;
+    if (in_bytes > d->slot_bytes || need > d->slot_bytes) {
+        set_err("%llu B in / %llu B out exceed the slot (%llu B)", (unsigned long long)in_bytes,
+                (unsigned long long)need, (unsigned long long)d->slot_bytes);
+        return VGPU_CU_ESIZE;
+    }
+    // the slot's workspace is 2 buffers (sgemm hi/lo splits: exactly 2 x input)
+    if (job_ws_bytes(kernel, in, in_bytes) > 2 * d->buf_bytes) {
+        set_err("%s workspace (%llu B) exceeds the slot's (%llu B)",
+                kernel == VGPU_CU_K_CG ? "nas-cg vector" : "device",
+                (unsigned long long)job_ws_bytes(kernel, in, in_bytes),
+                (unsigned long long)(2 * d->buf_bytes));
+        return VGPU_CU_ESIZE;
+    }
+    *out_bytes = need;
+    return VGPU_CU_OK;
+}
+
 int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes,
                  vgpu_cu_dev** out) {
     if (!out || max_clients == 0) return VGPU_CU_EINVAL;
@@ -1590,7 +1619,6 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
     *n_out = 0;
     if (d->outstanding.empty()) return VGPU_CU_OK;
     cudaSetDevice(d->device);
-    const cudaError_t sticky = cudaPeekAtLastError();
     // completion = the op's final event has completed (an event query: no
     // CUDA host callback, whose latency on B200 hosts is 100-300 us and
     // which would also hold the slot's stream until it ran)
@@ -1605,7 +1633,7 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
         // report it either way, with Internal status in the second case,
         // so the client's STP gets NACK(Internal) instead of waiting forever
         if (q != cudaSuccess) cudaGetLastError();
-        report_op(d, op, q == cudaSuccess ? sticky : q, out[(*n_out)++]);
+        report_op(d, op, q, out[(*n_out)++]);
         d->outstanding.erase(d->outstanding.begin() + i);
         d->release_op(op);
     }
@@ -1670,13 +1698,20 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     if (c.device != device) {
         rc = require_sm100(device);
         if (rc) return rc;
+        // the old device's buffers and stream (freed with that device current)
+        if (c.device >= 0 && cudaSetDevice(c.device) == cudaSuccess) {
+            if (c.stream) cudaStreamDestroy(c.stream);
+            if (c.d_in) cudaFree(c.d_in);
+            if (c.d_out) cudaFree(c.d_out);
+            if (c.d_scratch) cudaFree(c.d_scratch);
+            if (c.d_ws) cudaFree(c.d_ws);
+        }
+        cudaGetLastError();
+        c.stream = nullptr;
+        c.d_in = c.d_out = c.d_scratch = c.d_ws = nullptr;
+        c.cap_in = c.cap_out = c.cap_ws = 0;
+        c.device = -1;
         CK(cudaSetDevice(device));
-        if (c.stream) cudaStreamDestroy(c.stream);
-        if (c.d_in) cudaFree(c.d_in);
-        if (c.d_out) cudaFree(c.d_out);
-        if (c.d_scratch) cudaFree(c.d_scratch);
-        c.d_in = c.d_out = c.d_scratch = nullptr;
-        c.cap_in = c.cap_out = 0;
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         CK(cudaMalloc(&c.d_scratch, kScratchBytes));
         CK(cudaMemset(c.d_scratch, 0, kScratchBytes));

@@ -537,10 +537,13 @@ struct GvmDaemon::Impl {
                 (live && (s->input_resident || s->input_inline) && in_len <= sizeof s->head)
                     ? s->head
                     : src;
-            const int rc = vgpu_cu_output_size(dk->kernel, probe, in_len, &out_bytes);
+            // per-task preflight against the slot (input, result, workspace):
+            // a task that cannot run fails alone, before the batch is submitted
+            const int rc = vgpu_cu_task_check(dev, dk->kernel, probe, in_len, &out_bytes);
             if (rc != VGPU_CU_OK || !live) {
                 if (live)
-                    fail_session(t.client_id, t.generation, ErrCode::Payload,
+                    fail_session(t.client_id, t.generation,
+                                 rc == VGPU_CU_ESIZE ? ErrCode::Size : ErrCode::Payload,
                                  std::string(t.profile.payload_id) + ": " +
                                      vgpu_cu_last_error());
                 record_task(virt ? vm : TaskMetrics{t.task_id, t.client_id,

@@ -8,7 +8,8 @@
 // up) — or, with --native, uses its OWN CUDA context through NativeVgpu —
 // prints "READY", waits for one byte on stdin (the start barrier), runs R
 // tasks through the unchanged client API (run_task), checks every result
-// (vecadd: exact elementwise sums; others: identical checksum every round)
+// (vecadd: exact elementwise sums; others: identical checksum every round;
+// after the rounds, BS / SGEMM against a sampled binary64 recomputation)
 // and prints one JSON line with CLOCK_MONOTONIC timestamps per round.
 #include <malloc.h>
 #include <unistd.h>
@@ -147,6 +148,7 @@ int main(int argc, char** argv) {
     std::uint64_t first_sum = 0;
     vgpu::Bytes first_out, last_out;
     bool ok = true;
+    std::string check_json;
     const std::int64_t t_go = now_ns();
     if (connect_after_go && !connect()) return 3;
     try {
@@ -200,10 +202,42 @@ int main(int argc, char** argv) {
             ok = false;
             err = "result changed between rounds (full check)";
         }
+        // BS / SGEMM: the result against a binary64 recomputation of a sample
+        if (ok && (job.kind == vgpu::wl::Kind::Bs || job.kind == vgpu::wl::Kind::Mm)) {
+            const vgpu::wl::SampleCheck c = job.kind == vgpu::wl::Kind::Bs
+                                                ? vgpu::wl::check_bs_sample(job.input, last_out, 61)
+                                                : vgpu::wl::check_mm_sample(job.input, last_out, 128);
+            char buf[128];
+            std::snprintf(buf, sizeof buf, ", \"check\": {\"err\": %.3e, \"samples\": %llu}", c.err,
+                          static_cast<unsigned long long>(c.samples));
+            check_json = buf;
+            if (!c.ok) {
+                ok = false;
+                err = job.kind == vgpu::wl::Kind::Bs ? "black-scholes differs from binary64 (L1 > 1e-6)"
+                                                     : "sgemm differs from binary64 (Frobenius > 1e-5)";
+            }
+        }
         first_sum = vgpu::wl::fnv1a(last_out.data(), std::min<std::size_t>(last_out.size(), 1 << 16));
     } catch (const std::exception& e) {
         ok = false;
         err = e.what();
+    }
+    // NPB's own verification for CG: zeta within 1e-10 of the published
+    // value. Decided before the line is written so "ok" covers it.
+    std::string cg_json;
+    if (job.kind == vgpu::wl::Kind::Cg && last_out.size() == sizeof(vgpu_cg_result)) {
+        vgpu_cg_result r;
+        std::memcpy(&r, last_out.data(), sizeof r);
+        const double want = vgpu::npb::cg_class(sizes.cg_class).zeta_verify;
+        const bool verified = std::fabs(r.zeta - want) / want <= 1e-10;
+        char buf[160];
+        std::snprintf(buf, sizeof buf, ", \"cg\": {\"zeta\": %.15g, \"rnorm\": %.6g, \"verified\": %s}",
+                      r.zeta, r.rnorm, verified ? "true" : "false");
+        cg_json = buf;
+        if (!verified && ok) {
+            ok = false;
+            err = "nas-cg zeta differs from NPB's";
+        }
     }
     std::ostringstream os;
     os << "{\"worker\": " << worker << ", \"ok\": " << (ok ? "true" : "false")
@@ -222,22 +256,7 @@ int main(int argc, char** argv) {
         std::sort(v.begin(), v.end());
         os << (k ? ", " : "") << "\"" << names[k] << "\": " << (v.empty() ? 0 : v[v.size() / 2]);
     }
-    os << "}";
-    if (job.kind == vgpu::wl::Kind::Cg && last_out.size() == sizeof(vgpu_cg_result)) {
-        // NPB's own verification: zeta within 1e-10 of the published value
-        vgpu_cg_result r;
-        std::memcpy(&r, last_out.data(), sizeof r);
-        const double want = vgpu::npb::cg_class(sizes.cg_class).zeta_verify;
-        const bool verified = std::fabs(r.zeta - want) / want <= 1e-10;
-        char buf[160];
-        std::snprintf(buf, sizeof buf, ", \"cg\": {\"zeta\": %.15g, \"rnorm\": %.6g, \"verified\": %s}",
-                      r.zeta, r.rnorm, verified ? "true" : "false");
-        os << buf;
-        if (!verified && ok) {
-            ok = false;
-            err = "nas-cg zeta differs from NPB's";
-        }
-    }
+    os << "}" << cg_json << check_json;
     if (job.kind == vgpu::wl::Kind::Ep && last_out.size() == sizeof(vgpu_ep_result)) {
         // the job's partial for the final reduction, bit patterns in hex
         vgpu_ep_result r;

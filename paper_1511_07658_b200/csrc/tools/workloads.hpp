@@ -24,6 +24,7 @@
 //           iterations"), atoms ~ U(box), q ~ U[-1,1], seed 777+w.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -241,6 +242,83 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
         }
     }
     return j;
+}
+
+// ---- the SPMD program's own result check (sampled, binary64) -------------
+//
+// What a worker verifies about its result after the timed rounds, the way
+// NPB programs verify themselves: Black-Scholes prices of every `stride`-th
+// option recomputed in binary64 with the SDK formulation (polynomial CND,
+// R = 0.02, V = 0.30), L1-relative over the sample; SGEMM rows i = 0,
+// stride, 2 stride, ... of C recomputed with binary64 accumulation,
+// relative Frobenius over those rows. Tolerances are the GPU parity bars
+// (BS 1e-6, SGEMM 1e-5).
+struct SampleCheck {
+    bool ok = true;
+    double err = 0.0;        // L1-relative (BS) / relative Frobenius (SGEMM)
+    std::uint64_t samples = 0;
+};
+
+inline double bs_cnd64(double d) {
+    const double k = 1.0 / (1.0 + 0.2316419 * std::fabs(d));
+    const double poly =
+        k * (0.31938153 + k * (-0.356563782 + k * (1.781477937 + k * (-1.821255978 + k * 1.330274429))));
+    const double c = 0.39894228040143267793994605993438 * std::exp(-0.5 * d * d) * poly;
+    return d > 0.0 ? 1.0 - c : c;
+}
+
+inline SampleCheck check_bs_sample(const Bytes& in, const Bytes& out, std::uint64_t stride) {
+    SampleCheck r;
+    const std::uint64_t n = in.size() / 12;
+    if (out.size() != 8 * n || n == 0) return {false, 1.0, 0};
+    const float* S = reinterpret_cast<const float*>(in.data());
+    const float* call = reinterpret_cast<const float*>(out.data());
+    const double R = VGPU_BS_RISKFREE, V = VGPU_BS_VOLATILITY;
+    double num = 0.0, den = 0.0;
+    for (std::uint64_t i = 0; i < n; i += stride) {
+        const double s = S[i], x = S[n + i], t = S[2 * n + i];
+        const double vt = V * std::sqrt(t);
+        const double d1 = (std::log(s / x) + (R + 0.5 * V * V) * t) / vt, d2 = d1 - vt;
+        const double disc = x * std::exp(-R * t);
+        const double c = s * bs_cnd64(d1) - disc * bs_cnd64(d2);
+        const double p = disc * (1.0 - bs_cnd64(d2)) - s * (1.0 - bs_cnd64(d1));
+        num += std::fabs(call[i] - c) + std::fabs(call[n + i] - p);
+        den += std::fabs(c) + std::fabs(p);
+        ++r.samples;
+    }
+    r.err = den > 0.0 ? num / den : 0.0;
+    r.ok = r.err <= 1e-6;
+    return r;
+}
+
+inline SampleCheck check_mm_sample(const Bytes& in, const Bytes& out, std::uint64_t row_stride) {
+    SampleCheck r;
+    const std::uint64_t nn = in.size() / 8;
+    std::uint64_t n = static_cast<std::uint64_t>(std::sqrt(static_cast<double>(nn)));
+    while (n * n > nn) --n;
+    if (n == 0 || n * n != nn || out.size() != 4 * nn) return {false, 1.0, 0};
+    const float* A = reinterpret_cast<const float*>(in.data());
+    const float* B = A + nn;
+    const float* C = reinterpret_cast<const float*>(out.data());
+    std::vector<double> row(n);
+    double num = 0.0, den = 0.0;
+    for (std::uint64_t i = 0; i < n; i += row_stride) {
+        std::fill(row.begin(), row.end(), 0.0);
+        for (std::uint64_t k = 0; k < n; ++k) {
+            const double a = A[i * n + k];
+            const float* b = B + k * n;
+            for (std::uint64_t j = 0; j < n; ++j) row[j] += a * b[j];
+        }
+        for (std::uint64_t j = 0; j < n; ++j) {
+            const double dlt = C[i * n + j] - row[j];
+            num += dlt * dlt;
+            den += row[j] * row[j];
+        }
+        r.samples += n;
+    }
+    r.err = den > 0.0 ? std::sqrt(num / den) : 0.0;
+    r.ok = r.err <= 1e-5;
+    return r;
 }
 
 // Largest region any worker of `workload` needs.
