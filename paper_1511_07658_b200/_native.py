@@ -106,6 +106,7 @@ CUDA_API = {
     "vgpu_cu_free_pinned": (None, [_P, _P]),
     "vgpu_cu_payload": (C.c_int, [C.c_char_p, C.POINTER(_U32)]),
     "vgpu_cu_output_size": (C.c_int, [_U32, _P, _U64, C.POINTER(_U64)]),
+    "vgpu_cu_task_check": (C.c_int, [_P, _U32, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_upload": (C.c_int, [_P, _U32, _P, _U64, _U64]),
     "vgpu_cu_submit_batch": (C.c_int, [_P, C.c_int, _P, _U32, C.POINTER(_U64)]),
     "vgpu_cu_poll": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
