@@ -11,6 +11,9 @@
  *   vgpu_client_req        req(instance)                  client.hpp:69   (client.cpp:146-153)
  *   vgpu_client_snd/str/stp/stp_wait/rcv/rls/run_task
  *                          VgpuHandle::snd .. run_task    client.hpp:41-48 (client.cpp:71-142)
+ *   vgpu_client_region/snd_region/rcv_region/run_task_region
+ *                          B200 in-place data plane (no reference counterpart;
+ *                          same frames as snd/rcv, client.cpp:71-80, :116-127)
  *   vgpu_native_run_task   NativeVgpu::run_task           client.hpp:101  (client.cpp:250-256)
  * Status: 0 ok; 1..8 = vgpu::ErrCode (NACK codes verbatim); VGPU_E_* below.
  * The detail string of the last failure on this thread: vgpu_last_error().
@@ -114,6 +117,15 @@ int vgpu_client_rcv(vgpu_client* c, void* out, uint64_t cap, uint64_t* len);
 int vgpu_client_rls(vgpu_client* c);
 int vgpu_client_run_task(vgpu_client* c, const void* in, uint64_t in_bytes,
                          const vgpu_descriptor* d, void* out, uint64_t cap, uint64_t* len);
+/* In-place data plane (B200 extension, VgpuHandle::region / snd_region /
+ * rcv_region / run_task_region): the leased region, page-locked by the GVM,
+ * holds the input the caller wrote there and, after RCV, the result (a view:
+ * valid until the next SND or RLS; it overwrites the region from offset 0). */
+int vgpu_client_region(vgpu_client* c, void** base, uint64_t* bytes);
+int vgpu_client_snd_region(vgpu_client* c, uint64_t bytes);
+int vgpu_client_rcv_region(vgpu_client* c, const void** data, uint64_t* len);
+int vgpu_client_run_task_region(vgpu_client* c, uint64_t in_bytes, const vgpu_descriptor* d,
+                                const void** data, uint64_t* len);
 
 /* Non-virtualized baseline: this process's own CUDA context. */
 int vgpu_native_run_task(int cuda_device, const vgpu_descriptor* d, const void* in,

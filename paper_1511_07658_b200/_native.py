@@ -148,6 +148,11 @@ HOST_API = {
     "vgpu_client_stp": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "vgpu_client_stp_wait": (C.c_int, [_P]),
     "vgpu_client_rcv": (C.c_int, [_P, _P, _U64, C.POINTER(_U64)]),
+    "vgpu_client_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64)]),
+    "vgpu_client_snd_region": (C.c_int, [_P, _U64]),
+    "vgpu_client_rcv_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64)]),
+    "vgpu_client_run_task_region": (C.c_int, [_P, _U64, C.POINTER(DescriptorC), C.POINTER(_P),
+                                              C.POINTER(_U64)]),
     "vgpu_client_rls": (C.c_int, [_P]),
     "vgpu_client_run_task": (C.c_int, [_P, _P, _U64, C.POINTER(DescriptorC), _P, _U64,
                                        C.POINTER(_U64)]),

@@ -259,6 +259,39 @@ int vgpu_client_run_task(vgpu_client* c, const void* in, uint64_t in_bytes,
     });
 }
 
+int vgpu_client_region(vgpu_client* c, void** base, uint64_t* bytes) {
+    if (!c || !base || !bytes) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto r = c->handle.region();
+        *base = r.data();
+        *bytes = r.size();
+    });
+}
+
+int vgpu_client_snd_region(vgpu_client* c, uint64_t bytes) {
+    if (!c) return VGPU_E_INVALID;
+    return guarded([&] { c->handle.snd_region(bytes); });
+}
+
+int vgpu_client_rcv_region(vgpu_client* c, const void** data, uint64_t* len) {
+    if (!c || !data || !len) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto r = c->handle.rcv_region();
+        *data = r.data();
+        *len = r.size();
+    });
+}
+
+int vgpu_client_run_task_region(vgpu_client* c, uint64_t in_bytes, const vgpu_descriptor* d,
+                                const void** data, uint64_t* len) {
+    if (!c || !data || !len) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto r = c->handle.run_task_region(in_bytes, to_desc(d));
+        *data = r.data();
+        *len = r.size();
+    });
+}
+
 int vgpu_native_run_task(int cuda_device, const vgpu_descriptor* d, const void* in,
                          uint64_t in_bytes, void* out, uint64_t cap, uint64_t* len) {
     if (!len || (!in && in_bytes)) return VGPU_E_INVALID;

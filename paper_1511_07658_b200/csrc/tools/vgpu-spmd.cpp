@@ -2,7 +2,11 @@
 // reference harness, proj/src/bench/bench.cpp:186-231).
 //
 //   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul
-//             --rounds R [--instance NAME | --native [--device D]]
+//             --rounds R [--instance NAME [--inplace] | --native [--device D]]
+//
+// --inplace: the in-place data plane (VgpuHandle::region / snd_region /
+// rcv_region): every round the program writes its input into the leased,
+// page-locked region and reads the result where the D2H left it.
 //
 // Builds its private input, leases a VGPU (retrying until the daemon is
 // up) — or, with --native, uses its OWN CUDA context through NativeVgpu —
@@ -15,6 +19,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <span>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -40,7 +45,8 @@ std::int64_t now_ns() {
 // stride 1 checks every element; inside the timed loop a sparse stride keeps
 // the check cheap and identical for both modes; the full check runs after.
 // (vector-mul: mul = true, out = a * b)
-bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out, std::size_t stride, bool mul = false) {
+bool check_vecadd(std::span<const std::uint8_t> in, std::span<const std::uint8_t> out, std::size_t stride,
+                  bool mul = false) {
     const std::size_t n = in.size() / 8;
     if (out.size() != 4 * n) return false;
     const float* a = reinterpret_cast<const float*>(in.data());
@@ -52,7 +58,7 @@ bool check_vecadd(const vgpu::Bytes& in, const vgpu::Bytes& out, std::size_t str
     return n == 0 || o[n - 1] == want(n - 1);
 }
 
-std::uint64_t sample_hash(const vgpu::Bytes& out, std::size_t stride) {
+std::uint64_t sample_hash(std::span<const std::uint8_t> out, std::size_t stride) {
     std::uint64_t h = 0x9E3779B97F4A7C15ull ^ out.size();
     const std::size_t words = out.size() / 8;
     for (std::size_t i = 0; i < words; i += stride) {
@@ -68,7 +74,7 @@ std::uint64_t sample_hash(const vgpu::Bytes& out, std::size_t stride) {
 int main(int argc, char** argv) {
     std::string instance, workload = "vecadd";
     std::uint32_t worker = 0, workers = 1, rounds = 1;
-    bool native = false, connect_after_go = false;
+    bool native = false, connect_after_go = false, inplace = false;
     int device = 0;
     vgpu::wl::Sizes sizes;
     for (int i = 1; i < argc; ++i) {
@@ -84,6 +90,7 @@ int main(int argc, char** argv) {
             else if (a == "--workload") workload = val();
             else if (a == "--rounds") rounds = std::stoul(val());
             else if (a == "--native") native = true;
+            else if (a == "--inplace") inplace = true;
             else if (a == "--connect-after-go") connect_after_go = true;
             else if (a == "--device") device = std::stoi(val());
             else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(val());
@@ -155,16 +162,31 @@ int main(int argc, char** argv) {
         for (std::uint32_t r = 0; r < rounds; ++r) {
             t0[r] = now_ns();
             vgpu::Bytes out;
+            std::span<const std::uint8_t> view;
             if (native) {
                 out = nh->run_task(job.input, job.desc);
+                view = out;
             } else {  // run_task, verb by verb so each stage is timed
-                vh->snd(job.input);
+                if (inplace) {
+                    // the program produces its input in the page-locked
+                    // region (inside the timed round), then SND without a copy
+                    const auto reg = vh->region();
+                    vgpu::copy_into_region(reg, job.input);
+                    vh->snd_region(job.input.size());
+                } else {
+                    vh->snd(job.input);
+                }
                 const std::int64_t a = now_ns();
                 vh->str(job.desc);
                 const std::int64_t b = now_ns();
                 vh->stp_wait();
                 const std::int64_t c = now_ns();
-                out = vh->rcv();
+                if (inplace) {
+                    view = vh->rcv_region();  // consumed in place: no copy out
+                } else {
+                    out = vh->rcv();
+                    view = out;
+                }
                 st_snd[r] = a - t0[r];
                 st_str[r] = b - a;
                 st_stp[r] = c - b;
@@ -172,24 +194,24 @@ int main(int argc, char** argv) {
             }
             t1[r] = now_ns();
             constexpr std::size_t kStride = 257;
-            if (out.size() != job.output_bytes) {
+            if (view.size() != job.output_bytes) {
                 ok = false;
                 err = "wrong result size";
             } else if (job.kind == vgpu::wl::Kind::VecAdd || job.kind == vgpu::wl::Kind::VecMul) {
-                if (!check_vecadd(job.input, out, kStride, job.kind == vgpu::wl::Kind::VecMul)) {
+                if (!check_vecadd(job.input, view, kStride, job.kind == vgpu::wl::Kind::VecMul)) {
                     ok = false;
                     err = "vector-add/mul results differ";
                 }
             } else {
-                const std::uint64_t h = sample_hash(out, kStride);
+                const std::uint64_t h = sample_hash(view, kStride);
                 if (r == 0) first_sum = h;
                 if (h != first_sum) {
                     ok = false;
                     err = "result changed between rounds";
                 }
             }
-            if (r == 0) first_out = out;
-            if (r + 1 == rounds) last_out = std::move(out);
+            if (r == 0) first_out.assign(view.begin(), view.end());
+            if (r + 1 == rounds) last_out.assign(view.begin(), view.end());
         }
         if (vh) vh->rls();
         // full checks outside the timed loop

@@ -262,6 +262,34 @@ class VgpuHandle:
                                                  C.byref(got)))
         return bytes(out[: got.value])
 
+    # ---- in-place data plane (VgpuHandle::region / snd_region / rcv_region) ----
+
+    def region(self) -> memoryview:
+        """The leased region itself (page-locked by the GVM), writable."""
+        base, n = C.c_void_p(), C.c_uint64()
+        _check(_libs().host.vgpu_client_region(self._h, C.byref(base), C.byref(n)))
+        return memoryview((C.c_uint8 * n.value).from_address(base.value)).cast("B")
+
+    def snd_region(self, nbytes: int) -> None:
+        _check(_libs().host.vgpu_client_snd_region(self._h, nbytes))
+
+    def rcv_region(self) -> memoryview:
+        """The result in place (valid until the next SND or RLS)."""
+        p, n = C.c_void_p(), C.c_uint64()
+        _check(_libs().host.vgpu_client_rcv_region(self._h, C.byref(p), C.byref(n)))
+        if n.value == 0:
+            return memoryview(b"")
+        return memoryview((C.c_uint8 * n.value).from_address(p.value)).cast("B").toreadonly()
+
+    def run_task_region(self, nbytes: int, task: KernelDescriptor) -> memoryview:
+        p, n = C.c_void_p(), C.c_uint64()
+        d = task.to_c()
+        _check(_libs().host.vgpu_client_run_task_region(self._h, nbytes, C.byref(d), C.byref(p),
+                                                        C.byref(n)))
+        if n.value == 0:
+            return memoryview(b"")
+        return memoryview((C.c_uint8 * n.value).from_address(p.value)).cast("B").toreadonly()
+
 
 def req(instance: str = "") -> VgpuHandle:
     """Lease a VGPU (client.hpp:69; $VGPU_INSTANCE, else "default")."""
