@@ -4,7 +4,7 @@
 Each CSV is `ncu -i <capture>.ncu-rep --page raw --csv --metrics
 dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum` of ONE
 `ncu --set full --clock-control none` capture of the kind's dominant kernel,
-launched at bench.py's per-step shape (scripts/gpu_check*.sh). bench.py
+launched at bench.py's per-step shape (scripts/gpu_profiles.sh). bench.py
 reports read+write as roofline.traffic (bytes per launch)."""
 import csv
 import glob
