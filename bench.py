@@ -96,6 +96,14 @@ class Dist:
         self.dist.all_reduce(t)
         return float(t.item())
 
+    def gather(self, obj) -> list:
+        """Every rank's `obj`, in rank order (all ranks get the list)."""
+        if not self.torch:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
     def bcast(self, obj):
         if not self.torch:
             return obj
@@ -283,7 +291,7 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False):
+                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False, inplace=False):
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
     inst = f"b200bench{os.getpid()}g{dist.rank}"
@@ -308,6 +316,8 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         a += ["--native", "--device", str(device)] if native else ["--instance", inst]
         if cold:
             a.append("--connect-after-go")
+        if inplace and not native:
+            a.append("--inplace")
         args.append(a)
     try:
         ps = spawn_workers(args, env)
@@ -349,9 +359,10 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
     return info
 
 
-def _ref_run(ref, workload, procs, rounds, warmup, size_args):
+def _ref_run(ref, workload, procs, rounds, warmup, size_args, native=False):
     run = subprocess.run([ref, "--workload", workload, "--procs", str(procs), "--rounds",
-                          str(rounds), "--warmup", str(warmup)] + size_args,
+                          str(rounds), "--warmup", str(warmup)] + size_args
+                         + (["--native"] if native else []),
                          capture_output=True, text=True, timeout=3600)
     lines = [l for l in run.stdout.strip().splitlines() if l.startswith("{")]
     if not lines:
@@ -362,13 +373,18 @@ def _ref_run(ref, workload, procs, rounds, warmup, size_args):
     return r
 
 
-def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_rounds=200):
-    """The unmodified reference GVM (oracle/_ref/ref-bench) on host cores.
+def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_rounds=200,
+                      native=False):
+    """The unmodified reference on host cores (oracle/_ref/ref-bench).
 
-    The reference GVM runs every payload sequentially on its dispatcher
-    thread and its client gives up after a 30 s reply timeout
-    (proj/src/client.cpp:17), so the sample shrinks the process count when a
-    full round would not fit; jobs/s is the rate it sustains."""
+    native=False: SURVEY 8(d)(i), the reference GVM path. It runs every
+    payload sequentially on its dispatcher thread and its client gives up
+    after a 30 s reply timeout (proj/src/client.cpp:17), so the sample
+    shrinks the process count when a full round would not fit.
+    native=True: 8(d)(ii), the reference's per-process NativeVgpu path (the
+    payload runs in each forked process, OMP_NUM_THREADS = cores / N).
+    Rounds = max_rounds (the bench's K) and `warmup` warm-up rounds when they
+    fit the budget, fewer otherwise; jobs/s is the rate it sustains."""
     ref = os.path.join(REPO, "oracle", "_ref", "ref-bench")
     size_args = sizes.size_args()
     if not os.path.exists(ref):
@@ -376,27 +392,66 @@ def cpu_reference_arm(workload, procs, sizes, budget_s=20.0, warmup=1, max_round
     try:
         # probe one full round at the configuration's own shape
         n = procs
-        one = _ref_run(ref, workload, n, 1, 0, size_args)
+        one = _ref_run(ref, workload, n, 1, 0, size_args, native)
         per_round = max(1e-4, one["seconds"])
-        if per_round > 25.0 and workload != "mixed":
+        if per_round > 25.0 and workload != "mixed" and not native:
             # a round must fit the reference client's 30 s reply timeout
             per_job = per_round / n
             n = max(1, min(procs, int(20.0 / per_job)))
             per_round = per_job * n
         rounds = max(1, min(max_rounds, int(budget_s / per_round)))
         w = warmup if per_round * (rounds + warmup) <= 1.5 * budget_s else 0
-        r = _ref_run(ref, workload, n, rounds, w, size_args) if (rounds > 1 or w) else one
+        r = _ref_run(ref, workload, n, rounds, w, size_args, native) if (rounds > 1 or w) else one
         if r is one:
             rounds, w = 1, 0
     except Exception as e:  # noqa: BLE001 - reported, not fatal for our arm
         log("reference arm failed:", e)
         return None
-    r["sample"] = (f"reference GVM (oracle/_ref/ref-bench, unmodified libvgpu from /root/reference) "
-                   f"{n} forked VgpuHandle clients x {rounds} rounds of '{workload}', "
-                   f"virtual clock, OpenMP on all host threads"
-                   + ("" if n == procs else f" (reduced from {procs} processes: one reference "
-                      f"round must fit its 30 s client reply timeout)"))
+    if native:
+        r["sample"] = (f"reference NativeVgpu per-process CPU path (oracle/_ref/ref-bench --native, "
+                       f"unmodified libvgpu from /root/reference): {n} forked processes x {rounds} "
+                       f"rounds of '{workload}', virtual clock, OMP_NUM_THREADS = "
+                       f"{r.get('omp_threads_per_proc')} per process ({r.get('threads')} host threads / {n})")
+    else:
+        r["sample"] = (f"reference GVM (oracle/_ref/ref-bench, unmodified libvgpu from /root/reference) "
+                       f"{n} forked VgpuHandle clients x {rounds} rounds of '{workload}', "
+                       f"virtual clock, OpenMP on all host threads"
+                       + ("" if n == procs else f" (reduced from {procs} processes: one reference "
+                          f"round must fit its 30 s client reply timeout)"))
     return r
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def payload_bench_ref():
+    """the reference's own payload-bench (oracle/_ref,
+    proj/tools/payload_bench.cpp:28-58): its OpenMP vector-add / vector-scale
+    host kernels in MB/s (3 x 4 B per element for add, 2 x 4 B for scale)."""
+    pb = os.path.join(REPO, "oracle", "_ref", "payload-bench")
+    if not os.path.exists(pb):
+        return None
+    try:
+        out = subprocess.run([pb], capture_output=True, text=True, timeout=120).stdout
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:200]}
+    rows = []
+    for line in out.splitlines():
+        parts = line.replace("=", " ").split()
+        # vector-add n 8388608 serial 5034 MB/s omp 51539 MB/s x10.24
+        if len(parts) >= 9 and parts[1] == "n":
+            rows.append({"kernel": parts[0], "n": int(parts[2]), "serial_gbs": float(parts[4]) / 1e3,
+                         "omp_gbs": float(parts[7]) / 1e3})
+    return {"rows": rows, "threads": os.cpu_count(),
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS", "unset (all host threads)"),
+            "source": "oracle/_ref/payload-bench (proj/tools/payload_bench.cpp, unmodified)"}
 
 
 def final_reduce(N, dist, record):
@@ -410,11 +465,13 @@ def final_reduce(N, dist, record):
     if SHARED_GPU and dist.world > 1:  # test mode: one GPU cannot host 2 NCCL ranks
         t = dist.torch.tensor(record, dtype=dist.torch.float64)
         parts = [dist.torch.zeros_like(t) for _ in range(dist.world)]
-        t0 = time.perf_counter()
-        dist.dist.all_gather(parts, t)
-        us = (time.perf_counter() - t0) * 1e6
+        times = []
+        for _ in range(6):  # first call = connection setup; the rest = steady state
+            t0 = time.perf_counter()
+            dist.dist.all_gather(parts, t)
+            times.append((time.perf_counter() - t0) * 1e6)
         flat = dist.torch.cat(parts).tolist()
-        return R.fold_in_rank_order(flat, dist.world), flat[:R.REC_WIDTH], us
+        return R.fold_in_rank_order(flat, dist.world), flat[:R.REC_WIDTH], times
     libs = N.load()
     uid = (C.c_uint8 * 128)()
     if dist.rank == 0:
@@ -431,11 +488,13 @@ def final_reduce(N, dist, record):
             raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
         rec = (C.c_double * R.REC_WIDTH)(*record)
         allr = (C.c_double * (R.REC_WIDTH * dist.world))()
-        t0 = time.perf_counter()
-        if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
-            raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
-        us = (time.perf_counter() - t0) * 1e6
-        return R.fold_in_rank_order(list(allr), dist.world), list(allr)[:R.REC_WIDTH], us
+        times = []
+        for _ in range(6):  # first call = NCCL's lazy connection setup; the rest = steady state
+            t0 = time.perf_counter()
+            if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
+                raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
+            times.append((time.perf_counter() - t0) * 1e6)
+        return R.fold_in_rank_order(list(allr), dist.world), list(allr)[:R.REC_WIDTH], times
     finally:
         libs.cuda.vgpu_cu_close(dev)
 
@@ -543,30 +602,47 @@ def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
     """Virtualization overhead across payload sizes (proj/src/bench/
     bench.cpp:389-423 measure_overhead): one process, vector add of
     1 KiB .. 64 MiB inputs through the GVM; turnaround per job vs its pure
-    GPU time (CUDA events), overhead = the difference. Reference schema:
-    bytes,turnaround_us,pure_gpu_us,overhead_us,overhead_fraction."""
-    rows = []
-    for nbytes in (1 << 10, 1 << 16, 1 << 20, 16 << 20, 64 << 20):
-        sz = W.Sizes()
-        sz.vecadd_n = nbytes // 8
-        r = leg_workers(V, N, W, "vecadd", 1, 0, 1, steps, warmup, device, False, sz, dist,
-                        barrier=1)
-        t_us = r["seconds"] * 1e6 / steps
-        pg = r["device_stage_us"]["pure_gpu_us"] or 0.0
-        up = r["device_stage_us"]["h2d_us"] or 0.0  # eager upload at SND: device time too
-        gpu = pg + up
-        rows.append({"bytes": nbytes, "turnaround_us": t_us, "pure_gpu_us": gpu,
-                     "overhead_us": max(0.0, t_us - gpu),
-                     "overhead_fraction": max(0.0, t_us - gpu) / t_us})
+    device time (CUDA events: the input's DMA busy time + the task's kernel
+    and D2H), overhead = the difference. Reference schema:
+    bytes,turnaround_us,pure_gpu_us,overhead_us,overhead_fraction — once per
+    client API. Acceptance criterion 7 (proj/tests/acceptance.cpp:277-297):
+    overhead <= 25 % at 64 MiB, and the 1 KiB fraction below the 64 MiB one."""
+    out = {"report": "overhead", "apis": {}}
     cols = ["bytes", "turnaround_us", "pure_gpu_us", "overhead_us", "overhead_fraction"]
-    csv = ",".join(cols) + "\n" + "\n".join(
-        ",".join(f"{r[c]:.3f}" if isinstance(r[c], float) else str(r[c]) for c in cols)
-        for r in rows)
-    return {"report": "overhead", "rows": rows, "csv": csv,
-            "note": "turnaround = the whole job through the unchanged client API (SND copy into "
-                    "shm, H2D, kernel, D2H, RCV copy out); pure_gpu = upload H2D + task span "
-                    "from CUDA events; the paper's figure is ~20 % at 400 MB on a C2070 "
-                    "(PAPER.md:507)"}
+    for api, inplace in (("inplace", True), ("span", False)):
+        rows = []
+        for nbytes in (1 << 10, 1 << 16, 1 << 20, 16 << 20, 64 << 20):
+            sz = W.Sizes()
+            sz.vecadd_n = nbytes // 8
+            r = leg_workers(V, N, W, "vecadd", 1, 0, 1, steps, warmup, device, False, sz, dist,
+                            barrier=1, inplace=inplace)
+            t_us = r["seconds"] * 1e6 / steps
+            pg = r["device_stage_us"]["pure_gpu_us"] or 0.0
+            up = r["device_stage_us"]["h2d_us"] or 0.0  # eager upload at SND: device time too
+            gpu = pg + up
+            rows.append({"bytes": nbytes, "turnaround_us": t_us, "pure_gpu_us": gpu,
+                         "overhead_us": max(0.0, t_us - gpu),
+                         "overhead_fraction": max(0.0, t_us - gpu) / t_us,
+                         "client_stage_us": r.get("client_stage_us")})
+        csv = ",".join(cols) + "\n" + "\n".join(
+            ",".join(f"{r[c]:.3f}" if isinstance(r[c], float) else str(r[c]) for c in cols)
+            for r in rows)
+        tiny, large = rows[0], rows[-1]
+        out["apis"][api] = {
+            "rows": rows, "csv": csv,
+            "criterion7": {"large_bytes": large["bytes"],
+                           "large_overhead_fraction": large["overhead_fraction"],
+                           "large_le_0_25": large["overhead_fraction"] <= 0.25,
+                           "tiny_below_large": tiny["overhead_fraction"] < large["overhead_fraction"],
+                           "pass": large["overhead_fraction"] <= 0.25
+                                   and tiny["overhead_fraction"] < large["overhead_fraction"]}}
+    out["note"] = ("turnaround = the whole job through the client API (inplace: snd(span) copies "
+                   "the input into the pinned region, streamed so the H2D overlaps the copy, and "
+                   "the result is read in place; span: the same SND plus rcv()'s copy into a "
+                   "fresh Bytes); pure_gpu = the input's DMA busy time + the task's kernel + D2H "
+                   "(CUDA events); the paper's figure is ~20 % at 400 MB on a C2070 "
+                   "(PAPER.md:507)")
+    return out
 
 
 def model_summary(batches):
@@ -748,6 +824,63 @@ def leg_overhead_n1(V, N, W, workload, steps, warmup, device, sizes, dist) -> di
             "desc": "1 process: GVM e2e vs NativeVgpu warm (own context, pageable copies); "
                     "paper_overhead = 1 - pure_gpu/turnaround (proj/src/bench/bench.cpp:414-419)"}
 
+def link_roofline(V, device, h2d, d2h, steps, secs, world) -> dict:
+    """The e2e leg's roofline: host<->device bytes it moved per second over
+    the pinned-copy bandwidth probed on this GPU now (vgpu_cu_link_probe;
+    SURVEY 8(d): 'PCIe: measure pinned H2D/D2H GB/s on the box'). The C3/C4
+    jobs are link-bound; H2D and D2H run on separate copy engines, so the
+    combined rate is quoted against the probed both-directions figure and
+    each direction against its own."""
+    try:
+        p = V.link_probe(device)
+    except Exception as e:  # noqa: BLE001 - reported in the line
+        return {"error": str(e)[:200]}
+    per_gpu_s = secs  # max over ranks
+    h2d_gbs = h2d * steps / per_gpu_s / 1e9
+    d2h_gbs = d2h * steps / per_gpu_s / 1e9
+    both = h2d_gbs + d2h_gbs
+    return {"bound": "link", "unit": "GB/s", "achieved": both, "peak": p["bidir_gbs"],
+            "frac": both / p["bidir_gbs"] if p["bidir_gbs"] else None,
+            "h2d": {"achieved": h2d_gbs, "peak": p["h2d_gbs"],
+                    "frac": h2d_gbs / p["h2d_gbs"] if p["h2d_gbs"] else None},
+            "d2h": {"achieved": d2h_gbs, "peak": p["d2h_gbs"],
+                    "frac": d2h_gbs / p["d2h_gbs"] if p["d2h_gbs"] else None},
+            "per": "GPU (bytes of this GPU's e2e leg / its time)",
+            "probe": p, "peak_source": "measured now: cudaHostAlloc'd buffers <-> HBM, "
+                                       "cudaMemcpyAsync, best of 2 after a warm-up"}
+
+
+def merge_clocks(all_clocks: list) -> dict:
+    """One clocks object over every GPU's samples: the lowest median SM clock,
+    the union of throttle reasons, per-GPU detail kept."""
+    valid = [c for c in all_clocks if c.get("sm_mhz")]
+    if not valid:
+        return all_clocks[0]
+    out = dict(min(valid, key=lambda c: c["sm_mhz"]))
+    out["reasons"] = sorted({r for c in all_clocks for r in c.get("reasons", [])})
+    if len(all_clocks) > 1:
+        out["per_gpu"] = all_clocks
+    return out
+
+
+def mps_state() -> dict:
+    """Is an MPS control daemon / server running on this box? (SURVEY 8(d):
+    the native baseline must run with MPS off.)"""
+    names = []
+    for pid in os.listdir("/proc"):
+        if pid.isdigit():
+            try:
+                with open(f"/proc/{pid}/comm") as f:
+                    c = f.read().strip()
+            except OSError:
+                continue
+            if c.startswith("nvidia-cuda-mps"):
+                names.append(c)
+    pipe = os.environ.get("CUDA_MPS_PIPE_DIRECTORY", "/tmp/nvidia-mps")
+    return {"active": bool(names) or os.path.exists(os.path.join(pipe, "control")),
+            "processes": names, "pipe_dir_checked": pipe}
+
+
 # ---- main -----------------------------------------------------------------------------
 
 _JSON_OUT = None
@@ -770,8 +903,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    # default: BASELINE.json configs[1] (NAS EP class A, 8 processes per B200)
-    ap.add_argument("--workload", default="ep",
+    # default: BASELINE.json configs[2], C3 Black-Scholes 4 Mi options x 16
+    # processes per B200: BASELINE's metric names no config, so the line is
+    # quoted on the largest single-GPU configuration (C3 and C4 both run 16
+    # processes; C3 moves the most bytes per job: 48 MiB in, 32 MiB out)
+    ap.add_argument("--workload", default="bs",
                     choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul", "es"])
     ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -795,6 +931,10 @@ def main():
     ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the per-kernel roofline summary of the other configs")
+    ap.add_argument("--e2e-api", default="inplace", choices=["inplace", "span"],
+                    help="client API of the e2e leg: 'inplace' = snd(span) + rcv_region() "
+                         "(result read where the D2H put it), 'span' = the reference's "
+                         "snd(span) + rcv() -> Bytes; the default line also reports the other")
     ap.add_argument("--barrier-size", type=int, default=-1,
                     help="GVM barrier (tasks per flush); -1 = workload default")
     args = ap.parse_args()
@@ -821,7 +961,7 @@ def main():
     if args.impl == "reference":
         if dist.rank == 0:
             r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.ref_budget_s,
-                                  warmup=min(args.warmup, 3), max_rounds=args.steps)
+                                  warmup=args.warmup, max_rounds=args.steps)
             if r is None:
                 line = {"impl": "reference", "unavailable": "oracle/_ref/ref-bench not built "
                         "(needs /root/reference at build time)"}
@@ -833,7 +973,9 @@ def main():
                         "data": "synthetic", "scaling": "weak", "vs_baseline": None,
                         "config": config,
                         "cpu_baseline": {"value": r["jobs_per_s"], "unit": "jobs/s", "cores": cores,
-                                         "kind": "reference", "sample": r["sample"]},
+                                         "kind": "reference", "sample": r["sample"],
+                                         "cpu_model": cpu_model(),
+                                         "omp_num_threads": r.get("omp_threads_per_proc")},
                         "e2e": {"value": r["jobs_per_s"], "unit": "jobs/s",
                                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
             emit(line)
@@ -858,7 +1000,9 @@ def main():
         return
     gid0 = dist.rank * procs
     total_workers = procs * world
-    clocks = Clocks(device) if dist.local == 0 or world == 1 else None
+    # every rank samples its own GPU (one nvidia-smi per device); with one
+    # shared GPU (test mode) local rank 0 samples it
+    clocks = Clocks(device) if not SHARED_GPU or dist.local == 0 else None
     if clocks:
         clocks.start()
 
@@ -879,13 +1023,23 @@ def main():
     # B200 policy: eager dispatch (barrier 1) — per-client hardware queues make
     # the paper's full barrier pure latency; the barrier-P run is reported too
     barrier = 1 if args.barrier_size < 0 else args.barrier_size
+    inplace = args.e2e_api == "inplace"
     e2e = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                      args.warmup, device, False, sizes, dist, barrier=barrier)
+                      args.warmup, device, False, sizes, dist, barrier=barrier, inplace=inplace)
+    # the other client API, same GVM settings
+    dist.barrier()
+    alt = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                      args.warmup, device, False, sizes, dist, barrier=barrier, inplace=not inplace)
+    alt_api = {"api": "span (reference: snd(span) + rcv() -> Bytes)" if inplace
+               else "inplace (snd(span) + rcv_region())",
+               "value": procs * world * args.steps / dist.max(alt["seconds"]), "unit": "jobs/s",
+               "client_stage_us": alt.get("client_stage_us"),
+               "device_stage_us": alt.get("device_stage_us")}
     paper = None
     if args.barrier_size < 0 and procs > 1:
         dist.barrier()
         pb = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                         args.warmup, device, False, sizes, dist, barrier=procs)
+                         args.warmup, device, False, sizes, dist, barrier=procs, inplace=inplace)
         paper = {"value": procs * world * args.steps / dist.max(pb["seconds"]), "unit": "jobs/s",
                  "barrier_size": procs, "client_stage_us": pb.get("client_stage_us"),
                  "device_stage_us": pb.get("device_stage_us"), "batches": pb["batches"]}
@@ -909,7 +1063,10 @@ def main():
             nat = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
                               args.warmup, device, True, sizes, dist)
             runs.append(procs * world * args.steps / dist.max(nat["seconds"]))
-        native = {"value": max(runs), "runs": runs, "unit": "jobs/s",
+        mps = mps_state()
+        if mps["active"]:
+            log("WARNING: MPS is active; the native leg would not be the time-sliced baseline")
+        native = {"value": max(runs), "runs": runs, "unit": "jobs/s", "mps": mps,
                   "cold_turnaround_ms": dist.max(nat["cold_ms"]),
                   "desc": "NativeVgpu: one CUDA context per process, pageable cudaMemcpy, "
                           "time-sliced by the driver, no MPS; best of 3 runs (bimodal: the "
@@ -934,18 +1091,23 @@ def main():
         overhead = leg_overhead_n1(V, N, W, args.workload if args.workload != "mixed" else "vecadd",
                                    args.steps, args.warmup, device, sizes, dist)
     clock_info = clocks.stop() if clocks else None
+    all_clocks = [c for c in dist.gather(clock_info) if c]
+    clock_info = merge_clocks(all_clocks) if all_clocks else None
 
     # ---- final reduction (multi-GPU only) ----------------------------------------------
     reduce_info = None
     from paper_1511_07658_b200 import reduce as R
     record = R.record_from_workers(e2e["results"])
     try:
-        folded, rank0, us = final_reduce(N, dist, record)
+        folded, rank0, times = final_reduce(N, dist, record)
         via = ("torch.distributed all_gather over gloo (shared-GPU test mode)"
                if SHARED_GPU and world > 1 else "ncclAllGather")
         reduce_info = {"collective": f"{via} of {R.REC_WIDTH * 8} B per GPU "
                                      f"({world} rank(s)), host fold in rank order",
-                       "wall_us": us, "jobs_folded": folded[0]}
+                       "wall_us": statistics.median(times[1:]), "first_call_us": times[0],
+                       "wall_us_note": "steady state: median of 5 calls after the first "
+                                       "(the first carries the communicator's lazy setup)",
+                       "jobs_folded": folded[0]}
         if folded[14] > 0:
             reduce_info["ep"] = R.ep_verdict(folded, sizes.ep_m, sizes.ep_batches, rank0)
     except Exception as e:  # noqa: BLE001 - reported in the line
@@ -957,12 +1119,23 @@ def main():
         r = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s)
         if r is not None:
             cpu = {"value": r["jobs_per_s"], "unit": "jobs/s", "cores": os.cpu_count(),
-                   "kind": "reference", "sample": r["sample"]}
+                   "kind": "reference", "sample": r["sample"], "cpu_model": cpu_model(),
+                   "omp_num_threads": r.get("omp_threads_per_proc"),
+                   "path": "(i) reference GVM"}
+            rn = cpu_reference_arm(args.workload, procs, sizes, budget_s=args.cpu_budget_s,
+                                   native=True)
+            if rn is not None:
+                cpu["per_process_native"] = {
+                    "value": rn["jobs_per_s"], "unit": "jobs/s", "sample": rn["sample"],
+                    "omp_num_threads": rn.get("omp_threads_per_proc"),
+                    "path": "(ii) reference NativeVgpu per process"}
+            cpu["payload_bench"] = payload_bench_ref()
 
     if dist.rank == 0:
         peaks = device_peaks(V, device)
         accepted = record[13] if record[13] > 0 else None
         roof = roofline(W, dom, legs[dom], peaks, accepted)
+        roof["link"] = link_roofline(V, device, h2d, d2h, args.steps, secs, world)
         kernels = None
         if not args.no_kernels:
             kernels = kernel_summary(V, W, args.workload, device, peaks, sizes, args.steps,
@@ -974,13 +1147,20 @@ def main():
             "data": "synthetic", "config": config,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": secs * 1e3 / args.steps,
-                    "path": "bin/vgpu-spmd x P -> VgpuHandle::run_task -> UDS+shm -> GVM "
-                            "(libvgpu.so) -> per-client CUDA streams",
+                    "path": "bin/vgpu-spmd x P -> VgpuHandle snd/str/stp_wait/"
+                            + ("rcv_region" if inplace else "rcv") +
+                            " -> UDS+shm -> GVM (libvgpu.so) -> per-client CUDA streams",
+                    "api": ("inplace: snd(span) copies the program's input into the pinned "
+                            "region every step (streamed: the GVM uploads each filled part "
+                            "while the next is copied), the result is read where the D2H "
+                            "left it (rcv_region)") if inplace else
+                           "span: the reference's snd(span) + rcv() -> Bytes",
                     "client_stage_us": e2e.get("client_stage_us"),
                     "device_stage_us": e2e.get("device_stage_us")},
             "turnaround": turnaround,
             "e2e_paper_barrier": ({k: v for k, v in paper.items() if k != "batches"}
                                   if paper else None),
+            "e2e_other_api": alt_api,
             "native": native,
             "vs_native": (e2e_value / native["value"]) if native else None,
             "roofline": roof,

@@ -14,6 +14,9 @@
 // VgpuHandle::stp_wait() sleep on a futex instead of polling STP on a
 // 100 us -> 10 ms backoff (reference client.cpp:108-114). The wire protocol
 // is unchanged; a client without a doorbell falls back to the backoff.
+// The doorbell page also carries the streamed-SND fill counters: a client
+// that sees the capability copies its input into the region chunk by chunk
+// while the GVM already DMAs the filled part (SND frame sent first, flagged).
 #ifndef VGPU_TRANSPORT_HPP
 #define VGPU_TRANSPORT_HPP
 
@@ -76,6 +79,13 @@ public:
     // Block until the count moves past `seen` or the timeout passes.
     virtual void wait_notify(std::uint64_t /*seen*/,
                              std::chrono::microseconds /*timeout*/) {}
+    // B200 streamed SND: the attached slot's fill counter in shared memory
+    // (bytes of the current SND already in the region), or nullptr when the
+    // daemon does not take streamed SNDs.
+    virtual std::uint64_t* stream_fill() { return nullptr; }
+    // B200: leases the daemon holds right now (sizes the SDK's copy
+    // threads), 0 when unknown.
+    virtual std::uint32_t leased_clients() { return 0; }
 };
 
 struct Inbound {
@@ -101,6 +111,11 @@ public:
     // B200: false once the peer bound to this slot has disconnected (client
     // death); the GVM then reclaims the slot instead of leaking the lease.
     virtual bool route_alive(std::uint32_t /*client_id*/) const { return true; }
+    // B200 streamed SND: the slot's fill counter the client advances while
+    // it copies (nullptr: this transport has none, clients never stream).
+    virtual const std::uint64_t* stream_fill(std::uint32_t /*client_id*/) { return nullptr; }
+    // B200: publish how many slots are leased (clients size copy threads).
+    virtual void publish_leases(std::uint32_t /*leased*/) {}
 };
 
 // ---- in-process loopback --------------------------------------------------

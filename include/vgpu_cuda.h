@@ -144,7 +144,8 @@ typedef struct vgpu_cu_done {
     uint64_t batch;        /* batch sequence number from submit              */
     int32_t status;        /* VGPU_CU_OK or error                            */
     uint32_t slot;
-    float h2d_us;          /* CUDA-event stage durations                     */
+    float h2d_us;          /* CUDA-event stage durations (a streamed upload:
+                              the DMA busy time, summed over its parts)      */
     float comp_us;
     float d2h_us;
     float span_us;         /* this task: H2D start -> D2H end                */
@@ -198,6 +199,17 @@ int vgpu_cu_task_check(vgpu_cu_dev* dev, uint32_t kernel, const void* in, uint64
  * `tag`. Once reported, the bytes are captured in HBM (SND snapshot). */
 int vgpu_cu_upload(vgpu_cu_dev* dev, uint32_t slot, const void* h_in, uint64_t bytes,
                    uint64_t tag);
+
+/* Streamed SND upload: the same op as vgpu_cu_upload, issued in parts while
+ * the client is still filling its region. flags BEGIN opens the op (records
+ * its start event), each call copies [offset, offset + bytes) of the input
+ * from h_src into the slot's input buffer on the slot's stream, END closes
+ * it; poll() then reports one VGPU_CU_DONE_UPLOAD with `tag` (given with
+ * BEGIN). BEGIN|END in one call equals vgpu_cu_upload. */
+#define VGPU_CU_UPLOAD_BEGIN 1u
+#define VGPU_CU_UPLOAD_END 2u
+int vgpu_cu_upload_part(vgpu_cu_dev* dev, uint32_t slot, const void* h_src, uint64_t offset,
+                        uint64_t bytes, uint32_t flags, uint64_t tag);
 
 /* Enqueue a batch. style 0 = PS-1 (all H2D, then compute — one launch per
  * kernel kind over the whole batch's task table — then all D2H), 1 = PS-2
@@ -261,6 +273,19 @@ int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
  * (FP32) rooflines are quoted against, counting 2 FLOP per FMA. */
 enum vgpu_cu_peak_kind { VGPU_CU_PEAK_FP64 = 0, VGPU_CU_PEAK_FP32 = 1 };
 int vgpu_cu_peak_probe(int device, uint32_t kind, double* tflops);
+
+/* Host link (PCIe) probe: the e2e roofline's denominator. `bytes`-sized
+ * copies between page-locked host memory (cudaHostAlloc) and HBM, each
+ * direction alone and both at once on two streams (the copy engines are
+ * full duplex), best of `reps` after a warm-up, CUDA events. GB/s = 1e9 B/s;
+ * bidir counts the bytes of both directions. */
+typedef struct vgpu_cu_link_result {
+    double h2d_gbs;
+    double d2h_gbs;
+    double bidir_gbs;
+    uint64_t bytes;
+} vgpu_cu_link_result;
+int vgpu_cu_link_probe(int device, uint64_t bytes, uint32_t reps, vgpu_cu_link_result* out);
 
 /* ---- multi-GPU: the single final reduction (NCCL over NVLink) --------- */
 #define VGPU_CU_NCCL_ID_BYTES 128

@@ -12,7 +12,14 @@
 // arithmetic for, the oracle restatements (nas-ep, black-scholes, sgemm)
 // registered through the reference's register_payload (payload.hpp:36).
 //
+// --native: SURVEY.md §8(d)(ii), the reference's per-process CPU path: the
+// same N forked workers each run the reference's NativeVgpu (virtual clock:
+// the payload executes in the calling process, no daemon) with
+// OMP_NUM_THREADS = max(1, cores / N) so the processes do not oversubscribe
+// the host (proj/include/vgpu/client.hpp:87-113, proj/src/client.cpp:196-232).
+//
 // Output: one JSON line {jobs_per_s, per-round timestamps summary, ...}.
+#include <omp.h>
 #include <sys/mman.h>
 #include <sys/wait.h>
 #include <unistd.h>
@@ -133,7 +140,15 @@ int main(int argc, char** argv) {
     vgpu::wl::cg_builder() = cg_makea;
     std::string workload = "vecadd", instance = "refbench" + std::to_string(getpid());
     std::uint32_t procs = 4, rounds = 3, warmup = 1;
+    bool native = false;
     vgpu::wl::Sizes sizes;
+    for (int i = 1; i < argc; ++i)
+        if (std::string(argv[i]) == "--native") {
+            native = true;
+            for (int j = i; j + 1 < argc; ++j) argv[j] = argv[j + 1];
+            --argc;
+            break;
+        }
     for (int i = 1; i + 1 < argc; i += 2) {
         const std::string a = argv[i], v = argv[i + 1];
         if (a == "--workload") workload = v;
@@ -159,6 +174,16 @@ int main(int argc, char** argv) {
     if (pipe(go_pipe) != 0) return 1;
     vgpu::unlink_os_instance(instance, procs);
 
+    vgpu::PayloadRegistry reg = vgpu::PayloadRegistry::with_builtins();
+    reg.register_payload("nas-ep", ep_payload);
+    reg.register_payload("black-scholes", bs_payload);
+    reg.register_payload("sgemm", mm_payload);
+    reg.register_payload("nas-cg", cg_payload);
+    reg.register_payload("vector-mul", vmul_payload);
+    reg.register_payload("electrostatics", es_payload);
+    const unsigned cores = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned omp_threads = native ? std::max(1u, cores / procs) : cores;
+
     std::vector<pid_t> kids;
     for (std::uint32_t w = 0; w < procs; ++w) {
         const pid_t pid = fork();
@@ -175,6 +200,20 @@ int main(int argc, char** argv) {
                 d.grid_size = job.desc.grid_size;
                 char go = 0;
                 if (read(go_pipe[0], &go, 1) != 1) _exit(2);
+                if (native) {
+                    omp_set_num_threads(static_cast<int>(omp_threads));
+                    vgpu::NativeVgpu nv({}, &reg);  // virtual clock: no pacing sleeps
+                    st = 0;
+                    for (std::uint32_t r = 0; r < total; ++r) {
+                        ts[(w * total + r) * 2] = now_ns();
+                        const vgpu::Bytes out = nv.run_task(job.input, d);
+                        ts[(w * total + r) * 2 + 1] = now_ns();
+                        if (out.size() != job.output_bytes) st = 3;
+                    }
+                    nv.rls();
+                    status[w] = st;
+                    _exit(st);
+                }
                 std::unique_ptr<vgpu::VgpuHandle> h;
                 for (int attempt = 0; !h; ++attempt) {
                     try {
@@ -202,13 +241,6 @@ int main(int argc, char** argv) {
     }
     close(go_pipe[0]);
 
-    vgpu::PayloadRegistry reg = vgpu::PayloadRegistry::with_builtins();
-    reg.register_payload("nas-ep", ep_payload);
-    reg.register_payload("black-scholes", bs_payload);
-    reg.register_payload("sgemm", mm_payload);
-    reg.register_payload("nas-cg", cg_payload);
-    reg.register_payload("vector-mul", vmul_payload);
-    reg.register_payload("electrostatics", es_payload);
     vgpu::GvmConfig g;
     g.instance = instance;
     g.max_clients = procs;
@@ -216,8 +248,10 @@ int main(int argc, char** argv) {
     g.barrier_window = 1'000'000;
     g.per_client_shm_bytes = vgpu::wl::region_bytes(workload, sizes);
     g.clock = vgpu::ClockMode::Virtual;
-    auto daemon = vgpu::GvmDaemon::start(
-        g, vgpu::open_os_daemon_transport(instance, procs, g.per_client_shm_bytes), &reg);
+    std::unique_ptr<vgpu::GvmDaemon> daemon;
+    if (!native)
+        daemon = vgpu::GvmDaemon::start(
+            g, vgpu::open_os_daemon_transport(instance, procs, g.per_client_shm_bytes), &reg);
     std::vector<char> go(procs, 1);
     if (write(go_pipe[1], go.data(), procs) != static_cast<ssize_t>(procs)) return 1;
     bool ok = true;
@@ -226,7 +260,7 @@ int main(int argc, char** argv) {
         waitpid(k, &st, 0);
         ok &= WIFEXITED(st) && WEXITSTATUS(st) == 0;
     }
-    daemon->stop();
+    if (daemon) daemon->stop();
     // timed region: first finish of the warm-up rounds -> last finish
     std::int64_t t_begin = INT64_MAX, t_end = 0;
     for (std::uint32_t w = 0; w < procs; ++w) {
@@ -238,8 +272,9 @@ int main(int argc, char** argv) {
     const double secs = (t_end - t_begin) * 1e-9;
     const double jobs = static_cast<double>(procs) * rounds;
     std::printf("{\"ok\": %s, \"workload\": \"%s\", \"procs\": %u, \"rounds\": %u, \"warmup\": %u, "
-                "\"seconds\": %.6f, \"jobs_per_s\": %.3f, \"ms_per_round\": %.3f, \"threads\": %u}\n",
+                "\"seconds\": %.6f, \"jobs_per_s\": %.3f, \"ms_per_round\": %.3f, \"threads\": %u, "
+                "\"mode\": \"%s\", \"omp_threads_per_proc\": %u}\n",
                 ok ? "true" : "false", workload.c_str(), procs, rounds, warmup, secs, jobs / secs,
-                1e3 * secs / rounds, std::thread::hardware_concurrency());
+                1e3 * secs / rounds, cores, native ? "native" : "gvm", omp_threads);
     return ok ? 0 : 1;
 }

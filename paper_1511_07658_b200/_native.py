@@ -55,6 +55,11 @@ class ResidentResult(C.Structure):
                 ("pdl", C.c_uint32), ("reserved", C.c_uint32)]
 
 
+class LinkResult(C.Structure):
+    _fields_ = [("h2d_gbs", C.c_double), ("d2h_gbs", C.c_double), ("bidir_gbs", C.c_double),
+                ("bytes", C.c_uint64)]
+
+
 class CuStats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("tasks", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("batches", C.c_uint64)]
@@ -108,6 +113,7 @@ CUDA_API = {
     "vgpu_cu_output_size": (C.c_int, [_U32, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_task_check": (C.c_int, [_P, _U32, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_upload": (C.c_int, [_P, _U32, _P, _U64, _U64]),
+    "vgpu_cu_upload_part": (C.c_int, [_P, _U32, _P, _U64, _U64, _U32, _U64]),
     "vgpu_cu_submit_batch": (C.c_int, [_P, C.c_int, _P, _U32, C.POINTER(_U64)]),
     "vgpu_cu_poll": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_cu_wait": (C.c_int, [_P, _I64]),
@@ -122,6 +128,7 @@ CUDA_API = {
                                          C.POINTER(_U64), _U32, _U32, _U32, _U32,
                                          C.POINTER(ResidentResult)]),
     "vgpu_cu_peak_probe": (C.c_int, [C.c_int, _U32, C.POINTER(C.c_double)]),
+    "vgpu_cu_link_probe": (C.c_int, [C.c_int, _U64, _U32, C.POINTER(LinkResult)]),
     "vgpu_cu_nccl_unique_id": (C.c_int, [_P]),
     "vgpu_cu_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "vgpu_cu_reduce_final": (C.c_int, [_P, _P, _U64, _P]),

@@ -919,6 +919,7 @@ struct Op {
                                  // when nothing separates them on the slot's stream)
     bool mapped_out = false;     // the kernel wrote the result straight into host memory
     bool grouped = false;        // launched in a PS-1 group on another stream
+    std::vector<cudaEvent_t> parts;  // streamed upload: (start, end) per part: DMA busy time
     cudaEvent_t in_ready() const { return has_h2d ? ev[kEvH2d1] : ev[kEvH2d0]; }
     cudaEvent_t last() const { return kind == VGPU_CU_DONE_UPLOAD ? ev[kEvH2d1] : ev[kEvD2h1]; }
 };
@@ -935,6 +936,8 @@ struct SlotState {
     std::uint64_t reg_bytes = 0;
     bool task_busy = false;
     std::uint32_t ops_in_flight = 0;
+    Op* open_upload = nullptr;        // streamed SND between BEGIN and END
+    std::uint64_t open_upload_bytes = 0;
 };
 
 struct BatchRec {
@@ -996,6 +999,7 @@ struct vgpu_cu_dev {
     void release_op(Op* op) {
         for (auto& e : op->ev)
             if (e) event_pool.push_back(e);
+        for (auto e : op->parts) event_pool.push_back(e);
         delete op;
     }
 };
@@ -1267,6 +1271,8 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
     for (Op* op : d->outstanding) d->release_op(op);
     d->outstanding.clear();
     for (auto& s : d->slots) {
+        if (s.open_upload) d->release_op(s.open_upload);
+        s.open_upload = nullptr;
         if (s.reg_base) cudaHostUnregister(s.reg_base);
         if (s.stream) cudaStreamDestroy(s.stream);
     }
@@ -1361,6 +1367,70 @@ int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::ui
     ++s.ops_in_flight;
     d->outstanding.push_back(op);
     d->h2d_bytes += bytes;
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_upload_part(vgpu_cu_dev* d, std::uint32_t slot, const void* h_src, std::uint64_t offset,
+                        std::uint64_t bytes, std::uint32_t flags, std::uint64_t tag) {
+    if (!d || slot < 1 || slot > d->max_clients || (!h_src && bytes)) return VGPU_CU_EINVAL;
+    SlotState& s = d->slots[slot];
+    const bool begin = flags & VGPU_CU_UPLOAD_BEGIN, end = flags & VGPU_CU_UPLOAD_END;
+    if (begin == (s.open_upload != nullptr)) {
+        set_err(begin ? "slot %u: streamed upload already open" : "slot %u: no streamed upload open",
+                slot);
+        return VGPU_CU_EINVAL;
+    }
+    if (offset + bytes > d->slot_bytes || offset + bytes < offset) {
+        set_err("upload part [%llu, +%llu) exceeds the slot (%llu B)", (unsigned long long)offset,
+                (unsigned long long)bytes, (unsigned long long)d->slot_bytes);
+        return VGPU_CU_ESIZE;
+    }
+    if (begin && s.task_busy) {
+        set_err("slot %u has a task in flight", slot);
+        return VGPU_CU_EINVAL;
+    }
+    CK(cudaSetDevice(d->device));
+    cudaError_t e = cudaSuccess;
+    if (begin) {
+        int rc = d->new_op(slot, VGPU_CU_DONE_UPLOAD, tag, &s.open_upload);
+        if (rc) return rc;
+        s.open_upload_bytes = 0;
+        e = cudaEventRecord(s.open_upload->ev[kEvH2d0], s.stream);
+    }
+    Op* op = s.open_upload;
+    if (e == cudaSuccess && bytes) {
+        cudaEvent_t p0 = nullptr, p1 = nullptr;
+        int rc = d->pool_get(&p0);
+        if (!rc) rc = d->pool_get(&p1);
+        if (rc) {
+            if (p0) d->event_pool.push_back(p0);
+            cudaStreamSynchronize(s.stream);
+            d->release_op(op);
+            s.open_upload = nullptr;
+            return rc;
+        }
+        op->parts.push_back(p0);
+        op->parts.push_back(p1);
+        e = cudaEventRecord(p0, s.stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(s.d_in + offset, h_src, bytes, cudaMemcpyHostToDevice, s.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(p1, s.stream);
+    }
+    if (e == cudaSuccess) s.open_upload_bytes += bytes;
+    if (e == cudaSuccess && end) e = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(s.stream);
+        d->release_op(op);
+        s.open_upload = nullptr;
+        return cuda_fail(e, "vgpu_cu_upload_part");
+    }
+    d->h2d_bytes += bytes;
+    if (end) {
+        op->has_h2d = s.open_upload_bytes > 0;
+        ++s.ops_in_flight;
+        d->outstanding.push_back(op);
+        s.open_upload = nullptr;
+    }
     return VGPU_CU_OK;
 }
 
@@ -1591,6 +1661,12 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
     if (s.ops_in_flight) --s.ops_in_flight;
     if (op->kind == VGPU_CU_DONE_UPLOAD) {
         r.span_us = r.h2d_us;
+        if (!op->parts.empty()) {  // streamed: DMA busy time = the parts' sum
+            float busy = 0.0f;
+            for (std::size_t i = 0; i + 1 < op->parts.size(); i += 2)
+                busy += elapsed_ms(op->parts[i], op->parts[i + 1]);
+            r.h2d_us = 1000.0f * busy;
+        }
         return;
     }
     r.comp_us = op->has_comp ? 1000.0f * elapsed_ms(op->comp0, op->comp1) : 0.0f;
@@ -1941,6 +2017,72 @@ int vgpu_cu_peak_probe(int device, std::uint32_t kind, double* tflops) {
     if (err != cudaSuccess) return cuda_fail(err, "peak probe");
     const double flop = 2.0 * 8 * 16 * static_cast<double>(iters) * grid.x * block.x;
     *tflops = flop / (best * 1e-3) / 1e12;
+    return VGPU_CU_OK;
+}
+
+int vgpu_cu_link_probe(int device, std::uint64_t bytes, std::uint32_t reps,
+                       vgpu_cu_link_result* out) {
+    if (!out || bytes == 0) return VGPU_CU_EINVAL;
+    int rc = require_sm100(device);
+    if (rc) return rc;
+    CK(cudaSetDevice(device));
+    reps = std::max<std::uint32_t>(1, reps);
+    void *h_src = nullptr, *h_dst = nullptr, *d_src = nullptr, *d_dst = nullptr;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    auto cleanup = [&] {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto st : s)
+            if (st) cudaStreamDestroy(st);
+        if (d_src) cudaFree(d_src);
+        if (d_dst) cudaFree(d_dst);
+        if (h_src) cudaFreeHost(h_src);
+        if (h_dst) cudaFreeHost(h_dst);
+    };
+    cudaError_t err = cudaHostAlloc(&h_src, bytes, cudaHostAllocDefault);
+    if (err == cudaSuccess) err = cudaHostAlloc(&h_dst, bytes, cudaHostAllocDefault);
+    if (err == cudaSuccess) err = cudaMalloc(&d_src, bytes);
+    if (err == cudaSuccess) err = cudaMalloc(&d_dst, bytes);
+    for (int i = 0; i < 2 && err == cudaSuccess; ++i) err = cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && err == cudaSuccess; ++i) err = cudaEventCreate(&ev[i]);
+    if (err == cudaSuccess) err = cudaMemset(d_src, 1, bytes);
+    if (err == cudaSuccess) std::memset(h_src, 1, bytes);
+    // mode 0: H2D alone, 1: D2H alone, 2: both at once (one stream each)
+    auto run = [&](int mode, float* ms) -> cudaError_t {
+        cudaError_t e = cudaSuccess;
+        if (mode != 1) e = cudaEventRecord(ev[0], s[0]);
+        if (e == cudaSuccess && mode != 0) e = cudaEventRecord(ev[2], s[1]);
+        for (std::uint32_t r = 0; r < reps && e == cudaSuccess; ++r) {
+            if (mode != 1) e = cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, s[0]);
+            if (e == cudaSuccess && mode != 0)
+                e = cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, s[1]);
+        }
+        if (e == cudaSuccess && mode != 1) e = cudaEventRecord(ev[1], s[0]);
+        if (e == cudaSuccess && mode != 0) e = cudaEventRecord(ev[3], s[1]);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        float a = 0.0f, b = 0.0f;
+        if (e == cudaSuccess && mode != 1) e = cudaEventElapsedTime(&a, ev[0], ev[1]);
+        if (e == cudaSuccess && mode != 0) e = cudaEventElapsedTime(&b, ev[2], ev[3]);
+        *ms = std::max(a, b);
+        return e;
+    };
+    double best[3] = {0.0, 0.0, 0.0};
+    for (int mode = 0; mode < 3 && err == cudaSuccess; ++mode) {
+        for (int trial = 0; trial < 3 && err == cudaSuccess; ++trial) {  // first = warm-up
+            float ms = 0.0f;
+            err = run(mode, &ms);
+            const double moved = static_cast<double>(bytes) * reps * (mode == 2 ? 2 : 1);
+            if (err == cudaSuccess && trial > 0 && ms > 0.0f)
+                best[mode] = std::max(best[mode], moved / (ms * 1e-3) / 1e9);
+        }
+    }
+    cleanup();
+    if (err != cudaSuccess) return cuda_fail(err, "link probe");
+    out->h2d_gbs = best[0];
+    out->d2h_gbs = best[1];
+    out->bidir_gbs = best[2];
+    out->bytes = bytes;
     return VGPU_CU_OK;
 }
 

@@ -97,7 +97,18 @@ struct Session {
     std::uint8_t head[64] = {};  // first bytes of the input (EP parameters)
     float upload_h2d_us = 0.0f;
     std::deque<Inbound> backlog; // frames that arrived while an upload ran
+    // streamed SND (the client fills the region while the GVM uploads it)
+    struct Stream {
+        bool active = false;
+        bool eager = false;      // parts go to the device as they fill
+        std::uint64_t len = 0;
+        std::uint64_t issued = 0;
+        Message snd;             // deferred mode: replayed as a plain SND when filled
+    } stream;
 };
+
+// Streamed SND: upload granule (a part goes out once this much more is filled)
+constexpr std::uint64_t kStreamGranule = 2u << 20;
 
 struct Pending {
     std::uint64_t task_id = 0;
@@ -155,6 +166,7 @@ struct GvmDaemon::Impl {
     std::map<std::uint32_t, std::deque<std::uint64_t>> pending_snd_acks;
     std::map<std::uint64_t, BatchState> batches;     // batch key -> state
     std::uint64_t next_tag = 1;
+    std::uint32_t streams_active = 0;  // sessions with a streamed SND still filling
 
     mutable std::mutex metrics_mu;
     std::vector<TaskMetrics> task_metrics;
@@ -303,19 +315,22 @@ struct GvmDaemon::Impl {
         lease.stream_hint = slot - 1;
         lease.shm_name = transport->region_name(slot);
         transport->reply_origin(origin, {Opcode::Ack, slot, m.task_id, encode_lease(lease)});
+        publish_leases();
     }
 
     void on_snd(const Message& m, Session& s) {
         if (s.phase != Phase::Leased && s.phase != Phase::DataIn)
             return nack(m.client_id, m.task_id, ErrCode::Phase,
                         std::string("SND illegal in phase ") + to_string(s.phase));
-        const auto len = parse_u64(m.payload);
-        if (!len)
+        const auto snd = parse_snd(m.payload);
+        if (!snd)
             return nack(m.client_id, m.task_id, ErrCode::Malformed,
                         "SND payload must be a u64 length");
+        const std::uint64_t* len = &snd->length;
         DataRegion& region = transport->region(m.client_id);
         if (*len > region.size())
             return nack(m.client_id, m.task_id, ErrCode::Size, "data exceeds leased region");
+        if (snd->flags & kSndStreamed) return start_stream(m, s, *len);
         s.input_len = *len;
         s.input.clear();
         s.input_resident = false;
@@ -334,8 +349,7 @@ struct GvmDaemon::Impl {
             // HBM buffer; the ACK goes out when the copy has landed, so the
             // client's H2D overlaps the other clients' host work
             const int rc = vgpu_cu_upload(dev, m.client_id, region.data(), *len,
-                                          (static_cast<std::uint64_t>(m.client_id) << 32) |
-                                              (s.generation & 0xffffffffu));
+                                          upload_tag(m.client_id, s));
             if (rc != VGPU_CU_OK)
                 return nack(m.client_id, m.task_id, ErrCode::Internal,
                             std::string("upload failed: ") + vgpu_cu_last_error());
@@ -353,6 +367,111 @@ struct GvmDaemon::Impl {
         }
         s.phase = Phase::DataIn;
         ack(m.client_id, m.task_id);
+    }
+
+    // Streamed SND: the frame came first, the client is still copying its
+    // input into the region and advances the slot's fill counter as it goes.
+    // Eager upload (ZeroCopy + device): each filled part goes to the slot's
+    // HBM buffer at once, so the client's copy and the H2D overlap; the ACK
+    // goes out when the last part has landed (same as a plain SND). Other
+    // modes wait for the fill to complete and then take the plain SND path.
+    // Frames from this client meanwhile queue in its backlog, as for an
+    // eager upload, so per-client order is unchanged.
+    void start_stream(const Message& m, Session& s, std::uint64_t len) {
+        if (!transport->stream_fill(m.client_id))
+            return nack(m.client_id, m.task_id, ErrCode::Malformed,
+                        "streamed SND needs a transport with fill counters");
+        s.input_len = len;
+        s.input.clear();
+        s.input_resident = false;
+        s.input_inline = false;
+        s.stream = {};
+        s.stream.active = true;
+        s.stream.len = len;
+        if (dev && cfg.data_plane == DataPlane::ZeroCopy && len > sizeof s.head) {
+            const int rc = vgpu_cu_upload_part(dev, m.client_id, nullptr, 0, 0, VGPU_CU_UPLOAD_BEGIN,
+                                               upload_tag(m.client_id, s));
+            if (rc != VGPU_CU_OK) {
+                s.stream.active = false;
+                return nack(m.client_id, m.task_id, ErrCode::Internal,
+                            std::string("upload failed: ") + vgpu_cu_last_error());
+            }
+            s.stream.eager = true;
+            s.phase = Phase::DataIn;
+            pending_snd_acks[m.client_id].push_back(m.task_id);
+        } else {
+            s.stream.snd = {Opcode::Snd, m.client_id, m.task_id, encode_u64(len)};
+        }
+        ++s.uploads;  // holds the client's later frames until the SND is answered
+        ++streams_active;
+    }
+
+    static std::uint64_t upload_tag(std::uint32_t id, const Session& s) {
+        return (static_cast<std::uint64_t>(id) << 32) | (s.generation & 0xffffffffu);
+    }
+
+    // Issue the filled parts of every active stream (dispatcher thread).
+    bool pump_streams() {
+        if (streams_active == 0) return false;
+        bool moved = false;
+        for (std::uint32_t id = 1; id <= cfg.max_clients; ++id) {
+            Session& s = sessions[id - 1];
+            if (!s.stream.active) continue;
+            std::uint64_t fill = __atomic_load_n(transport->stream_fill(id), __ATOMIC_ACQUIRE);
+            if (!transport->route_alive(id)) fill = s.stream.len;  // client died mid-copy: close it
+            fill = std::min(fill, s.stream.len);
+            const bool full = fill == s.stream.len;
+            if (!s.stream.eager) {
+                if (!full) continue;
+                moved = true;
+                s.stream.active = false;
+                --streams_active;
+                --s.uploads;
+                const Message snd = std::move(s.stream.snd);
+                on_snd(snd, s);
+                replay_backlog(&s);
+                continue;
+            }
+            if (fill <= s.stream.issued || (!full && fill - s.stream.issued < kStreamGranule))
+                continue;
+            moved = true;
+            std::uint8_t* base = transport->region(id).data();
+            const int rc = vgpu_cu_upload_part(dev, id, base + s.stream.issued, s.stream.issued,
+                                               fill - s.stream.issued, full ? VGPU_CU_UPLOAD_END : 0,
+                                               0);
+            s.stream.issued = fill;
+            if (full || rc != VGPU_CU_OK) {
+                s.stream.active = false;
+                --streams_active;
+                std::memcpy(s.head, base, std::min<std::uint64_t>(s.stream.len, sizeof s.head));
+            }
+            if (rc != VGPU_CU_OK) {
+                // the op was released by the backend: answer the SND here
+                --s.uploads;
+                auto& q = pending_snd_acks[id];
+                const std::uint64_t task = q.empty() ? 0 : q.front();
+                if (!q.empty()) q.pop_front();
+                s.phase = Phase::Leased;
+                nack(id, task, ErrCode::Internal,
+                     std::string("upload failed: ") + vgpu_cu_last_error());
+                replay_backlog(&s);
+            }
+        }
+        return moved;
+    }
+
+    void replay_backlog(Session* s) {
+        while (s->uploads == 0 && !s->backlog.empty()) {
+            const Inbound in = std::move(s->backlog.front());
+            s->backlog.pop_front();
+            dispatch(in.msg, s);
+        }
+    }
+
+    void publish_leases() {
+        std::uint32_t n = 0;
+        for (const Session& s : sessions) n += leased(s) ? 1 : 0;
+        transport->publish_leases(n);
     }
 
     void on_str(const Message& m, Session& s) {
@@ -445,6 +564,7 @@ struct GvmDaemon::Impl {
         s.input.clear();
         s.output.clear();
         ack(m.client_id, m.task_id);
+        publish_leases();
     }
 
     // ---- barrier ------------------------------------------------------------
@@ -763,11 +883,7 @@ struct GvmDaemon::Impl {
             ack(d.slot, task);
         }
         // replay what the client sent meanwhile, until another upload starts
-        while (s->uploads == 0 && !s->backlog.empty()) {
-            const Inbound in = std::move(s->backlog.front());
-            s->backlog.pop_front();
-            dispatch(in.msg, s);
-        }
+        replay_backlog(s);
     }
 
     // ---- thread --------------------------------------------------------------
@@ -797,7 +913,8 @@ struct GvmDaemon::Impl {
         while (running.load(std::memory_order_relaxed)) {
             try {
                 if (drain_device()) last_event = Clock::now();
-                const bool pending = dev && vgpu_cu_pending(dev) > 0;
+                if (pump_streams()) last_event = Clock::now();
+                const bool pending = (dev && vgpu_cu_pending(dev) > 0) || streams_active > 0;
                 const bool hot = spin_us > 0 &&
                                  (pending || us_between(last_event, Clock::now()) < spin_us);
                 const Micros idle_wait = pending ? kPendingNapUs : 500;

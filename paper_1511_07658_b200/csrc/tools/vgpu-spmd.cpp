@@ -4,9 +4,10 @@
 //   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul
 //             --rounds R [--instance NAME [--inplace] | --native [--device D]]
 //
-// --inplace: the in-place data plane (VgpuHandle::region / snd_region /
-// rcv_region): every round the program writes its input into the leased,
-// page-locked region and reads the result where the D2H left it.
+// --inplace: the in-place result (VgpuHandle::rcv_region): every round the
+// program reads the result where the D2H left it in the leased, page-locked
+// region instead of rcv()'s copy into a fresh Bytes. The input still goes in
+// by snd(span) — a real copy of the program's private input every round.
 //
 // Builds its private input, leases a VGPU (retrying until the daemon is
 // up) — or, with --native, uses its OWN CUDA context through NativeVgpu —
@@ -167,15 +168,10 @@ int main(int argc, char** argv) {
                 out = nh->run_task(job.input, job.desc);
                 view = out;
             } else {  // run_task, verb by verb so each stage is timed
-                if (inplace) {
-                    // the program produces its input in the page-locked
-                    // region (inside the timed round), then SND without a copy
-                    const auto reg = vh->region();
-                    vgpu::copy_into_region(reg, job.input);
-                    vh->snd_region(job.input.size());
-                } else {
-                    vh->snd(job.input);
-                }
+                // SND copies the program's input into the page-locked region
+                // (streamed: the GVM uploads each filled part while the next
+                // is copied) in both modes
+                vh->snd(job.input);
                 const std::int64_t a = now_ns();
                 vh->str(job.desc);
                 const std::int64_t b = now_ns();

@@ -366,6 +366,15 @@ def peak_probe(kind: str, device: int = 0) -> float:
     return t.value
 
 
+def link_probe(device: int = 0, nbytes: int = 256 << 20, reps: int = 8) -> dict:
+    """Pinned host <-> HBM copy bandwidth (vgpu_cu_link_probe): H2D alone,
+    D2H alone, both directions at once; GB/s (1e9 B/s)."""
+    r = N.LinkResult()
+    _cu_check(_libs().cuda.vgpu_cu_link_probe(device, nbytes, reps, C.byref(r)))
+    return {"h2d_gbs": r.h2d_gbs, "d2h_gbs": r.d2h_gbs, "bidir_gbs": r.bidir_gbs,
+            "bytes": r.bytes, "reps": reps}
+
+
 def model_simulate(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int = 1,
                    sms: int = 14, max_kernels: int = 16, slots: int = 8) -> int:
     return _libs().host.vgpu_model_simulate(style, n, t_in, t_comp, t_out, grid, sms,

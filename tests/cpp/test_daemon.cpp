@@ -565,3 +565,86 @@ TEST_CASE("gvm: a dead client's lease is reclaimed by the next REQ") {
     CHECK(c.await().opcode == Opcode::Ack);
     CHECK(c.stp(1).opcode == Opcode::Ack);
 }
+
+TEST_CASE("gvm os: streamed SND — the ACK waits for the fill, odd sizes, copy threads") {
+    // The SDK streams SNDs >= 4 MiB to a daemon that advertises it on its
+    // doorbell page: frame first, then the (multi-threaded) copy publishes
+    // the filled prefix. Host payloads: the daemon waits for the fill and
+    // takes the plain SND path (the device path uploads the parts as they fill).
+    GvmConfig g = cfg(2, 1, 1000);
+    g.instance = "stream" + std::to_string(getpid());
+    g.per_client_shm_bytes = 16 << 20;
+    unlink_os_instance(g.instance, g.max_clients);
+    auto d = GvmDaemon::start(g, open_os_daemon_transport(g.instance, 2, g.per_client_shm_bytes),
+                              &host_registry());
+    {
+        VgpuHandle h = req(g.instance);
+        std::mt19937 rng(11);
+        for (std::size_t n : {std::size_t{4} << 20, (std::size_t{4} << 20) + 37,
+                              (std::size_t{13} << 20) - 5, std::size_t{3} << 20}) {
+            Bytes in(n + 5);
+            for (auto& b : in) b = static_cast<std::uint8_t>(rng());
+            const std::span<const std::uint8_t> view(in.data() + 5, n);  // misaligned source
+            const Bytes out = h.run_task(view, descr(1, 1, 1, "reverse"));
+            REQUIRE(out.size() == n);
+            CHECK(std::equal(out.rbegin(), out.rend(), view.begin()));
+        }
+        // second SND wins, also when both are streamed
+        Bytes a(5 << 20, 1), b(6 << 20, 2);
+        h.snd(a);
+        h.snd(b);
+        h.str(descr(1, 1, 1, "reverse"));
+        h.stp_wait();
+        const Bytes out = h.rcv();
+        CHECK(out.size() == b.size());
+        CHECK(out.front() == 2);
+        h.rls();
+    }
+    {
+        // raw protocol: SND flagged streamed before the region is filled
+        auto ch = open_os_client_channel(g.instance);
+        ch->send({Opcode::Req, 0, 0, {}});
+        auto lease_msg = ch->recv(2s);
+        REQUIRE(lease_msg.has_value());
+        const LeaseInfo lease = *parse_lease(lease_msg->payload);
+        ch->attach_lease(lease);
+        std::uint64_t* fill = ch->stream_fill();
+        REQUIRE(fill != nullptr);
+        CHECK(ch->leased_clients() == 1);
+        const std::size_t n = 8 << 20;
+        __atomic_store_n(fill, 0, __ATOMIC_RELEASE);
+        std::memset(ch->region().data(), 7, n / 2);
+        __atomic_store_n(fill, n / 2, __ATOMIC_RELEASE);
+        ch->send({Opcode::Snd, lease.client_id, 0, encode_snd(n, kSndStreamed)});
+        CHECK(!ch->recv(50ms).has_value());  // half filled: no answer yet
+        // a frame sent meanwhile is answered after the SND, in order
+        ch->send({Opcode::Str, lease.client_id, 1, encode_descriptor(descr(1, 1, 1, "reverse"))});
+        CHECK(!ch->recv(20ms).has_value());
+        std::memset(ch->region().data() + n / 2, 9, n / 2);
+        __atomic_store_n(fill, n, __ATOMIC_RELEASE);
+        auto ack = ch->recv(2s);
+        REQUIRE(ack.has_value());
+        CHECK(ack->opcode == Opcode::Ack);
+        CHECK(ack->task_id == 0);
+        auto str_ack = ch->recv(2s);
+        REQUIRE(str_ack.has_value());
+        CHECK(str_ack->opcode == Opcode::Ack);
+        CHECK(str_ack->task_id == 1);
+        for (int i = 0; i < 200; ++i) {
+            ch->send({Opcode::Stp, lease.client_id, 1, {}});
+            auto r = ch->recv(2s);
+            REQUIRE(r.has_value());
+            if (r->opcode == Opcode::Ack) break;
+            std::this_thread::sleep_for(1ms);
+        }
+        ch->send({Opcode::Rcv, lease.client_id, 1, {}});
+        auto rcv = ch->recv(2s);
+        REQUIRE(rcv.has_value());
+        CHECK(parse_u64(rcv->payload).value_or(0) == n);
+        CHECK(ch->region().data()[0] == 9);      // reversed: the second half first
+        CHECK(ch->region().data()[n - 1] == 7);
+        ch->send({Opcode::Rls, lease.client_id, 0, {}});
+        CHECK(ch->recv(2s).has_value());
+    }
+    d->stop();
+}

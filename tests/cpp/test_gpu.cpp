@@ -389,7 +389,9 @@ TEST_CASE("[gpu] OS transport: forked SPMD clients through one GVM (real clock)"
                 try {
                     VgpuHandle h = req(g.instance);
                     for (int rep = 0; rep < 10; ++rep) {
-                        const Bytes in = vadd_input(1u << 20, w * 100 + rep);
+                        // >= 4 MiB inputs: streamed SNDs (parts uploaded while
+                        // the copy runs), odd lengths included
+                        const Bytes in = vadd_input((1u << 20) + 5u * (rep % 3), w * 100 + rep);
                         if (h.run_task(in, desc("vector-add", false)) != vadd_expect(in)) _exit(3);
                     }
                     h.rls();
