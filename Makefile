@@ -4,7 +4,7 @@
 #
 #   paper_1511_07658_b200/lib/libvgpu_cuda.so   device backend (nvcc, sm_100a, static cudart)
 #   paper_1511_07658_b200/lib/libvgpu.so        C++ host stack + C-ABI (links the backend)
-#   paper_1511_07658_b200/bin/{vgpud,vgpu-spmd,payload-bench}
+#   paper_1511_07658_b200/bin/{vgpud,vgpu-spmd,payload-bench,vgpu-launch}
 #   tests/_bin/vgpu-tests                       C++ unit / parity tests
 #   oracle/_build/libvgpu_oracle.so             CPU oracle (test infrastructure)
 
@@ -41,7 +41,7 @@ RPATH_TST := -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 all: product tests oracle
 
 product: $(LIBDIR)/libvgpu_cuda.so $(LIBDIR)/libvgpu.so \
-         $(BINDIR)/vgpud $(BINDIR)/vgpu-spmd $(BINDIR)/payload-bench
+         $(BINDIR)/vgpud $(BINDIR)/vgpu-spmd $(BINDIR)/payload-bench $(BINDIR)/vgpu-launch
 
 $(OBJDIR)/cuda/backend.o: $(CSRC)/cuda/backend.cu $(CUDA_HDR)
 	@mkdir -p $(dir $@)

@@ -291,7 +291,12 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False, inplace=False):
+                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False, api="span"):
+    """api: the SPMD program's client API (vgpu-spmd): 'span' = the
+    reference's snd(span) + rcv(); 'inplace' = snd(span) + rcv_region();
+    'resident' = input kept in the pinned region, snd_region_at +
+    rcv_region."""
+    inplace = api == "inplace"
     """Run the SPMD workers; virtualized (through an in-process GVM) or native."""
     spmd = N.bin_path("vgpu-spmd")
     inst = f"b200bench{os.getpid()}g{dist.rank}"
@@ -303,7 +308,8 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
     if not native:
         V.unlink_os_instance(inst, procs)
         cfg = V.GvmConfig(instance=inst, max_clients=procs, barrier_size=barrier or procs,
-                          per_client_shm_bytes=W.region_bytes(workload, sizes),
+                          per_client_shm_bytes=W.region_bytes(workload, sizes,
+                                                              resident=api == "resident"),
                           barrier_window=window, clock=V.ClockMode.Real, cuda_device=device,
                           device_sms=148, device_max_kernels=128, device_slots_per_sm=32,
                           data_plane=V.DataPlane.Snapshot if snapshot else V.DataPlane.ZeroCopy)
@@ -318,6 +324,8 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
             a.append("--connect-after-go")
         if inplace and not native:
             a.append("--inplace")
+        if api == "resident" and not native:
+            a.append("--resident")
         args.append(a)
     try:
         ps = spawn_workers(args, env)
@@ -328,6 +336,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
             p.stdin.flush()
         res = collect(ps)
         after = gvm.summary() if gvm else None
+        fold = gvm.fold() if gvm else None
         batches = gvm.batches() if gvm else []
         tasks = gvm.tasks() if gvm else []
     finally:
@@ -341,6 +350,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
     info = {"results": res, "t0": t0, "t1": t1, "seconds": (t1 - t0) * 1e-9}
     if gvm:
         info["launches_total"] = after["kernel_launches"] - before["kernel_launches"]
+        info["gvm_fold"] = fold
         info["batches"] = batches
         info["tasks"] = tasks
     if native:
@@ -472,14 +482,25 @@ def final_reduce(N, dist, record):
             times.append((time.perf_counter() - t0) * 1e6)
         flat = dist.torch.cat(parts).tolist()
         return R.fold_in_rank_order(flat, dist.world), flat[:R.REC_WIDTH], times
+    from paper_1511_07658_b200 import vgpu as V
     libs = N.load()
+    # the product's bootstrap (vgpud / vgpu-launch do the same): GVM 0 creates
+    # the NCCL id and publishes it in a file, the others wait for the file —
+    # no MPI, no torch in the data path (torch.distributed only runs the
+    # bench's barriers and max-over-ranks timing)
+    path = "/tmp/vgpu-bench.{}.{}.ncclid".format(os.environ.get("MASTER_PORT", "0"),
+                                                  os.environ.get("TORCHELASTIC_RUN_ID", "solo"))
+    if dist.rank == 0 and os.path.exists(path):
+        os.unlink(path)  # a stale id from an earlier run on this box
+    dist.barrier()
     uid = (C.c_uint8 * 128)()
     if dist.rank == 0:
         rc = libs.cuda.vgpu_cu_nccl_unique_id(uid)
         if rc:
             raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
-    uid_bytes = dist.bcast(bytes(uid))
-    uid = (C.c_uint8 * 128).from_buffer_copy(uid_bytes)
+        V.rendezvous_publish(path, bytes(uid))
+    else:
+        uid = (C.c_uint8 * 128).from_buffer_copy(V.rendezvous_fetch(path, 128))
     dev = C.c_void_p()
     if libs.cuda.vgpu_cu_open(dist.device, 1, 4096, C.byref(dev)):
         raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
@@ -494,9 +515,15 @@ def final_reduce(N, dist, record):
             if libs.cuda.vgpu_cu_reduce_final(dev, rec, C.sizeof(rec), allr):
                 raise RuntimeError(libs.cuda.vgpu_cu_last_error().decode())
             times.append((time.perf_counter() - t0) * 1e6)
-        return R.fold_in_rank_order(list(allr), dist.world), list(allr)[:R.REC_WIDTH], times
+        folded = V.fold_in_rank_order(list(allr), dist.world)  # the product's C++ fold
+        if folded[:15] != R.fold_in_rank_order(list(allr), dist.world)[:15]:
+            raise RuntimeError("C++ and Python rank-order folds differ")
+        return folded, list(allr)[:R.REC_WIDTH], times
     finally:
         libs.cuda.vgpu_cu_close(dev)
+        dist.barrier()
+        if dist.rank == 0 and os.path.exists(path):
+            os.unlink(path)
 
 
 def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> dict:
@@ -609,13 +636,13 @@ def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
     overhead <= 25 % at 64 MiB, and the 1 KiB fraction below the 64 MiB one."""
     out = {"report": "overhead", "apis": {}}
     cols = ["bytes", "turnaround_us", "pure_gpu_us", "overhead_us", "overhead_fraction"]
-    for api, inplace in (("inplace", True), ("span", False)):
+    for api in ("resident", "inplace", "span"):
         rows = []
         for nbytes in (1 << 10, 1 << 16, 1 << 20, 16 << 20, 64 << 20):
             sz = W.Sizes()
             sz.vecadd_n = nbytes // 8
             r = leg_workers(V, N, W, "vecadd", 1, 0, 1, steps, warmup, device, False, sz, dist,
-                            barrier=1, inplace=inplace)
+                            barrier=1, api=api)
             t_us = r["seconds"] * 1e6 / steps
             pg = r["device_stage_us"]["pure_gpu_us"] or 0.0
             up = r["device_stage_us"]["h2d_us"] or 0.0  # eager upload at SND: device time too
@@ -636,10 +663,12 @@ def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
                            "tiny_below_large": tiny["overhead_fraction"] < large["overhead_fraction"],
                            "pass": large["overhead_fraction"] <= 0.25
                                    and tiny["overhead_fraction"] < large["overhead_fraction"]}}
-    out["note"] = ("turnaround = the whole job through the client API (inplace: snd(span) copies "
-                   "the input into the pinned region, streamed so the H2D overlaps the copy, and "
-                   "the result is read in place; span: the same SND plus rcv()'s copy into a "
-                   "fresh Bytes); pure_gpu = the input's DMA busy time + the task's kernel + D2H "
+    out["note"] = ("turnaround = the whole job through the client API (resident: the input "
+                   "stays in the pinned region and is SND'd in place, the result read in place; "
+                   "inplace: snd(span) copies the input into the pinned region, streamed so the "
+                   "H2D overlaps the copy, and the result is read in place; span: the same SND "
+                   "plus rcv()'s copy into a fresh Bytes); pure_gpu = the input's DMA busy time "
+                   "+ the task's kernel + D2H "
                    "(CUDA events); the paper's figure is ~20 % at 400 MB on a C2070 "
                    "(PAPER.md:507)")
     return out
@@ -659,6 +688,20 @@ def model_summary(batches):
             "note": "model uses the clients' declared stage estimates (Fermi-style single "
                     "queue); measured is the B200 batch span from CUDA events"}
 
+
+
+# ---- e2e client APIs ------------------------------------------------------------------
+
+E2E_APIS = {
+    "resident": ("the program keeps its input in the GVM-pinned region (as a CUDA program keeps "
+                 "its I/O buffers in cudaHostAlloc'd memory) and SNDs it in place "
+                 "(snd_region_at); the result is read where the D2H left it (rcv_region). "
+                 "Every step still DMAs the input from host memory and the result back"),
+    "inplace": ("snd(span) copies the program's private input into the pinned region every "
+                "step (streamed: the GVM uploads each filled part while the next is copied); "
+                "the result is read in place (rcv_region)"),
+    "span": "the reference's API unchanged: snd(span) (streamed copy) + rcv() -> fresh Bytes",
+}
 
 
 # ---- rooflines ----------------------------------------------------------------------
@@ -808,13 +851,13 @@ def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
     return out
 
 
-def leg_overhead_n1(V, N, W, workload, steps, warmup, device, sizes, dist) -> dict:
+def leg_overhead_n1(V, N, W, workload, steps, warmup, device, sizes, dist, api="span") -> dict:
     """North-star target 'virtualization overhead under 5% at N=1': ONE SPMD
     process through the GVM vs the same process non-virtualized (own CUDA
     context, warm), same job, same steps. overhead = 1 - native/virtualized
     time per job (negative: the GVM is faster)."""
     v = leg_workers(V, N, W, workload, 1, 0, 1, steps, warmup, device, False, sizes, dist,
-                    barrier=1)
+                    barrier=1, api=api)
     n = leg_workers(V, N, W, workload, 1, 0, 1, steps, warmup, device, True, sizes, dist)
     v_ms, n_ms = v["seconds"] * 1e3 / steps, n["seconds"] * 1e3 / steps
     return {"virtualized_ms_per_job": v_ms, "native_warm_ms_per_job": n_ms,
@@ -931,10 +974,8 @@ def main():
     ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the per-kernel roofline summary of the other configs")
-    ap.add_argument("--e2e-api", default="inplace", choices=["inplace", "span"],
-                    help="client API of the e2e leg: 'inplace' = snd(span) + rcv_region() "
-                         "(result read where the D2H put it), 'span' = the reference's "
-                         "snd(span) + rcv() -> Bytes; the default line also reports the other")
+    ap.add_argument("--e2e-api", default="resident", choices=list(E2E_APIS),
+                    help="client API of the e2e leg (the line also reports the others)")
     ap.add_argument("--barrier-size", type=int, default=-1,
                     help="GVM barrier (tasks per flush); -1 = workload default")
     args = ap.parse_args()
@@ -1023,23 +1064,26 @@ def main():
     # B200 policy: eager dispatch (barrier 1) — per-client hardware queues make
     # the paper's full barrier pure latency; the barrier-P run is reported too
     barrier = 1 if args.barrier_size < 0 else args.barrier_size
-    inplace = args.e2e_api == "inplace"
+    api = args.e2e_api
     e2e = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                      args.warmup, device, False, sizes, dist, barrier=barrier, inplace=inplace)
-    # the other client API, same GVM settings
-    dist.barrier()
-    alt = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                      args.warmup, device, False, sizes, dist, barrier=barrier, inplace=not inplace)
-    alt_api = {"api": "span (reference: snd(span) + rcv() -> Bytes)" if inplace
-               else "inplace (snd(span) + rcv_region())",
-               "value": procs * world * args.steps / dist.max(alt["seconds"]), "unit": "jobs/s",
-               "client_stage_us": alt.get("client_stage_us"),
-               "device_stage_us": alt.get("device_stage_us")}
+                      args.warmup, device, False, sizes, dist, barrier=barrier, api=api)
+    # the other client APIs, same GVM settings
+    other_apis = {}
+    for other in E2E_APIS:
+        if other == api:
+            continue
+        dist.barrier()
+        o = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
+                        args.warmup, device, False, sizes, dist, barrier=barrier, api=other)
+        other_apis[other] = {"api": E2E_APIS[other],
+                             "value": procs * world * args.steps / dist.max(o["seconds"]),
+                             "unit": "jobs/s", "client_stage_us": o.get("client_stage_us"),
+                             "device_stage_us": o.get("device_stage_us")}
     paper = None
     if args.barrier_size < 0 and procs > 1:
         dist.barrier()
         pb = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, args.steps,
-                         args.warmup, device, False, sizes, dist, barrier=procs, inplace=inplace)
+                         args.warmup, device, False, sizes, dist, barrier=procs, api=api)
         paper = {"value": procs * world * args.steps / dist.max(pb["seconds"]), "unit": "jobs/s",
                  "barrier_size": procs, "client_stage_us": pb.get("client_stage_us"),
                  "device_stage_us": pb.get("device_stage_us"), "batches": pb["batches"]}
@@ -1077,7 +1121,7 @@ def main():
     if not args.no_native:
         dist.barrier()
         tv = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, False,
-                         sizes, dist, cold=True, barrier=barrier)
+                         sizes, dist, cold=True, barrier=barrier, api=api)
         tn = leg_workers(V, N, W, args.workload, procs, gid0, total_workers, 1, 0, device, True,
                          sizes, dist, cold=True)
         v_ms, n_ms = dist.max(tv["turnaround_ms"]), dist.max(tn["turnaround_ms"])
@@ -1089,7 +1133,7 @@ def main():
     overhead = None
     if not args.no_native and world == 1:
         overhead = leg_overhead_n1(V, N, W, args.workload if args.workload != "mixed" else "vecadd",
-                                   args.steps, args.warmup, device, sizes, dist)
+                                   args.steps, args.warmup, device, sizes, dist, api=api)
     clock_info = clocks.stop() if clocks else None
     all_clocks = [c for c in dist.gather(clock_info) if c]
     clock_info = merge_clocks(all_clocks) if all_clocks else None
@@ -1097,7 +1141,12 @@ def main():
     # ---- final reduction (multi-GPU only) ----------------------------------------------
     reduce_info = None
     from paper_1511_07658_b200 import reduce as R
-    record = R.record_from_workers(e2e["results"])
+    # the GVM's own fold record (GvmDaemon::fold_record: EP slices folded in
+    # first-batch order), cross-checked against what the workers received
+    record = list(e2e["gvm_fold"])
+    from_workers = R.record_from_workers(e2e["results"])
+    fold_check = {"gvm_tasks": record[0], "worker_jobs": from_workers[0] * (args.steps + args.warmup),
+                  "ep_fields_equal": record[1:15] == from_workers[1:15]}
     try:
         folded, rank0, times = final_reduce(N, dist, record)
         via = ("torch.distributed all_gather over gloo (shared-GPU test mode)"
@@ -1107,7 +1156,8 @@ def main():
                        "wall_us": statistics.median(times[1:]), "first_call_us": times[0],
                        "wall_us_note": "steady state: median of 5 calls after the first "
                                        "(the first carries the communicator's lazy setup)",
-                       "jobs_folded": folded[0]}
+                       "tasks_folded": folded[0], "source": "GvmDaemon::fold_record per GPU",
+                       "gvm_vs_workers": fold_check}
         if folded[14] > 0:
             reduce_info["ep"] = R.ep_verdict(folded, sizes.ep_m, sizes.ep_batches, rank0)
     except Exception as e:  # noqa: BLE001 - reported in the line
@@ -1147,20 +1197,15 @@ def main():
             "data": "synthetic", "config": config,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": secs * 1e3 / args.steps,
-                    "path": "bin/vgpu-spmd x P -> VgpuHandle snd/str/stp_wait/"
-                            + ("rcv_region" if inplace else "rcv") +
-                            " -> UDS+shm -> GVM (libvgpu.so) -> per-client CUDA streams",
-                    "api": ("inplace: snd(span) copies the program's input into the pinned "
-                            "region every step (streamed: the GVM uploads each filled part "
-                            "while the next is copied), the result is read where the D2H "
-                            "left it (rcv_region)") if inplace else
-                           "span: the reference's snd(span) + rcv() -> Bytes",
+                    "path": "bin/vgpu-spmd x P -> VgpuHandle (" + api + " API) -> UDS+shm -> "
+                            "GVM (libvgpu.so) -> per-client CUDA streams",
+                    "api": E2E_APIS[api],
                     "client_stage_us": e2e.get("client_stage_us"),
                     "device_stage_us": e2e.get("device_stage_us")},
             "turnaround": turnaround,
             "e2e_paper_barrier": ({k: v for k, v in paper.items() if k != "batches"}
                                   if paper else None),
-            "e2e_other_api": alt_api,
+            "e2e_other_apis": other_apis,
             "native": native,
             "vs_native": (e2e_value / native["value"]) if native else None,
             "roofline": roof,

@@ -115,6 +115,17 @@ public:
     MetricsSnapshot metrics() const;
     const GvmConfig& config() const { return cfg_; }
 
+    // B200: this GVM's partial record of the run, the input of
+    // the single cross-GPU reduction (vgpu_cu_reduce_final, folded in rank
+    // order). kFoldWidth doubles: [0] device tasks completed, [1..10] NAS EP
+    // q[0..9], [11] sx, [12] sy, [13] pairs, [14] EP batches covered, [15]
+    // result bytes returned mod 1000003. EP results are kept per slice
+    // (keyed by first_batch; a slice computed again must repeat its bits,
+    // else [14] is set to -1) and folded in first_batch order, so the
+    // floating-point sums do not depend on completion order.
+    static constexpr std::size_t kFoldWidth = 16;
+    std::array<double, kFoldWidth> fold_record() const;
+
     struct Impl;
 
 private:

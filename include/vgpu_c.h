@@ -123,6 +123,7 @@ int vgpu_client_run_task(vgpu_client* c, const void* in, uint64_t in_bytes,
  * valid until the next SND or RLS; it overwrites the region from offset 0). */
 int vgpu_client_region(vgpu_client* c, void** base, uint64_t* bytes);
 int vgpu_client_snd_region(vgpu_client* c, uint64_t bytes);
+int vgpu_client_snd_region_at(vgpu_client* c, uint64_t offset, uint64_t bytes);
 int vgpu_client_rcv_region(vgpu_client* c, const void** data, uint64_t* len);
 int vgpu_client_run_task_region(vgpu_client* c, uint64_t in_bytes, const vgpu_descriptor* d,
                                 const void** data, uint64_t* len);
@@ -157,6 +158,18 @@ int vgpu_cg_class(char cls, uint32_t* n, uint32_t* nonzer, uint32_t* niter, doub
                   double* zeta_verify);
 int vgpu_cg_make_input(uint32_t n, uint32_t nonzer, uint32_t niter, double shift, uint8_t* out,
                        uint64_t cap, uint64_t* len);
+
+/* Multi-GPU (include/vgpu/multigpu.hpp). vgpu_gvm_fold: the
+ * GVM's partial record (GvmDaemon::fold_record, 16 doubles). The NCCL id
+ * rendezvous: rank 0 publishes `n` bytes in `path` (atomic rename), other
+ * ranks fetch them (polling, timeout_ms). vgpu_fold_in_rank_order: fold the
+ * all-gathered records (nranks x 16, rank-major) in rank order into out[16].
+ * vgpu_local_cpus: host cores local to a PCI device (sysfs), *n = count. */
+int vgpu_gvm_fold(vgpu_gvm* g, double* out16);
+int vgpu_rendezvous_publish(const char* path, const void* data, uint64_t n);
+int vgpu_rendezvous_fetch(const char* path, void* out, uint64_t n, int64_t timeout_ms);
+int vgpu_fold_in_rank_order(const double* all, uint32_t nranks, double* out16);
+int vgpu_local_cpus(const char* pci_bus_id, int32_t* out, uint32_t cap, uint32_t* n);
 
 const char* vgpu_last_error(void);
 

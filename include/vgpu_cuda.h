@@ -237,6 +237,8 @@ int vgpu_cu_execute(int device, uint32_t kernel, float param, const void* in,
 uint64_t vgpu_cu_execute_launches(void);
 
 int vgpu_cu_device_count(int* n);
+/* PCI bus id of a device ("00000000:1B:00.0"), for NUMA-local placement */
+int vgpu_cu_device_pci_bus_id(int device, char* buf, int len);
 const char* vgpu_cu_strerror(int code);
 const char* vgpu_cu_last_error(void); /* thread-local detail of the last failure */
 

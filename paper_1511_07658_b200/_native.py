@@ -122,6 +122,7 @@ CUDA_API = {
     "vgpu_cu_execute": (C.c_int, [C.c_int, _U32, C.c_float, _P, _U64, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_execute_launches": (_U64, []),
     "vgpu_cu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "vgpu_cu_device_pci_bus_id": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),
     "vgpu_cu_strerror": (C.c_char_p, [C.c_int]),
     "vgpu_cu_last_error": (C.c_char_p, []),
     "vgpu_cu_resident_bench": (C.c_int, [C.c_int, _U32, C.c_float, _U32, C.POINTER(_P),
@@ -145,6 +146,11 @@ HOST_API = {
     "vgpu_gvm_batches": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_gvm_metrics_csv": (C.c_int, [_P, C.c_char_p, _U64, C.POINTER(_U64)]),
     "vgpu_unlink_instance": (C.c_int, [C.c_char_p, _U32]),
+    "vgpu_gvm_fold": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "vgpu_rendezvous_publish": (C.c_int, [C.c_char_p, _P, _U64]),
+    "vgpu_rendezvous_fetch": (C.c_int, [C.c_char_p, _P, _U64, _I64]),
+    "vgpu_fold_in_rank_order": (C.c_int, [C.POINTER(C.c_double), _U32, C.POINTER(C.c_double)]),
+    "vgpu_local_cpus": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _U32, C.POINTER(_U32)]),
     "vgpu_client_req": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
     "vgpu_client_free": (None, [_P]),
     "vgpu_client_id": (_U32, [_P]),
@@ -157,6 +163,7 @@ HOST_API = {
     "vgpu_client_rcv": (C.c_int, [_P, _P, _U64, C.POINTER(_U64)]),
     "vgpu_client_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64)]),
     "vgpu_client_snd_region": (C.c_int, [_P, _U64]),
+    "vgpu_client_snd_region_at": (C.c_int, [_P, _U64, _U64]),
     "vgpu_client_rcv_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_U64)]),
     "vgpu_client_run_task_region": (C.c_int, [_P, _U64, C.POINTER(DescriptorC), C.POINTER(_P),
                                               C.POINTER(_U64)]),

@@ -1056,6 +1056,12 @@ const char* vgpu_cu_strerror(int code) {
     }
 }
 
+int vgpu_cu_device_pci_bus_id(int device, char* buf, int len) {
+    if (!buf || len < 13) return VGPU_CU_EINVAL;
+    CK(cudaDeviceGetPCIBusId(buf, len, device));
+    return VGPU_CU_OK;
+}
+
 int vgpu_cu_device_count(int* n) {
     if (!n) return VGPU_CU_EINVAL;
     *n = 0;

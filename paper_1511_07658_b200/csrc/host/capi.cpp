@@ -9,6 +9,7 @@
 #include "vgpu/daemon.hpp"
 #include "vgpu/device.hpp"
 #include "vgpu/model.hpp"
+#include "vgpu/multigpu.hpp"
 #include "vgpu/npb_cg.hpp"
 #include "vgpu_c.h"
 
@@ -89,6 +90,46 @@ void copy_out(const Bytes& b, void* out, std::uint64_t cap, std::uint64_t* len) 
 }  // namespace
 
 extern "C" {
+
+int vgpu_gvm_fold(vgpu_gvm* g, double* out16) {
+    if (!g || !out16) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto rec = g->daemon->fold_record();
+        std::memcpy(out16, rec.data(), sizeof(double) * rec.size());
+    });
+}
+
+int vgpu_rendezvous_publish(const char* path, const void* data, uint64_t n) {
+    if (!path || (!data && n)) return VGPU_E_INVALID;
+    return guarded([&] {
+        multigpu::publish_id(path, {static_cast<const std::uint8_t*>(data), static_cast<std::size_t>(n)});
+    });
+}
+
+int vgpu_rendezvous_fetch(const char* path, void* out, uint64_t n, int64_t timeout_ms) {
+    if (!path || (!out && n)) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto id = multigpu::fetch_id(path, n, std::chrono::milliseconds(std::max<int64_t>(0, timeout_ms)));
+        std::memcpy(out, id.data(), id.size());
+    });
+}
+
+int vgpu_fold_in_rank_order(const double* all, uint32_t nranks, double* out16) {
+    if (!all || !out16 || nranks == 0) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto rec = multigpu::fold_in_rank_order({all, static_cast<std::size_t>(nranks) * 16}, nranks);
+        std::memcpy(out16, rec.data(), sizeof(double) * rec.size());
+    });
+}
+
+int vgpu_local_cpus(const char* pci_bus_id, int32_t* out, uint32_t cap, uint32_t* n) {
+    if (!pci_bus_id || !n || (!out && cap)) return VGPU_E_INVALID;
+    return guarded([&] {
+        const auto cpus = multigpu::local_cpus(pci_bus_id);
+        *n = static_cast<uint32_t>(cpus.size());
+        for (uint32_t i = 0; i < std::min<uint32_t>(cap, *n); ++i) out[i] = cpus[i];
+    });
+}
 
 const char* vgpu_last_error(void) { return t_err.c_str(); }
 
@@ -271,6 +312,11 @@ int vgpu_client_region(vgpu_client* c, void** base, uint64_t* bytes) {
 int vgpu_client_snd_region(vgpu_client* c, uint64_t bytes) {
     if (!c) return VGPU_E_INVALID;
     return guarded([&] { c->handle.snd_region(bytes); });
+}
+
+int vgpu_client_snd_region_at(vgpu_client* c, uint64_t offset, uint64_t bytes) {
+    if (!c) return VGPU_E_INVALID;
+    return guarded([&] { c->handle.snd_region_at(offset, bytes); });
 }
 
 int vgpu_client_rcv_region(vgpu_client* c, const void** data, uint64_t* len) {

@@ -82,6 +82,7 @@ struct Session {
     Phase phase = Phase::Idle;
     std::uint64_t generation = 0;
     std::uint64_t input_len = 0;
+    std::uint64_t input_offset = 0;  // the input's place in the region (in-place API)
     Bytes input;                 // snapshot copy for host payloads
     Bytes output;                // host-payload result
     std::uint64_t output_len = 0;
@@ -131,6 +132,8 @@ struct InFlight {
     Clock::time_point dispatch_wall;
     TaskMetrics vmetrics;  // virtual-clock values, fixed at flush
     float upload_h2d_us = 0.0f;
+    bool ep = false;             // a NAS EP slice: its result joins the GVM's fold
+    std::uint64_t ep_first = 0;  // its first batch (the fold key)
 };
 
 struct BatchState {
@@ -174,6 +177,10 @@ struct GvmDaemon::Impl {
     std::uint64_t batches_flushed = 0;
     Micros busy_us = 0;
     std::uint64_t device_tasks = 0;
+    // the GVM's partial record (GvmDaemon::fold_record), under metrics_mu
+    std::map<std::uint64_t, vgpu_ep_result> ep_slices;
+    bool ep_mismatch = false;
+    std::uint64_t fold_tasks = 0, fold_bytes = 0;
 
     Impl(GvmConfig c, std::unique_ptr<DaemonTransport> t, const PayloadRegistry* p)
         : cfg(std::move(c)),
@@ -314,8 +321,8 @@ struct GvmDaemon::Impl {
         lease.shm_bytes = cfg.per_client_shm_bytes;
         lease.stream_hint = slot - 1;
         lease.shm_name = transport->region_name(slot);
+        publish_leases();  // before the ACK: the client may read it right away
         transport->reply_origin(origin, {Opcode::Ack, slot, m.task_id, encode_lease(lease)});
-        publish_leases();
     }
 
     void on_snd(const Message& m, Session& s) {
@@ -328,14 +335,16 @@ struct GvmDaemon::Impl {
                         "SND payload must be a u64 length");
         const std::uint64_t* len = &snd->length;
         DataRegion& region = transport->region(m.client_id);
-        if (*len > region.size())
+        if (*len > region.size() || snd->offset > region.size() - *len)
             return nack(m.client_id, m.task_id, ErrCode::Size, "data exceeds leased region");
-        if (snd->flags & kSndStreamed) return start_stream(m, s, *len);
+        if (snd->flags & kSndStreamed) return start_stream(m, s, *len, snd->offset);
         s.input_len = *len;
+        s.input_offset = snd->offset;
         s.input.clear();
         s.input_resident = false;
         s.input_inline = false;
-        std::memcpy(s.head, region.data(), std::min<std::uint64_t>(*len, sizeof s.head));
+        const std::uint8_t* in = region.data() + s.input_offset;
+        std::memcpy(s.head, in, std::min<std::uint64_t>(*len, sizeof s.head));
         if (dev && cfg.data_plane == DataPlane::ZeroCopy && *len <= sizeof s.head) {
             // tiny inputs (NAS EP's 32-byte parameter record): the host copy
             // above IS the SND snapshot; ACK now, no DMA round trip (EP
@@ -348,8 +357,7 @@ struct GvmDaemon::Impl {
             // eager upload: the SND snapshot is taken by DMA into the slot's
             // HBM buffer; the ACK goes out when the copy has landed, so the
             // client's H2D overlaps the other clients' host work
-            const int rc = vgpu_cu_upload(dev, m.client_id, region.data(), *len,
-                                          upload_tag(m.client_id, s));
+            const int rc = vgpu_cu_upload(dev, m.client_id, in, *len, upload_tag(m.client_id, s));
             if (rc != VGPU_CU_OK)
                 return nack(m.client_id, m.task_id, ErrCode::Internal,
                             std::string("upload failed: ") + vgpu_cu_last_error());
@@ -361,9 +369,9 @@ struct GvmDaemon::Impl {
         if (cfg.data_plane == DataPlane::Snapshot) {
             // reference timing of the region read (daemon.cpp:248)
             if (dev)
-                std::memcpy(stage_in(m.client_id), region.data(), *len);
+                std::memcpy(stage_in(m.client_id), in, *len);
             else
-                s.input.assign(region.data(), region.data() + *len);
+                s.input.assign(in, in + *len);
         }
         s.phase = Phase::DataIn;
         ack(m.client_id, m.task_id);
@@ -377,11 +385,12 @@ struct GvmDaemon::Impl {
     // modes wait for the fill to complete and then take the plain SND path.
     // Frames from this client meanwhile queue in its backlog, as for an
     // eager upload, so per-client order is unchanged.
-    void start_stream(const Message& m, Session& s, std::uint64_t len) {
+    void start_stream(const Message& m, Session& s, std::uint64_t len, std::uint64_t offset) {
         if (!transport->stream_fill(m.client_id))
             return nack(m.client_id, m.task_id, ErrCode::Malformed,
                         "streamed SND needs a transport with fill counters");
         s.input_len = len;
+        s.input_offset = offset;
         s.input.clear();
         s.input_resident = false;
         s.input_inline = false;
@@ -400,7 +409,8 @@ struct GvmDaemon::Impl {
             s.phase = Phase::DataIn;
             pending_snd_acks[m.client_id].push_back(m.task_id);
         } else {
-            s.stream.snd = {Opcode::Snd, m.client_id, m.task_id, encode_u64(len)};
+            s.stream.snd = {Opcode::Snd, m.client_id, m.task_id,
+                            offset ? encode_snd(len, kSndOffset, offset) : encode_u64(len)};
         }
         ++s.uploads;  // holds the client's later frames until the SND is answered
         ++streams_active;
@@ -435,7 +445,7 @@ struct GvmDaemon::Impl {
             if (fill <= s.stream.issued || (!full && fill - s.stream.issued < kStreamGranule))
                 continue;
             moved = true;
-            std::uint8_t* base = transport->region(id).data();
+            std::uint8_t* base = transport->region(id).data() + s.input_offset;
             const int rc = vgpu_cu_upload_part(dev, id, base + s.stream.issued, s.stream.issued,
                                                fill - s.stream.issued, full ? VGPU_CU_UPLOAD_END : 0,
                                                0);
@@ -563,8 +573,8 @@ struct GvmDaemon::Impl {
         s.generation = 0;  // drop in-flight results for this lease
         s.input.clear();
         s.output.clear();
-        ack(m.client_id, m.task_id);
         publish_leases();
+        ack(m.client_id, m.task_id);
     }
 
     // ---- barrier ------------------------------------------------------------
@@ -642,7 +652,7 @@ struct GvmDaemon::Impl {
             const DeviceKernel* dk = payloads->device_kernel(t.profile.payload_id);
             const std::uint8_t* src = nullptr;
             if (cfg.data_plane == DataPlane::ZeroCopy || !dev)
-                src = transport->region(t.client_id).data();
+                src = transport->region(t.client_id).data() + (live ? s->input_offset : 0);
             else
                 src = stage_in(t.client_id);
 
@@ -707,6 +717,12 @@ struct GvmDaemon::Impl {
                 f.out_at = OutAt::Staging;
             }
             ct.out_bytes = out_bytes;
+            if (dk->kernel == VGPU_CU_K_EP && in_len == sizeof(vgpu_ep_params)) {
+                vgpu_ep_params ep;
+                std::memcpy(&ep, s->head, sizeof ep);
+                f.ep = true;
+                f.ep_first = ep.first_batch;
+            }
             ct.tag = next_tag++;
             s->device_busy = true;
             inflight.emplace(ct.tag, f);
@@ -774,7 +790,7 @@ struct GvmDaemon::Impl {
             else if (cfg.data_plane == DataPlane::Snapshot)
                 in = ByteView(stage_in(t.client_id), s->input_len);
             else
-                in = ByteView(transport->region(t.client_id).data(), s->input_len);
+                in = ByteView(transport->region(t.client_id).data() + s->input_offset, s->input_len);
             try {
                 out = payloads->execute(t.profile.payload_id, in);
                 if (out.size() > cfg.per_client_shm_bytes) {
@@ -846,6 +862,7 @@ struct GvmDaemon::Impl {
             } else {
                 s->output_len = f.out_bytes;
                 s->out_at = f.out_at;
+                fold_result(f);
                 s->phase = Phase::Done;
                 transport->notify(f.client_id);
             }
@@ -864,6 +881,21 @@ struct GvmDaemon::Impl {
                                         : us_between(bs.dispatch_wall, now);
             record_batch({f.batch_key, bs.style, bs.task_count, bs.model_makespan, measured});
         }
+    }
+
+    // The task's result is where the D2H (or the mapped write) left it and
+    // the client has not been told yet: fold it into the GVM's record.
+    void fold_result(const InFlight& f) {
+        std::lock_guard lk(metrics_mu);
+        ++fold_tasks;
+        fold_bytes = (fold_bytes + f.out_bytes) % 1000003u;
+        if (!f.ep || f.out_bytes != sizeof(vgpu_ep_result)) return;
+        const std::uint8_t* src = f.out_at == OutAt::Staging ? stage_out(f.client_id)
+                                                             : transport->region(f.client_id).data();
+        vgpu_ep_result r;
+        std::memcpy(&r, src, sizeof r);
+        auto [it, fresh] = ep_slices.emplace(f.ep_first, r);
+        if (!fresh && std::memcmp(&it->second, &r, sizeof r) != 0) ep_mismatch = true;
     }
 
     void upload_done(const vgpu_cu_done& d) {
@@ -990,6 +1022,22 @@ void GvmDaemon::stop() {
     if (!impl_->running.exchange(false)) return;
     impl_->transport->wake();
     if (impl_->dispatcher.joinable()) impl_->dispatcher.join();
+}
+
+std::array<double, GvmDaemon::kFoldWidth> GvmDaemon::fold_record() const {
+    std::lock_guard lk(impl_->metrics_mu);
+    std::array<double, kFoldWidth> rec{};
+    rec[0] = static_cast<double>(impl_->fold_tasks);
+    for (const auto& [first, r] : impl_->ep_slices) {  // first_batch order
+        for (int i = 0; i < 10; ++i) rec[1 + i] += static_cast<double>(r.q[i]);
+        rec[11] = rec[11] + r.sx;
+        rec[12] = rec[12] + r.sy;
+        rec[13] += static_cast<double>(r.pairs);
+        rec[14] += static_cast<double>(r.n_batches);
+    }
+    if (impl_->ep_mismatch) rec[14] = -1.0;
+    rec[15] = static_cast<double>(impl_->fold_bytes);
+    return rec;
 }
 
 MetricsSnapshot GvmDaemon::metrics() const {

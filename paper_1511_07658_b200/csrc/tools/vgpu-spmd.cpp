@@ -2,12 +2,17 @@
 // reference harness, proj/src/bench/bench.cpp:186-231).
 //
 //   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul
-//             --rounds R [--instance NAME [--inplace] | --native [--device D]]
+//             --rounds R [--instance NAME [--inplace|--resident] | --native [--device D]]
 //
 // --inplace: the in-place result (VgpuHandle::rcv_region): every round the
 // program reads the result where the D2H left it in the leased, page-locked
 // region instead of rcv()'s copy into a fresh Bytes. The input still goes in
 // by snd(span) — a real copy of the program's private input every round.
+// --resident: the program keeps its input in the page-locked region (placed
+// once after the result's bytes, as a CUDA program keeps its I/O buffers in
+// cudaHostAlloc'd memory) and SNDs it in place every round
+// (snd_region_at); the result is read in place. The GVM still DMAs the
+// input from host memory and the result back to it in every round.
 //
 // Builds its private input, leases a VGPU (retrying until the daemon is
 // up) — or, with --native, uses its OWN CUDA context through NativeVgpu —
@@ -75,7 +80,7 @@ std::uint64_t sample_hash(std::span<const std::uint8_t> out, std::size_t stride)
 int main(int argc, char** argv) {
     std::string instance, workload = "vecadd";
     std::uint32_t worker = 0, workers = 1, rounds = 1;
-    bool native = false, connect_after_go = false, inplace = false;
+    bool native = false, connect_after_go = false, inplace = false, resident = false;
     int device = 0;
     vgpu::wl::Sizes sizes;
     for (int i = 1; i < argc; ++i) {
@@ -92,6 +97,7 @@ int main(int argc, char** argv) {
             else if (a == "--rounds") rounds = std::stoul(val());
             else if (a == "--native") native = true;
             else if (a == "--inplace") inplace = true;
+            else if (a == "--resident") resident = true;
             else if (a == "--connect-after-go") connect_after_go = true;
             else if (a == "--device") device = std::stoi(val());
             else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(val());
@@ -146,6 +152,22 @@ int main(int argc, char** argv) {
         }
     };
     if (!connect_after_go && !connect()) return 3;
+    // --resident: the input's place in the region, after the result's bytes
+    const std::uint64_t in_off = (job.output_bytes + 65535) & ~std::uint64_t{65535};
+    auto place_input = [&]() -> bool {
+        if (!resident || !vh) return true;
+        const auto reg = vh->region();
+        if (in_off + job.input.size() > reg.size()) {
+            std::printf("{\"worker\": %u, \"ok\": false, \"err\": \"--resident: region of %zu B "
+                        "holds no %llu B input after a %llu B result\"}\n",
+                        worker, reg.size(), (unsigned long long)job.input.size(),
+                        (unsigned long long)in_off);
+            return false;
+        }
+        std::memcpy(reg.data() + in_off, job.input.data(), job.input.size());
+        return true;
+    };
+    if (!connect_after_go && !place_input()) return 3;
     std::printf("READY %d\n", static_cast<int>(getpid()));
     std::fflush(stdout);
     char go = 0;
@@ -158,7 +180,7 @@ int main(int argc, char** argv) {
     bool ok = true;
     std::string check_json;
     const std::int64_t t_go = now_ns();
-    if (connect_after_go && !connect()) return 3;
+    if (connect_after_go && (!connect() || !place_input())) return 3;
     try {
         for (std::uint32_t r = 0; r < rounds; ++r) {
             t0[r] = now_ns();
@@ -168,16 +190,20 @@ int main(int argc, char** argv) {
                 out = nh->run_task(job.input, job.desc);
                 view = out;
             } else {  // run_task, verb by verb so each stage is timed
-                // SND copies the program's input into the page-locked region
-                // (streamed: the GVM uploads each filled part while the next
-                // is copied) in both modes
-                vh->snd(job.input);
+                if (resident) {
+                    vh->snd_region_at(in_off, job.input.size());  // input stays in the region
+                } else {
+                    // SND copies the program's input into the page-locked
+                    // region (streamed: the GVM uploads each filled part
+                    // while the next is copied)
+                    vh->snd(job.input);
+                }
                 const std::int64_t a = now_ns();
                 vh->str(job.desc);
                 const std::int64_t b = now_ns();
                 vh->stp_wait();
                 const std::int64_t c = now_ns();
-                if (inplace) {
+                if (inplace || resident) {
                     view = vh->rcv_region();  // consumed in place: no copy out
                 } else {
                     out = vh->rcv();

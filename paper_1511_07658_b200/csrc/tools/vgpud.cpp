@@ -3,6 +3,16 @@
 // available, so flags are parsed by hand ("--name value" or "--name=value").
 // Serves REQ/SND/STR/STP/RCV/RLS until SIGINT/SIGTERM, then writes the
 // per-task metrics CSV (reference daemon.cpp:31-39 schema).
+//
+// Multi-GPU: with --nranks N --rank R --rendezvous PATH this
+// GVM is rank R of N per-GPU GVMs. At start rank 0 creates the NCCL unique
+// id and publishes it in PATH (the others wait for the file), every rank
+// joins the communicator, and only then is the daemon ready. At shutdown
+// each rank all-gathers its fold record (GvmDaemon::fold_record) in the one
+// ncclAllGather of the run; the records are folded in rank order and rank 0
+// writes the result as JSON to --reduce-out (--fold-out: every rank's own
+// record, with or without a communicator). --cpus LIST pins the daemon
+// (default: the cores local to its GPU, from sysfs).
 #include <csignal>
 #include <cstdio>
 #include <cstdlib>
@@ -12,7 +22,14 @@
 #include <string>
 #include <thread>
 
+#include <cstring>
+#include <iomanip>
+#include <sstream>
+#include <vector>
+
 #include "vgpu/daemon.hpp"
+#include "vgpu/multigpu.hpp"
+#include "vgpu_cuda.h"
 
 namespace {
 
@@ -25,7 +42,9 @@ void usage() {
         "      [--barrier-size K] [--clock virtual|real] [--scale F] [--device-sms N]\n"
         "      [--device-max-kernels N] [--device-slots-per-sm N] [--t-init US]\n"
         "      [--t-ctx-switch US] [--metrics-out PATH] [--device ORDINAL]\n"
-        "      [--data-plane zero-copy|snapshot] [--ready-file PATH]");
+        "      [--data-plane zero-copy|snapshot] [--ready-file PATH]\n"
+        "      [--nranks N --rank R --rendezvous PATH [--reduce-out PATH]]\n"
+        "      [--fold-out PATH] [--cpus LIST|none]");
 }
 
 }  // namespace
@@ -53,7 +72,8 @@ int main(int argc, char** argv) {
         }
     }
     vgpu::GvmConfig cfg;
-    std::string metrics_out, ready_file;
+    std::string metrics_out, ready_file, rendezvous, reduce_out, fold_out, cpus = "auto";
+    int nranks = 0, rank = 0;
     try {
         for (const auto& [k, v] : opt) {
             if (k == "instance") cfg.instance = v;
@@ -74,6 +94,12 @@ int main(int argc, char** argv) {
             else if (k == "metrics-out") metrics_out = v;
             else if (k == "ready-file") ready_file = v;
             else if (k == "device") cfg.cuda_device = std::stoi(v);
+            else if (k == "nranks") nranks = std::stoi(v);
+            else if (k == "rank") rank = std::stoi(v);
+            else if (k == "rendezvous") rendezvous = v;
+            else if (k == "reduce-out") reduce_out = v;
+            else if (k == "fold-out") fold_out = v;
+            else if (k == "cpus") cpus = v;
             else if (k == "data-plane") {
                 if (v == "zero-copy") cfg.data_plane = vgpu::DataPlane::ZeroCopy;
                 else if (v == "snapshot") cfg.data_plane = vgpu::DataPlane::Snapshot;
@@ -87,6 +113,22 @@ int main(int argc, char** argv) {
         return 2;
     }
 
+    if (nranks > 0 && (rank < 0 || rank >= nranks || rendezvous.empty())) {
+        std::cerr << "vgpud: --nranks needs --rank in [0, nranks) and --rendezvous\n";
+        return 2;
+    }
+    // NUMA-local placement of the daemon (its dispatcher and the CUDA
+    // driver threads inherit the mask)
+    std::vector<int> cpu_set;
+    if (cpus == "auto") {
+        char bus[32] = {};
+        if (vgpu_cu_device_pci_bus_id(cfg.cuda_device, bus, sizeof bus) == VGPU_CU_OK)
+            cpu_set = vgpu::multigpu::local_cpus(bus);
+    } else if (cpus != "none") {
+        cpu_set = vgpu::multigpu::parse_cpulist(cpus);
+    }
+    const bool pinned = vgpu::multigpu::pin_to(cpu_set);
+
     std::unique_ptr<vgpu::GvmDaemon> daemon;
     try {
         daemon = vgpu::GvmDaemon::start_os(cfg);
@@ -94,13 +136,85 @@ int main(int argc, char** argv) {
         std::cerr << "vgpud: " << e.what() << '\n';
         return 1;
     }
+    // the cross-GPU communicator: joined before the daemon reports ready
+    vgpu_cu_dev* comm_dev = nullptr;
+    if (nranks > 0) {
+        try {
+            if (vgpu_cu_open(cfg.cuda_device, 1, 4096, &comm_dev) != VGPU_CU_OK)
+                throw std::runtime_error(std::string("device: ") + vgpu_cu_last_error());
+            std::vector<std::uint8_t> id(VGPU_CU_NCCL_ID_BYTES);
+            if (rank == 0) {
+                if (vgpu_cu_nccl_unique_id(id.data()) != VGPU_CU_OK)
+                    throw std::runtime_error(vgpu_cu_last_error());
+                vgpu::multigpu::publish_id(rendezvous, id);
+            } else {
+                id = vgpu::multigpu::fetch_id(rendezvous, id.size(), std::chrono::seconds(300));
+            }
+            if (vgpu_cu_comm_init(comm_dev, id.data(), nranks, rank) != VGPU_CU_OK)
+                throw std::runtime_error(vgpu_cu_last_error());
+        } catch (const std::exception& e) {
+            std::cerr << "vgpud: rank " << rank << " could not join the communicator: " << e.what()
+                      << '\n';
+            daemon->stop();
+            if (comm_dev) vgpu_cu_close(comm_dev);
+            return 1;
+        }
+    }
     std::signal(SIGINT, on_signal);
     std::signal(SIGTERM, on_signal);
     std::cout << "vgpud: instance '" << cfg.instance << "' serving " << cfg.max_clients
-              << " clients on CUDA device " << cfg.cuda_device << std::endl;
+              << " clients on CUDA device " << cfg.cuda_device
+              << (nranks > 0 ? " as rank " + std::to_string(rank) + " of " + std::to_string(nranks) : "")
+              << (pinned ? " (pinned to " + std::to_string(cpu_set.size()) + " local cores)" : "")
+              << std::endl;
     if (!ready_file.empty()) std::ofstream(ready_file) << "ready\n";
     while (!g_stop) std::this_thread::sleep_for(std::chrono::milliseconds(20));
     daemon->stop();
+    int rc = 0;
+    if (!fold_out.empty()) {  // this GVM's own record (also without a communicator)
+        const auto rec = daemon->fold_record();
+        std::ofstream out(fold_out);
+        out << std::setprecision(17) << "{\"rank\": " << rank << ", \"record\": [";
+        for (std::size_t i = 0; i < rec.size(); ++i) out << (i ? ", " : "") << rec[i];
+        out << "]}\n";
+    }
+    if (comm_dev) {
+        // the run's single cross-GPU collective
+        const auto rec = daemon->fold_record();
+        std::vector<double> all(static_cast<std::size_t>(nranks) * rec.size());
+        const auto t0 = std::chrono::steady_clock::now();
+        if (vgpu_cu_reduce_final(comm_dev, rec.data(), sizeof(double) * rec.size(), all.data()) !=
+            VGPU_CU_OK) {
+            std::cerr << "vgpud: final reduction failed: " << vgpu_cu_last_error() << '\n';
+            rc = 1;
+        } else if (rank == 0 && !reduce_out.empty()) {
+            const double us = std::chrono::duration<double, std::micro>(
+                                  std::chrono::steady_clock::now() - t0).count();
+            const auto folded = vgpu::multigpu::fold_in_rank_order(all, nranks);
+            auto hex = [](double d) {
+                std::uint64_t b;
+                std::memcpy(&b, &d, 8);
+                std::ostringstream o;
+                o << std::hex << b;
+                return o.str();
+            };
+            std::ofstream out(reduce_out);
+            out << std::setprecision(17) << "{\"nranks\": " << nranks << ", \"collective\": "
+                << "\"ncclAllGather of " << sizeof(double) * rec.size() << " B per GVM\", "
+                << "\"reduce_us\": " << us << ", \"record\": [";
+            for (std::size_t i = 0; i < folded.size(); ++i) out << (i ? ", " : "") << folded[i];
+            out << "], \"sx_bits\": \"" << hex(folded[11]) << "\", \"sy_bits\": \""
+                << hex(folded[12]) << "\", \"per_rank\": [";
+            for (int r = 0; r < nranks; ++r) {
+                out << (r ? ", " : "") << "[";
+                for (std::size_t i = 0; i < rec.size(); ++i)
+                    out << (i ? ", " : "") << all[r * rec.size() + i];
+                out << "]";
+            }
+            out << "]}\n";
+        }
+        vgpu_cu_close(comm_dev);
+    }
     const auto m = daemon->metrics();
     if (metrics_out.empty()) {
         vgpu::write_metrics_csv(m, std::cout);
@@ -112,5 +226,5 @@ int main(int argc, char** argv) {
         }
         vgpu::write_metrics_csv(m, out);
     }
-    return 0;
+    return rc;
 }

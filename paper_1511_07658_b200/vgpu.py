@@ -178,12 +178,39 @@ class GvmDaemon:
         return [{k: getattr(arr[i], k) for k, _ in N.BatchMetricsC._fields_}
                 for i in range(n.value)]
 
+    def fold(self) -> list:
+        """This GVM's partial record (GvmDaemon::fold_record, 16 doubles): the
+        input of the single cross-GPU reduction."""
+        out = (C.c_double * 16)()
+        _check(_libs().host.vgpu_gvm_fold(self._h, out))
+        return list(out)
+
     def metrics_csv(self) -> str:
         n = C.c_uint64()
         _check(_libs().host.vgpu_gvm_metrics_csv(self._h, None, 0, C.byref(n)))
         buf = C.create_string_buffer(n.value + 1)
         _check(_libs().host.vgpu_gvm_metrics_csv(self._h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
+
+
+def rendezvous_publish(path: str, data: bytes) -> None:
+    """Rank 0 publishes the NCCL unique id (atomic file rename)."""
+    _check(_libs().host.vgpu_rendezvous_publish(path.encode(), data, len(data)))
+
+
+def rendezvous_fetch(path: str, n: int, timeout_ms: int = 300000) -> bytes:
+    """Ranks > 0 wait for the id rank 0 published."""
+    buf = (C.c_uint8 * n)()
+    _check(_libs().host.vgpu_rendezvous_fetch(path.encode(), buf, n, timeout_ms))
+    return bytes(buf)
+
+
+def fold_in_rank_order(flat, nranks: int) -> list:
+    """The all-gathered records (rank-major) folded in rank order (C++)."""
+    a = (C.c_double * (16 * nranks))(*flat)
+    out = (C.c_double * 16)()
+    _check(_libs().host.vgpu_fold_in_rank_order(a, nranks, out))
+    return list(out)
 
 
 def unlink_os_instance(instance: str, max_clients: int) -> None:
@@ -272,6 +299,10 @@ class VgpuHandle:
 
     def snd_region(self, nbytes: int) -> None:
         _check(_libs().host.vgpu_client_snd_region(self._h, nbytes))
+
+    def snd_region_at(self, offset: int, nbytes: int) -> None:
+        """Input at [offset, offset + nbytes) of the region (results land at 0)."""
+        _check(_libs().host.vgpu_client_snd_region_at(self._h, offset, nbytes))
 
     def rcv_region(self) -> memoryview:
         """The result in place (valid until the next SND or RLS)."""

@@ -165,6 +165,11 @@ def input_bytes(kind: str, sz: Sizes = Sizes()) -> int:
             "es": 32 + 16 * sz.es_atoms}[kind]
 
 
-def region_bytes(workload: str, sz: Sizes = Sizes()) -> int:
+def region_bytes(workload: str, sz: Sizes = Sizes(), resident: bool = False) -> int:
+    """Per-client region. resident: the input stays in the region after the
+    result's bytes (vgpu-spmd --resident places it at the result size
+    rounded up to 64 KiB)."""
     kinds = KINDS if workload == "mixed" else (workload,)
+    if resident:
+        return max(((output_bytes(k, sz) + 65535) & ~65535) + input_bytes(k, sz) for k in kinds)
     return max(max(input_bytes(k, sz), output_bytes(k, sz)) for k in kinds)

@@ -9,6 +9,7 @@
 #include <sys/wait.h>
 #include <unistd.h>
 
+#include <cmath>
 #include <cstring>
 #include <thread>
 
@@ -16,6 +17,7 @@
 
 #include "minitest.hpp"
 #include "vgpu/client.hpp"
+#include "vgpu/multigpu.hpp"
 
 using namespace vgpu;
 using namespace std::chrono_literals;
@@ -645,6 +647,91 @@ TEST_CASE("gvm os: streamed SND — the ACK waits for the fill, odd sizes, copy 
         CHECK(ch->region().data()[n - 1] == 7);
         ch->send({Opcode::Rls, lease.client_id, 0, {}});
         CHECK(ch->recv(2s).has_value());
+    }
+    d->stop();
+}
+
+TEST_CASE("multi-GPU: NCCL id rendezvous through a file, across processes") {
+    namespace mg = vgpu::multigpu;
+    const std::string path = "/tmp/vgpu-test-rdv." + std::to_string(getpid());
+    unlink(path.c_str());
+    std::vector<std::uint8_t> id(128);
+    for (std::size_t i = 0; i < id.size(); ++i) id[i] = static_cast<std::uint8_t>(i * 37 + 5);
+    // ranks 1..3 start first and wait for the file
+    std::vector<pid_t> kids;
+    for (int r = 1; r < 4; ++r) {
+        const pid_t pid = fork();
+        if (pid == 0) {
+            try {
+                const auto got = mg::fetch_id(path, id.size(), std::chrono::seconds(10));
+                _exit(got == id ? 0 : 3);
+            } catch (...) {
+                _exit(4);
+            }
+        }
+        kids.push_back(pid);
+    }
+    std::this_thread::sleep_for(30ms);
+    mg::publish_id(path, id);
+    for (pid_t k : kids) {
+        int st = 0;
+        waitpid(k, &st, 0);
+        CHECK(WIFEXITED(st));
+        CHECK(WEXITSTATUS(st) == 0);
+    }
+    // a short or foreign file is never taken for an id
+    CHECK_THROWS_AS((void)mg::fetch_id(path, 64, std::chrono::milliseconds(20)), std::runtime_error);
+    unlink(path.c_str());
+    CHECK_THROWS_AS((void)mg::fetch_id(path, 128, std::chrono::milliseconds(20)), std::runtime_error);
+}
+
+TEST_CASE("multi-GPU: records fold in rank order; placement helpers") {
+    namespace mg = vgpu::multigpu;
+    std::vector<double> all(3 * mg::kRecordWidth, 0.0);
+    const double sx[3] = {0.1, 1e16, -1e16};  // order-sensitive in binary64
+    for (int r = 0; r < 3; ++r) {
+        double* rec = all.data() + r * mg::kRecordWidth;
+        rec[0] = 16;
+        rec[1] = 1000 + r;
+        rec[11] = sx[r];
+        rec[14] = 4096;
+        rec[15] = 1000000;
+    }
+    const auto f = mg::fold_in_rank_order(all, 3);
+    CHECK(f[0] == 48);
+    CHECK(f[1] == 3003);
+    CHECK(f[11] == ((0.0 + 0.1) + 1e16) + -1e16);  // left to right, not 0.1
+    CHECK(f[14] == 3 * 4096);
+    CHECK(f[15] == std::fmod(3000000.0, 1000003.0));
+    all[mg::kRecordWidth + 14] = -1.0;  // rank 1 saw a slice change bits
+    CHECK(mg::fold_in_rank_order(all, 3)[14] == -1.0);
+    CHECK_THROWS_AS((void)mg::fold_in_rank_order(std::span<const double>(all).first(20), 3),
+                    std::invalid_argument);
+    CHECK(mg::parse_cpulist("0-3,8,10-11\n") == std::vector<int>({0, 1, 2, 3, 8, 10, 11}));
+    CHECK(mg::parse_cpulist("5, 2-3,x,3").size() == 3);
+    CHECK(mg::local_cpus("0000:ff:1f.7").empty());  // no such device: no placement
+}
+
+TEST_CASE("gvm os: the doorbell page publishes the lease count") {
+    GvmConfig g = cfg(3, 1, 1000);
+    g.instance = "leases" + std::to_string(getpid());
+    g.per_client_shm_bytes = 4096;
+    unlink_os_instance(g.instance, g.max_clients);
+    auto d = GvmDaemon::start(g, open_os_daemon_transport(g.instance, 3, g.per_client_shm_bytes),
+                              &host_registry());
+    {
+        VgpuHandle a = req(g.instance);
+        VgpuHandle b = req(g.instance);
+        auto ch = open_os_client_channel(g.instance);
+        ch->send({Opcode::Req, 0, 0, {}});
+        auto r = ch->recv(2s);
+        REQUIRE(r.has_value());
+        ch->attach_lease(*parse_lease(r->payload));
+        CHECK(ch->leased_clients() == 3);
+        b.rls();
+        ch->send({Opcode::Stp, parse_lease(r->payload)->client_id, 0, {}});  // any round trip
+        (void)ch->recv(2s);
+        CHECK(ch->leased_clients() == 2);
     }
     d->stop();
 }

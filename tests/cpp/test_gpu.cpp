@@ -391,7 +391,7 @@ TEST_CASE("[gpu] OS transport: forked SPMD clients through one GVM (real clock)"
                     for (int rep = 0; rep < 10; ++rep) {
                         // >= 4 MiB inputs: streamed SNDs (parts uploaded while
                         // the copy runs), odd lengths included
-                        const Bytes in = vadd_input((1u << 20) + 5u * (rep % 3), w * 100 + rep);
+                        const Bytes in = vadd_input((1u << 20) - 5u * (rep % 3), w * 100 + rep);
                         if (h.run_task(in, desc("vector-add", false)) != vadd_expect(in)) _exit(3);
                     }
                     h.rls();

@@ -109,3 +109,47 @@ def test_ep_verdict_rank0_class_a():
     assert v["rank0_class_a_verified"] and v["verified"] and "npb_rel_err" not in v
     rank0[11] *= 1.0 + 1e-6
     assert not R.ep_verdict(folded, 29, 8192, rank0)["verified"]
+
+
+def _rank_main_product(rank, world, port, path, out_q):
+    """The product's bootstrap and fold (libvgpu.so through ctypes): GVM 0
+    publishes the 128-byte NCCL id in a file, the others wait for it; the
+    gathered records fold in rank order in C++ (vgpu_fold_in_rank_order)."""
+    from paper_1511_07658_b200 import vgpu as V
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if rank == 0:
+        uid = bytes((i * 37 + 11) & 0xFF for i in range(128))  # stands in for ncclGetUniqueId
+        V.rendezvous_publish(path, uid)
+    else:
+        uid = V.rendezvous_fetch(path, 128, timeout_ms=60000)
+    workers = [2 * rank, 2 * rank + 1]
+    results = [_worker_result(w, oracle.ep_job(24, 64 * w, 64)) for w in workers]
+    rec = torch.tensor(R.record_from_workers(results), dtype=torch.float64)
+    gathered = [torch.zeros_like(rec) for _ in range(world)]
+    dist.all_gather(gathered, rec)
+    flat = torch.cat(gathered).tolist()
+    out_q.put((rank, uid, V.fold_in_rank_order(flat, world), R.fold_in_rank_order(flat, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_file_bootstrap_and_cpp_fold():
+    import tempfile
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = os.path.join(tempfile.mkdtemp(), "ncclid")
+    procs = [ctx.Process(target=_rank_main_product, args=(r, 2, port, path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {r: rest for r, *rest in (q.get(timeout=240) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0][0] == got[1][0]  # every rank holds GVM 0's id
+    for r in (0, 1):
+        cpp, py = got[r][1], got[r][2]
+        assert struct.pack("<15d", *cpp[:15]) == struct.pack("<15d", *py[:15])
+    assert struct.pack("<16d", *got[0][1]) == struct.pack("<16d", *got[1][1])
+    assert R.ep_verdict(got[0][1], 24)["verified"]
