@@ -51,7 +51,7 @@ METRIC = "aggregate SPMD jobs/sec per GPU at N procs/GPU vs non-virtualized; ker
 L2_BYTES = 126 << 20
 # arithmetic type each workload's path computes in (EP: binary64 + integer LCG)
 DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f64", "cg": "f64",
-         "vmul": "f32", "es": "f32"}
+         "vmul": "f32", "es": "f32", "mg": "f64"}
 
 
 def log(*a):
@@ -546,8 +546,12 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> d
     t_in = max(1, int(round(st["h2d_us"] or 0)))
     t_comp = max(1, int(round(st["comp_us"] or 0)))
     t_out = max(1, int(round(st["d2h_us"] or 0)))
-    rows = {"concurrent": [], "device_filling": []}
+    rows = {"concurrent": [], "device_filling": [], "b200_blocks": []}
     style = None
+    # the B200 block-scheduler spec: this task's real CTA count and resident
+    # CTAs per SM (vgpu_cu_task_shape), CTAs drawing free slots in queue order
+    kind = W.kind_of(workload, 0)
+    grid_b, per_sm = V.task_shape(W.PAYLOAD[kind], W.job_input(workload, 0, procs, sizes), device)
     for n in range(1, procs + 1):
         r = leg_workers(V, N, W, workload, n, 0, procs, reps, 2, device, False, sizes, dist,
                         barrier=n, window=1_000_000, snapshot=True)
@@ -561,12 +565,20 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> d
             model = V.model_simulate(style, n, t_in, t_comp, t_out, grid, sms, kern, slots)
             rows[name].append({"n": n, "model_us": model, "measured_us": measured,
                                "deviation_pct": 100.0 * abs(measured - model) / max(1, model)})
+        model = V.model_simulate_fluid(style, n, t_in, t_comp, t_out, grid_b, 148, per_sm)
+        rows["b200_blocks"].append({"n": n, "model_us": model, "measured_us": measured,
+                                    "deviation_pct": 100.0 * abs(measured - model) / max(1, model)})
     out = {"workload": W.CONFIG_NAME[workload], "style": "PS2" if style else "PS1",
            "task_triple_us": {"t_in": t_in, "t_comp": t_comp, "t_out": t_out},
+           "b200_blocks_spec": {"ctas_per_task": grid_b, "ctas_per_sm": per_sm, "sms": 148,
+                                "rule": "DeviceSpec::fluid_blocks: CTAs draw free slots in "
+                                        "queue order"},
+           "criterion6": "proj/tests/acceptance.cpp:246-268: real-clock mean deviation < 5 %",
            "paper": "PAPER.md:505: EP(M24) 0.42 %, VecMult 4.76 % mean deviation on a C2070"}
     for name, rs in rows.items():
-        out[name] = {"rows": rs, "mean_deviation_pct":
-                     statistics.mean([x["deviation_pct"] for x in rs]) if rs else None}
+        mean = statistics.mean([x["deviation_pct"] for x in rs]) if rs else None
+        out[name] = {"rows": rs, "mean_deviation_pct": mean,
+                     "criterion6_pass": mean is not None and mean < 5.0}
     return out
 
 
@@ -601,7 +613,7 @@ def sweep(V, N, W, workload, device, sizes, dist, procs=0) -> dict:
     return {"report": "sweep", "workload": W.CONFIG_NAME[workload], "rows": rows, "csv": csv}
 
 
-def speedup(V, N, W, device, dist, procs=8) -> dict:
+def speedup(V, N, W, device, dist, procs=8, warm=False) -> dict:
     """The paper's speedup summary (Fig. "sp": seven
     benchmarks at 8 SPMD processes, 1.4x-7.4x on its 2015 GPU) on B200:
     per workload, 8 processes started together, each running one job;
@@ -609,20 +621,72 @@ def speedup(V, N, W, device, dist, procs=8) -> dict:
     pageable copies) / virtualized turnaround (REQ on the open GVM). Same
     definitions as --sweep, at N = 8 only, over every workload built."""
     rows = []
-    for wl in ("ep", "vecadd", "mm", "bs", "cg", "es", "vmul"):
+    for wl in ("ep", "vecadd", "mm", "bs", "cg", "es", "vmul", "mg"):
         sz = W.Sizes()
         try:
             tv = leg_workers(V, N, W, wl, procs, 0, procs, 1, 0, device, False, sz, dist,
                              cold=True, barrier=procs)
             tn = leg_workers(V, N, W, wl, procs, 0, procs, 1, 0, device, True, sz, dist, cold=True)
             v_ms, n_ms = tv["turnaround_ms"], tn["turnaround_ms"]
-            rows.append({"benchmark": wl, "workload": W.CONFIG_NAME[wl], "n": procs,
-                         "virtualized_ms": v_ms, "native_ms": n_ms, "speedup": n_ms / v_ms})
+            row = {"benchmark": wl, "workload": W.CONFIG_NAME[wl], "n": procs,
+                   "virtualized_ms": v_ms, "native_ms": n_ms, "speedup": n_ms / v_ms}
+            if warm:
+                # contexts already up: 3 timed rounds after 2 warm-up rounds
+                wv = leg_workers(V, N, W, wl, procs, 0, procs, 3, 2, device, False, sz, dist,
+                                 barrier=1, api="resident")
+                wn = leg_workers(V, N, W, wl, procs, 0, procs, 3, 2, device, True, sz, dist)
+                row["warm_speedup"] = wn["seconds"] / wv["seconds"]
+            rows.append(row)
         except Exception as e:  # noqa: BLE001 - reported in the row
             rows.append({"benchmark": wl, "error": str(e)[:200]})
     return {"report": "speedup", "procs": procs, "rows": rows,
             "paper": "8 processes, 7 benchmarks (EP M30, VecAdd, MM, MG, BS, CG, ES): 1.4x-7.4x "
-                     "(PAPER.md:513); here MG is not built and VecMul is added"}
+                     "(PAPER.md:513); VecMul is added"}
+
+
+def acceptance(V, N, W, device, dist, steps, warmup) -> dict:
+    """The reference's acceptance criteria 5-7 (proj/tests/acceptance.cpp:
+    203-297) re-run on B200 data as pass/fail rows. The reference checks
+    them on its simulated Fermi timings; on real hardware some premises do
+    not hold, and the rows say so rather than bending the thresholds."""
+    rows = []
+    sp = speedup(V, N, W, device, dist, warm=True)
+    good = {r["benchmark"]: r for r in sp["rows"] if "speedup" in r}
+    for key, label in (("speedup", "cold (native creates its context)"),
+                       ("warm_speedup", "warm (contexts already up)")):
+        vals = {b: r[key] for b, r in good.items() if key in r}
+        band = all(1.4 <= v <= 7.4 for v in vals.values())
+        rows.append({"criterion": 5, "check": f"speedup at N=8 in [1.4, 7.4], {label}",
+                     "values": vals, "pass": band})
+        fast = [b for b in ("ep", "cg", "mg") if b in vals]
+        slow = [b for b in ("vecadd", "vmul", "bs") if b in vals]
+        order = all(vals[f] > vals[sl] for f in fast for sl in slow)
+        rows.append({"criterion": 5, "check": f"compute-intensive (EP, CG, MG) > transfer-bound "
+                                              f"(VecAdd, VecMul, BS), {label}",
+                     "values": vals, "pass": order})
+    for wl in ("ep", "vecadd"):
+        vm = validate_model(V, N, W, wl, device, W.Sizes(), dist)
+        for spec in ("concurrent", "device_filling", "b200_blocks"):
+            rows.append({"criterion": 6, "check": f"{wl}: model mean deviation < 5 % ({spec} spec)",
+                         "value": vm[spec]["mean_deviation_pct"], "pass": vm[spec]["criterion6_pass"]})
+    oc = overhead_curve(V, N, W, device, dist, steps, warmup)
+    for api, v in oc["apis"].items():
+        c7 = v["criterion7"]
+        rows.append({"criterion": 7, "check": f"{api} API: overhead <= 25 % at 64 MiB",
+                     "value": c7["large_overhead_fraction"], "pass": c7["large_le_0_25"]})
+        rows.append({"criterion": 7, "check": f"{api} API: 1 KiB overhead fraction below 64 MiB's",
+                     "value": [v["rows"][0]["overhead_fraction"], c7["large_overhead_fraction"]],
+                     "pass": c7["tiny_below_large"]})
+    return {"report": "acceptance", "rows": rows, "speedup": sp, "overhead": oc,
+            "notes": {
+                "5": "the band is the paper's C2070 figure; on B200 a native process spends ~2.4 s "
+                     "creating its context (cold) and the GVM's batched kernels are far shorter "
+                     "than a timeslice (warm), so speedups leave the band upward",
+                "6": "b200_blocks is the B200 block-scheduler spec (DeviceSpec::fluid_blocks with "
+                     "the task's real CTA count and occupancy)",
+                "7": "the reference's 1 KiB-below-64 MiB rule assumes a 400 ms simulated compute "
+                     "per job; a real 1 KiB vector add runs ~25 us on the device, below the "
+                     "~60 us fixed protocol round trips"}}
 
 
 def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
@@ -707,7 +771,7 @@ E2E_APIS = {
 # ---- rooflines ----------------------------------------------------------------------
 
 KIND_BOUND = {"vecadd": "hbm", "bs": "hbm", "ep": "fp64", "mm": "fp32", "cg": "hbm", "vmul": "hbm",
-              "es": "rsqrt"}
+              "es": "rsqrt", "mg": "hbm"}
 
 
 def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
@@ -832,7 +896,7 @@ def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
     workloads (8 x NAS CG class A, 8 x electrostatics, 4 x vector-mul),
     device-resident. The headline workload's own entry is the line's
     `roofline`."""
-    shapes = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "cg": 8, "es": 8, "vmul": 4}
+    shapes = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "cg": 8, "es": 8, "vmul": 4, "mg": 8}
     out = {}
     for kind, procs in shapes.items():
         if kind == workload:
@@ -951,7 +1015,7 @@ def main():
     # quoted on the largest single-GPU configuration (C3 and C4 both run 16
     # processes; C3 moves the most bytes per job: 48 MiB in, 32 MiB out)
     ap.add_argument("--workload", default="bs",
-                    choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul", "es"])
+                    choices=["vecadd", "ep", "bs", "mm", "mixed", "cg", "vmul", "es", "mg"])
     ap.add_argument("--procs", type=int, default=0, help="SPMD processes per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-native", action="store_true")
@@ -968,6 +1032,8 @@ def main():
     ap.add_argument("--speedup", action="store_true",
                     help="paper speedup summary: every workload at 8 processes, turnaround "
                          "native / virtualized (report)")
+    ap.add_argument("--acceptance", action="store_true",
+                    help="the reference's acceptance criteria 5-7 on B200 data (report)")
     ap.add_argument("--overhead-curve", action="store_true",
                     help="virtualization overhead across payload sizes, 1 process (report)")
     ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
@@ -1027,8 +1093,10 @@ def main():
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
     device = dist.device
-    if args.validate_model or args.sweep or args.overhead_curve or args.speedup:
+    if args.validate_model or args.sweep or args.overhead_curve or args.speedup or args.acceptance:
         if dist.rank == 0:
+            if args.acceptance:
+                emit(acceptance(V, N, W, device, dist, args.steps, args.warmup))
             if args.speedup:
                 emit(speedup(V, N, W, device, dist))
             if args.validate_model:

@@ -137,6 +137,11 @@ int vgpu_native_run_task(int cuda_device, const vgpu_descriptor* d, const void* 
 uint64_t vgpu_model_simulate(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
                              uint64_t t_out, uint32_t grid, uint32_t sms,
                              uint32_t max_kernels, uint32_t slots_per_sm);
+/* simulate() with DeviceSpec::fluid_blocks (B200 block scheduler as a
+ * fluid): grid = the task's CTAs, ctas_per_sm = its resident CTAs per SM */
+uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
+                                   uint64_t t_out, uint32_t grid, uint32_t sms,
+                                   uint32_t ctas_per_sm);
 int vgpu_model_classify(uint64_t t_in, uint64_t t_comp, uint64_t t_out);
 uint64_t vgpu_model_no_vt(uint32_t n, uint64_t t_init, uint64_t t_ctx, uint64_t t_in,
                           uint64_t t_comp, uint64_t t_out);
@@ -170,6 +175,14 @@ int vgpu_rendezvous_publish(const char* path, const void* data, uint64_t n);
 int vgpu_rendezvous_fetch(const char* path, void* out, uint64_t n, int64_t timeout_ms);
 int vgpu_fold_in_rank_order(const double* all, uint32_t nranks, double* out16);
 int vgpu_local_cpus(const char* pci_bus_id, int32_t* out, uint32_t cap, uint32_t* n);
+
+/* NPB MG problems for the nas-mg payload (client side, NPB's untimed zran3;
+ * include/vgpu/npb_mg.hpp). vgpu_mg_class: class 'S','W','A','B','C' ->
+ * nx, nit, smoother set and the published rnm2. vgpu_mg_make_input: the
+ * input bytes into out (cap); *len = bytes needed (out = NULL sizes it). */
+int vgpu_mg_class(char cls, uint32_t* nx, uint32_t* nit, uint32_t* coeffs, double* rnm2_verify);
+int vgpu_mg_make_input(uint32_t nx, uint32_t nit, uint32_t coeffs, uint8_t* out, uint64_t cap,
+                       uint64_t* len);
 
 const char* vgpu_last_error(void);
 

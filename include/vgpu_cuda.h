@@ -50,7 +50,8 @@ enum vgpu_cu_kernel {
     VGPU_CU_K_VMUL = 6,      /* "vector-mul"    a||b fp32 -> a*b               */
     VGPU_CU_K_CG = 7,        /* "nas-cg"        vgpu_cg_header + CSR -> vgpu_cg_result */
     VGPU_CU_K_ES = 8,        /* "electrostatics" vgpu_es_header + atoms -> lattice potential */
-    VGPU_CU_K_COUNT = 9
+    VGPU_CU_K_MG = 9,        /* "nas-mg"        vgpu_mg_header + v -> vgpu_mg_result */
+    VGPU_CU_K_COUNT = 10
 };
 
 /* NAS EP job (input, 32 bytes little-endian). The job computes batches
@@ -115,6 +116,39 @@ typedef struct vgpu_es_header {
     float spacing;
     uint32_t reserved[3]; /* must be 0 */
 } vgpu_es_header;
+
+/* NAS MG job (NPB 3.x mg.f, the timed part): `nit` V-cycles (mg3P + resid)
+ * of the 3-D Poisson problem A u = v on an nx^3 periodic grid from u = 0,
+ * then ||r||_2 / sqrt(nx^3) and max |r| (NPB's rnm2, rnmu). The SPMD
+ * program builds v with NPB's zran3 (untimed in NPB too): input =
+ * vgpu_mg_header | double v[nx][nx][nx] (the interior, i1 fastest).
+ * coeffs 0: the smoother of classes S/W/A, 1: of classes B/C/D. */
+typedef struct vgpu_mg_header {
+    uint32_t nx;       /* power of two, 4 .. 512 */
+    uint32_t nit;
+    uint32_t coeffs;
+    uint32_t reserved; /* must be 0 */
+} vgpu_mg_header;
+
+typedef struct vgpu_mg_result {
+    double rnm2;
+    double rnmu;
+    uint32_t nx;
+    uint32_t nit;
+    uint64_t reserved;
+} vgpu_mg_result;
+
+/* Bytes of the nas-mg input, and of the job's device workspace (u and r on
+ * every level k = 1..log2(nx), (2^k + 2)^3 doubles each, plus the norm's
+ * per-plane partials). */
+static inline uint64_t vgpu_mg_input_bytes(uint32_t nx) {
+    return sizeof(vgpu_mg_header) + 8ull * nx * nx * nx;
+}
+static inline uint64_t vgpu_mg_workspace_bytes(uint32_t nx) {
+    uint64_t b = 0;
+    for (uint32_t m = 2; m <= nx; m *= 2) b += 2ull * 8ull * (m + 2ull) * (m + 2ull) * (m + 2ull);
+    return b + 16ull * nx + 256;
+}
 
 /* Black-Scholes constants (CUDA SDK formulation). */
 #define VGPU_BS_RISKFREE 0.02f
@@ -237,6 +271,12 @@ int vgpu_cu_execute(int device, uint32_t kernel, float param, const void* in,
 uint64_t vgpu_cu_execute_launches(void);
 
 int vgpu_cu_device_count(int* n);
+/* One task's launch shape: the CTAs its share of a batched launch gets and
+ * the kernel's resident CTAs per SM (cudaOccupancy), for the model's B200
+ * block-scheduler spec. Kernels that size their grid to the device report
+ * the SM count and 1. */
+int vgpu_cu_task_shape(int device, uint32_t kernel, const void* in, uint64_t in_bytes,
+                       uint32_t* ctas, uint32_t* ctas_per_sm);
 /* PCI bus id of a device ("00000000:1B:00.0"), for NUMA-local placement */
 int vgpu_cu_device_pci_bus_id(int device, char* buf, int len);
 const char* vgpu_cu_strerror(int code);
@@ -287,7 +327,9 @@ typedef struct vgpu_cu_link_result {
     double bidir_gbs;
     uint64_t bytes;
 } vgpu_cu_link_result;
-int vgpu_cu_link_probe(int device, uint64_t bytes, uint32_t reps, vgpu_cu_link_result* out);
+#define VGPU_CU_LINK_SHM 1u /* flags: POSIX shm pages registered in place (the data plane's kind) */
+int vgpu_cu_link_probe(int device, uint64_t bytes, uint32_t reps, uint32_t flags,
+                       vgpu_cu_link_result* out);
 
 /* ---- multi-GPU: the single final reduction (NCCL over NVLink) --------- */
 #define VGPU_CU_NCCL_ID_BYTES 128

@@ -36,6 +36,21 @@ class CgResult(C.Structure):
                 ("n", C.c_uint32), ("nnz", C.c_uint64)]
 
 
+class MgResult(C.Structure):
+    _fields_ = [("rnm2", C.c_double), ("rnmu", C.c_double), ("nx", C.c_uint32),
+                ("nit", C.c_uint32), ("reserved", C.c_uint64)]
+
+
+# NPB 3.x MG classes (mg.f / npbparams): nx (= ny = nz), nit, smoother set,
+# published verification value of rnm2 (epsilon 1e-8)
+NPB_MG = {
+    "S": (32, 4, 0, 0.5307707005734e-04),
+    "W": (128, 4, 0, 0.6467329375339e-05),
+    "A": (256, 4, 0, 0.2433365309069e-05),
+    "B": (256, 20, 1, 0.1800564401355e-05),
+}
+
+
 class EpResult(C.Structure):
     _fields_ = [("q", C.c_uint64 * 10), ("sx", C.c_double), ("sy", C.c_double),
                 ("pairs", C.c_uint64), ("n_batches", C.c_uint64)]
@@ -72,6 +87,10 @@ def lib() -> C.CDLL:
         L.vo_es.restype = C.c_int
         L.vo_cg_run.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(CgResult)]
         L.vo_cg_run.restype = C.c_int
+        L.vo_mg_make_input.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64]
+        L.vo_mg_make_input.restype = C.c_uint64
+        L.vo_mg_run.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(MgResult), C.c_void_p]
+        L.vo_mg_run.restype = C.c_int
         _lib = L
     return _lib
 
@@ -172,6 +191,29 @@ def cg_run(inp: bytes) -> "CgResult":
     if lib().vo_cg_run(inp, len(inp), C.byref(r)):
         raise ValueError("malformed nas-cg input")
     return r
+
+
+def mg_make_input(nx: int, nit: int, coeffs: int) -> bytes:
+    """NPB zran3's right-hand side as the nas-mg input (header + nx^3 doubles)."""
+    need = lib().vo_mg_make_input(nx, nit, coeffs, None, 0)
+    buf = C.create_string_buffer(need)
+    lib().vo_mg_make_input(nx, nit, coeffs, buf, need)
+    return buf.raw
+
+
+def mg_run(inp: bytes, with_u: bool = False):
+    """The timed part of NPB MG on the CPU: MgResult (and the finest u with
+    its ghost layer, (nx+2)^3, when with_u)."""
+    r = MgResult()
+    nx = int(np.frombuffer(inp[:4], np.uint32)[0])
+    u = np.empty((nx + 2) ** 3, np.float64) if with_u else None
+    if lib().vo_mg_run(inp, len(inp), C.byref(r), u.ctypes.data if with_u else None):
+        raise ValueError("malformed nas-mg input")
+    return (r, u) if with_u else r
+
+
+def mg_from_bytes(b: bytes) -> "MgResult":
+    return MgResult.from_buffer_copy(bytes(b[:C.sizeof(MgResult)]))
 
 
 def cg_from_bytes(b: bytes) -> "CgResult":

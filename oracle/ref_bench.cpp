@@ -9,7 +9,8 @@
 //
 // Registry: the reference builtins (vector-add is the reference's own CPU
 // arithmetic, OpenMP-parallel) plus, for workloads the reference has no
-// arithmetic for, the oracle restatements (nas-ep, black-scholes, sgemm)
+// arithmetic for, the oracle restatements (nas-ep, black-scholes, sgemm,
+// nas-cg, nas-mg, vector-mul, electrostatics)
 // registered through the reference's register_payload (payload.hpp:36).
 //
 // --native: SURVEY.md §8(d)(ii), the reference's per-process CPU path: the
@@ -134,10 +135,33 @@ vgpu::Bytes cg_makea(char cls) {
     throw std::invalid_argument("unknown NPB CG class");
 }
 
+vgpu::Bytes mg_payload(vgpu::ByteView in) {
+    vgpu_mg_result r;
+    if (vo_mg_run(in.data(), in.size(), &r, nullptr) != 0)
+        throw vgpu::PayloadError(vgpu::PayloadError::Kind::MalformedInput, "nas-mg input");
+    vgpu::Bytes out(sizeof r);
+    std::memcpy(out.data(), &r, sizeof r);
+    return out;
+}
+
+// the MG program's zran3: the oracle's NPB restatement
+vgpu::Bytes mg_make(char cls) {
+    static const struct { char c; std::uint32_t nx, nit, coeffs; } kClasses[] = {
+        {'S', 32, 4, 0}, {'W', 128, 4, 0}, {'A', 256, 4, 0}, {'B', 256, 20, 1}, {'C', 512, 20, 1}};
+    for (const auto& k : kClasses)
+        if (k.c == cls) {
+            vgpu::Bytes b(vo_mg_make_input(k.nx, k.nit, k.coeffs, nullptr, 0));
+            vo_mg_make_input(k.nx, k.nit, k.coeffs, b.data(), b.size());
+            return b;
+        }
+    throw std::invalid_argument("unknown NPB MG class");
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     vgpu::wl::cg_builder() = cg_makea;
+    vgpu::wl::mg_builder() = mg_make;
     std::string workload = "vecadd", instance = "refbench" + std::to_string(getpid());
     std::uint32_t procs = 4, rounds = 3, warmup = 1;
     bool native = false;
@@ -162,6 +186,7 @@ int main(int argc, char** argv) {
         else if (a == "--bs-n") sizes.bs_n = std::stoull(v);
         else if (a == "--mm-n") sizes.mm_n = std::stoul(v);
         else if (a == "--cg-class") sizes.cg_class = v[0];
+        else if (a == "--mg-class") sizes.mg_class = v[0];
         else if (a == "--es-atoms") sizes.es_atoms = std::stoul(v);
     }
     const std::uint32_t total = warmup + rounds;
@@ -181,6 +206,7 @@ int main(int argc, char** argv) {
     reg.register_payload("nas-cg", cg_payload);
     reg.register_payload("vector-mul", vmul_payload);
     reg.register_payload("electrostatics", es_payload);
+    reg.register_payload("nas-mg", mg_payload);
     const unsigned cores = std::max(1u, std::thread::hardware_concurrency());
     const unsigned omp_threads = native ? std::max(1u, cores / procs) : cores;
 

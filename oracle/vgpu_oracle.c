@@ -439,3 +439,305 @@ float vo_rng_uniform(uint64_t* s, float lo, float hi) {
     const double u = (double)(vo_rng_next(s) >> 11) * (1.0 / 9007199254740992.0);
     return (float)(lo + (hi - lo) * u);
 }
+
+/* ---- NAS MG (NPB 3.x mg.f, serial: zran3, resid, psinv, rprj3, interp,
+ * comm3, norm2u3, mg3P) -------------------------------------------------
+ * Arrays are Fortran-ordered with 1-based indices (i1 fastest) and one
+ * ghost layer: level k holds (2^k + 2)^3 points. Every point's arithmetic
+ * follows mg.f's expression order (left to right, no contraction: the file
+ * is built with -ffp-contract=off); the GPU evaluates the same expressions
+ * with explicitly rounded operations, so grids match bit for bit. The only
+ * reduction, norm2u3's sum of squares, uses the fixed order both sides
+ * share: per i3 plane, 256 lanes each summing the points
+ * p = lane, lane + 256, ... of the plane's nx^2 interior points in order,
+ * lanes combined by the stride-doubling tree, planes added in i3 order. */
+
+#define MGI(n, i1, i2, i3) ((size_t)((i1) - 1) + (size_t)(n) * ((size_t)((i2) - 1) + (size_t)(n) * (size_t)((i3) - 1)))
+
+/* NPB randlc: x <- a x mod 2^46, returns x 2^-46 (integer form, exact) */
+static double mg_randlc(uint64_t* x, uint64_t a) {
+    *x = (*x * a) & ((1ull << 46) - 1);
+    return (double)*x * 0x1p-46;
+}
+
+static uint64_t mg_power(uint64_t a, uint64_t n) { /* mg.f power(): a^n mod 2^46 */
+    uint64_t r = 1, aj = a;
+    while (n) {
+        if (n & 1) r = (r * aj) & ((1ull << 46) - 1);
+        aj = (aj * aj) & ((1ull << 46) - 1);
+        n >>= 1;
+    }
+    return r;
+}
+
+/* comm3: periodic ghost layer (serial mg.f comm3, three sweeps in order) */
+static void mg_comm3(double* u, int n) {
+    for (int i3 = 2; i3 <= n - 1; ++i3)
+        for (int i2 = 2; i2 <= n - 1; ++i2) {
+            u[MGI(n, 1, i2, i3)] = u[MGI(n, n - 1, i2, i3)];
+            u[MGI(n, n, i2, i3)] = u[MGI(n, 2, i2, i3)];
+        }
+    for (int i3 = 2; i3 <= n - 1; ++i3)
+        for (int i1 = 1; i1 <= n; ++i1) {
+            u[MGI(n, i1, 1, i3)] = u[MGI(n, i1, n - 1, i3)];
+            u[MGI(n, i1, n, i3)] = u[MGI(n, i1, 2, i3)];
+        }
+    for (int i2 = 1; i2 <= n; ++i2)
+        for (int i1 = 1; i1 <= n; ++i1) {
+            u[MGI(n, i1, i2, 1)] = u[MGI(n, i1, i2, n - 1)];
+            u[MGI(n, i1, i2, n)] = u[MGI(n, i1, i2, 2)];
+        }
+}
+
+/* resid: r = v - A u (a(1) = 0 as mg.f assumes), then comm3(r). v and r
+ * may be the same array. */
+static void mg_resid(const double* u, const double* v, double* r, int n, const double a[4]) {
+    double* u1 = malloc(sizeof(double) * (size_t)n);
+    double* u2 = malloc(sizeof(double) * (size_t)n);
+    for (int i3 = 2; i3 <= n - 1; ++i3)
+        for (int i2 = 2; i2 <= n - 1; ++i2) {
+            for (int i1 = 1; i1 <= n; ++i1) {
+                u1[i1 - 1] = u[MGI(n, i1, i2 - 1, i3)] + u[MGI(n, i1, i2 + 1, i3)] +
+                             u[MGI(n, i1, i2, i3 - 1)] + u[MGI(n, i1, i2, i3 + 1)];
+                u2[i1 - 1] = u[MGI(n, i1, i2 - 1, i3 - 1)] + u[MGI(n, i1, i2 + 1, i3 - 1)] +
+                             u[MGI(n, i1, i2 - 1, i3 + 1)] + u[MGI(n, i1, i2 + 1, i3 + 1)];
+            }
+            for (int i1 = 2; i1 <= n - 1; ++i1)
+                r[MGI(n, i1, i2, i3)] = v[MGI(n, i1, i2, i3)] - a[0] * u[MGI(n, i1, i2, i3)] -
+                                        a[2] * (u2[i1 - 1] + u1[i1 - 2] + u1[i1]) -
+                                        a[3] * (u2[i1 - 2] + u2[i1]);
+        }
+    free(u1);
+    free(u2);
+    mg_comm3(r, n);
+}
+
+/* psinv: u = u + C r (c(3) = 0 as mg.f assumes), then comm3(u) */
+static void mg_psinv(const double* r, double* u, int n, const double c[4]) {
+    double* r1 = malloc(sizeof(double) * (size_t)n);
+    double* r2 = malloc(sizeof(double) * (size_t)n);
+    for (int i3 = 2; i3 <= n - 1; ++i3)
+        for (int i2 = 2; i2 <= n - 1; ++i2) {
+            for (int i1 = 1; i1 <= n; ++i1) {
+                r1[i1 - 1] = r[MGI(n, i1, i2 - 1, i3)] + r[MGI(n, i1, i2 + 1, i3)] +
+                             r[MGI(n, i1, i2, i3 - 1)] + r[MGI(n, i1, i2, i3 + 1)];
+                r2[i1 - 1] = r[MGI(n, i1, i2 - 1, i3 - 1)] + r[MGI(n, i1, i2 + 1, i3 - 1)] +
+                             r[MGI(n, i1, i2 - 1, i3 + 1)] + r[MGI(n, i1, i2 + 1, i3 + 1)];
+            }
+            for (int i1 = 2; i1 <= n - 1; ++i1)
+                u[MGI(n, i1, i2, i3)] = u[MGI(n, i1, i2, i3)] + c[0] * r[MGI(n, i1, i2, i3)] +
+                                        c[1] * (r[MGI(n, i1 - 1, i2, i3)] + r[MGI(n, i1 + 1, i2, i3)] +
+                                                r1[i1 - 1]) +
+                                        c[2] * (r2[i1 - 1] + r1[i1 - 2] + r1[i1]);
+        }
+    free(r1);
+    free(r2);
+    mg_comm3(u, n);
+}
+
+/* rprj3: restrict r (fine, m points per dim) to s (coarse, mj = m/2 + 1),
+ * then comm3(s); d = 1 (the fine grid is never 3 wide here) */
+static void mg_rprj3(const double* r, int m, double* s, int mj) {
+    double* x1 = malloc(sizeof(double) * (size_t)m);
+    double* y1 = malloc(sizeof(double) * (size_t)m);
+    for (int j3 = 2; j3 <= mj - 1; ++j3) {
+        const int i3 = 2 * j3 - 1;
+        for (int j2 = 2; j2 <= mj - 1; ++j2) {
+            const int i2 = 2 * j2 - 1;
+            for (int j1 = 2; j1 <= mj; ++j1) {
+                const int i1 = 2 * j1 - 1;
+                x1[i1 - 2] = r[MGI(m, i1 - 1, i2 - 1, i3)] + r[MGI(m, i1 - 1, i2 + 1, i3)] +
+                             r[MGI(m, i1 - 1, i2, i3 - 1)] + r[MGI(m, i1 - 1, i2, i3 + 1)];
+                y1[i1 - 2] = r[MGI(m, i1 - 1, i2 - 1, i3 - 1)] + r[MGI(m, i1 - 1, i2 - 1, i3 + 1)] +
+                             r[MGI(m, i1 - 1, i2 + 1, i3 - 1)] + r[MGI(m, i1 - 1, i2 + 1, i3 + 1)];
+            }
+            for (int j1 = 2; j1 <= mj - 1; ++j1) {
+                const int i1 = 2 * j1 - 1;
+                const double y2 = r[MGI(m, i1, i2 - 1, i3 - 1)] + r[MGI(m, i1, i2 - 1, i3 + 1)] +
+                                  r[MGI(m, i1, i2 + 1, i3 - 1)] + r[MGI(m, i1, i2 + 1, i3 + 1)];
+                const double x2 = r[MGI(m, i1, i2 - 1, i3)] + r[MGI(m, i1, i2 + 1, i3)] +
+                                  r[MGI(m, i1, i2, i3 - 1)] + r[MGI(m, i1, i2, i3 + 1)];
+                s[MGI(mj, j1, j2, j3)] =
+                    0.5 * r[MGI(m, i1, i2, i3)] +
+                    0.25 * (r[MGI(m, i1 - 1, i2, i3)] + r[MGI(m, i1 + 1, i2, i3)] + x2) +
+                    0.125 * (x1[i1 - 2] + x1[i1] + y2) + 0.0625 * (y1[i1 - 2] + y1[i1]);
+            }
+        }
+    }
+    free(x1);
+    free(y1);
+    mg_comm3(s, mj);
+}
+
+/* interp: u (fine, n points) += prolongation of z (coarse, mm points) */
+static void mg_interp(const double* z, int mm, double* u, int n) {
+    double* z1 = malloc(sizeof(double) * (size_t)mm);
+    double* z2 = malloc(sizeof(double) * (size_t)mm);
+    double* z3 = malloc(sizeof(double) * (size_t)mm);
+    for (int i3 = 1; i3 <= mm - 1; ++i3)
+        for (int i2 = 1; i2 <= mm - 1; ++i2) {
+            for (int i1 = 1; i1 <= mm; ++i1) {
+                z1[i1 - 1] = z[MGI(mm, i1, i2 + 1, i3)] + z[MGI(mm, i1, i2, i3)];
+                z2[i1 - 1] = z[MGI(mm, i1, i2, i3 + 1)] + z[MGI(mm, i1, i2, i3)];
+                z3[i1 - 1] = z[MGI(mm, i1, i2 + 1, i3 + 1)] + z[MGI(mm, i1, i2, i3 + 1)] + z1[i1 - 1];
+            }
+            for (int i1 = 1; i1 <= mm - 1; ++i1) {
+                u[MGI(n, 2 * i1 - 1, 2 * i2 - 1, 2 * i3 - 1)] += z[MGI(mm, i1, i2, i3)];
+                u[MGI(n, 2 * i1, 2 * i2 - 1, 2 * i3 - 1)] +=
+                    0.5 * (z[MGI(mm, i1 + 1, i2, i3)] + z[MGI(mm, i1, i2, i3)]);
+            }
+            for (int i1 = 1; i1 <= mm - 1; ++i1) {
+                u[MGI(n, 2 * i1 - 1, 2 * i2, 2 * i3 - 1)] += 0.5 * z1[i1 - 1];
+                u[MGI(n, 2 * i1, 2 * i2, 2 * i3 - 1)] += 0.25 * (z1[i1 - 1] + z1[i1]);
+            }
+            for (int i1 = 1; i1 <= mm - 1; ++i1) {
+                u[MGI(n, 2 * i1 - 1, 2 * i2 - 1, 2 * i3)] += 0.5 * z2[i1 - 1];
+                u[MGI(n, 2 * i1, 2 * i2 - 1, 2 * i3)] += 0.25 * (z2[i1 - 1] + z2[i1]);
+            }
+            for (int i1 = 1; i1 <= mm - 1; ++i1) {
+                u[MGI(n, 2 * i1 - 1, 2 * i2, 2 * i3)] += 0.25 * z3[i1 - 1];
+                u[MGI(n, 2 * i1, 2 * i2, 2 * i3)] += 0.125 * (z3[i1 - 1] + z3[i1]);
+            }
+        }
+    free(z1);
+    free(z2);
+    free(z3);
+}
+
+/* norm2u3 in the fixed order (above): rnm2 = sqrt(sum / nx^3), rnmu = max|u| */
+static void mg_norm(const double* u, int n, int nx, double* rnm2, double* rnmu) {
+    double s = 0.0, mx = 0.0;
+    const size_t plane = (size_t)nx * nx;
+    for (int i3 = 2; i3 <= n - 1; ++i3) {
+        double lane[256];
+        for (int l = 0; l < 256; ++l) {
+            double acc = 0.0;
+            for (size_t p = (size_t)l; p < plane; p += 256) {
+                const int i1 = 2 + (int)(p % (size_t)nx), i2 = 2 + (int)(p / (size_t)nx);
+                const double x = u[MGI(n, i1, i2, i3)];
+                acc = acc + x * x;
+                if (fabs(x) > mx) mx = fabs(x);
+            }
+            lane[l] = acc;
+        }
+        for (int st = 1; st < 256; st *= 2)
+            for (int l = 0; l + st < 256; l += 2 * st) lane[l] = lane[l] + lane[l + st];
+        s = s + lane[0];
+    }
+    *rnm2 = sqrt(s / ((double)nx * nx * nx));
+    *rnmu = mx;
+}
+
+static void mg_coeffs(uint32_t set, double a[4], double c[4]) {
+    a[0] = -8.0 / 3.0; a[1] = 0.0; a[2] = 1.0 / 6.0; a[3] = 1.0 / 12.0;
+    if (set == 0) { c[0] = -3.0 / 8.0; c[1] = 1.0 / 32.0; c[2] = -1.0 / 64.0; }
+    else { c[0] = -3.0 / 17.0; c[1] = 1.0 / 33.0; c[2] = -1.0 / 61.0; }
+    c[3] = 0.0;
+}
+
+static int mg_header_ok(const uint8_t* in, uint64_t bytes, vgpu_mg_header* h) {
+    if (bytes < sizeof *h) return 0;
+    memcpy(h, in, sizeof *h);
+    if (h->nx < 4 || h->nx > 512 || (h->nx & (h->nx - 1)) || h->coeffs > 1 || h->reserved) return 0;
+    return bytes == vgpu_mg_input_bytes(h->nx);
+}
+
+/* zran3 (mg.f): v = 0 except +1 at the 10 largest and -1 at the 10 smallest
+ * of nx^3 NPB random numbers (seed 314159265, a = 5^13, i1 fastest) */
+uint64_t vo_mg_make_input(uint32_t nx, uint32_t nit, uint32_t coeffs, uint8_t* out, uint64_t cap) {
+    const uint64_t need = vgpu_mg_input_bytes(nx);
+    if (!out || cap < need) return need;
+    vgpu_mg_header h = {nx, nit, coeffs, 0};
+    memcpy(out, &h, sizeof h);
+    double* v = (double*)(out + sizeof h);
+    const uint64_t a = 1220703125ull; /* 5^13 */
+    uint64_t x0 = 314159265ull;
+    const uint64_t a1 = mg_power(a, nx), a2 = mg_power(a, (uint64_t)nx * nx);
+    double big_v[10], small_v[10];
+    size_t big_i[10], small_i[10];
+    for (int i = 0; i < 10; ++i) { big_v[i] = 0.0; small_v[i] = 1.0; big_i[i] = small_i[i] = 0; }
+    for (uint32_t i3 = 0; i3 < nx; ++i3) {
+        uint64_t x1 = x0;
+        for (uint32_t i2 = 0; i2 < nx; ++i2) {
+            uint64_t xx = x1;
+            for (uint32_t i1 = 0; i1 < nx; ++i1) {
+                const double z = mg_randlc(&xx, a);
+                const size_t idx = i1 + (size_t)nx * (i2 + (size_t)nx * i3);
+                /* mg.f's bubble: ten(1,1) is the smallest of the 10 largest */
+                if (z > big_v[0]) {
+                    big_v[0] = z; big_i[0] = idx;
+                    for (int k = 0; k < 9 && big_v[k] > big_v[k + 1]; ++k) {
+                        double t = big_v[k]; big_v[k] = big_v[k + 1]; big_v[k + 1] = t;
+                        size_t ti = big_i[k]; big_i[k] = big_i[k + 1]; big_i[k + 1] = ti;
+                    }
+                }
+                if (z < small_v[0]) {
+                    small_v[0] = z; small_i[0] = idx;
+                    for (int k = 0; k < 9 && small_v[k] < small_v[k + 1]; ++k) {
+                        double t = small_v[k]; small_v[k] = small_v[k + 1]; small_v[k + 1] = t;
+                        size_t ti = small_i[k]; small_i[k] = small_i[k + 1]; small_i[k + 1] = ti;
+                    }
+                }
+            }
+            mg_randlc(&x1, a1);
+        }
+        mg_randlc(&x0, a2);
+    }
+    memset(v, 0, sizeof(double) * (size_t)nx * nx * nx);
+    for (int i = 0; i < 10; ++i) v[small_i[i]] = -1.0;
+    for (int i = 0; i < 10; ++i) v[big_i[i]] = 1.0;
+    return need;
+}
+
+int vo_mg_run(const uint8_t* in, uint64_t bytes, vgpu_mg_result* res, double* u_top) {
+    vgpu_mg_header h;
+    if (!res || !mg_header_ok(in, bytes, &h)) return -1;
+    const int nx = (int)h.nx;
+    int lt = 0;
+    while ((1 << lt) < nx) ++lt;
+    double a[4], c[4];
+    mg_coeffs(h.coeffs, a, c);
+    double* u[16] = {0};
+    double* r[16] = {0};
+    int m[16] = {0};
+    for (int k = 1; k <= lt; ++k) {
+        m[k] = (1 << k) + 2;
+        const size_t pts = (size_t)m[k] * m[k] * m[k];
+        u[k] = calloc(pts, sizeof(double));
+        r[k] = calloc(pts, sizeof(double));
+    }
+    const int n = m[lt];
+    /* v with its ghost layer (only the interior is ever read) */
+    double* v = calloc((size_t)n * n * n, sizeof(double));
+    const double* vin = (const double*)(in + sizeof h);
+    for (int i3 = 0; i3 < nx; ++i3)
+        for (int i2 = 0; i2 < nx; ++i2)
+            for (int i1 = 0; i1 < nx; ++i1)
+                v[MGI(n, i1 + 2, i2 + 2, i3 + 2)] = vin[i1 + (size_t)nx * (i2 + (size_t)nx * i3)];
+    mg_comm3(v, n);
+    /* the timed part of mg.f: resid, then nit x (mg3P, resid), then norm2u3 */
+    mg_resid(u[lt], v, r[lt], n, a);
+    for (uint32_t it = 0; it < h.nit; ++it) {
+        for (int k = lt; k >= 2; --k) mg_rprj3(r[k], m[k], r[k - 1], m[k - 1]);
+        memset(u[1], 0, sizeof(double) * (size_t)m[1] * m[1] * m[1]);
+        mg_psinv(r[1], u[1], m[1], c);
+        for (int k = 2; k <= lt - 1; ++k) {
+            memset(u[k], 0, sizeof(double) * (size_t)m[k] * m[k] * m[k]);
+            mg_interp(u[k - 1], m[k - 1], u[k], m[k]);
+            mg_resid(u[k], r[k], r[k], m[k], a);
+            mg_psinv(r[k], u[k], m[k], c);
+        }
+        mg_interp(u[lt - 1], m[lt - 1], u[lt], n);
+        mg_resid(u[lt], v, r[lt], n, a);
+        mg_psinv(r[lt], u[lt], n, c);
+        mg_resid(u[lt], v, r[lt], n, a);
+    }
+    memset(res, 0, sizeof *res);
+    mg_norm(r[lt], n, nx, &res->rnm2, &res->rnmu);
+    res->nx = h.nx;
+    res->nit = h.nit;
+    if (u_top) memcpy(u_top, u[lt], sizeof(double) * (size_t)n * n * n);
+    for (int k = 1; k <= lt; ++k) { free(u[k]); free(r[k]); }
+    free(v);
+    return 0;
+}

@@ -74,6 +74,13 @@ int vo_cg_run(const uint8_t* in, uint64_t in_bytes, vgpu_cg_result* res);
 int vo_es(const uint8_t* in, uint64_t in_bytes, double* out);
 
 /* deterministic generators shared by tests and bench (xorshift64*) */
+/* NAS MG (NPB 3.x mg.f): zran3's right-hand side as the nas-mg input
+ * (returns the bytes needed; writes when cap suffices), and the timed part
+ * (resid, nit x (mg3P, resid), norm2u3). u_top (optional): the finest u
+ * with its ghost layer, (nx + 2)^3 doubles, for bit-exact grid checks. */
+uint64_t vo_mg_make_input(uint32_t nx, uint32_t nit, uint32_t coeffs, uint8_t* out, uint64_t cap);
+int vo_mg_run(const uint8_t* in, uint64_t bytes, vgpu_mg_result* res, double* u_top);
+
 uint64_t vo_rng_next(uint64_t* state);
 float vo_rng_uniform(uint64_t* state, float lo, float hi);
 

@@ -123,13 +123,14 @@ CUDA_API = {
     "vgpu_cu_execute_launches": (_U64, []),
     "vgpu_cu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "vgpu_cu_device_pci_bus_id": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),
+    "vgpu_cu_task_shape": (C.c_int, [C.c_int, _U32, _P, _U64, C.POINTER(_U32), C.POINTER(_U32)]),
     "vgpu_cu_strerror": (C.c_char_p, [C.c_int]),
     "vgpu_cu_last_error": (C.c_char_p, []),
     "vgpu_cu_resident_bench": (C.c_int, [C.c_int, _U32, C.c_float, _U32, C.POINTER(_P),
                                          C.POINTER(_U64), _U32, _U32, _U32, _U32,
                                          C.POINTER(ResidentResult)]),
     "vgpu_cu_peak_probe": (C.c_int, [C.c_int, _U32, C.POINTER(C.c_double)]),
-    "vgpu_cu_link_probe": (C.c_int, [C.c_int, _U64, _U32, C.POINTER(LinkResult)]),
+    "vgpu_cu_link_probe": (C.c_int, [C.c_int, _U64, _U32, _U32, C.POINTER(LinkResult)]),
     "vgpu_cu_nccl_unique_id": (C.c_int, [_P]),
     "vgpu_cu_comm_init": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "vgpu_cu_reduce_final": (C.c_int, [_P, _P, _U64, _P]),
@@ -173,11 +174,15 @@ HOST_API = {
     "vgpu_native_run_task": (C.c_int, [C.c_int, C.POINTER(DescriptorC), _P, _U64, _P, _U64,
                                        C.POINTER(_U64)]),
     "vgpu_model_simulate": (_U64, [C.c_int, _U32, _U64, _U64, _U64, _U32, _U32, _U32, _U32]),
+    "vgpu_model_simulate_fluid": (_U64, [C.c_int, _U32, _U64, _U64, _U64, _U32, _U32, _U32]),
     "vgpu_model_classify": (C.c_int, [_U64, _U64, _U64]),
     "vgpu_model_no_vt": (_U64, [_U32, _U64, _U64, _U64, _U64, _U64]),
     "vgpu_encode_frame": (C.c_int, [C.c_uint8, _U32, _U64, _P, _U64, _P, _U64, C.POINTER(_U64)]),
     "vgpu_decode_frame": (C.c_int, [_P, _U64, C.POINTER(C.c_uint8), C.POINTER(_U32),
                                     C.POINTER(_U64), C.POINTER(_U64)]),
+    "vgpu_mg_class": (C.c_int, [C.c_char, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
+                                C.POINTER(C.c_double)]),
+    "vgpu_mg_make_input": (C.c_int, [_U32, _U32, _U32, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cg_class": (C.c_int, [C.c_char, C.POINTER(_U32), C.POINTER(_U32), C.POINTER(_U32),
                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "vgpu_cg_make_input": (C.c_int, [_U32, _U32, _U32, C.c_double, _P, _U64, C.POINTER(_U64)]),

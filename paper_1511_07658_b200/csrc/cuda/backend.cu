@@ -36,6 +36,9 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 #include <vector>
 
 #include "vgpu_cuda.h"
@@ -43,6 +46,7 @@
 #include "k_cg.cuh"
 #include "k_ep.cuh"
 #include "k_es.cuh"
+#include "k_mg.cuh"
 #include "k_sgemm.cuh"
 #include "k_sgemm_tc.cuh"
 #include "k_stream.cuh"
@@ -128,6 +132,7 @@ struct DevJob {
     vgpu_ep_params ep{};
     vgpu_cg_header cg{};
     vgpu_es_header es{};
+    vgpu_mg_header mg{};
 };
 
 // Device workspace a job needs besides in/out/scratch (0: none).
@@ -138,6 +143,11 @@ std::uint64_t job_ws_bytes(std::uint32_t kernel, const void* h_in, std::uint64_t
         std::memcpy(&h, h_in, sizeof h);
         // x, z, p, q, r, then the grid variant's barrier and partials
         return ((5ull * 8ull * h.n + 255) & ~255ull) + sizeof(vgk::CgGridSync);
+    }
+    if (kernel == VGPU_CU_K_MG && h_in && in_bytes >= sizeof(vgpu_mg_header)) {
+        vgpu_mg_header h;
+        std::memcpy(&h, h_in, sizeof h);
+        if (h.nx >= 4 && h.nx <= 512 && !(h.nx & (h.nx - 1))) return vgpu_mg_workspace_bytes(h.nx);
     }
     return 0;
 }
@@ -554,6 +564,96 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
     return cudaSuccess;
 }
 
+// NAS MG: jobs with the same (nx, nit, coeffs) share one table; mg.f's
+// timed sequence — resid, nit x (mg3P, resid), norm2u3 — is issued as one
+// launch per grid operator and level over all jobs of the table.
+cudaError_t launch_mg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::uint64_t* launches) {
+    using namespace vgk;
+    std::vector<bool> done(n, false);
+    for (std::uint32_t first = 0; first < n; ++first) {
+        if (done[first]) continue;
+        const vgpu_mg_header h0 = jobs[first].mg;
+        MgTable t{};
+        t.nx = h0.nx;
+        t.nit = h0.nit;
+        while ((1u << t.lt) < t.nx) ++t.lt;
+        t.a[0] = -8.0 / 3.0; t.a[1] = 0.0; t.a[2] = 1.0 / 6.0; t.a[3] = 1.0 / 12.0;
+        if (h0.coeffs == 0) { t.c[0] = -3.0 / 8.0; t.c[1] = 1.0 / 32.0; t.c[2] = -1.0 / 64.0; }
+        else { t.c[0] = -3.0 / 17.0; t.c[1] = 1.0 / 33.0; t.c[2] = -1.0 / 61.0; }
+        t.c[3] = 0.0;
+        for (std::uint32_t i = first; i < n && t.njobs < kMaxMgJobs; ++i) {
+            const vgpu_mg_header& h = jobs[i].mg;
+            if (done[i] || h.nx != h0.nx || h.nit != h0.nit || h.coeffs != h0.coeffs) continue;
+            done[i] = true;
+            MgJob& j = t.job[t.njobs++];
+            j.v = reinterpret_cast<const double*>(jobs[i].in + sizeof(vgpu_mg_header));
+            double* w = reinterpret_cast<double*>(jobs[i].ws);
+            for (std::uint32_t k = 1; k <= t.lt; ++k) {
+                const std::size_t pts = static_cast<std::size_t>((1u << k) + 2) * ((1u << k) + 2) * ((1u << k) + 2);
+                j.u[k] = w;
+                j.r[k] = w + pts;
+                w += 2 * pts;
+            }
+            j.plane_sum = w;
+            j.plane_max = w + t.nx;
+            j.out = reinterpret_cast<vgpu_mg_result*>(jobs[i].out);
+        }
+        const unsigned nj = t.njobs;
+        auto grid = [nj](std::uint64_t points) {
+            const std::uint64_t b = (points + kMgThreads - 1) / kMgThreads;
+            return dim3(static_cast<unsigned>(std::min<std::uint64_t>(b, 148ull * 8)), nj);
+        };
+        auto interior = [](int k) { return std::uint64_t{1} << (3 * k); };
+        auto all = [](int k) { const std::uint64_t m = (1u << k) + 2; return m * m * m; };
+        auto faces = [](int k) { const std::uint64_t m = (1u << k) + 2; return 6 * m * m; };
+        cudaError_t e = cudaSuccess;
+        std::uint64_t l = 0;
+        auto go = [&](auto kern, dim3 g, auto... args) {
+            if (e != cudaSuccess) return;
+            kern<<<g, kMgThreads, 0, s>>>(t, args...);
+            e = cudaGetLastError();
+            ++l;
+        };
+        const int lt = static_cast<int>(t.lt);
+        go(mg_zero_kernel, grid(all(lt)), lt, 0);
+        go(mg_resid_kernel, grid(interior(lt)), lt, 1);
+        go(mg_comm3_kernel, grid(faces(lt)), lt, 1);
+        for (std::uint32_t it = 0; it < t.nit; ++it) {
+            for (int k = lt; k >= 2; --k) {  // restrict the residual down to level 1
+                go(mg_rprj3_kernel, grid(interior(k - 1)), k);
+                go(mg_comm3_kernel, grid(faces(k - 1)), k - 1, 1);
+            }
+            go(mg_zero_kernel, grid(all(1)), 1, 0);  // coarsest level: one smoothing
+            go(mg_psinv_kernel, grid(interior(1)), 1);
+            go(mg_comm3_kernel, grid(faces(1)), 1, 0);
+            for (int k = 2; k <= lt - 1; ++k) {  // prolongate, residual, smooth
+                go(mg_zero_kernel, grid(all(k)), k, 0);
+                go(mg_interp_kernel, grid(all(k)), k);
+                go(mg_resid_kernel, grid(interior(k)), k, 0);
+                go(mg_comm3_kernel, grid(faces(k)), k, 1);
+                go(mg_psinv_kernel, grid(interior(k)), k);
+                go(mg_comm3_kernel, grid(faces(k)), k, 0);
+            }
+            go(mg_interp_kernel, grid(all(lt)), lt);  // finest level
+            go(mg_resid_kernel, grid(interior(lt)), lt, 1);
+            go(mg_comm3_kernel, grid(faces(lt)), lt, 1);
+            go(mg_psinv_kernel, grid(interior(lt)), lt);
+            go(mg_comm3_kernel, grid(faces(lt)), lt, 0);
+            go(mg_resid_kernel, grid(interior(lt)), lt, 1);  // mg.f's resid after mg3P
+            go(mg_comm3_kernel, grid(faces(lt)), lt, 1);
+        }
+        go(mg_norm_kernel, dim3(t.nx, nj));
+        if (e == cudaSuccess) {
+            mg_norm_fold_kernel<<<nj, 32, 0, s>>>(t);
+            e = cudaGetLastError();
+            ++l;
+        }
+        *launches += l;
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 // Launch every job (all of one kernel kind) on `s`; counts launches.
 cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t n,
                         cudaStream_t s, std::uint64_t* launches, bool pdl = false) {
@@ -825,6 +925,8 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
         }
         case VGPU_CU_K_CG:
             return launch_cg(jobs, n, s, launches);
+        case VGPU_CU_K_MG:
+            return launch_mg(jobs, n, s, launches);
         default:
             return cudaErrorInvalidValue;
     }
@@ -853,6 +955,27 @@ void job_work(const DevJob& j, std::uint64_t* bytes, double* flops) {
             const double pts = static_cast<double>(j.es.nx) * j.es.ny * j.es.nz;
             *bytes += j.in_bytes + static_cast<std::uint64_t>(4.0 * pts);
             *flops += pts * j.es.natoms;
+            break;
+        }
+        case VGPU_CU_K_MG: {
+            // per V-cycle, every operator streams its arrays once (reads +
+            // writes, 8 B per point each): on the finest level 2 resids
+            // (u, v, r: 24 B), psinv (24), interp (16 + 1 coarse), rprj3
+            // (8 + 1); on each coarser level k an in-place resid (24), psinv
+            // (24), zero + interp (8 + 17), rprj3 (9); plus the first resid
+            // and the norm (8 B per top point). Flops: resid 11 adds + 3
+            // muls... counted as 2 x the bytes / 8 (stencil sums).
+            const std::uint32_t nx = j.mg.nx;
+            int lt = 0;
+            while ((1u << lt) < nx) ++lt;
+            double b = 0.0;
+            for (int k = 1; k <= lt; ++k) {
+                const double pts = static_cast<double>(1ull << (3 * k));
+                b += (k == lt ? 98.0 : 82.0) * pts;
+            }
+            const double top = static_cast<double>(nx) * nx * nx;
+            *bytes += static_cast<std::uint64_t>(j.mg.nit * b + 32.0 * top);
+            *flops += j.mg.nit * b / 4.0;
             break;
         }
         case VGPU_CU_K_CG: {
@@ -920,6 +1043,7 @@ struct Op {
     bool mapped_out = false;     // the kernel wrote the result straight into host memory
     bool grouped = false;        // launched in a PS-1 group on another stream
     std::vector<cudaEvent_t> parts;  // streamed upload: (start, end) per part: DMA busy time
+    cudaEvent_t d2h_start = nullptr; // FIFO D2H: the copy's own start on the D2H queue
     cudaEvent_t in_ready() const { return has_h2d ? ev[kEvH2d1] : ev[kEvH2d0]; }
     cudaEvent_t last() const { return kind == VGPU_CU_DONE_UPLOAD ? ev[kEvH2d1] : ev[kEvD2h1]; }
 };
@@ -955,6 +1079,17 @@ struct vgpu_cu_dev {
     std::uint8_t* arena = nullptr;
     std::vector<SlotState> slots;  // [0] unused
     cudaStream_t anchor_stream = nullptr;
+    // Large copies go through one FIFO queue per direction instead of the
+    // slot streams: with every client's copy on its own stream the copy
+    // engine shares bandwidth among them, all clients' H2Ds finish together,
+    // then all their D2Hs run while the H2D direction idles (a convoy,
+    // measured: 55 GB/s of the 97 GB/s duplex link on C3). FIFO order
+    // completes one client's copy after another, so their D2Hs start
+    // staggered and both directions stay busy. VGPU_COPY_FIFO=0 turns it off.
+    cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    bool fifo = true;
+    static constexpr std::uint64_t kFifoFrom = 1u << 20;
+    bool fifo_for(std::uint64_t bytes) const { return fifo && bytes >= kFifoFrom; }
     std::vector<cudaEvent_t> event_pool;
     std::map<std::uint64_t, BatchRec> batches;
     std::uint64_t next_batch = 1;
@@ -1000,6 +1135,7 @@ struct vgpu_cu_dev {
         for (auto& e : op->ev)
             if (e) event_pool.push_back(e);
         for (auto e : op->parts) event_pool.push_back(e);
+        if (op->d2h_start) event_pool.push_back(op->d2h_start);
         delete op;
     }
 };
@@ -1056,6 +1192,53 @@ const char* vgpu_cu_strerror(int code) {
     }
 }
 
+int vgpu_cu_task_shape(int device, std::uint32_t kernel, const void* in, std::uint64_t in_bytes,
+                       std::uint32_t* ctas, std::uint32_t* ctas_per_sm) {
+    if (!ctas || !ctas_per_sm || (!in && in_bytes)) return VGPU_CU_EINVAL;
+    int rc = require_sm100(device);
+    if (rc) return rc;
+    CK(cudaSetDevice(device));
+    int per_sm = 0, sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    std::uint64_t grid = 0;
+    cudaError_t e = cudaSuccess;
+    using namespace vgk;
+    switch (kernel) {
+        case VGPU_CU_K_VADD:
+        case VGPU_CU_K_VMUL:
+        case VGPU_CU_K_VSCALE: {
+            const std::uint64_t elems = kernel == VGPU_CU_K_VSCALE ? in_bytes / 4 : in_bytes / 8;
+            grid = (elems + kStreamChunk - 1) / kStreamChunk;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stream_table_kernel<kOpAdd>,
+                                                              kStreamThreads, 0);
+            break;
+        }
+        case VGPU_CU_K_EP: {
+            if (in_bytes != sizeof(vgpu_ep_params)) return VGPU_CU_EINVAL;
+            vgpu_ep_params p;
+            std::memcpy(&p, in, sizeof p);
+            grid = p.n_batches;  // one CTA per NPB batch
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ep_table_kernel<4, 1, true>,
+                                                              kEpThreads, 0);
+            break;
+        }
+        case VGPU_CU_K_BS:
+            grid = (in_bytes / 12 + kBsChunk - 1) / kBsChunk;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bs_table_kernel, kBsThreads, 0);
+            break;
+        default:
+            // the GEMM / CG / electrostatics launches size their grids to the
+            // device: one task fills it
+            per_sm = 1;
+            grid = static_cast<std::uint64_t>(sms);
+            break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "vgpu_cu_task_shape");
+    *ctas = static_cast<std::uint32_t>(std::min<std::uint64_t>(grid, 0xffffffffu));
+    *ctas_per_sm = static_cast<std::uint32_t>(std::max(1, per_sm));
+    return VGPU_CU_OK;
+}
+
 int vgpu_cu_device_pci_bus_id(int device, char* buf, int len) {
     if (!buf || len < 13) return VGPU_CU_EINVAL;
     CK(cudaDeviceGetPCIBusId(buf, len, device));
@@ -1078,7 +1261,8 @@ int vgpu_cu_device_count(int* n) {
 int vgpu_cu_payload(const char* id, std::uint32_t* kernel) {
     static const char* names[VGPU_CU_K_COUNT] = {"identity",      "vector-add", "vector-scale",
                                                  "nas-ep",        "black-scholes", "sgemm",
-                                                 "vector-mul",    "nas-cg",     "electrostatics"};
+                                                 "vector-mul",    "nas-cg",     "electrostatics",
+                                                 "nas-mg"};
     if (!id || !kernel) return VGPU_CU_EINVAL;
     for (std::uint32_t k = 0; k < VGPU_CU_K_COUNT; ++k)
         if (std::strcmp(id, names[k]) == 0) {
@@ -1152,6 +1336,23 @@ int vgpu_cu_output_size(std::uint32_t kernel, const void* in, std::uint64_t in_b
             *out_bytes = 4 * pts;
             return VGPU_CU_OK;
         }
+        case VGPU_CU_K_MG: {
+            if (in_bytes < sizeof(vgpu_mg_header)) {
+                set_err("nas-mg: input shorter than its %zu-byte header", sizeof(vgpu_mg_header));
+                return VGPU_CU_EPAYLOAD;
+            }
+            if (!in) return VGPU_CU_EINVAL;
+            vgpu_mg_header h;
+            std::memcpy(&h, in, sizeof h);
+            if (h.nx < 4 || h.nx > 512 || (h.nx & (h.nx - 1)) || h.coeffs > 1 || h.reserved ||
+                h.nit > 10000 || in_bytes != vgpu_mg_input_bytes(h.nx)) {
+                set_err("nas-mg: %llu bytes do not match a header (nx a power of two in 4..512, "
+                        "coeffs 0/1, nit <= 1e4) + nx^3 doubles", (unsigned long long)in_bytes);
+                return VGPU_CU_EPAYLOAD;
+            }
+            *out_bytes = sizeof(vgpu_mg_result);
+            return VGPU_CU_OK;
+        }
         case VGPU_CU_K_VSCALE:
             if (in_bytes % 4) {
                 set_err("vector-scale: input must be packed float32");
@@ -1209,7 +1410,7 @@ int vgpu_cu_task_check(vgpu_cu_dev* d, std::uint32_t kernel, const void* in,
     // the slot's workspace is 2 buffers (sgemm hi/lo splits: exactly 2 x input)
     if (job_ws_bytes(kernel, in, in_bytes) > 2 * d->buf_bytes) {
         set_err("%s workspace (%llu B) exceeds the slot's (%llu B)",
-                kernel == VGPU_CU_K_CG ? "nas-cg vector" : "device",
+                kernel == VGPU_CU_K_CG ? "nas-cg vector" : kernel == VGPU_CU_K_MG ? "nas-mg grid" : "device",
                 (unsigned long long)job_ws_bytes(kernel, in, in_bytes),
                 (unsigned long long)(2 * d->buf_bytes));
         return VGPU_CU_ESIZE;
@@ -1257,6 +1458,10 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
     }
     e = cudaStreamCreateWithFlags(&d->anchor_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(anchor)"));
+    e = cudaStreamCreateWithFlags(&d->up_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->down_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(copy queues)"));
+    if (const char* f = std::getenv("VGPU_COPY_FIFO")) d->fifo = std::atoi(f) != 0;
     // warm the event pool: 6 events per slot for two ops in flight + batch events
     for (std::uint32_t i = 0; i < 16 * max_clients + 16; ++i) {
         cudaEvent_t ev;
@@ -1274,6 +1479,8 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
     for (auto& s : d->slots)
         if (s.stream) cudaStreamSynchronize(s.stream);
     if (d->anchor_stream) cudaStreamSynchronize(d->anchor_stream);
+    if (d->up_stream) cudaStreamSynchronize(d->up_stream);
+    if (d->down_stream) cudaStreamSynchronize(d->down_stream);
     for (Op* op : d->outstanding) d->release_op(op);
     d->outstanding.clear();
     for (auto& s : d->slots) {
@@ -1288,6 +1495,8 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
     }
     for (auto ev : d->event_pool) cudaEventDestroy(ev);
     if (d->anchor_stream) cudaStreamDestroy(d->anchor_stream);
+    if (d->up_stream) cudaStreamDestroy(d->up_stream);
+    if (d->down_stream) cudaStreamDestroy(d->down_stream);
     for (void* p : d->pinned) cudaFreeHost(p);
     if (d->arena) cudaFree(d->arena);
     if (d->comm && nccl().ok) nccl().comm_destroy(d->comm);
@@ -1361,11 +1570,15 @@ int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::ui
     int rc = d->new_op(slot, VGPU_CU_DONE_UPLOAD, tag, &op);
     if (rc) return rc;
     op->has_h2d = bytes > 0;
-    cudaError_t e = cudaEventRecord(op->ev[kEvH2d0], s.stream);
+    const cudaStream_t cs = d->fifo_for(bytes) ? d->up_stream : s.stream;
+    cudaError_t e = cudaEventRecord(op->ev[kEvH2d0], cs);
     if (e == cudaSuccess && bytes)
-        e = cudaMemcpyAsync(s.d_in, h_in, bytes, cudaMemcpyHostToDevice, s.stream);
-    if (e == cudaSuccess) e = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+        e = cudaMemcpyAsync(s.d_in, h_in, bytes, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(op->ev[kEvH2d1], cs);
+    // the slot's later work (its task) runs after the input landed
+    if (e == cudaSuccess && cs != s.stream) e = cudaStreamWaitEvent(s.stream, op->ev[kEvH2d1], 0);
     if (e != cudaSuccess) {
+        cudaStreamSynchronize(cs);
         cudaStreamSynchronize(s.stream);
         d->release_op(op);
         return cuda_fail(e, "vgpu_cu_upload");
@@ -1397,11 +1610,13 @@ int vgpu_cu_upload_part(vgpu_cu_dev* d, std::uint32_t slot, const void* h_src, s
     }
     CK(cudaSetDevice(d->device));
     cudaError_t e = cudaSuccess;
+    // a streamed input is large (the SDK streams from 4 MiB)
+    const cudaStream_t cs = d->fifo ? d->up_stream : s.stream;
     if (begin) {
         int rc = d->new_op(slot, VGPU_CU_DONE_UPLOAD, tag, &s.open_upload);
         if (rc) return rc;
         s.open_upload_bytes = 0;
-        e = cudaEventRecord(s.open_upload->ev[kEvH2d0], s.stream);
+        e = cudaEventRecord(s.open_upload->ev[kEvH2d0], cs);
     }
     Op* op = s.open_upload;
     if (e == cudaSuccess && bytes) {
@@ -1410,22 +1625,23 @@ int vgpu_cu_upload_part(vgpu_cu_dev* d, std::uint32_t slot, const void* h_src, s
         if (!rc) rc = d->pool_get(&p1);
         if (rc) {
             if (p0) d->event_pool.push_back(p0);
-            cudaStreamSynchronize(s.stream);
+            cudaStreamSynchronize(cs);
             d->release_op(op);
             s.open_upload = nullptr;
             return rc;
         }
         op->parts.push_back(p0);
         op->parts.push_back(p1);
-        e = cudaEventRecord(p0, s.stream);
+        e = cudaEventRecord(p0, cs);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(s.d_in + offset, h_src, bytes, cudaMemcpyHostToDevice, s.stream);
-        if (e == cudaSuccess) e = cudaEventRecord(p1, s.stream);
+            e = cudaMemcpyAsync(s.d_in + offset, h_src, bytes, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(p1, cs);
     }
     if (e == cudaSuccess) s.open_upload_bytes += bytes;
-    if (e == cudaSuccess && end) e = cudaEventRecord(op->ev[kEvH2d1], s.stream);
+    if (e == cudaSuccess && end) e = cudaEventRecord(op->ev[kEvH2d1], cs);
+    if (e == cudaSuccess && end && cs != s.stream) e = cudaStreamWaitEvent(s.stream, op->ev[kEvH2d1], 0);
     if (e != cudaSuccess) {
-        cudaStreamSynchronize(s.stream);
+        cudaStreamSynchronize(cs);
         d->release_op(op);
         s.open_upload = nullptr;
         return cuda_fail(e, "vgpu_cu_upload_part");
@@ -1485,6 +1701,13 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         j.scratch = s.d_scratch;
         j.ws = s.d_ws;
         if (t.kernel == VGPU_CU_K_ES) std::memcpy(&j.es, t.h_in, sizeof j.es);
+        if (t.kernel == VGPU_CU_K_MG) {
+            std::memcpy(&j.mg, t.h_in, sizeof j.mg);
+            if (job_ws_bytes(t.kernel, t.h_in, t.in_bytes) > 2 * d->buf_bytes) {
+                set_err("task %u: nas-mg grids (nx = %u) exceed the slot workspace", i, j.mg.nx);
+                return VGPU_CU_ESIZE;
+            }
+        }
         if (t.kernel == VGPU_CU_K_CG) {
             std::memcpy(&j.cg, t.h_in, sizeof j.cg);
             if (job_ws_bytes(t.kernel, t.h_in, t.in_bytes) > 2 * d->buf_bytes) {
@@ -1555,9 +1778,20 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
             op->d2h0 = op->ev[kEvD2h0];
             err = cudaEventRecord(op->d2h0, s.stream);
         }
+        cudaStream_t cs = s.stream;
+        if (err == cudaSuccess && d->fifo_for(bytes)) {
+            // the D2H queue: in order after the result is ready; the stage
+            // time starts when the copy itself starts
+            cs = d->down_stream;
+            err = cudaStreamWaitEvent(cs, op->d2h0, 0);
+            if (err == cudaSuccess && d->pool_get(&op->d2h_start) != VGPU_CU_OK)
+                err = cudaErrorMemoryAllocation;
+            if (err == cudaSuccess) err = cudaEventRecord(op->d2h_start, cs);
+            if (err == cudaSuccess) op->d2h0 = op->d2h_start;
+        }
         if (err == cudaSuccess && bytes)
-            err = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, s.stream);
-        if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvD2h1], s.stream);
+            err = cudaMemcpyAsync(t.h_out, src, bytes, cudaMemcpyDeviceToHost, cs);
+        if (err == cudaSuccess) err = cudaEventRecord(op->ev[kEvD2h1], cs);
         if (err == cudaSuccess) {
             d->outstanding.push_back(op);
             ops[i] = nullptr;  // owned by outstanding now
@@ -1637,6 +1871,7 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
         // drain whatever got enqueued; armed callbacks still report, the
         // daemon fails the batch on the error return and ignores them
         for (std::uint32_t i = 0; i < n; ++i) cudaStreamSynchronize(d->slots[tasks[i].slot].stream);
+        cudaStreamSynchronize(d->down_stream);
         rec.remaining = static_cast<std::uint32_t>(enqueued.size());
         if (rec.remaining) {
             d->batches.emplace(bid, std::move(rec));
@@ -1835,6 +2070,7 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     }
     if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, in, sizeof j.ep);
     if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, in, sizeof j.cg);
+    if (kernel == VGPU_CU_K_MG) std::memcpy(&j.mg, in, sizeof j.mg);
     if (kernel == VGPU_CU_K_ES) std::memcpy(&j.es, in, sizeof j.es);
     // pageable copies, exactly what an unvirtualized CUDA program does
     if (in_bytes) CK(cudaMemcpyAsync(c.d_in, in, in_bytes, cudaMemcpyHostToDevice, c.stream));
@@ -1901,6 +2137,7 @@ int vgpu_cu_resident_bench(int device, std::uint32_t kernel, float param, std::u
             }
             if (kernel == VGPU_CU_K_EP) std::memcpy(&j.ep, h_inputs[i], sizeof j.ep);
             if (kernel == VGPU_CU_K_CG) std::memcpy(&j.cg, h_inputs[i], sizeof j.cg);
+            if (kernel == VGPU_CU_K_MG) std::memcpy(&j.mg, h_inputs[i], sizeof j.mg);
             if (kernel == VGPU_CU_K_ES) std::memcpy(&j.es, h_inputs[i], sizeof j.es);
             if (in_bytes[i])
                 CK(cudaMemcpy(const_cast<std::uint8_t*>(j.in), h_inputs[i], in_bytes[i],
@@ -2026,7 +2263,7 @@ int vgpu_cu_peak_probe(int device, std::uint32_t kind, double* tflops) {
     return VGPU_CU_OK;
 }
 
-int vgpu_cu_link_probe(int device, std::uint64_t bytes, std::uint32_t reps,
+int vgpu_cu_link_probe(int device, std::uint64_t bytes, std::uint32_t reps, std::uint32_t flags,
                        vgpu_cu_link_result* out) {
     if (!out || bytes == 0) return VGPU_CU_EINVAL;
     int rc = require_sm100(device);
@@ -2034,6 +2271,10 @@ int vgpu_cu_link_probe(int device, std::uint64_t bytes, std::uint32_t reps,
     CK(cudaSetDevice(device));
     reps = std::max<std::uint32_t>(1, reps);
     void *h_src = nullptr, *h_dst = nullptr, *d_src = nullptr, *d_dst = nullptr;
+    // host memory as the data plane has it: POSIX shm pages page-locked in
+    // place (flags & VGPU_CU_LINK_SHM), or cudaHostAlloc'd buffers
+    const bool shm = flags & VGPU_CU_LINK_SHM;
+    void* maps[2] = {nullptr, nullptr};
     cudaStream_t s[2] = {nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     auto cleanup = [&] {
@@ -2043,11 +2284,39 @@ int vgpu_cu_link_probe(int device, std::uint64_t bytes, std::uint32_t reps,
             if (st) cudaStreamDestroy(st);
         if (d_src) cudaFree(d_src);
         if (d_dst) cudaFree(d_dst);
-        if (h_src) cudaFreeHost(h_src);
-        if (h_dst) cudaFreeHost(h_dst);
+        if (shm) {
+            for (void* m : maps)
+                if (m) {
+                    cudaHostUnregister(m);
+                    munmap(m, bytes);
+                }
+            cudaGetLastError();  // an unregister of a page set that never registered
+        } else {
+            if (h_src) cudaFreeHost(h_src);
+            if (h_dst) cudaFreeHost(h_dst);
+        }
     };
-    cudaError_t err = cudaHostAlloc(&h_src, bytes, cudaHostAllocDefault);
-    if (err == cudaSuccess) err = cudaHostAlloc(&h_dst, bytes, cudaHostAllocDefault);
+    cudaError_t err = cudaSuccess;
+    if (shm) {
+        for (int i = 0; i < 2 && err == cudaSuccess; ++i) {
+            const std::string name = "/vgpu.linkprobe." + std::to_string(getpid()) + "." + std::to_string(i);
+            const int fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+            if (fd < 0) { err = cudaErrorMemoryAllocation; break; }
+            shm_unlink(name.c_str());
+            void* m = ftruncate(fd, static_cast<off_t>(bytes)) == 0
+                          ? mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0)
+                          : MAP_FAILED;
+            close(fd);
+            if (m == MAP_FAILED) { err = cudaErrorMemoryAllocation; break; }
+            maps[i] = m;
+            err = cudaHostRegister(m, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+        }
+        h_src = maps[0];
+        h_dst = maps[1];
+    } else {
+        err = cudaHostAlloc(&h_src, bytes, cudaHostAllocDefault);
+        if (err == cudaSuccess) err = cudaHostAlloc(&h_dst, bytes, cudaHostAllocDefault);
+    }
     if (err == cudaSuccess) err = cudaMalloc(&d_src, bytes);
     if (err == cudaSuccess) err = cudaMalloc(&d_dst, bytes);
     for (int i = 0; i < 2 && err == cudaSuccess; ++i) err = cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking);

@@ -11,7 +11,9 @@
 #include "vgpu/model.hpp"
 #include "vgpu/multigpu.hpp"
 #include "vgpu/npb_cg.hpp"
+#include "vgpu/npb_mg.hpp"
 #include "vgpu_c.h"
+#include "vgpu_cuda.h"
 
 using namespace vgpu;
 
@@ -128,6 +130,29 @@ int vgpu_local_cpus(const char* pci_bus_id, int32_t* out, uint32_t cap, uint32_t
         const auto cpus = multigpu::local_cpus(pci_bus_id);
         *n = static_cast<uint32_t>(cpus.size());
         for (uint32_t i = 0; i < std::min<uint32_t>(cap, *n); ++i) out[i] = cpus[i];
+    });
+}
+
+int vgpu_mg_class(char cls, uint32_t* nx, uint32_t* nit, uint32_t* coeffs, double* rnm2_verify) {
+    if (!nx || !nit || !coeffs || !rnm2_verify) return VGPU_E_INVALID;
+    return guarded([&] {
+        const npb::MgClass c = npb::mg_class(cls);
+        *nx = c.nx;
+        *nit = c.nit;
+        *coeffs = c.coeffs;
+        *rnm2_verify = c.rnm2_verify;
+    });
+}
+
+int vgpu_mg_make_input(uint32_t nx, uint32_t nit, uint32_t coeffs, uint8_t* out, uint64_t cap,
+                       uint64_t* len) {
+    if (!len) return VGPU_E_INVALID;
+    return guarded([&] {
+        *len = vgpu_mg_input_bytes(nx);
+        if (!out) return;
+        if (cap < *len) throw VgpuError(ErrCode::Size, "nas-mg input exceeds the buffer");
+        const auto b = npb::make_mg_input(nx, nit, coeffs);
+        std::memcpy(out, b.data(), b.size());
     });
 }
 
@@ -365,6 +390,29 @@ uint64_t vgpu_model_simulate(int style, uint32_t n, uint64_t t_in, uint64_t t_co
         dev.num_sms = sms;
         dev.max_concurrent_kernels = max_kernels;
         dev.block_slots_per_sm = slots_per_sm;
+        return simulate(build_work_queue(style ? ProgrammingStyle::PS2 : ProgrammingStyle::PS1, ps),
+                        dev)
+            .makespan;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return 0;
+    }
+}
+
+uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
+                                   uint64_t t_out, uint32_t grid, uint32_t sms,
+                                   uint32_t ctas_per_sm) {
+    try {
+        KernelProfile p;
+        p.t_data_in = t_in;
+        p.t_comp = t_comp;
+        p.t_data_out = t_out;
+        p.grid_size = grid;
+        std::vector<KernelProfile> ps(n, p);
+        DeviceSpec dev = DeviceSpec::b200();
+        dev.num_sms = sms;
+        dev.block_slots_per_sm = ctas_per_sm;
+        dev.fluid_blocks = true;
         return simulate(build_work_queue(style ? ProgrammingStyle::PS2 : ProgrammingStyle::PS1, ps),
                         dev)
             .makespan;

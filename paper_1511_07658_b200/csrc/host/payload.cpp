@@ -20,7 +20,8 @@ int default_device() {
 }
 
 const char* kBuiltinIds[VGPU_CU_K_COUNT] = {
-    "identity", "vector-add", "vector-scale", "nas-ep", "black-scholes", "sgemm", "vector-mul", "nas-cg", "electrostatics"};
+    "identity", "vector-add", "vector-scale", "nas-ep",         "black-scholes",
+    "sgemm",    "vector-mul", "nas-cg",       "electrostatics", "nas-mg"};
 
 }  // namespace
 

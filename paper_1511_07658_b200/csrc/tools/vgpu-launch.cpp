@@ -192,7 +192,7 @@ int main(int argc, char** argv) {
             else if (a == "--tag") tag = val();
             else if (a == "--out") out_path = val();
             else if (a == "--ep-m" || a == "--ep-batches" || a == "--bs-n" || a == "--mm-n" ||
-                     a == "--vecadd-n" || a == "--cg-class" || a == "--es-atoms") {
+                     a == "--vecadd-n" || a == "--cg-class" || a == "--es-atoms" || a == "--mg-class") {
                 const std::string v = val();
                 size_args.push_back(a);
                 size_args.push_back(v);
@@ -202,6 +202,7 @@ int main(int argc, char** argv) {
                 else if (a == "--mm-n") sizes.mm_n = std::stoul(v);
                 else if (a == "--vecadd-n") sizes.vecadd_n = std::stoull(v);
                 else if (a == "--cg-class") sizes.cg_class = v[0];
+                else if (a == "--mg-class") sizes.mg_class = v[0];
                 else if (a == "--es-atoms") sizes.es_atoms = std::stoul(v);
             } else if (a == "-h" || a == "--help") {
                 std::puts("vgpu-launch [--gpus N] [--procs-per-gpu P] [--workload W] [--rounds R]\n"

@@ -1,7 +1,7 @@
 // vgpu-spmd — one SPMD process of a benchmark run (the forked worker of the
 // reference harness, proj/src/bench/bench.cpp:186-231).
 //
-//   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul
+//   vgpu-spmd --worker W --workers N --workload vecadd|ep|bs|mm|mixed|cg|vmul|es|mg
 //             --rounds R [--instance NAME [--inplace|--resident] | --native [--device D]]
 //
 // --inplace: the in-place result (VgpuHandle::rcv_region): every round the
@@ -38,6 +38,7 @@
 
 #include "vgpu/client.hpp"
 #include "vgpu/npb_cg.hpp"
+#include "vgpu/npb_mg.hpp"
 #include "workloads.hpp"
 
 namespace {
@@ -106,6 +107,7 @@ int main(int argc, char** argv) {
             else if (a == "--bs-n") sizes.bs_n = std::stoull(val());
             else if (a == "--mm-n") sizes.mm_n = std::stoul(val());
             else if (a == "--cg-class") sizes.cg_class = val()[0];
+            else if (a == "--mg-class") sizes.mg_class = val()[0];
             else if (a == "--es-atoms") sizes.es_atoms = std::stoul(val());
             else throw std::invalid_argument("unknown argument " + a);
         } catch (const std::exception& e) {
@@ -118,6 +120,10 @@ int main(int argc, char** argv) {
     mallopt(M_TRIM_THRESHOLD, 1 << 30);
 
     // NPB CG workers build their matrix with the product's makea
+    vgpu::wl::mg_builder() = [](char cls) {
+        const vgpu::npb::MgClass c = vgpu::npb::mg_class(cls);
+        return vgpu::npb::make_mg_input(c.nx, c.nit, c.coeffs);
+    };
     vgpu::wl::cg_builder() = [](char cls) {
         const vgpu::npb::CgClass c = vgpu::npb::cg_class(cls);
         return vgpu::npb::make_cg_input(c.n, c.nonzer, c.niter, c.shift);
@@ -283,6 +289,22 @@ int main(int argc, char** argv) {
             err = "nas-cg zeta differs from NPB's";
         }
     }
+    // NPB's own verification for MG: rnm2 within 1e-8 of the published value
+    std::string mg_json;
+    if (job.kind == vgpu::wl::Kind::Mg && last_out.size() == sizeof(vgpu_mg_result)) {
+        vgpu_mg_result r;
+        std::memcpy(&r, last_out.data(), sizeof r);
+        const double want = vgpu::npb::mg_class(sizes.mg_class).rnm2_verify;
+        const bool verified = std::fabs(r.rnm2 - want) / want <= 1e-8;
+        char buf[160];
+        std::snprintf(buf, sizeof buf, ", \"mg\": {\"rnm2\": %.15g, \"rnmu\": %.6g, \"verified\": %s}",
+                      r.rnm2, r.rnmu, verified ? "true" : "false");
+        mg_json = buf;
+        if (!verified && ok) {
+            ok = false;
+            err = "nas-mg rnm2 differs from NPB's";
+        }
+    }
     std::ostringstream os;
     os << "{\"worker\": " << worker << ", \"ok\": " << (ok ? "true" : "false")
        << ", \"kind\": " << static_cast<int>(job.kind) << ", \"native\": " << (native ? 1 : 0)
@@ -300,7 +322,7 @@ int main(int argc, char** argv) {
         std::sort(v.begin(), v.end());
         os << (k ? ", " : "") << "\"" << names[k] << "\": " << (v.empty() ? 0 : v[v.size() / 2]);
     }
-    os << "}" << cg_json << check_json;
+    os << "}" << cg_json << mg_json << check_json;
     if (job.kind == vgpu::wl::Kind::Ep && last_out.size() == sizeof(vgpu_ep_result)) {
         // the job's partial for the final reduction, bit patterns in hex
         vgpu_ep_result r;

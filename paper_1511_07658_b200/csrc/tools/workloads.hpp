@@ -21,7 +21,10 @@
 //   vmul    VecMul, vecadd's shapes and values, payload vector-mul;
 //   es      Electrostatics (VMD direct Coulomb summation): 100K atoms,
 //           64 x 64 lattice x 25 slices (the paper's "100K atoms / 25
-//           iterations"), atoms ~ U(box), q ~ U[-1,1], seed 777+w.
+//           iterations"), atoms ~ U(box), q ~ U[-1,1], seed 777+w;
+//   mg      NAS MG, every worker runs the whole NPB class (default S, the
+//           paper's 32^3 / 4 iterations): the program builds v with NPB's
+//           zran3 (untimed in NPB) through mg_builder().
 #pragma once
 
 #include <algorithm>
@@ -38,7 +41,7 @@
 
 namespace vgpu::wl {
 
-enum class Kind { VecAdd, Ep, Bs, Mm, Cg, VecMul, Es };
+enum class Kind { VecAdd, Ep, Bs, Mm, Cg, VecMul, Es, Mg };
 
 struct Sizes {
     std::uint64_t vecadd_n = 1ull << 20;
@@ -47,6 +50,7 @@ struct Sizes {
     std::uint64_t bs_n = 4ull << 20;
     std::uint32_t mm_n = 2048;
     char cg_class = 'A';
+    char mg_class = 'S';
     std::uint32_t es_atoms = 100000;
     std::uint32_t es_nx = 64, es_ny = 64, es_nz = 25;
     float es_h = 0.5f;
@@ -65,6 +69,24 @@ inline CgShape cg_shape(char cls) {
         case 'B': return {75000, 13};
         case 'C': return {150000, 15};
         default: throw std::invalid_argument(std::string("unknown NPB CG class ") + cls);
+    }
+}
+
+// The program's NPB zran3: nas-mg input bytes for a class
+using MgBuilder = Bytes (*)(char cls);
+inline MgBuilder& mg_builder() {
+    static MgBuilder b = nullptr;
+    return b;
+}
+
+// NPB MG classes (mg.f): grid points per dimension
+inline std::uint32_t mg_nx(char cls) {
+    switch (cls) {
+        case 'S': return 32;
+        case 'W': return 128;
+        case 'A': case 'B': return 256;
+        case 'C': return 512;
+        default: throw std::invalid_argument("unknown NPB MG class");
     }
 }
 
@@ -90,6 +112,7 @@ inline Kind kind_of(const std::string& workload, std::uint32_t worker) {
     if (workload == "cg") return Kind::Cg;
     if (workload == "vmul") return Kind::VecMul;
     if (workload == "es") return Kind::Es;
+    if (workload == "mg") return Kind::Mg;
     if (workload == "mixed") return static_cast<Kind>(worker % 4);
     throw std::invalid_argument("unknown workload: " + workload);
 }
@@ -209,6 +232,22 @@ inline Job make_job(const std::string& workload, std::uint32_t worker, std::uint
             j.desc.t_data_out = pcie_us(4 * pts);
             j.desc.grid_size = static_cast<std::uint32_t>((h.nx + 63) / 64 * ((h.ny + 7) / 8) * h.nz);
             j.output_bytes = 4 * pts;
+            break;
+        }
+        case Kind::Mg: {
+            if (!mg_builder()) throw std::logic_error("mg workload: no NPB zran3 set (mg_builder)");
+            j.input = mg_builder()(sz.mg_class);
+            vgpu_mg_header h;
+            std::memcpy(&h, j.input.data(), sizeof h);
+            j.desc.payload_id = "nas-mg";
+            j.desc.t_data_in = pcie_us(j.input.size());
+            // ~100 B per finest point per V-cycle at ~2 TB/s, plus ~150
+            // launches of ~3 us per cycle set
+            const double pts = static_cast<double>(h.nx) * h.nx * h.nx;
+            j.desc.t_comp = static_cast<Micros>(h.nit * (pts * 115.0 / 2e6 + 110.0)) + 1;
+            j.desc.t_data_out = 1;
+            j.desc.grid_size = 64;  // the paper's MG grid
+            j.output_bytes = sizeof(vgpu_mg_result);
             break;
         }
         case Kind::Cg: {
@@ -333,6 +372,10 @@ inline std::uint64_t region_bytes(const std::string& workload, const Sizes& sz =
     if (workload == "es")
         return std::max<std::uint64_t>(sizeof(vgpu_es_header) + 16ull * sz.es_atoms,
                                        4ull * sz.es_nx * sz.es_ny * sz.es_nz);
+    if (workload == "mg") {  // the input, or half the grids' workspace (slot ws = 2 x region)
+        const std::uint32_t nx = mg_nx(sz.mg_class);
+        return std::max<std::uint64_t>(vgpu_mg_input_bytes(nx), (vgpu_mg_workspace_bytes(nx) + 1) / 2);
+    }
     if (workload == "cg") {  // upper bound: nnz <= n (nonzer + 1)^2
         const CgShape c = cg_shape(sz.cg_class);
         return vgpu_cg_input_bytes(c.n, c.n * (c.nonzer + 1) * (c.nonzer + 1));

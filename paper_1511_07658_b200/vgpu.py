@@ -346,7 +346,7 @@ def native_run_task(data, task: KernelDescriptor, cuda_device: int = 0,
 
 KERNELS = {"identity": 0, "vector-add": 1, "vector-scale": 2, "nas-ep": 3,
            "black-scholes": 4, "sgemm": 5, "vector-mul": 6, "nas-cg": 7,
-           "electrostatics": 8}
+           "electrostatics": 8, "nas-mg": 9}
 
 
 def _cu_check(rc: int) -> None:
@@ -397,13 +397,31 @@ def peak_probe(kind: str, device: int = 0) -> float:
     return t.value
 
 
-def link_probe(device: int = 0, nbytes: int = 256 << 20, reps: int = 8) -> dict:
+def link_probe(device: int = 0, nbytes: int = 256 << 20, reps: int = 8, shm: bool = False) -> dict:
     """Pinned host <-> HBM copy bandwidth (vgpu_cu_link_probe): H2D alone,
-    D2H alone, both directions at once; GB/s (1e9 B/s)."""
+    D2H alone, both directions at once; GB/s (1e9 B/s). shm: POSIX shm pages
+    registered in place (the data plane's memory) instead of cudaHostAlloc."""
     r = N.LinkResult()
-    _cu_check(_libs().cuda.vgpu_cu_link_probe(device, nbytes, reps, C.byref(r)))
+    _cu_check(_libs().cuda.vgpu_cu_link_probe(device, nbytes, reps, 1 if shm else 0, C.byref(r)))
     return {"h2d_gbs": r.h2d_gbs, "d2h_gbs": r.d2h_gbs, "bidir_gbs": r.bidir_gbs,
-            "bytes": r.bytes, "reps": reps}
+            "bytes": r.bytes, "reps": reps, "host_memory": "shm, cudaHostRegister" if shm
+            else "cudaHostAlloc"}
+
+
+def model_simulate_fluid(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int,
+                         sms: int, ctas_per_sm: int) -> int:
+    """simulate() with the B200 fluid block-scheduler spec (DeviceSpec::fluid_blocks)."""
+    return _libs().host.vgpu_model_simulate_fluid(style, n, t_in, t_comp, t_out, grid, sms,
+                                                  ctas_per_sm)
+
+
+def task_shape(payload_id: str, data: bytes, device: int = 0) -> tuple:
+    """(CTAs of one task, resident CTAs per SM) of the payload's kernel."""
+    c, p = C.c_uint32(), C.c_uint32()
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data) if data else None
+    _cu_check(_libs().cuda.vgpu_cu_task_shape(device, KERNELS[payload_id], buf, len(data),
+                                              C.byref(c), C.byref(p)))
+    return c.value, p.value
 
 
 def model_simulate(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int = 1,
@@ -454,6 +472,47 @@ def cg_input_for_class(cls: str, niter: Optional[int] = None) -> bytes:
 def cg_result(out: bytes) -> tuple:
     """(zeta, rnorm, niter, n, nnz) from a nas-cg result."""
     return CG_RESULT.unpack(bytes(out[:CG_RESULT.size]))
+
+
+# ---- NPB MG problems (client side of the nas-mg payload) -------------------------
+
+MG_RESULT = struct.Struct("<ddIIQ")  # vgpu_mg_result
+
+
+@dataclass
+class MgClass:
+    nx: int
+    nit: int
+    coeffs: int
+    rnm2_verify: float
+
+
+def mg_class(cls: str) -> MgClass:
+    """NPB MG class parameters and the published rnm2 (S, W, A, B, C)."""
+    nx, nit, co, v = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_double()
+    _check(_libs().host.vgpu_mg_class(cls.encode()[:1], C.byref(nx), C.byref(nit), C.byref(co),
+                                      C.byref(v)))
+    return MgClass(nx.value, nit.value, co.value, v.value)
+
+
+def mg_make_input(nx: int, nit: int, coeffs: int) -> bytes:
+    """The nas-mg input: header + NPB zran3's right-hand side (untimed in NPB)."""
+    lib = _libs().host
+    need = C.c_uint64()
+    _check(lib.vgpu_mg_make_input(nx, nit, coeffs, None, 0, C.byref(need)))
+    buf = (C.c_uint8 * need.value)()
+    _check(lib.vgpu_mg_make_input(nx, nit, coeffs, buf, need.value, C.byref(need)))
+    return bytes(buf)
+
+
+def mg_input_for_class(cls: str, nit: Optional[int] = None) -> bytes:
+    c = mg_class(cls)
+    return mg_make_input(c.nx, c.nit if nit is None else nit, c.coeffs)
+
+
+def mg_result(out: bytes) -> tuple:
+    """(rnm2, rnmu, nx, nit) from a nas-mg result."""
+    return MG_RESULT.unpack(bytes(out[:MG_RESULT.size]))[:4]
 
 
 # ---- electrostatics inputs ------------------------------------------------------

@@ -14,10 +14,10 @@ import numpy as np
 from ._native import EpParams
 
 PAYLOAD = {"vecadd": "vector-add", "ep": "nas-ep", "bs": "black-scholes", "mm": "sgemm",
-           "cg": "nas-cg", "vmul": "vector-mul", "es": "electrostatics"}
+           "cg": "nas-cg", "vmul": "vector-mul", "es": "electrostatics", "mg": "nas-mg"}
 KINDS = ("vecadd", "ep", "bs", "mm")  # the kinds `mixed` cycles through (C5)
 DEFAULT_PROCS = {"vecadd": 4, "ep": 8, "bs": 16, "mm": 16, "mixed": 16, "cg": 8, "vmul": 4,
-                 "es": 8}
+                 "es": 8, "mg": 8}
 CONFIG_NAME = {
     "vecadd": "C1 vector addition, 1M floats per process",
     "ep": "C2 NAS EP class A split over the processes",
@@ -27,7 +27,10 @@ CONFIG_NAME = {
     "cg": "NAS CG class A per process (paper workload, not a BASELINE config)",
     "vmul": "VecMul 1M floats per process (paper workload, not a BASELINE config)",
     "es": "Electrostatics 100K atoms x 64x64x25 lattice per process (paper workload, not a BASELINE config)",
+    "mg": "NAS MG class S (32^3, 4 V-cycles) per process (paper workload, not a BASELINE config)",
 }
+MG_NX = {"S": 32, "W": 128, "A": 256, "B": 256, "C": 512}
+_mg_cache = {}
 
 # NPB CG shapes (n, nonzer) for the region bound (mirror of workloads.hpp)
 CG_SHAPES = {"S": (1400, 7), "W": (7000, 8), "A": (14000, 11), "B": (75000, 13), "C": (150000, 15)}
@@ -56,10 +59,11 @@ class Sizes:
         return ["--vecadd-n", str(self.vecadd_n), "--ep-m", str(self.ep_m),
                 "--ep-batches", str(self.ep_batches), "--bs-n", str(self.bs_n),
                 "--mm-n", str(self.mm_n), "--cg-class", self.cg_class,
-                "--es-atoms", str(self.es_atoms)]
+                "--es-atoms", str(self.es_atoms), "--mg-class", self.mg_class]
     bs_n: int = 4 << 20
     mm_n: int = 2048
     cg_class: str = "A"
+    mg_class: str = "S"
     es_atoms: int = 100000
     es_lattice: tuple = (64, 64, 25)
     es_h: float = 0.5
@@ -106,10 +110,30 @@ def cg_input(cls: str) -> bytes:
     return _cg_cache[cls]
 
 
+def mg_input(cls: str) -> bytes:
+    """The MG program's right-hand side (NPB zran3 through the product's
+    client-side builder, vgpu_mg_make_input); the same for every worker."""
+    if cls not in _mg_cache:
+        from .vgpu import mg_input_for_class
+        _mg_cache[cls] = mg_input_for_class(cls)
+    return _mg_cache[cls]
+
+
+def mg_workspace_bytes(nx: int) -> int:
+    """vgpu_mg_workspace_bytes: u and r on every level plus the norm partials."""
+    b, m = 0, 2
+    while m <= nx:
+        b += 2 * 8 * (m + 2) ** 3
+        m *= 2
+    return b + 16 * nx + 256
+
+
 def job_input(workload: str, worker: int, workers: int, sz: Sizes = Sizes()) -> bytes:
     k = kind_of(workload, worker)
     if k == "cg":
         return cg_input(sz.cg_class)
+    if k == "mg":
+        return mg_input(sz.mg_class)
     if k == "es":
         return es_input_native(worker, sz)
     if k in ("vecadd", "vmul"):
@@ -145,7 +169,7 @@ def es_input_native(worker: int, sz: Sizes) -> bytes:
 
 def output_bytes(kind: str, sz: Sizes = Sizes()) -> int:
     return {"vecadd": 4 * sz.vecadd_n, "ep": 112, "bs": 8 * sz.bs_n,
-            "mm": 4 * sz.mm_n * sz.mm_n, "cg": 32, "vmul": 4 * sz.vecadd_n,
+            "mm": 4 * sz.mm_n * sz.mm_n, "cg": 32, "mg": 32, "vmul": 4 * sz.vecadd_n,
             "es": 4 * sz.es_lattice[0] * sz.es_lattice[1] * sz.es_lattice[2]}[kind]
 
 
@@ -160,6 +184,8 @@ def cg_input_bound(cls: str) -> int:
 def input_bytes(kind: str, sz: Sizes = Sizes()) -> int:
     if kind == "cg":
         return cg_input_bound(sz.cg_class)
+    if kind == "mg":
+        return 16 + 8 * MG_NX[sz.mg_class] ** 3
     return {"vecadd": 8 * sz.vecadd_n, "ep": 32, "bs": 12 * sz.bs_n,
             "mm": 8 * sz.mm_n * sz.mm_n, "vmul": 8 * sz.vecadd_n,
             "es": 32 + 16 * sz.es_atoms}[kind]
@@ -170,6 +196,10 @@ def region_bytes(workload: str, sz: Sizes = Sizes(), resident: bool = False) -> 
     result's bytes (vgpu-spmd --resident places it at the result size
     rounded up to 64 KiB)."""
     kinds = KINDS if workload == "mixed" else (workload,)
+    if workload == "mg":  # the slot workspace (2 x region) must hold the grids
+        nx = MG_NX[sz.mg_class]
+        base = max(input_bytes("mg", sz), (mg_workspace_bytes(nx) + 1) // 2)
+        return base + (input_bytes("mg", sz) + 65536 if resident else 0)
     if resident:
         return max(((output_bytes(k, sz) + 65535) & ~65535) + input_bytes(k, sz) for k in kinds)
     return max(max(input_bytes(k, sz), output_bytes(k, sz)) for k in kinds)

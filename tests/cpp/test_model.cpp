@@ -216,3 +216,36 @@ TEST_CASE("device: capacity waves, determinism, timeline csv") {
     CHECK(DeviceSpec::b200().num_sms == 148);
     CHECK_THROWS_AS((void)simulate(WorkQueue{}, dev), std::invalid_argument);
 }
+
+TEST_CASE("device: B200 fluid block scheduler (DeviceSpec::fluid_blocks)") {
+    // 148 SMs x 4 resident CTAs = 592 slots; a NAS EP slice = 512 CTAs
+    DeviceSpec dev = DeviceSpec::b200();
+    dev.block_slots_per_sm = 4;
+    dev.fluid_blocks = true;
+    KernelProfile p;
+    p.t_data_in = 0;
+    p.t_comp = 100;
+    p.t_data_out = 0;
+    p.grid_size = 512;
+    auto span = [&](std::size_t n) {
+        std::vector<KernelProfile> ps(n, p);
+        return simulate(build_work_queue(ProgrammingStyle::PS1, ps), dev).makespan;
+    };
+    CHECK(span(1) == 100);
+    // the second kernel runs on the 80 free slots, then on 512 once the first
+    // is done: 512*100 work, 8000 by t = 100, the rest at 512 per us
+    CHECK(span(2) == 100 + static_cast<Micros>(std::ceil(43200.0 / 512)));
+    // n kernels saturate the device: total work / 592 slots, to within a
+    // kernel's tail (the last one cannot use more than 512 slots)
+    const Micros s8 = span(8);
+    CHECK(s8 >= static_cast<Micros>(8 * 512 * 100 / 592));
+    CHECK(s8 <= static_cast<Micros>(8 * 512 * 100 / 592) + 20);
+    // the reference's rule charges the late kernel whole waves on its 80 slots
+    dev.fluid_blocks = false;
+    CHECK(span(2) == 700);
+    // a grid larger than the device: its solo time already holds its waves
+    dev.fluid_blocks = true;
+    p.grid_size = 2 * 592;
+    CHECK(span(1) == 100);
+    CHECK(span(2) == 200);
+}

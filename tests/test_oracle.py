@@ -232,3 +232,41 @@ def test_es_oracle_single_charge_closed_form_and_superposition():
     assert np.allclose(vab, va + vb, rtol=1e-12, atol=1e-12)
     with pytest.raises(ValueError):
         oracle.es(V.es_input(a, 9, 7, 3, 0.45)[:-4])
+
+
+# ---- NAS MG (NPB 3.x mg.f): the oracle pinned to NPB's published rnm2 ------
+
+@pytest.mark.parametrize("cls", ["S", "W", "A", "B"])
+def test_mg_oracle_matches_npb_published_rnm2(cls):
+    """zran3 + the timed V-cycles reproduce NPB's verification value of each
+    class within NPB's own epsilon (1e-8); B uses the other smoother set."""
+    nx, nit, coeffs, verify = oracle.NPB_MG[cls]
+    r = oracle.mg_run(oracle.mg_make_input(nx, nit, coeffs))
+    assert abs(r.rnm2 - verify) / verify <= 1e-8, (cls, r.rnm2)
+    assert r.nx == nx and r.nit == nit and 0 < r.rnmu < 1
+
+
+@pytest.mark.parametrize("cls", ["S", "W", "A"])
+def test_mg_client_builder_matches_oracle_zran3_bytes(cls):
+    from paper_1511_07658_b200 import vgpu as V
+    nx, nit, coeffs, verify = oracle.NPB_MG[cls]
+    c = V.mg_class(cls)
+    assert (c.nx, c.nit, c.coeffs, c.rnm2_verify) == (nx, nit, coeffs, verify)
+    inp = V.mg_input_for_class(cls)
+    assert inp == oracle.mg_make_input(nx, nit, coeffs)
+    v = np.frombuffer(inp[16:], np.float64)
+    assert (v == 1.0).sum() == 10 and (v == -1.0).sum() == 10 and (v != 0).sum() == 20
+
+
+def test_mg_oracle_shapes_and_rejects():
+    from paper_1511_07658_b200 import vgpu as V
+    r, u = oracle.mg_run(oracle.mg_make_input(8, 2, 0), with_u=True)
+    assert u.shape == (10 ** 3,) and np.isfinite(u).all()
+    with pytest.raises(ValueError):
+        oracle.mg_run(oracle.mg_make_input(8, 2, 0)[:-8])
+    with pytest.raises(ValueError):
+        oracle.mg_run(oracle.mg_make_input(12, 2, 0))  # not a power of two
+    with pytest.raises(ValueError):
+        V.mg_class("Q")
+    # the payload's host-side contract
+    assert V.output_size("nas-mg", V.mg_make_input(32, 4, 0)) == 32
