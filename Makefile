@@ -20,7 +20,8 @@ CXX      ?= g++
 CC       ?= gcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
-CXXFLAGS := -O2 -g -std=c++20 -fPIC -Wall -Wextra -pthread -Iinclude
+CUDA_HOME ?= /usr/local/cuda
+CXXFLAGS := -O2 -g -std=c++20 -fPIC -Wall -Wextra -pthread -Iinclude -I$(CUDA_HOME)/include
 CFLAGS   := -O2 -g -fPIC -ffp-contract=off -std=c11 -Wall -Wextra -Wno-unknown-pragmas
 # the oracle's batch loops are OpenMP-parallel when the system gcc has libgomp
 # (the image's CC wrapper does not); results do not depend on the thread count

@@ -94,6 +94,10 @@ struct MetricsSnapshot {
     // B200: device work issued so far.
     std::uint64_t kernel_launches = 0;
     std::uint64_t device_tasks = 0;
+    // B200: the measured schedule — each device task's H2D / kernel / D2H
+    // interval from its CUDA events, in us since the GVM opened the device,
+    // stream_id = slot - 1 (write_timeline_csv's schema, device.cpp).
+    Timeline device_timeline;
 };
 
 void write_metrics_csv(const MetricsSnapshot& m, std::ostream& out);

@@ -102,6 +102,9 @@ int vgpu_gvm_tasks(vgpu_gvm* g, vgpu_task_metrics* out, uint32_t cap, uint32_t* 
 int vgpu_gvm_batches(vgpu_gvm* g, vgpu_batch_metrics* out, uint32_t cap, uint32_t* n);
 /* write_metrics_csv into buf; *len = full length even when truncated */
 int vgpu_gvm_metrics_csv(vgpu_gvm* g, char* buf, uint64_t cap, uint64_t* len);
+/* the measured schedule (MetricsSnapshot::device_timeline) in the
+ * reference's timeline CSV schema (write_timeline_csv, device.cpp) */
+int vgpu_gvm_timeline_csv(vgpu_gvm* g, char* buf, uint64_t cap, uint64_t* len);
 int vgpu_unlink_instance(const char* instance, uint32_t max_clients);
 
 int vgpu_client_req(const char* instance, vgpu_client** out);

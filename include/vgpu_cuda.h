@@ -188,6 +188,12 @@ typedef struct vgpu_cu_done {
     uint32_t batch_done;   /* 1 on the batch's last completion               */
     uint32_t kind;         /* vgpu_cu_done_kind                              */
     uint32_t reserved;
+    /* stage starts in us since the handle's epoch event (vgpu_cu_open), for
+     * the measured timeline; -1: the stage did not run on the device       */
+    float t_h2d_us;
+    float t_comp_us;
+    float t_d2h_us;
+    uint32_t reserved2;
 } vgpu_cu_done;
 
 typedef struct vgpu_cu_stats {
@@ -269,6 +275,17 @@ int vgpu_cu_execute(int device, uint32_t kernel, float param, const void* in,
                     uint64_t* out_bytes);
 /* Kernel launches issued by vgpu_cu_execute in this process. */
 uint64_t vgpu_cu_execute_launches(void);
+
+/* Fault containment. A sticky device fault (illegal address, trap, ...)
+ * seen by vgpu_cu_poll resets and rebuilds the context (slot buffers,
+ * streams, events, region and staging registrations) and reports every
+ * op that was in flight with status VGPU_CU_EINTERNAL. The generation
+ * counts the resets (inputs uploaded before one are gone); last_fault says
+ * what caused the last. inject_fault (tests; only with
+ * VGPU_ENABLE_FAULT_INJECTION=1) queues a trapping kernel as a task op. */
+uint64_t vgpu_cu_generation(vgpu_cu_dev* dev);
+const char* vgpu_cu_last_fault(vgpu_cu_dev* dev);
+int vgpu_cu_inject_fault(vgpu_cu_dev* dev, uint32_t slot, uint64_t tag);
 
 int vgpu_cu_device_count(int* n);
 /* One task's launch shape: the CTAs its share of a batched launch gets and

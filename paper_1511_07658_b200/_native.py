@@ -121,6 +121,9 @@ CUDA_API = {
     "vgpu_cu_get_stats": (C.c_int, [_P, C.POINTER(CuStats)]),
     "vgpu_cu_execute": (C.c_int, [C.c_int, _U32, C.c_float, _P, _U64, _P, _U64, C.POINTER(_U64)]),
     "vgpu_cu_execute_launches": (_U64, []),
+    "vgpu_cu_generation": (_U64, [_P]),
+    "vgpu_cu_last_fault": (C.c_char_p, [_P]),
+    "vgpu_cu_inject_fault": (C.c_int, [_P, _U32, _U64]),
     "vgpu_cu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "vgpu_cu_device_pci_bus_id": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),
     "vgpu_cu_task_shape": (C.c_int, [C.c_int, _U32, _P, _U64, C.POINTER(_U32), C.POINTER(_U32)]),
@@ -146,6 +149,7 @@ HOST_API = {
     "vgpu_gvm_tasks": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_gvm_batches": (C.c_int, [_P, _P, _U32, C.POINTER(_U32)]),
     "vgpu_gvm_metrics_csv": (C.c_int, [_P, C.c_char_p, _U64, C.POINTER(_U64)]),
+    "vgpu_gvm_timeline_csv": (C.c_int, [_P, C.c_char_p, _U64, C.POINTER(_U64)]),
     "vgpu_unlink_instance": (C.c_int, [C.c_char_p, _U32]),
     "vgpu_gvm_fold": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "vgpu_rendezvous_publish": (C.c_int, [C.c_char_p, _P, _U64]),

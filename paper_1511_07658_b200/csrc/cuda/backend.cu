@@ -42,6 +42,7 @@
 #include <vector>
 
 #include "vgpu_cuda.h"
+#include "../common/trace.h"
 #include "k_bs.cuh"
 #include "k_cg.cuh"
 #include "k_ep.cuh"
@@ -119,6 +120,9 @@ std::uint64_t isqrt(std::uint64_t v) {
 }
 
 // ---- device jobs and launches ------------------------------------------------
+
+// context resets done by fault containment in this process (any handle)
+std::atomic<std::uint64_t> g_context_resets{0};
 
 struct DevJob {
     std::uint32_t kernel = 0;
@@ -1093,7 +1097,13 @@ struct vgpu_cu_dev {
     std::vector<cudaEvent_t> event_pool;
     std::map<std::uint64_t, BatchRec> batches;
     std::uint64_t next_batch = 1;
-    std::vector<void*> pinned;
+    std::vector<std::pair<void*, std::uint64_t>> pinned;  // host buffers registered here
+    // fault containment: ops failed by a context reset, reported by the next
+    // poll; the reset count (vgpu_cu_generation) and what caused the last one
+    std::vector<vgpu_cu_done> fault_reports;
+    std::uint64_t generation = 0;
+    std::string last_fault;
+    cudaEvent_t epoch = nullptr;  // t = 0 of the measured timeline
 
     // armed ops in submission order, not yet reported; owned by the
     // dispatcher thread (submit/upload/poll are only called from it)
@@ -1419,6 +1429,135 @@ int vgpu_cu_task_check(vgpu_cu_dev* d, std::uint32_t kernel, const void* in,
     return VGPU_CU_OK;
 }
 
+namespace {
+
+// Device-side state of a handle: the slot arena, the streams, the event
+// pool. Built at open and again after a context reset.
+int init_state(vgpu_cu_dev* d) {
+    const std::uint64_t buf = d->buf_bytes;
+    // in | out | EP scratch | sgemm workspace (hi/lo splits: 2 x input)
+    const std::uint64_t per_slot = 4 * buf + round_up(kScratchBytes, kAlign);
+    cudaError_t e = cudaMalloc(&d->arena, per_slot * d->max_clients);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(arena)");
+    e = cudaMemset(d->arena, 0, per_slot * d->max_clients);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(arena)");
+    for (std::uint32_t i = 1; i <= d->max_clients; ++i) {
+        SlotState& s = d->slots[i];
+        s.index = i;
+        std::uint8_t* base = d->arena + per_slot * (i - 1);
+        s.d_in = base;
+        s.d_out = base + buf;
+        s.d_scratch = base + 2 * buf;
+        s.d_ws = s.d_scratch + round_up(kScratchBytes, kAlign);
+        e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    }
+    e = cudaStreamCreateWithFlags(&d->anchor_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(anchor)");
+    e = cudaStreamCreateWithFlags(&d->up_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->down_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(copy queues)");
+    // warm the event pool: 6 events per slot for two ops in flight + batch events
+    for (std::uint32_t i = 0; i < 16 * d->max_clients + 16; ++i) {
+        cudaEvent_t ev;
+        e = cudaEventCreate(&ev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+        d->event_pool.push_back(ev);
+    }
+    e = cudaEventCreate(&d->epoch);
+    if (e == cudaSuccess) e = cudaEventRecord(d->epoch, d->anchor_stream);
+    if (e == cudaSuccess) e = cudaEventSynchronize(d->epoch);
+    if (e != cudaSuccess) return cuda_fail(e, "epoch event");
+    return VGPU_CU_OK;
+}
+
+// Forget (live = false: the context is gone) or release (live) the
+// device-side state; registered host memory is handled by the callers.
+void drop_state(vgpu_cu_dev* d, bool live) {
+    if (live) {
+        for (auto& s : d->slots)
+            if (s.stream) cudaStreamSynchronize(s.stream);
+        for (cudaStream_t st : {d->anchor_stream, d->up_stream, d->down_stream})
+            if (st) cudaStreamSynchronize(st);
+    }
+    for (Op* op : d->outstanding) d->release_op(op);
+    d->outstanding.clear();
+    for (auto& s : d->slots) {
+        if (s.open_upload) d->release_op(s.open_upload);
+        s.open_upload = nullptr;
+        if (live && s.stream) cudaStreamDestroy(s.stream);
+        s.stream = nullptr;
+        s.task_busy = false;
+        s.ops_in_flight = 0;
+    }
+    for (auto& [id, b] : d->batches) {
+        if (b.anchor) d->event_pool.push_back(b.anchor);
+        for (auto ev : b.pooled) d->event_pool.push_back(ev);
+    }
+    d->batches.clear();
+    if (live)
+        for (auto ev : d->event_pool) cudaEventDestroy(ev);
+    d->event_pool.clear();
+    if (live && d->epoch) cudaEventDestroy(d->epoch);
+    d->epoch = nullptr;
+    for (cudaStream_t* st : {&d->anchor_stream, &d->up_stream, &d->down_stream}) {
+        if (live && *st) cudaStreamDestroy(*st);
+        *st = nullptr;
+    }
+    if (live && d->arena) cudaFree(d->arena);
+    d->arena = nullptr;
+    if (live && d->comm && nccl().ok) nccl().comm_destroy(d->comm);
+    d->comm = nullptr;
+}
+
+// Sticky device fault (an illegal address, a trap, ...): the context is
+// unusable for every client of this GVM. Contain it: every in-flight op is
+// reported failed (the daemon NACKs those tasks with Internal), the context
+// is reset and rebuilt — arena, streams, events, and the registration of
+// the clients' regions and staging buffers — and the generation count
+// tells the daemon that inputs already in HBM are gone. The reference
+// contains a failing payload to its own task (proj/src/daemon.cpp:524-527).
+void recover(vgpu_cu_dev* d, cudaError_t cause) {
+    vgpu::trace::Range range("cu fault containment (context reset)");
+    d->last_fault = cudaGetErrorString(cause);
+    ++g_context_resets;
+    auto fail_report = [&](Op* op) {
+        vgpu_cu_done r{};
+        r.tag = op->tag;
+        r.batch = op->batch;
+        r.slot = op->slot;
+        r.kind = op->kind;
+        r.status = VGPU_CU_EINTERNAL;
+        r.t_h2d_us = r.t_comp_us = r.t_d2h_us = -1.0f;
+        d->fault_reports.push_back(r);
+    };
+    for (Op* op : d->outstanding) fail_report(op);
+    for (auto& s : d->slots)
+        if (s.open_upload) fail_report(s.open_upload);
+    drop_state(d, false);
+    cudaDeviceReset();
+    cudaGetLastError();
+    cudaSetDevice(d->device);
+    int rc = init_state(d);
+    for (std::uint32_t i = 1; i <= d->max_clients && rc == VGPU_CU_OK; ++i) {
+        SlotState& s = d->slots[i];
+        if (!s.reg_base) continue;
+        void* dev = nullptr;
+        if (cudaHostRegister(s.reg_base, s.reg_bytes, cudaHostRegisterPortable | cudaHostRegisterMapped) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer(&dev, s.reg_base, 0) != cudaSuccess)
+            rc = VGPU_CU_EINTERNAL;
+        s.reg_dev = static_cast<std::uint8_t*>(dev);
+    }
+    for (auto& [p, n] : d->pinned)
+        if (rc == VGPU_CU_OK && cudaHostRegister(p, n, cudaHostRegisterPortable) != cudaSuccess)
+            rc = VGPU_CU_EINTERNAL;
+    if (rc != VGPU_CU_OK) d->last_fault += " (and the rebuild after the reset failed)";
+    ++d->generation;
+}
+
+}  // namespace
+
 int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes,
                  vgpu_cu_dev** out) {
     if (!out || max_clients == 0) return VGPU_CU_EINVAL;
@@ -1433,41 +1572,12 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
     d->max_clients = max_clients;
     d->slot_bytes = slot_bytes;
     d->slots.resize(max_clients + 1);
-    const std::uint64_t buf = round_up(std::max<std::uint64_t>(slot_bytes, 256), kAlign);
-    d->buf_bytes = buf;
-    // in | out | EP scratch | sgemm workspace (hi/lo splits: 2 x input)
-    const std::uint64_t per_slot = 4 * buf + round_up(kScratchBytes, kAlign);
-    auto fail = [&](int code) {
-        vgpu_cu_close(d);
-        return code;
-    };
-    cudaError_t e = cudaMalloc(&d->arena, per_slot * max_clients);
-    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(arena)"));
-    e = cudaMemset(d->arena, 0, per_slot * max_clients);
-    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemset(arena)"));
-    for (std::uint32_t i = 1; i <= max_clients; ++i) {
-        SlotState& s = d->slots[i];
-        s.index = i;
-        std::uint8_t* base = d->arena + per_slot * (i - 1);
-        s.d_in = base;
-        s.d_out = base + buf;
-        s.d_scratch = base + 2 * buf;
-        s.d_ws = s.d_scratch + round_up(kScratchBytes, kAlign);
-        e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
-    }
-    e = cudaStreamCreateWithFlags(&d->anchor_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(anchor)"));
-    e = cudaStreamCreateWithFlags(&d->up_stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->down_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate(copy queues)"));
+    d->buf_bytes = round_up(std::max<std::uint64_t>(slot_bytes, 256), kAlign);
     if (const char* f = std::getenv("VGPU_COPY_FIFO")) d->fifo = std::atoi(f) != 0;
-    // warm the event pool: 6 events per slot for two ops in flight + batch events
-    for (std::uint32_t i = 0; i < 16 * max_clients + 16; ++i) {
-        cudaEvent_t ev;
-        e = cudaEventCreate(&ev);
-        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
-        d->event_pool.push_back(ev);
+    rc = init_state(d);
+    if (rc != VGPU_CU_OK) {
+        vgpu_cu_close(d);
+        return rc;
     }
     *out = d;
     return VGPU_CU_OK;
@@ -1476,33 +1586,59 @@ int vgpu_cu_open(int device, std::uint32_t max_clients, std::uint64_t slot_bytes
 void vgpu_cu_close(vgpu_cu_dev* d) {
     if (!d) return;
     cudaSetDevice(d->device);
+    drop_state(d, true);
     for (auto& s : d->slots)
-        if (s.stream) cudaStreamSynchronize(s.stream);
-    if (d->anchor_stream) cudaStreamSynchronize(d->anchor_stream);
-    if (d->up_stream) cudaStreamSynchronize(d->up_stream);
-    if (d->down_stream) cudaStreamSynchronize(d->down_stream);
-    for (Op* op : d->outstanding) d->release_op(op);
-    d->outstanding.clear();
-    for (auto& s : d->slots) {
-        if (s.open_upload) d->release_op(s.open_upload);
-        s.open_upload = nullptr;
         if (s.reg_base) cudaHostUnregister(s.reg_base);
-        if (s.stream) cudaStreamDestroy(s.stream);
+    for (auto& [p, n] : d->pinned) {
+        cudaHostUnregister(p);
+        std::free(p);
     }
-    for (auto& [id, b] : d->batches) {
-        if (b.anchor) d->event_pool.push_back(b.anchor);
-        for (auto ev : b.pooled) d->event_pool.push_back(ev);
-    }
-    for (auto ev : d->event_pool) cudaEventDestroy(ev);
-    if (d->anchor_stream) cudaStreamDestroy(d->anchor_stream);
-    if (d->up_stream) cudaStreamDestroy(d->up_stream);
-    if (d->down_stream) cudaStreamDestroy(d->down_stream);
-    for (void* p : d->pinned) cudaFreeHost(p);
-    if (d->arena) cudaFree(d->arena);
-    if (d->comm && nccl().ok) nccl().comm_destroy(d->comm);
     cudaGetLastError();
     delete d;
 }
+
+std::uint64_t vgpu_cu_generation(vgpu_cu_dev* d) { return d ? d->generation : 0; }
+
+}  // extern "C"
+
+namespace {
+__global__ void fault_inject_kernel() { __trap(); }
+}  // namespace
+
+extern "C" {
+
+int vgpu_cu_inject_fault(vgpu_cu_dev* d, std::uint32_t slot, std::uint64_t tag) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("VGPU_ENABLE_FAULT_INJECTION");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    if (!enabled) {
+        set_err("fault injection is off (VGPU_ENABLE_FAULT_INJECTION=1 enables it)");
+        return VGPU_CU_EINVAL;
+    }
+    if (!d || slot < 1 || slot > d->max_clients) return VGPU_CU_EINVAL;
+    CK(cudaSetDevice(d->device));
+    SlotState& s = d->slots[slot];
+    Op* op = nullptr;
+    int rc = d->new_op(slot, VGPU_CU_DONE_TASK, tag, &op);
+    if (rc) return rc;
+    cudaError_t e = cudaEventRecord(op->ev[kEvH2d0], s.stream);
+    if (e == cudaSuccess) {
+        fault_inject_kernel<<<1, 32, 0, s.stream>>>();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(op->ev[kEvD2h1], s.stream);
+    if (e != cudaSuccess) {
+        d->release_op(op);
+        return cuda_fail(e, "vgpu_cu_inject_fault");
+    }
+    ++s.ops_in_flight;
+    s.task_busy = true;
+    d->outstanding.push_back(op);
+    return VGPU_CU_OK;
+}
+
+const char* vgpu_cu_last_fault(vgpu_cu_dev* d) { return d ? d->last_fault.c_str() : ""; }
 
 int vgpu_cu_register_region(vgpu_cu_dev* d, std::uint32_t slot, void* base, std::uint64_t bytes) {
     if (!d || slot < 1 || slot > d->max_clients || !base) return VGPU_CU_EINVAL;
@@ -1528,17 +1664,31 @@ int vgpu_cu_register_region(vgpu_cu_dev* d, std::uint32_t slot, void* base, std:
 int vgpu_cu_alloc_pinned(vgpu_cu_dev* d, std::uint64_t bytes, void** out) {
     if (!d || !out) return VGPU_CU_EINVAL;
     CK(cudaSetDevice(d->device));
-    CK(cudaHostAlloc(out, std::max<std::uint64_t>(bytes, 1), cudaHostAllocPortable));
-    d->pinned.push_back(*out);
+    // host memory page-locked by registration (not cudaHostAlloc): it
+    // survives a context reset and is registered again (fault containment)
+    bytes = round_up(std::max<std::uint64_t>(bytes, 1), 4096);
+    void* p = nullptr;
+    if (posix_memalign(&p, 4096, bytes) != 0) {
+        set_err("pinned staging: no host memory for %llu B", (unsigned long long)bytes);
+        return VGPU_CU_EINTERNAL;
+    }
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        std::free(p);
+        return cuda_fail(e, "cudaHostRegister(staging)");
+    }
+    d->pinned.push_back({p, bytes});
+    *out = p;
     return VGPU_CU_OK;
 }
 
 void vgpu_cu_free_pinned(vgpu_cu_dev* d, void* p) {
     if (!d || !p) return;
-    auto it = std::find(d->pinned.begin(), d->pinned.end(), p);
+    auto it = std::find_if(d->pinned.begin(), d->pinned.end(), [p](const auto& e) { return e.first == p; });
     if (it == d->pinned.end()) return;
     d->pinned.erase(it);
-    cudaFreeHost(p);
+    cudaHostUnregister(p);
+    std::free(p);
 }
 
 
@@ -1554,6 +1704,7 @@ int vgpu_cu_get_stats(vgpu_cu_dev* d, vgpu_cu_stats* out) {
 
 int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::uint64_t bytes,
                    std::uint64_t tag) {
+    vgpu::trace::Range range("cu upload");
     if (!d || slot < 1 || slot > d->max_clients || (!h_in && bytes)) return VGPU_CU_EINVAL;
     if (bytes > d->slot_bytes) {
         set_err("upload of %llu B exceeds the slot (%llu B)", (unsigned long long)bytes,
@@ -1658,6 +1809,7 @@ int vgpu_cu_upload_part(vgpu_cu_dev* d, std::uint32_t slot, const void* h_src, s
 
 int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, std::uint32_t n,
                          std::uint64_t* batch_id) {
+    vgpu::trace::Range range("cu submit_batch");
     if (!d || (!tasks && n)) return VGPU_CU_EINVAL;
     if (n == 0) return VGPU_CU_OK;
     // validate everything before enqueueing anything
@@ -1899,6 +2051,10 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
     r.kind = op->kind;
     r.status = sticky == cudaSuccess ? VGPU_CU_OK : VGPU_CU_EINTERNAL;
     r.h2d_us = op->has_h2d ? 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvH2d1]) : 0.0f;
+    auto since_epoch = [&](cudaEvent_t ev) { return 1000.0f * elapsed_ms(d->epoch, ev); };
+    r.t_h2d_us = op->has_h2d ? since_epoch(op->parts.empty() ? op->ev[kEvH2d0] : op->parts[0]) : -1.0f;
+    r.t_comp_us = -1.0f;
+    r.t_d2h_us = -1.0f;
     if (s.ops_in_flight) --s.ops_in_flight;
     if (op->kind == VGPU_CU_DONE_UPLOAD) {
         r.span_us = r.h2d_us;
@@ -1912,6 +2068,8 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
     }
     r.comp_us = op->has_comp ? 1000.0f * elapsed_ms(op->comp0, op->comp1) : 0.0f;
     r.d2h_us = 1000.0f * elapsed_ms(op->d2h0 ? op->d2h0 : op->ev[kEvD2h0], op->ev[kEvD2h1]);
+    if (op->has_comp) r.t_comp_us = since_epoch(op->comp0);
+    r.t_d2h_us = since_epoch(op->d2h0 ? op->d2h0 : op->ev[kEvD2h0]);
     r.span_us = 1000.0f * elapsed_ms(op->ev[kEvH2d0], op->ev[kEvD2h1]);
     auto it = d->batches.find(op->batch);
     if (it != d->batches.end()) {
@@ -1934,6 +2092,12 @@ void report_op(vgpu_cu_dev* d, Op* op, cudaError_t sticky, vgpu_cu_done& r) {
 int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint32_t* n_out) {
     if (!d || !n_out || (!out && cap)) return VGPU_CU_EINVAL;
     *n_out = 0;
+    auto drain_faults = [&] {
+        std::size_t k = 0;
+        for (; k < d->fault_reports.size() && *n_out < cap; ++k) out[(*n_out)++] = d->fault_reports[k];
+        d->fault_reports.erase(d->fault_reports.begin(), d->fault_reports.begin() + k);
+    };
+    drain_faults();
     if (d->outstanding.empty()) return VGPU_CU_OK;
     cudaSetDevice(d->device);
     // completion = the op's final event has completed (an event query: no
@@ -1946,10 +2110,18 @@ int vgpu_cu_poll(vgpu_cu_dev* d, vgpu_cu_done* out, std::uint32_t cap, std::uint
             ++i;
             continue;
         }
-        // done, or the device failed (e.g. a sticky launch/kernel error):
-        // report it either way, with Internal status in the second case,
-        // so the client's STP gets NACK(Internal) instead of waiting forever
-        if (q != cudaSuccess) cudaGetLastError();
+        // done, or the device failed: a sticky fault (the context cannot
+        // run anything any more) is contained by a reset and rebuild that
+        // fails every in-flight op; a non-sticky error fails this op alone.
+        // Either way the client's STP gets NACK(Internal), never a hang.
+        if (q != cudaSuccess) {
+            cudaGetLastError();
+            if (cudaDeviceSynchronize() != cudaSuccess) {
+                recover(d, q);
+                drain_faults();
+                return VGPU_CU_OK;
+            }
+        }
         report_op(d, op, q, out[(*n_out)++]);
         d->outstanding.erase(d->outstanding.begin() + i);
         d->release_op(op);
@@ -1981,6 +2153,7 @@ int vgpu_cu_wait(vgpu_cu_dev* d, std::int64_t timeout_us) {
 namespace {
 struct ProcCtx {
     std::mutex mu;
+    std::uint64_t resets = 0;  // g_context_resets when the buffers were made
     int device = -1;
     cudaStream_t stream = nullptr;
     std::uint8_t* d_in = nullptr;
@@ -2012,6 +2185,15 @@ int vgpu_cu_execute(int device, std::uint32_t kernel, float param, const void* i
     }
     ProcCtx& c = proc();
     std::lock_guard lk(c.mu);
+    if (c.resets != g_context_resets.load()) {
+        // a GVM handle in this process reset the context after a fault: the
+        // old buffers and stream died with it
+        c.resets = g_context_resets.load();
+        c.stream = nullptr;
+        c.d_in = c.d_out = c.d_scratch = c.d_ws = nullptr;
+        c.cap_in = c.cap_out = c.cap_ws = 0;
+        c.device = -1;
+    }
     if (c.device != device) {
         rc = require_sm100(device);
         if (rc) return rc;

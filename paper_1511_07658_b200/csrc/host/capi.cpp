@@ -258,6 +258,21 @@ int vgpu_gvm_metrics_csv(vgpu_gvm* g, char* buf, uint64_t cap, uint64_t* len) {
     });
 }
 
+int vgpu_gvm_timeline_csv(vgpu_gvm* g, char* buf, uint64_t cap, uint64_t* len) {
+    if (!g || !len) return VGPU_E_INVALID;
+    return guarded([&] {
+        std::ostringstream os;
+        write_timeline_csv(g->daemon->metrics().device_timeline, os);
+        const std::string s = os.str();
+        *len = s.size();
+        if (buf && cap) {
+            const std::size_t k = std::min<std::size_t>(cap - 1, s.size());
+            std::memcpy(buf, s.data(), k);
+            buf[k] = '\0';
+        }
+    });
+}
+
 int vgpu_unlink_instance(const char* instance, uint32_t max_clients) {
     if (!instance) return VGPU_E_INVALID;
     return guarded([&] { unlink_os_instance(instance, max_clients); });

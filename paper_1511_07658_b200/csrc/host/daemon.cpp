@@ -34,6 +34,7 @@
 #include "vgpu/daemon.hpp"
 #include "vgpu/model.hpp"
 #include "vgpu_cuda.h"
+#include "../common/trace.h"
 
 namespace vgpu {
 
@@ -95,8 +96,10 @@ struct Session {
     std::uint32_t uploads = 0;   // eager SND uploads in flight
     bool input_resident = false; // the current input already sits in HBM
     bool input_inline = false;   // the current input is the <= 64 B snapshot in head
+    bool input_lost = false;     // its HBM copy died in a device reset: SND again
     std::uint8_t head[64] = {};  // first bytes of the input (EP parameters)
     float upload_h2d_us = 0.0f;
+    float upload_t0_us = -1.0f;  // its start since the device epoch
     std::deque<Inbound> backlog; // frames that arrived while an upload ran
     // streamed SND (the client fills the region while the GVM uploads it)
     struct Stream {
@@ -132,6 +135,7 @@ struct InFlight {
     Clock::time_point dispatch_wall;
     TaskMetrics vmetrics;  // virtual-clock values, fixed at flush
     float upload_h2d_us = 0.0f;
+    float upload_t0_us = -1.0f;
     bool ep = false;             // a NAS EP slice: its result joins the GVM's fold
     std::uint64_t ep_first = 0;  // its first batch (the fold key)
 };
@@ -170,9 +174,11 @@ struct GvmDaemon::Impl {
     std::map<std::uint64_t, BatchState> batches;     // batch key -> state
     std::uint64_t next_tag = 1;
     std::uint32_t streams_active = 0;  // sessions with a streamed SND still filling
+    std::uint64_t device_generation = 0;  // context resets seen (fault containment)
 
     mutable std::mutex metrics_mu;
     std::vector<TaskMetrics> task_metrics;
+    Timeline timeline;  // measured (CUDA events), under metrics_mu
     std::vector<BatchMetrics> batch_metrics;
     std::uint64_t batches_flushed = 0;
     Micros busy_us = 0;
@@ -274,6 +280,10 @@ struct GvmDaemon::Impl {
     void dispatch(const Message& m, Session* s) {
         if (!leased(*s)) return nack(m.client_id, m.task_id, ErrCode::NoLease,
                                      "no lease for client");
+        static constexpr const char* kVerb[] = {"gvm ?",   "gvm REQ", "gvm SND", "gvm STR",
+                                                "gvm STP", "gvm RCV", "gvm RLS"};
+        const auto op = static_cast<unsigned>(m.opcode);
+        trace::Range range(op < 7 ? kVerb[op] : "gvm frame");
         switch (m.opcode) {
             case Opcode::Snd: return on_snd(m, *s);
             case Opcode::Str: return on_str(m, *s);
@@ -286,6 +296,7 @@ struct GvmDaemon::Impl {
     }
 
     void on_req(const Message& m, const std::string& origin) {
+        trace::Range range("gvm REQ");
         std::uint32_t slot = 0;
         for (std::uint32_t i = 1; i <= cfg.max_clients && slot == 0; ++i) {
             const Session& s = sessions[i - 1];
@@ -340,6 +351,7 @@ struct GvmDaemon::Impl {
         if (snd->flags & kSndStreamed) return start_stream(m, s, *len, snd->offset);
         s.input_len = *len;
         s.input_offset = snd->offset;
+        s.input_lost = false;
         s.input.clear();
         s.input_resident = false;
         s.input_inline = false;
@@ -391,6 +403,7 @@ struct GvmDaemon::Impl {
                         "streamed SND needs a transport with fill counters");
         s.input_len = len;
         s.input_offset = offset;
+        s.input_lost = false;
         s.input.clear();
         s.input_resident = false;
         s.input_inline = false;
@@ -423,6 +436,7 @@ struct GvmDaemon::Impl {
     // Issue the filled parts of every active stream (dispatcher thread).
     bool pump_streams() {
         if (streams_active == 0) return false;
+        trace::Range range("gvm streamed SND parts");
         bool moved = false;
         for (std::uint32_t id = 1; id <= cfg.max_clients; ++id) {
             Session& s = sessions[id - 1];
@@ -615,6 +629,7 @@ struct GvmDaemon::Impl {
     }
 
     void flush() {
+        trace::Range range("gvm flush (barrier dispatch)");
         if (batch.empty()) return;
         const bool virt = cfg.clock == ClockMode::Virtual;
         const ProgrammingStyle style = batch_style();
@@ -659,6 +674,12 @@ struct GvmDaemon::Impl {
             if (!dk) {
                 // user host payload: the reference's execution model
                 run_host(t, vm, live, virt, s);
+                continue;
+            }
+            if (live && s->input_lost) {
+                fail_session(t.client_id, t.generation, ErrCode::Internal,
+                             "the device was reset after a fault; SND the input again");
+                record_task(vm);
                 continue;
             }
             std::uint64_t out_bytes = 0;
@@ -708,6 +729,7 @@ struct GvmDaemon::Impl {
                 ct.flags |= VGPU_CU_TASK_INPUT_RESIDENT;
                 if (in_len <= sizeof s->head) ct.h_in = s->head;  // SND-time bytes
                 f.upload_h2d_us = s->upload_h2d_us;
+                f.upload_t0_us = s->upload_t0_us;
             }
             if (cfg.data_plane == DataPlane::ZeroCopy) {
                 ct.h_out = transport->region(t.client_id).data();
@@ -827,10 +849,25 @@ struct GvmDaemon::Impl {
         bool any = false;
         for (;;) {
             std::uint32_t n = 0;
-            if (vgpu_cu_poll(dev, done, 64, &n) != VGPU_CU_OK || n == 0) return any;
+            if (vgpu_cu_poll(dev, done, 64, &n) != VGPU_CU_OK || n == 0) break;
             any = true;
             for (std::uint32_t i = 0; i < n; ++i) complete(done[i]);
         }
+        if (const std::uint64_t g = vgpu_cu_generation(dev); g != device_generation) {
+            // a sticky device fault was contained by a context reset: the
+            // in-flight tasks were failed above (NACK Internal at STP); inputs
+            // that sat in HBM are gone, so their next task fails until the
+            // client sends them again. The GVM keeps serving.
+            device_generation = g;
+            std::fprintf(stderr, "gvm: device fault contained by a context reset (#%llu): %s\n",
+                         static_cast<unsigned long long>(g), vgpu_cu_last_fault(dev));
+            for (Session& s : sessions) {
+                if (s.input_resident) s.input_lost = true;
+                s.input_resident = false;
+                s.device_busy = false;
+            }
+        }
+        return any;
     }
 
     void complete(const vgpu_cu_done& d) {
@@ -845,6 +882,7 @@ struct GvmDaemon::Impl {
         if (s) s->device_busy = false;
 
         TaskMetrics tm = f.vmetrics;
+        record_timeline(d, f);
         if (!virt) {
             tm.queue_wait_us = us_between(f.arrival_wall, f.dispatch_wall);
             tm.pure_gpu_us = static_cast<Micros>(d.span_us + 0.5f);
@@ -898,6 +936,23 @@ struct GvmDaemon::Impl {
         if (!fresh && std::memcmp(&it->second, &r, sizeof r) != 0) ep_mismatch = true;
     }
 
+    // the measured schedule (MetricsSnapshot::device_timeline): an eager
+    // upload's H2D belongs to the task that follows it on the slot
+    void record_timeline(const vgpu_cu_done& d, const InFlight& f) {
+        std::lock_guard lk(metrics_mu);
+        const std::uint32_t stream = f.client_id - 1;
+        auto add = [&](CommandKind k, float t0, float dur) {
+            if (t0 < 0.0f) return;
+            const Micros a = static_cast<Micros>(t0 + 0.5f);
+            timeline.entries.push_back({f.task_id, stream, k, a, a + static_cast<Micros>(dur + 0.5f)});
+            timeline.makespan = std::max(timeline.makespan, a + static_cast<Micros>(dur + 0.5f));
+        };
+        if (d.t_h2d_us >= 0.0f) add(CommandKind::SendData, d.t_h2d_us, d.h2d_us);
+        else if (f.upload_t0_us >= 0.0f) add(CommandKind::SendData, f.upload_t0_us, f.upload_h2d_us);
+        add(CommandKind::Compute, d.t_comp_us, d.comp_us);
+        add(CommandKind::RtrvData, d.t_d2h_us, d.d2h_us);
+    }
+
     void upload_done(const vgpu_cu_done& d) {
         Session* s = session(d.slot);
         if (!s) return;
@@ -912,6 +967,7 @@ struct GvmDaemon::Impl {
         } else {
             if (s->uploads == 0) s->input_resident = true;  // the last SND's bytes
             s->upload_h2d_us = d.h2d_us;
+            s->upload_t0_us = d.t_h2d_us;
             ack(d.slot, task);
         }
         // replay what the client sent meanwhile, until another upload starts
@@ -1052,6 +1108,7 @@ MetricsSnapshot GvmDaemon::metrics() const {
                       ? impl_->cfg.t_init + impl_->busy_us
                       : us_between(impl_->started, Clock::now());
     m.device_tasks = impl_->device_tasks;
+    m.device_timeline = impl_->timeline;
     if (impl_->dev) {
         vgpu_cu_stats st{};
         if (vgpu_cu_get_stats(impl_->dev, &st) == VGPU_CU_OK)

@@ -7,18 +7,24 @@
 #include <string>
 #include <vector>
 
+#include "vgpu/npb_mg.hpp"
 #include "vgpu_cuda.h"
 #include "workloads.hpp"
 
 int main(int argc, char** argv) {
-    // payload-bench [device] [kind|all] [tasks|0=1,4,16] [steps]
+    // payload-bench [device] [kind|all] [tasks|0=1,4,16] [steps]   (mg: NPB class S)
     int device = argc > 1 ? std::atoi(argv[1]) : 0;
     const std::string only = argc > 2 ? argv[2] : "all";
     const std::uint32_t only_tasks = argc > 3 ? std::atoi(argv[3]) : 0;
     const std::uint32_t steps = argc > 4 ? std::atoi(argv[4]) : 20;
-    const char* kinds[] = {"vecadd", "ep", "bs", "mm"};
-    const std::uint32_t kernels[] = {VGPU_CU_K_VADD, VGPU_CU_K_EP, VGPU_CU_K_BS, VGPU_CU_K_SGEMM};
-    for (int k = 0; k < 4; ++k) {
+    vgpu::wl::mg_builder() = [](char cls) {
+        const vgpu::npb::MgClass c = vgpu::npb::mg_class(cls);
+        return vgpu::npb::make_mg_input(c.nx, c.nit, c.coeffs);
+    };
+    const char* kinds[] = {"vecadd", "ep", "bs", "mm", "mg"};
+    const std::uint32_t kernels[] = {VGPU_CU_K_VADD, VGPU_CU_K_EP, VGPU_CU_K_BS, VGPU_CU_K_SGEMM,
+                                     VGPU_CU_K_MG};
+    for (int k = 0; k < 5; ++k) {
         if (only != "all" && only != kinds[k]) continue;
         const std::vector<std::uint32_t> counts =
             only_tasks ? std::vector<std::uint32_t>{only_tasks} : std::vector<std::uint32_t>{1, 4, 16};

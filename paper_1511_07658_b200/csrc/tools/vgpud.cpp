@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "vgpu/daemon.hpp"
+#include "vgpu/device.hpp"
 #include "vgpu/multigpu.hpp"
 #include "vgpu_cuda.h"
 
@@ -44,7 +45,7 @@ void usage() {
         "      [--t-ctx-switch US] [--metrics-out PATH] [--device ORDINAL]\n"
         "      [--data-plane zero-copy|snapshot] [--ready-file PATH]\n"
         "      [--nranks N --rank R --rendezvous PATH [--reduce-out PATH]]\n"
-        "      [--fold-out PATH] [--cpus LIST|none]");
+        "      [--fold-out PATH] [--timeline-out PATH] [--cpus LIST|none]");
 }
 
 }  // namespace
@@ -72,7 +73,7 @@ int main(int argc, char** argv) {
         }
     }
     vgpu::GvmConfig cfg;
-    std::string metrics_out, ready_file, rendezvous, reduce_out, fold_out, cpus = "auto";
+    std::string metrics_out, ready_file, rendezvous, reduce_out, fold_out, timeline_out, cpus = "auto";
     int nranks = 0, rank = 0;
     try {
         for (const auto& [k, v] : opt) {
@@ -99,6 +100,7 @@ int main(int argc, char** argv) {
             else if (k == "rendezvous") rendezvous = v;
             else if (k == "reduce-out") reduce_out = v;
             else if (k == "fold-out") fold_out = v;
+            else if (k == "timeline-out") timeline_out = v;
             else if (k == "cpus") cpus = v;
             else if (k == "data-plane") {
                 if (v == "zero-copy") cfg.data_plane = vgpu::DataPlane::ZeroCopy;
@@ -216,6 +218,10 @@ int main(int argc, char** argv) {
         vgpu_cu_close(comm_dev);
     }
     const auto m = daemon->metrics();
+    if (!timeline_out.empty()) {  // the measured schedule, reference timeline schema
+        std::ofstream out(timeline_out);
+        vgpu::write_timeline_csv(m.device_timeline, out);
+    }
     if (metrics_out.empty()) {
         vgpu::write_metrics_csv(m, std::cout);
     } else {

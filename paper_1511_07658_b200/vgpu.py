@@ -192,6 +192,15 @@ class GvmDaemon:
         _check(_libs().host.vgpu_gvm_metrics_csv(self._h, buf, n.value + 1, C.byref(n)))
         return buf.value.decode()
 
+    def timeline_csv(self) -> str:
+        """The measured schedule (CUDA events) in the reference's timeline
+        schema: task_id,stream_id,kind,start_us,end_us."""
+        n = C.c_uint64()
+        _check(_libs().host.vgpu_gvm_timeline_csv(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(_libs().host.vgpu_gvm_timeline_csv(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
 
 def rendezvous_publish(path: str, data: bytes) -> None:
     """Rank 0 publishes the NCCL unique id (atomic file rename)."""

@@ -1,0 +1,16 @@
+# round 2: the default (C3) bench line, its reference arm, acceptance 5-7,
+# MG line, the C3 launch list and ncu captures, the FP64/FP32 peak probes
+python -c "
+from paper_1511_07658_b200 import vgpu as V
+import json
+print(json.dumps({'fp64_tflops': V.peak_probe('fp64'), 'fp32_tflops': V.peak_probe('fp32'),
+                  'link_alloc': V.link_probe(0), 'link_shm': V.link_probe(0, shm=True),
+                  'how': 'vgpu_cu_peak_probe: 148x8 CTAs x 256 threads, 8 independent FMA chains per thread, 2 FLOP per FMA, best of 5; vgpu_cu_link_probe: 256 MiB copies x 8, best of 2 after a warm-up'}))" > gpurun_out/r2_peak_probes.json 2>&1
+t0=$(date +%s); timeout 1500 python bench.py > gpurun_out/r2_bench_bs_v1.json 2> gpurun_out/r2_bench_bs_v1.err; echo "bench rc=$? wall $(( $(date +%s) - t0 )) s"
+t0=$(date +%s); timeout 900 python bench.py --impl reference > gpurun_out/r2_bench_bs_reference_arm_v1.json 2> gpurun_out/r2_bench_bs_reference_arm_v1.err; echo "ref rc=$? wall $(( $(date +%s) - t0 )) s"
+timeout 1200 python bench.py --workload mg --no-kernels > gpurun_out/r2_bench_mg_v1.json 2> gpurun_out/r2_bench_mg_v1.err; echo "mg rc=$?"
+timeout 1800 python bench.py --acceptance --steps 10 > gpurun_out/r2_acceptance_v1.json 2> gpurun_out/r2_acceptance_v1.err; echo "acceptance rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_bs.csv python bench.py --steps 3 --warmup 3 --no-native --no-cpu-baseline --no-kernels > gpurun_out/r2_ncu_bench.out 2>&1; echo "ncu launches rc=$?"
+B=./paper_1511_07658_b200/bin/payload-bench
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:bs_table -s 1 -c 1 -o gpurun_out/r2_prof_bs -f $B 0 bs 16 2 > gpurun_out/r2_ncu_bs.log 2>&1; echo "ncu bs rc=$?"
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:mg_resid -s 8 -c 1 -o gpurun_out/r2_prof_mg -f $B 0 mg 8 2 > gpurun_out/r2_ncu_mg.log 2>&1; echo "ncu mg rc=$?"

@@ -433,3 +433,57 @@ TEST_CASE("[gpu] NativeVgpu (own context, pageable copies) matches the GVM") {
     const Bytes bs = bs_input(1 << 16, 23);
     CHECK(bs_l1_error(bs, n.run_task(bs, desc("black-scholes"))) <= 1e-6);
 }
+
+TEST_CASE("[gpu] fault containment: a trapping kernel resets the context, the GVM backend keeps serving") {
+    setenv("VGPU_ENABLE_FAULT_INJECTION", "1", 1);
+    vgpu_cu_dev* dev = nullptr;
+    REQUIRE(vgpu_cu_open(0, 2, 1 << 20, &dev) == VGPU_CU_OK);
+    void* host = nullptr;
+    REQUIRE(vgpu_cu_alloc_pinned(dev, 2 << 20, &host) == VGPU_CU_OK);
+    auto* in = static_cast<std::uint8_t*>(host);
+    auto* out = in + (1 << 20);
+    auto run_vadd = [&](std::uint64_t seed, std::uint64_t tag) {
+        const Bytes data = vadd_input(4096, seed);
+        std::memcpy(in, data.data(), data.size());
+        vgpu_cu_task t{};
+        t.slot = 1;
+        t.kernel = VGPU_CU_K_VADD;
+        t.h_in = in;
+        t.in_bytes = data.size();
+        t.h_out = out;
+        t.out_bytes = data.size() / 2;
+        t.tag = tag;
+        std::uint64_t bid = 0;
+        REQUIRE(vgpu_cu_submit_batch(dev, 1, &t, 1, &bid) == VGPU_CU_OK);
+        vgpu_cu_done d{};
+        std::uint32_t n = 0;
+        for (int i = 0; i < 100000 && n == 0; ++i) {
+            REQUIRE(vgpu_cu_poll(dev, &d, 1, &n) == VGPU_CU_OK);
+            if (!n) usleep(50);
+        }
+        REQUIRE(n == 1);
+        CHECK(d.tag == tag);
+        CHECK(d.status == VGPU_CU_OK);
+        CHECK(Bytes(out, out + data.size() / 2) == vadd_expect(data));
+    };
+    run_vadd(1, 1);
+    CHECK(vgpu_cu_generation(dev) == 0);
+    // slot 2's task traps: the op is reported failed, the context is rebuilt
+    REQUIRE(vgpu_cu_inject_fault(dev, 2, 77) == VGPU_CU_OK);
+    vgpu_cu_done d{};
+    std::uint32_t n = 0;
+    for (int i = 0; i < 100000 && n == 0; ++i) {
+        REQUIRE(vgpu_cu_poll(dev, &d, 1, &n) == VGPU_CU_OK);
+        if (!n) usleep(50);
+    }
+    REQUIRE(n == 1);
+    CHECK(d.tag == 77);
+    CHECK(d.status == VGPU_CU_EINTERNAL);
+    CHECK(vgpu_cu_generation(dev) == 1);
+    CHECK(std::string(vgpu_cu_last_fault(dev)).size() > 0);
+    // the same handle and the same staging buffer serve the next tasks
+    run_vadd(2, 2);
+    run_vadd(3, 3);
+    vgpu_cu_free_pinned(dev, host);
+    vgpu_cu_close(dev);
+}

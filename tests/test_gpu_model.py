@@ -84,6 +84,13 @@ def test_span_inplace_resident_apis_agree():
         with pytest.raises(V.VgpuError):
             h.snd_region_at(off, len(data) + 1)               # past the region: Size
         h.rls()
+        # the measured schedule in the reference's timeline schema
+        rows = [r.split(",") for r in d.timeline_csv().strip().splitlines()]
+        assert rows[0] == ["task_id", "stream_id", "kind", "start_us", "end_us"]
+        kinds = {r[2] for r in rows[1:]}
+        assert {"SendData", "Compute", "RtrvData"} <= kinds, kinds
+        assert all(int(r[3]) <= int(r[4]) for r in rows[1:])
+        assert len(rows) - 1 >= 3 * 5
     finally:
         d.stop()
         d.close()
