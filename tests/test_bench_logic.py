@@ -140,3 +140,51 @@ def test_vgpu_bench_cli_takes_the_reference_flags():
     assert vb.main(["validate", "--profile", "NOPE"]) == 2
     assert set(vb.PROFILES.values()) <= {"ep", "vecadd", "vmul", "mm", "bs", "cg", "es"}
     assert vb.rows_to_csv([{"n": 1, "a": 2}, {"n": 2, "b": 3}]).splitlines()[0] == "n,a,b"
+
+
+def test_link_roofline_is_bytes_over_the_probed_link(bench):
+    class FakeV:
+        @staticmethod
+        def link_probe(device):
+            return {"h2d_gbs": 50.0, "d2h_gbs": 50.0, "bidir_gbs": 100.0, "bytes": 1, "reps": 1}
+
+    # 16 jobs of 48 MiB in / 32 MiB out per step, 10 steps in 0.25 s
+    h2d, d2h = 16 * (48 << 20), 16 * (32 << 20)
+    r = bench.link_roofline(FakeV, 0, h2d, d2h, 10, 0.25, 1)
+    assert r["bound"] == "link" and r["unit"] == "GB/s"
+    assert r["achieved"] == pytest.approx((h2d + d2h) * 10 / 0.25 / 1e9)
+    assert r["frac"] == pytest.approx(r["achieved"] / 100.0)
+    assert r["h2d"]["frac"] == pytest.approx(h2d * 10 / 0.25 / 1e9 / 50.0)
+
+
+def test_clocks_merge_takes_the_slowest_gpu_and_every_reason(bench):
+    a = {"sm_mhz": 1965.0, "sm_max_mhz": 1965.0, "reasons": []}
+    b = {"sm_mhz": 1800.0, "sm_max_mhz": 1965.0, "reasons": ["sw_power_cap"]}
+    m = bench.merge_clocks([a, b])
+    assert m["sm_mhz"] == 1800.0 and m["reasons"] == ["sw_power_cap"] and len(m["per_gpu"]) == 2
+    assert bench.merge_clocks([a])["sm_mhz"] == 1965.0
+
+
+def test_e2e_apis_and_mg_workload_shapes(bench, W):
+    assert set(bench.E2E_APIS) == {"resident", "inplace", "span"}
+    sz = W.Sizes()
+    # resident: the input lives after the result (rounded to 64 KiB) in the region
+    assert W.region_bytes("bs", sz, resident=True) == ((8 * sz.bs_n + 65535) & ~65535) + 12 * sz.bs_n
+    # nas-mg: the slot workspace (2 x region) holds every level's u and r
+    assert 2 * W.region_bytes("mg", sz) >= W.mg_workspace_bytes(32)
+    assert W.input_bytes("mg", sz) == 16 + 8 * 32 ** 3 and W.output_bytes("mg", sz) == 32
+    assert bench.KIND_BOUND["mg"] == "hbm" and bench.DTYPE["mg"] == "f64"
+
+
+def test_payload_bench_rows_parse(bench, monkeypatch):
+    import subprocess
+
+    class R:
+        stdout = ("vector-add   n= 8388608  serial     5034 MB/s  omp    51539 MB/s  x10.24\n"
+                  "vector-scale n= 8388608  serial     5144 MB/s  omp    49619 MB/s  x9.65\n")
+
+    monkeypatch.setattr(bench.os.path, "exists", lambda p: True)
+    monkeypatch.setattr(subprocess, "run", lambda *a, **k: R())
+    out = bench.payload_bench_ref()
+    assert out["rows"][0] == {"kernel": "vector-add", "n": 8388608, "serial_gbs": 5.034, "omp_gbs": 51.539}
+    assert len(out["rows"]) == 2
