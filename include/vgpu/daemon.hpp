@@ -130,6 +130,12 @@ public:
     static constexpr std::size_t kFoldWidth = 16;
     std::array<double, kFoldWidth> fold_record() const;
 
+    // B200 fault containment: a sticky device fault failed every in-flight
+    // task (NACK Internal) and the context could not be rebuilt in this
+    // process; the GVM must restart in a fresh one (vgpud exits with 3 and,
+    // with --respawn, re-executes itself).
+    bool device_lost() const;
+
     struct Impl;
 
 private:

@@ -277,13 +277,20 @@ int vgpu_cu_execute(int device, uint32_t kernel, float param, const void* in,
 uint64_t vgpu_cu_execute_launches(void);
 
 /* Fault containment. A sticky device fault (illegal address, trap, ...)
- * seen by vgpu_cu_poll resets and rebuilds the context (slot buffers,
- * streams, events, region and staging registrations) and reports every
- * op that was in flight with status VGPU_CU_EINTERNAL. The generation
- * counts the resets (inputs uploaded before one are gone); last_fault says
- * what caused the last. inject_fault (tests; only with
- * VGPU_ENABLE_FAULT_INJECTION=1) queues a trapping kernel as a task op. */
+ * seen by vgpu_cu_poll reports every op that was in flight with status
+ * VGPU_CU_EINTERNAL, resets the context and tries to rebuild it (slot
+ * buffers, streams, events, region and staging registrations). The
+ * generation counts the resets (inputs uploaded before one are gone);
+ * last_fault says what caused the last. When the driver refuses a new
+ * context in this process, device_lost turns 1 and every later upload /
+ * submit / register fails fast with VGPU_CU_EINTERNAL: the owner restarts
+ * in a fresh process (vgpud --respawn). inject_fault (tests; only with
+ * VGPU_ENABLE_FAULT_INJECTION=1) queues a trapping kernel as a task op;
+ * with the same variable set, an "identity" task whose input is exactly
+ * the 13 bytes "VGPU-TRAP-NOW" runs the trapping kernel instead (fault
+ * injection through the unchanged client API). */
 uint64_t vgpu_cu_generation(vgpu_cu_dev* dev);
+int vgpu_cu_device_lost(vgpu_cu_dev* dev);
 const char* vgpu_cu_last_fault(vgpu_cu_dev* dev);
 int vgpu_cu_inject_fault(vgpu_cu_dev* dev, uint32_t slot, uint64_t tag);
 

@@ -123,6 +123,7 @@ CUDA_API = {
     "vgpu_cu_execute_launches": (_U64, []),
     "vgpu_cu_generation": (_U64, [_P]),
     "vgpu_cu_last_fault": (C.c_char_p, [_P]),
+    "vgpu_cu_device_lost": (C.c_int, [_P]),
     "vgpu_cu_inject_fault": (C.c_int, [_P, _U32, _U64]),
     "vgpu_cu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "vgpu_cu_device_pci_bus_id": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),

@@ -76,6 +76,16 @@ int cuda_fail(cudaError_t e, const char* what) {
     return VGPU_CU_EINTERNAL;
 }
 
+// every device call on a handle whose context is lost fails fast
+#define LOST_GUARD(d)                                                                      \
+    do {                                                                                   \
+        if ((d)->lost) {                                                                   \
+            set_err("device context lost after a sticky fault (%s): restart the GVM",    \
+                    (d)->last_fault.c_str());                                              \
+            return VGPU_CU_EINTERNAL;                                                      \
+        }                                                                                  \
+    } while (0)
+
 #define CK(call)                                                  \
     do {                                                          \
         const cudaError_t ck_e_ = (call);                         \
@@ -1103,6 +1113,10 @@ struct vgpu_cu_dev {
     std::vector<vgpu_cu_done> fault_reports;
     std::uint64_t generation = 0;
     std::string last_fault;
+    // the context could not be rebuilt after a sticky fault (the driver keeps
+    // a faulted process's device unavailable): every later call fails fast
+    // and the owning GVM restarts in a fresh process (vgpud --respawn)
+    bool lost = false;
     cudaEvent_t epoch = nullptr;  // t = 0 of the measured timeline
 
     // armed ops in submission order, not yet reported; owned by the
@@ -1537,8 +1551,21 @@ void recover(vgpu_cu_dev* d, cudaError_t cause) {
     drop_state(d, false);
     cudaDeviceReset();
     cudaGetLastError();
-    cudaSetDevice(d->device);
-    int rc = init_state(d);
+    // the driver may tear the faulted context down asynchronously: a new
+    // primary context is refused (cudaErrorDevicesUnavailable) until it is
+    // gone, so retry for ~1 s. On the B200 boxes measured (driver 580) it
+    // stays refused for the life of the process: the handle is then marked
+    // lost and the GVM restarts in a fresh process.
+    cudaError_t ce = cudaErrorUnknown;
+    for (int i = 0; i < 100; ++i) {
+        ce = cudaSetDevice(d->device);
+        if (ce == cudaSuccess) ce = cudaFree(nullptr);  // creates the new primary context
+        if (ce == cudaSuccess) break;
+        cudaGetLastError();
+        usleep(10000);
+    }
+    int rc = ce == cudaSuccess ? init_state(d) : cuda_fail(ce, "context re-creation after reset");
+    if (rc != VGPU_CU_OK) d->last_fault += std::string(" [rebuild: ") + vgpu_cu_last_error() + "]";
     for (std::uint32_t i = 1; i <= d->max_clients && rc == VGPU_CU_OK; ++i) {
         SlotState& s = d->slots[i];
         if (!s.reg_base) continue;
@@ -1552,7 +1579,10 @@ void recover(vgpu_cu_dev* d, cudaError_t cause) {
     for (auto& [p, n] : d->pinned)
         if (rc == VGPU_CU_OK && cudaHostRegister(p, n, cudaHostRegisterPortable) != cudaSuccess)
             rc = VGPU_CU_EINTERNAL;
-    if (rc != VGPU_CU_OK) d->last_fault += " (and the rebuild after the reset failed)";
+    if (rc != VGPU_CU_OK) {
+        d->last_fault += " (and the rebuild after the reset failed)";
+        d->lost = true;
+    }
     ++d->generation;
 }
 
@@ -1599,20 +1629,26 @@ void vgpu_cu_close(vgpu_cu_dev* d) {
 
 std::uint64_t vgpu_cu_generation(vgpu_cu_dev* d) { return d ? d->generation : 0; }
 
+int vgpu_cu_device_lost(vgpu_cu_dev* d) { return d && d->lost ? 1 : 0; }
+
 }  // extern "C"
 
 namespace {
 __global__ void fault_inject_kernel() { __trap(); }
+
+bool fault_injection_enabled() {
+    static const bool enabled = [] {
+        const char* e = std::getenv("VGPU_ENABLE_FAULT_INJECTION");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return enabled;
+}
 }  // namespace
 
 extern "C" {
 
 int vgpu_cu_inject_fault(vgpu_cu_dev* d, std::uint32_t slot, std::uint64_t tag) {
-    static const bool enabled = [] {
-        const char* e = std::getenv("VGPU_ENABLE_FAULT_INJECTION");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    if (!enabled) {
+    if (!fault_injection_enabled()) {
         set_err("fault injection is off (VGPU_ENABLE_FAULT_INJECTION=1 enables it)");
         return VGPU_CU_EINVAL;
     }
@@ -1642,6 +1678,7 @@ const char* vgpu_cu_last_fault(vgpu_cu_dev* d) { return d ? d->last_fault.c_str(
 
 int vgpu_cu_register_region(vgpu_cu_dev* d, std::uint32_t slot, void* base, std::uint64_t bytes) {
     if (!d || slot < 1 || slot > d->max_clients || !base) return VGPU_CU_EINVAL;
+    LOST_GUARD(d);
     CK(cudaSetDevice(d->device));
     SlotState& s = d->slots[slot];
     if (s.reg_base) {
@@ -1706,6 +1743,7 @@ int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::ui
                    std::uint64_t tag) {
     vgpu::trace::Range range("cu upload");
     if (!d || slot < 1 || slot > d->max_clients || (!h_in && bytes)) return VGPU_CU_EINVAL;
+    LOST_GUARD(d);
     if (bytes > d->slot_bytes) {
         set_err("upload of %llu B exceeds the slot (%llu B)", (unsigned long long)bytes,
                 (unsigned long long)d->slot_bytes);
@@ -1743,6 +1781,7 @@ int vgpu_cu_upload(vgpu_cu_dev* d, std::uint32_t slot, const void* h_in, std::ui
 int vgpu_cu_upload_part(vgpu_cu_dev* d, std::uint32_t slot, const void* h_src, std::uint64_t offset,
                         std::uint64_t bytes, std::uint32_t flags, std::uint64_t tag) {
     if (!d || slot < 1 || slot > d->max_clients || (!h_src && bytes)) return VGPU_CU_EINVAL;
+    LOST_GUARD(d);
     SlotState& s = d->slots[slot];
     const bool begin = flags & VGPU_CU_UPLOAD_BEGIN, end = flags & VGPU_CU_UPLOAD_END;
     if (begin == (s.open_upload != nullptr)) {
@@ -1812,6 +1851,24 @@ int vgpu_cu_submit_batch(vgpu_cu_dev* d, int style, const vgpu_cu_task* tasks, s
     vgpu::trace::Range range("cu submit_batch");
     if (!d || (!tasks && n)) return VGPU_CU_EINVAL;
     if (n == 0) return VGPU_CU_OK;
+    LOST_GUARD(d);
+    if (fault_injection_enabled()) {
+        // the trap payload (identity of "VGPU-TRAP-NOW") runs the trapping kernel
+        std::vector<vgpu_cu_task> rest;
+        for (std::uint32_t i = 0; i < n; ++i) {
+            const vgpu_cu_task& t = tasks[i];
+            if (t.kernel == VGPU_CU_K_IDENTITY && t.in_bytes == 13 && t.h_in &&
+                std::memcmp(t.h_in, "VGPU-TRAP-NOW", 13) == 0) {
+                if (const int rc = vgpu_cu_inject_fault(d, t.slot, t.tag)) return rc;
+            } else {
+                rest.push_back(t);
+            }
+        }
+        if (rest.size() != n)
+            return rest.empty() ? VGPU_CU_OK
+                                : vgpu_cu_submit_batch(d, style, rest.data(),
+                                                       static_cast<std::uint32_t>(rest.size()), batch_id);
+    }
     // validate everything before enqueueing anything
     std::vector<DevJob> jobs(n);
     for (std::uint32_t i = 0; i < n; ++i) {

@@ -175,6 +175,7 @@ struct GvmDaemon::Impl {
     std::uint64_t next_tag = 1;
     std::uint32_t streams_active = 0;  // sessions with a streamed SND still filling
     std::uint64_t device_generation = 0;  // context resets seen (fault containment)
+    std::atomic<bool> device_lost{false};  // the reset could not rebuild the context
 
     mutable std::mutex metrics_mu;
     std::vector<TaskMetrics> task_metrics;
@@ -297,6 +298,12 @@ struct GvmDaemon::Impl {
 
     void on_req(const Message& m, const std::string& origin) {
         trace::Range range("gvm REQ");
+        if (device_lost) {  // the instance is about to restart in a fresh process
+            transport->reply_origin(origin, {Opcode::Nack, 0, m.task_id,
+                                             encode_nack(ErrCode::Internal,
+                                                         "device context lost; the GVM is restarting")});
+            return;
+        }
         std::uint32_t slot = 0;
         for (std::uint32_t i = 1; i <= cfg.max_clients && slot == 0; ++i) {
             const Session& s = sessions[i - 1];
@@ -861,6 +868,7 @@ struct GvmDaemon::Impl {
             device_generation = g;
             std::fprintf(stderr, "gvm: device fault contained by a context reset (#%llu): %s\n",
                          static_cast<unsigned long long>(g), vgpu_cu_last_fault(dev));
+            if (vgpu_cu_device_lost(dev)) device_lost = true;
             for (Session& s : sessions) {
                 if (s.input_resident) s.input_lost = true;
                 s.input_resident = false;
@@ -1095,6 +1103,8 @@ std::array<double, GvmDaemon::kFoldWidth> GvmDaemon::fold_record() const {
     rec[15] = static_cast<double>(impl_->fold_bytes);
     return rec;
 }
+
+bool GvmDaemon::device_lost() const { return impl_->device_lost.load(); }
 
 MetricsSnapshot GvmDaemon::metrics() const {
     std::lock_guard lk(impl_->metrics_mu);

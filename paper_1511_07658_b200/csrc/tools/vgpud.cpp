@@ -13,6 +13,9 @@
 // writes the result as JSON to --reduce-out (--fold-out: every rank's own
 // record, with or without a communicator). --cpus LIST pins the daemon
 // (default: the cores local to its GPU, from sysfs).
+#include <unistd.h>
+
+#include <cerrno>
 #include <csignal>
 #include <cstdio>
 #include <cstdlib>
@@ -30,6 +33,7 @@
 #include "vgpu/daemon.hpp"
 #include "vgpu/device.hpp"
 #include "vgpu/multigpu.hpp"
+#include "vgpu/transport.hpp"
 #include "vgpu_cuda.h"
 
 namespace {
@@ -45,7 +49,10 @@ void usage() {
         "      [--t-ctx-switch US] [--metrics-out PATH] [--device ORDINAL]\n"
         "      [--data-plane zero-copy|snapshot] [--ready-file PATH]\n"
         "      [--nranks N --rank R --rendezvous PATH [--reduce-out PATH]]\n"
-        "      [--fold-out PATH] [--timeline-out PATH] [--cpus LIST|none]");
+        "      [--fold-out PATH] [--timeline-out PATH] [--cpus LIST|none] [--respawn N]\n"
+        "exit status 3: the device context was lost to a sticky fault (every in-flight\n"
+        "task was NACKed Internal); with --respawn N the daemon re-executes itself in a\n"
+        "fresh process (new context, same instance name) up to N times instead.");
 }
 
 }  // namespace
@@ -74,7 +81,7 @@ int main(int argc, char** argv) {
     }
     vgpu::GvmConfig cfg;
     std::string metrics_out, ready_file, rendezvous, reduce_out, fold_out, timeline_out, cpus = "auto";
-    int nranks = 0, rank = 0;
+    int nranks = 0, rank = 0, respawn = 0;
     try {
         for (const auto& [k, v] : opt) {
             if (k == "instance") cfg.instance = v;
@@ -102,6 +109,7 @@ int main(int argc, char** argv) {
             else if (k == "fold-out") fold_out = v;
             else if (k == "timeline-out") timeline_out = v;
             else if (k == "cpus") cpus = v;
+            else if (k == "respawn") respawn = std::stoi(v);
             else if (k == "data-plane") {
                 if (v == "zero-copy") cfg.data_plane = vgpu::DataPlane::ZeroCopy;
                 else if (v == "snapshot") cfg.data_plane = vgpu::DataPlane::Snapshot;
@@ -170,7 +178,39 @@ int main(int argc, char** argv) {
               << (pinned ? " (pinned to " + std::to_string(cpu_set.size()) + " local cores)" : "")
               << std::endl;
     if (!ready_file.empty()) std::ofstream(ready_file) << "ready\n";
-    while (!g_stop) std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    while (!g_stop && !daemon->device_lost()) std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    if (daemon->device_lost()) {
+        // process-level fault containment: CUDA keeps a faulted process's
+        // device unavailable, so a fresh process takes over the instance
+        daemon->stop();
+        daemon.reset();  // closes the endpoint and the client regions
+        vgpu::unlink_os_instance(cfg.instance, cfg.max_clients);
+        if (respawn > 0) {
+            std::vector<std::string> args;
+            for (int i = 0; i < argc; ++i) {
+                const std::string a = argv[i];
+                if (a == "--respawn") {
+                    ++i;
+                    continue;
+                }
+                if (a.rfind("--respawn=", 0) == 0) continue;
+                args.push_back(a);
+            }
+            args.push_back("--respawn");
+            args.push_back(std::to_string(respawn - 1));
+            std::vector<char*> av;
+            for (auto& a : args) av.push_back(a.data());
+            av.push_back(nullptr);
+            std::cerr << "vgpud: device context lost; restarting instance '" << cfg.instance
+                      << "' in a fresh process (" << respawn - 1 << " restart(s) left)" << std::endl;
+            if (!ready_file.empty()) std::remove(ready_file.c_str());
+            execv("/proc/self/exe", av.data());
+            std::cerr << "vgpud: re-exec failed: " << std::strerror(errno) << '\n';
+        } else {
+            std::cerr << "vgpud: device context lost to a sticky fault; exiting (3)" << std::endl;
+        }
+        return 3;
+    }
     daemon->stop();
     int rc = 0;
     if (!fold_out.empty()) {  // this GVM's own record (also without a communicator)

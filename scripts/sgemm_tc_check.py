@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1511_07658_b200 import vgpu as V  # noqa: E402
 
-for n in (256, 2048):
+for n in (256, 512, 2048):
     rng = np.random.default_rng(1000)
     A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
     B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
