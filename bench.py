@@ -552,6 +552,10 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> d
     # CTAs per SM (vgpu_cu_task_shape), CTAs drawing free slots in queue order
     kind = W.kind_of(workload, 0)
     grid_b, per_sm = V.task_shape(W.PAYLOAD[kind], W.job_input(workload, 0, procs, sizes), device)
+    # the fixed part of an event-timed kernel span, paid once per kernel
+    # (DeviceSpec::kernel_launch_us), measured on this GPU now
+    launch_us = V.launch_probe(device)
+    stages = []
     for n in range(1, procs + 1):
         r = leg_workers(V, N, W, workload, n, 0, procs, reps, 2, device, False, sizes, dist,
                         barrier=n, window=1_000_000, snapshot=True)
@@ -560,19 +564,26 @@ def validate_model(V, N, W, workload, device, sizes, dist, reps=8, procs=0) -> d
             continue
         measured = statistics.median([b["measured_makespan_us"] for b in full])
         style = full[-1]["style"]
+        timed = r["tasks"][-n * reps:]
+        stages.append({"n": n, **{k: statistics.median([t[k] for t in timed])
+                                  for k in ("h2d_us", "comp_us", "d2h_us")}})
         for name, spec in (("concurrent", (1, 148, 128, 32)), ("device_filling", (1, 1, 128, 1))):
             grid, sms, kern, slots = spec
             model = V.model_simulate(style, n, t_in, t_comp, t_out, grid, sms, kern, slots)
             rows[name].append({"n": n, "model_us": model, "measured_us": measured,
                                "deviation_pct": 100.0 * abs(measured - model) / max(1, model)})
-        model = V.model_simulate_fluid(style, n, t_in, t_comp, t_out, grid_b, 148, per_sm)
+        model = V.model_simulate_fluid(style, n, t_in, t_comp, t_out, grid_b, 148, per_sm,
+                                       int(round(launch_us)))
         rows["b200_blocks"].append({"n": n, "model_us": model, "measured_us": measured,
                                     "deviation_pct": 100.0 * abs(measured - model) / max(1, model)})
     out = {"workload": W.CONFIG_NAME[workload], "style": "PS2" if style else "PS1",
            "task_triple_us": {"t_in": t_in, "t_comp": t_comp, "t_out": t_out},
            "b200_blocks_spec": {"ctas_per_task": grid_b, "ctas_per_sm": per_sm, "sms": 148,
+                                "kernel_launch_us": launch_us,
                                 "rule": "DeviceSpec::fluid_blocks: CTAs draw free slots in "
-                                        "queue order"},
+                                        "queue order; the kernel's fixed span (launch probe) "
+                                        "once per kernel"},
+           "measured_stage_us_per_n": stages,
            "criterion6": "proj/tests/acceptance.cpp:246-268: real-clock mean deviation < 5 %",
            "paper": "PAPER.md:505: EP(M24) 0.42 %, VecMult 4.76 % mean deviation on a C2070"}
     for name, rs in rows.items():

@@ -141,10 +141,12 @@ uint64_t vgpu_model_simulate(int style, uint32_t n, uint64_t t_in, uint64_t t_co
                              uint64_t t_out, uint32_t grid, uint32_t sms,
                              uint32_t max_kernels, uint32_t slots_per_sm);
 /* simulate() with DeviceSpec::fluid_blocks (B200 block scheduler as a
- * fluid): grid = the task's CTAs, ctas_per_sm = its resident CTAs per SM */
+ * fluid): grid = the task's CTAs, ctas_per_sm = its resident CTAs per SM,
+ * launch_us = the fixed part of a kernel's measured span (once per kernel,
+ * not per wave; vgpu_cu_launch_probe) */
 uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
                                    uint64_t t_out, uint32_t grid, uint32_t sms,
-                                   uint32_t ctas_per_sm);
+                                   uint32_t ctas_per_sm, uint64_t launch_us);
 int vgpu_model_classify(uint64_t t_in, uint64_t t_comp, uint64_t t_out);
 uint64_t vgpu_model_no_vt(uint32_t n, uint64_t t_init, uint64_t t_ctx, uint64_t t_in,
                           uint64_t t_comp, uint64_t t_out);

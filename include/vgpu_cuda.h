@@ -339,6 +339,10 @@ int vgpu_cu_resident_bench(int device, uint32_t kernel, float param,
  * (FP32) rooflines are quoted against, counting 2 FLOP per FMA. */
 enum vgpu_cu_peak_kind { VGPU_CU_PEAK_FP64 = 0, VGPU_CU_PEAK_FP32 = 1 };
 int vgpu_cu_peak_probe(int device, uint32_t kind, double* tflops);
+/* The fixed cost inside a CUDA-event-timed kernel span: median event span of
+ * an empty 148-CTA kernel on its own stream (us). The model's B200 spec
+ * charges it once per kernel instead of once per wave. */
+int vgpu_cu_launch_probe(int device, double* us);
 
 /* Host link (PCIe) probe: the e2e roofline's denominator. `bytes`-sized
  * copies between page-locked host memory (cudaHostAlloc) and HBM, each

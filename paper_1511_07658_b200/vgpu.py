@@ -418,10 +418,18 @@ def link_probe(device: int = 0, nbytes: int = 256 << 20, reps: int = 8, shm: boo
 
 
 def model_simulate_fluid(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int,
-                         sms: int, ctas_per_sm: int) -> int:
-    """simulate() with the B200 fluid block-scheduler spec (DeviceSpec::fluid_blocks)."""
+                         sms: int, ctas_per_sm: int, launch_us: int = 0) -> int:
+    """simulate() with the B200 fluid block-scheduler spec (DeviceSpec::fluid_blocks);
+    launch_us = the fixed part of a kernel span (DeviceSpec::kernel_launch_us)."""
     return _libs().host.vgpu_model_simulate_fluid(style, n, t_in, t_comp, t_out, grid, sms,
-                                                  ctas_per_sm)
+                                                  ctas_per_sm, launch_us)
+
+
+def launch_probe(device: int = 0) -> float:
+    """The fixed part of an event-timed kernel span in us (vgpu_cu_launch_probe)."""
+    t = C.c_double()
+    _cu_check(_libs().cuda.vgpu_cu_launch_probe(device, C.byref(t)))
+    return t.value
 
 
 def task_shape(payload_id: str, data: bytes, device: int = 0) -> tuple:

@@ -249,3 +249,11 @@ TEST_CASE("device: B200 fluid block scheduler (DeviceSpec::fluid_blocks)") {
     CHECK(span(1) == 100);
     CHECK(span(2) == 200);
 }
+
+TEST_CASE("DeviceSpec keeps the reference's layout (it sits inside GvmConfig)") {
+    // the reference's DeviceSpec: five uint32 fields (20 bytes); B200 fields
+    // live in its tail padding so reference-built programs keep GvmConfig's
+    // layout when they link libvgpu
+    CHECK(sizeof(vgpu::DeviceSpec) <= 24);
+    CHECK(alignof(vgpu::DeviceSpec) == 4);
+}
