@@ -578,6 +578,17 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
     return cudaSuccess;
 }
 
+// NAS MG on one cluster per job (mg_cluster_kernel) up to nx = 64 (the
+// operators are launch-bound there), one launch per operator above;
+// VGPU_MG_CLUSTER=0 / 1 forces either.
+bool mg_use_cluster(std::uint32_t nx) {
+    static const int forced = [] {
+        const char* e = std::getenv("VGPU_MG_CLUSTER");
+        return e ? std::atoi(e) : -1;
+    }();
+    return forced >= 0 ? forced != 0 : nx <= 64;
+}
+
 // NAS MG: jobs with the same (nx, nit, coeffs) share one table; mg.f's
 // timed sequence — resid, nit x (mg3P, resid), norm2u3 — is issued as one
 // launch per grid operator and level over all jobs of the table.
@@ -629,6 +640,32 @@ cudaError_t launch_mg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
             ++l;
         };
         const int lt = static_cast<int>(t.lt);
+        if (mg_use_cluster(t.nx)) {
+            // small grids: the whole sequence in one launch, one cluster per job
+            static const int fit1024 = [] {  // co-resident 8-CTA clusters of 1024 threads
+                cudaLaunchConfig_t c{};
+                c.gridDim = dim3(kMgCluster * 64);
+                c.blockDim = dim3(1024);
+                int n = 0;
+                if (cudaOccupancyMaxActiveClusters(&n, mg_cluster_kernel<1024>, &c) != cudaSuccess) {
+                    cudaGetLastError();
+                    n = 0;
+                }
+                return n;
+            }();
+            const int forced = [] {
+                const char* v = std::getenv("VGPU_MG_THREADS");
+                return v ? std::atoi(v) : 0;
+            }();
+            if (forced == 1024 || (forced != 512 && static_cast<int>(nj) <= fit1024))
+                mg_cluster_kernel<1024><<<nj * kMgCluster, 1024, 0, s>>>(t);
+            else
+                mg_cluster_kernel<512><<<nj * kMgCluster, 512, 0, s>>>(t);
+            e = cudaGetLastError();
+            *launches += 1;
+            if (e != cudaSuccess) return e;
+            continue;
+        }
         go(mg_zero_kernel, grid(all(lt)), lt, 0);
         go(mg_resid_kernel, grid(interior(lt)), lt, 1);
         go(mg_comm3_kernel, grid(faces(lt)), lt, 1);

@@ -57,10 +57,11 @@ __device__ __forceinline__ std::size_t mg_idx(int n, int i1, int i2, int i3) {
 
 // interior point number p (0-based) of an m^3 interior -> 1-based coords 2..m+1
 __device__ __forceinline__ void mg_interior(std::uint64_t p, int m, int* i1, int* i2, int* i3) {
-    *i1 = 2 + static_cast<int>(p % m);
-    const std::uint64_t q = p / m;
-    *i2 = 2 + static_cast<int>(q % m);
-    *i3 = 2 + static_cast<int>(q / m);
+    // m is a power of two and p < 2^32 (nx <= 512): shifts, no 64-bit division
+    const std::uint32_t q = static_cast<std::uint32_t>(p), lg = __ffs(m) - 1, mask = m - 1;
+    *i1 = 2 + static_cast<int>(q & mask);
+    *i2 = 2 + static_cast<int>((q >> lg) & mask);
+    *i3 = 2 + static_cast<int>(q >> (2 * lg));
 }
 
 __device__ __forceinline__ double add4(double a, double b, double c, double d) {
@@ -68,29 +69,31 @@ __device__ __forceinline__ double add4(double a, double b, double c, double d) {
 }
 
 // all points of u_k (or r_k) = 0
-__global__ void __launch_bounds__(kMgThreads) mg_zero_kernel(const __grid_constant__ MgTable t, int k,
-                                                             int which) {
-    const MgJob& j = t.job[blockIdx.y];
+__device__ __forceinline__ void mg_zero(const MgTable& t, const MgJob& j, int k,
+                                                             int which,
+        std::uint64_t p0, std::uint64_t ps) {
     const int n = (1 << k) + 2;
     const std::uint64_t total = static_cast<std::uint64_t>(n) * n * n;
     double* a = which ? j.r[k] : j.u[k];
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < total;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    for (std::uint64_t p = p0; p < total; p += ps)
         a[p] = 0.0;
 }
 
 // comm3: the ghost layer of u_k / r_k from the wrapped interior (the serial
 // comm3's three sweeps end with exactly these copies, corners included)
-__global__ void __launch_bounds__(kMgThreads) mg_comm3_kernel(const __grid_constant__ MgTable t, int k,
-                                                              int which) {
-    const MgJob& j = t.job[blockIdx.y];
+__device__ __forceinline__ void mg_comm3(const MgTable& t, const MgJob& j, int k,
+                                                              int which,
+        std::uint64_t p0, std::uint64_t ps) {
     const int n = (1 << k) + 2;
     double* a = which ? j.r[k] : j.u[k];
     const std::uint64_t face = static_cast<std::uint64_t>(n) * n;
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < 6 * face;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const int f = static_cast<int>(p / face);
-        const int x = 1 + static_cast<int>(p % face % n), y = 1 + static_cast<int>(p % face / n);
+    for (std::uint64_t p = p0; p < 6 * face; p += ps) {
+        // 32-bit index arithmetic (6 n^2 < 2^32)
+        const std::uint32_t q = static_cast<std::uint32_t>(p), fc = static_cast<std::uint32_t>(face);
+        const int f = static_cast<int>(q / fc);
+        const std::uint32_t in_face = q - static_cast<std::uint32_t>(f) * fc;
+        const int y = 1 + static_cast<int>(in_face / static_cast<std::uint32_t>(n));
+        const int x = 1 + static_cast<int>(in_face - static_cast<std::uint32_t>(y - 1) * n);
         int c[3];
         c[f >> 1] = (f & 1) ? n : 1;
         c[(f >> 1) == 0 ? 1 : 0] = x;
@@ -100,19 +103,41 @@ __global__ void __launch_bounds__(kMgThreads) mg_comm3_kernel(const __grid_const
     }
 }
 
+// Store an interior point (coordinates 2..n-1) and, with Ghosts, every ghost
+// point comm3 would copy from it: along each axis, interior n-1 is also
+// ghost 1 and interior 2 is also ghost n, so a point has up to 7 mirrors
+// (comm3's three sweeps end with exactly these copies, corners included).
+// The fused operators below need no separate comm3 pass: no operator reads
+// the ghosts of the grid it writes.
+template <bool Ghosts>
+__device__ __forceinline__ void mg_store(double* a, int n, int i1, int i2, int i3, double val) {
+    a[mg_idx(n, i1, i2, i3)] = val;
+    if constexpr (Ghosts) {
+        const int g1 = i1 == n - 1 ? 1 : (i1 == 2 ? n : 0);
+        const int g2 = i2 == n - 1 ? 1 : (i2 == 2 ? n : 0);
+        const int g3 = i3 == n - 1 ? 1 : (i3 == 2 ? n : 0);
+        if (g1) a[mg_idx(n, g1, i2, i3)] = val;
+        if (g2) a[mg_idx(n, i1, g2, i3)] = val;
+        if (g3) a[mg_idx(n, i1, i2, g3)] = val;
+        if (g1 && g2) a[mg_idx(n, g1, g2, i3)] = val;
+        if (g1 && g3) a[mg_idx(n, g1, i2, g3)] = val;
+        if (g2 && g3) a[mg_idx(n, i1, g2, g3)] = val;
+        if (g1 && g2 && g3) a[mg_idx(n, g1, g2, g3)] = val;
+    }
+}
+
 // resid: r_k = v - A u_k on the interior. top: v is the job's input
 // (interior-only layout); else v is r_k itself (in place: each thread reads
 // and writes only its own point of r_k).
-__global__ void __launch_bounds__(kMgThreads) mg_resid_kernel(const __grid_constant__ MgTable t, int k,
-                                                              int top) {
-    const MgJob& j = t.job[blockIdx.y];
+template <bool Ghosts = false>
+__device__ __forceinline__ void mg_resid(const MgTable& t, const MgJob& j, int k, int top,
+                                         std::uint64_t p0, std::uint64_t ps) {
     const int m = 1 << k, n = m + 2;
     const std::uint64_t total = static_cast<std::uint64_t>(m) * m * m;
     const double* __restrict__ u = j.u[k];
     double* r = j.r[k];
     const double a0 = t.a[0], a2 = t.a[2], a3 = t.a[3];
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < total;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    for (std::uint64_t p = p0; p < total; p += ps) {
         int i1, i2, i3;
         mg_interior(p, m, &i1, &i2, &i3);
         auto U = [&](int x, int y, int z) { return u[mg_idx(n, x, y, z)]; };
@@ -123,20 +148,21 @@ __global__ void __launch_bounds__(kMgThreads) mg_resid_kernel(const __grid_const
         const double v = top ? j.v[p] : r[mg_idx(n, i1, i2, i3)];
         const double s1 = __dsub_rn(v, __dmul_rn(a0, U(i1, i2, i3)));
         const double s2 = __dsub_rn(s1, __dmul_rn(a2, __dadd_rn(__dadd_rn(u2(i1), u1(i1 - 1)), u1(i1 + 1))));
-        r[mg_idx(n, i1, i2, i3)] = __dsub_rn(s2, __dmul_rn(a3, __dadd_rn(u2(i1 - 1), u2(i1 + 1))));
+        mg_store<Ghosts>(r, n, i1, i2, i3, __dsub_rn(s2, __dmul_rn(a3, __dadd_rn(u2(i1 - 1), u2(i1 + 1)))));
     }
 }
 
-// psinv: u_k = u_k + C r_k on the interior
-__global__ void __launch_bounds__(kMgThreads) mg_psinv_kernel(const __grid_constant__ MgTable t, int k) {
-    const MgJob& j = t.job[blockIdx.y];
+// psinv: u_k = u_k + C r_k on the interior (Fresh: u_k was just zeroed, so
+// its value is the literal 0.0 in the same addition)
+template <bool Ghosts = false, bool Fresh = false>
+__device__ __forceinline__ void mg_psinv(const MgTable& t, const MgJob& j, int k,
+                                         std::uint64_t p0, std::uint64_t ps) {
     const int m = 1 << k, n = m + 2;
     const std::uint64_t total = static_cast<std::uint64_t>(m) * m * m;
     const double* __restrict__ r = j.r[k];
     double* u = j.u[k];
     const double c0 = t.c[0], c1 = t.c[1], c2 = t.c[2];
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < total;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    for (std::uint64_t p = p0; p < total; p += ps) {
         int i1, i2, i3;
         mg_interior(p, m, &i1, &i2, &i3);
         auto R = [&](int x, int y, int z) { return r[mg_idx(n, x, y, z)]; };
@@ -144,23 +170,24 @@ __global__ void __launch_bounds__(kMgThreads) mg_psinv_kernel(const __grid_const
         auto r2 = [&](int x) {
             return add4(R(x, i2 - 1, i3 - 1), R(x, i2 + 1, i3 - 1), R(x, i2 - 1, i3 + 1), R(x, i2 + 1, i3 + 1));
         };
-        const std::size_t at = mg_idx(n, i1, i2, i3);
-        const double s1 = __dadd_rn(u[at], __dmul_rn(c0, R(i1, i2, i3)));
+        const double u0 = Fresh ? 0.0 : u[mg_idx(n, i1, i2, i3)];
+        const double s1 = __dadd_rn(u0, __dmul_rn(c0, R(i1, i2, i3)));
         const double s2 =
             __dadd_rn(s1, __dmul_rn(c1, __dadd_rn(__dadd_rn(R(i1 - 1, i2, i3), R(i1 + 1, i2, i3)), r1(i1))));
-        u[at] = __dadd_rn(s2, __dmul_rn(c2, __dadd_rn(__dadd_rn(r2(i1), r1(i1 - 1)), r1(i1 + 1))));
+        mg_store<Ghosts>(u, n, i1, i2, i3,
+                         __dadd_rn(s2, __dmul_rn(c2, __dadd_rn(__dadd_rn(r2(i1), r1(i1 - 1)), r1(i1 + 1)))));
     }
 }
 
 // rprj3: r_{k-1} (coarse interior) = restriction of r_k
-__global__ void __launch_bounds__(kMgThreads) mg_rprj3_kernel(const __grid_constant__ MgTable t, int k) {
-    const MgJob& j = t.job[blockIdx.y];
+template <bool Ghosts = false>
+__device__ __forceinline__ void mg_rprj3(const MgTable& t, const MgJob& j, int k,
+                                         std::uint64_t p0, std::uint64_t ps) {
     const int mf = 1 << k, nf = mf + 2, mc = mf / 2, nc = mc + 2;
     const std::uint64_t total = static_cast<std::uint64_t>(mc) * mc * mc;
     const double* __restrict__ r = j.r[k];
     double* s = j.r[k - 1];
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < total;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    for (std::uint64_t p = p0; p < total; p += ps) {
         int j1, j2, j3;
         mg_interior(p, mc, &j1, &j2, &j3);
         const int i1 = 2 * j1 - 1, i2 = 2 * j2 - 1, i3 = 2 * j3 - 1;
@@ -175,22 +202,25 @@ __global__ void __launch_bounds__(kMgThreads) mg_rprj3_kernel(const __grid_const
         const double t2 = __dmul_rn(0.25, __dadd_rn(__dadd_rn(R(i1 - 1, i2, i3), R(i1 + 1, i2, i3)), x2));
         const double t3 = __dmul_rn(0.125, __dadd_rn(__dadd_rn(x1(i1 - 1), x1(i1 + 1)), y2));
         const double t4 = __dmul_rn(0.0625, __dadd_rn(y1(i1 - 1), y1(i1 + 1)));
-        s[mg_idx(nc, j1, j2, j3)] = __dadd_rn(__dadd_rn(__dadd_rn(t1, t2), t3), t4);
+        mg_store<Ghosts>(s, nc, j1, j2, j3, __dadd_rn(__dadd_rn(__dadd_rn(t1, t2), t3), t4));
     }
 }
 
 // interp: u_k (every point, ghosts included) += prolongation of u_{k-1};
 // each fine point takes exactly one term of mg.f's interp loops
-__global__ void __launch_bounds__(kMgThreads) mg_interp_kernel(const __grid_constant__ MgTable t, int k) {
-    const MgJob& j = t.job[blockIdx.y];
+template <bool Fresh = false>
+__device__ __forceinline__ void mg_interp(const MgTable& t, const MgJob& j, int k,
+                                          std::uint64_t p0, std::uint64_t ps) {
     const int nf = (1 << k) + 2, mm = (1 << (k - 1)) + 2;
     const std::uint64_t total = static_cast<std::uint64_t>(nf) * nf * nf;
     const double* __restrict__ z = j.u[k - 1];
     double* u = j.u[k];
-    for (std::uint64_t p = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; p < total;
-         p += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-        const int f1 = 1 + static_cast<int>(p % nf), f2 = 1 + static_cast<int>(p / nf % nf),
-                  f3 = 1 + static_cast<int>(p / nf / nf);
+    for (std::uint64_t p = p0; p < total; p += ps) {
+        // 32-bit index arithmetic (nf^3 < 2^32)
+        const std::uint32_t q = static_cast<std::uint32_t>(p), un = static_cast<std::uint32_t>(nf);
+        const std::uint32_t q1 = q / un, q2 = q1 / un;
+        const int f1 = 1 + static_cast<int>(q - q1 * un), f2 = 1 + static_cast<int>(q1 - q2 * un),
+                  f3 = 1 + static_cast<int>(q2);
         const int i1 = (f1 + 1) / 2, i2 = (f2 + 1) / 2, i3 = (f3 + 1) / 2;
         const bool e1 = !(f1 & 1), e2 = !(f2 & 1), e3 = !(f3 & 1);
         auto Z = [&](int x, int y, int zz) { return z[mg_idx(mm, x, y, zz)]; };
@@ -202,19 +232,53 @@ __global__ void __launch_bounds__(kMgThreads) mg_interp_kernel(const __grid_cons
         else if (e2 && !e3) v = e1 ? __dmul_rn(0.25, __dadd_rn(z1(i1), z1(i1 + 1))) : __dmul_rn(0.5, z1(i1));
         else if (!e2 && e3) v = e1 ? __dmul_rn(0.25, __dadd_rn(z2(i1), z2(i1 + 1))) : __dmul_rn(0.5, z2(i1));
         else v = e1 ? __dmul_rn(0.125, __dadd_rn(z3(i1), z3(i1 + 1))) : __dmul_rn(0.25, z3(i1));
-        u[p] = __dadd_rn(u[p], v);
+        u[p] = __dadd_rn(Fresh ? 0.0 : u[p], v);
     }
+}
+
+
+// one launch per operator and level over every job (blockIdx.y = job)
+__global__ void __launch_bounds__(kMgThreads) mg_zero_kernel(const __grid_constant__ MgTable t, int k, int which) {
+    mg_zero(t, t.job[blockIdx.y], k, which, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_comm3_kernel(const __grid_constant__ MgTable t, int k, int which) {
+    mg_comm3(t, t.job[blockIdx.y], k, which, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_resid_kernel(const __grid_constant__ MgTable t, int k, int top) {
+    mg_resid(t, t.job[blockIdx.y], k, top, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_psinv_kernel(const __grid_constant__ MgTable t, int k) {
+    mg_psinv(t, t.job[blockIdx.y], k, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_rprj3_kernel(const __grid_constant__ MgTable t, int k) {
+    mg_rprj3(t, t.job[blockIdx.y], k, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_interp_kernel(const __grid_constant__ MgTable t, int k) {
+    mg_interp(t, t.job[blockIdx.y], k, blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x,
+           static_cast<std::uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // norm2u3, stage 1: per i3 plane of r_lt, the fixed-order sum of squares
 // and the maximum magnitude (one CTA per plane)
-__global__ void __launch_bounds__(kMgThreads) mg_norm_kernel(const __grid_constant__ MgTable t) {
-    const MgJob& j = t.job[blockIdx.y];
-    const int nx = static_cast<int>(t.nx), n = nx + 2, i3 = 2 + static_cast<int>(blockIdx.x);
+// (threads 0..kMgThreads-1 of the CTA take part; Named: they sync on named
+// barrier 1 so a larger CTA's other threads need not)
+template <bool Named = false>
+__device__ __forceinline__ void mg_norm_plane(const MgTable& t, const MgJob& j, unsigned plane) {
+    const int nx = static_cast<int>(t.nx), n = nx + 2, i3 = 2 + static_cast<int>(plane);
     const double* r = j.r[t.lt];
-    const std::uint32_t plane = static_cast<std::uint32_t>(nx) * nx;
+    const std::uint32_t points = static_cast<std::uint32_t>(nx) * nx;
     double acc = 0.0, mx = 0.0;
-    for (std::uint32_t q = threadIdx.x; q < plane; q += kMgThreads) {
+    for (std::uint32_t q = threadIdx.x; q < points; q += kMgThreads) {
         const double x = r[mg_idx(n, 2 + static_cast<int>(q % nx), 2 + static_cast<int>(q / nx), i3)];
         acc = __dadd_rn(acc, __dmul_rn(x, x));
         mx = fmax(mx, fabs(x));
@@ -231,7 +295,8 @@ __global__ void __launch_bounds__(kMgThreads) mg_norm_kernel(const __grid_consta
         ws[warp] = acc;
         wm[warp] = mx;
     }
-    __syncthreads();
+    if constexpr (Named) asm volatile("bar.sync 1, %0;" ::"n"(kMgThreads) : "memory");
+    else __syncthreads();
     // ... then over the 8 warp sums (strides 32, 64, 128 in lane terms)
     if (threadIdx.x == 0) {
         for (int st = 1; st < kMgThreads / 32; st *= 2)
@@ -239,15 +304,20 @@ __global__ void __launch_bounds__(kMgThreads) mg_norm_kernel(const __grid_consta
                 ws[w] = __dadd_rn(ws[w], ws[w + st]);
                 wm[w] = fmax(wm[w], wm[w + st]);
             }
-        j.plane_sum[blockIdx.x] = ws[0];
-        j.plane_max[blockIdx.x] = wm[0];
+        j.plane_sum[plane] = ws[0];
+        j.plane_max[plane] = wm[0];
     }
+    // ws / wm are reused by the CTA's next plane
+    if constexpr (Named) asm volatile("bar.sync 1, %0;" ::"n"(kMgThreads) : "memory");
+    else __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMgThreads) mg_norm_kernel(const __grid_constant__ MgTable t) {
+    mg_norm_plane(t, t.job[blockIdx.y], blockIdx.x);
 }
 
 // norm2u3, stage 2: planes in i3 order -> rnm2 = sqrt(sum / nx^3), rnmu
-__global__ void mg_norm_fold_kernel(const __grid_constant__ MgTable t) {
-    const MgJob& j = t.job[blockIdx.x];
-    if (threadIdx.x != 0) return;
+__device__ __forceinline__ void mg_norm_fold(const MgTable& t, const MgJob& j) {
     double s = 0.0, mx = 0.0;
     for (std::uint32_t p = 0; p < t.nx; ++p) {
         s = __dadd_rn(s, j.plane_sum[p]);
@@ -260,6 +330,77 @@ __global__ void mg_norm_fold_kernel(const __grid_constant__ MgTable t) {
     res.nx = t.nx;
     res.nit = t.nit;
     *j.out = res;
+}
+
+__global__ void mg_norm_fold_kernel(const __grid_constant__ MgTable t) {
+    if (threadIdx.x == 0) mg_norm_fold(t, t.job[blockIdx.x]);
+}
+
+// ---- one cluster per job: the whole timed sequence in one launch --------------
+//
+// For small grids (classes S..W) every operator above is a few microseconds
+// of work and the launch-per-operator sequence (149 launches for class S) is
+// launch-bound. Here one thread-block cluster of kMgCluster CTAs runs the
+// job's whole sequence: the same per-point operators (same arithmetic, same
+// bits) over the cluster's threads, a cluster barrier (release / acquire at
+// cluster scope: the grids live in global memory, L2-resident at these
+// sizes) between operators where the launch boundary was, and the norm's
+// planes spread over the CTAs with the same per-plane tree, folded in plane
+// order by CTA 0. Clusters of different jobs run independently.
+constexpr int kMgCluster = 8;
+
+__device__ __forceinline__ void mg_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Threads per CTA: 1024 (8 K threads per job) while every job's cluster is
+// co-resident, else 512 (two CTAs per SM; backend.cu picks by occupancy).
+template <int Threads>
+__global__ void __cluster_dims__(kMgCluster, 1, 1) __launch_bounds__(Threads, 1024 / Threads)
+    mg_cluster_kernel(const __grid_constant__ MgTable t) {
+    constexpr int kMgClusterThreads = Threads;
+    std::uint32_t rank;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const MgJob& j = t.job[blockIdx.x / kMgCluster];
+    const std::uint64_t p0 = rank * static_cast<std::uint64_t>(kMgClusterThreads) + threadIdx.x;
+    constexpr std::uint64_t ps = static_cast<std::uint64_t>(kMgCluster) * kMgClusterThreads;
+    const int lt = static_cast<int>(t.lt);
+    // mg.f's timed sequence with comm3 fused into the operator that writes
+    // the grid (mg_store<true>) and each zero3 fused into the operator that
+    // then adds into the zeroed grid (Fresh): 74 cluster barriers instead
+    // of the 149 launches of the per-operator path for class S
+    mg_zero(t, j, lt, 0, p0, ps);
+    mg_cluster_sync();
+    mg_resid<true>(t, j, lt, 1, p0, ps);
+    mg_cluster_sync();
+    for (std::uint32_t it = 0; it < t.nit; ++it) {
+        for (int k = lt; k >= 2; --k) {  // restrict down to level 1 (ghosts included)
+            mg_rprj3<true>(t, j, k, p0, ps);
+            mg_cluster_sync();
+        }
+        mg_psinv<true, true>(t, j, 1, p0, ps);  // zero3 + psinv + comm3 on the coarsest level
+        mg_cluster_sync();
+        for (int k = 2; k <= lt - 1; ++k) {
+            mg_interp<true>(t, j, k, p0, ps);  // zero3 + interp
+            mg_cluster_sync();
+            mg_resid<true>(t, j, k, 0, p0, ps);
+            mg_cluster_sync();
+            mg_psinv<true>(t, j, k, p0, ps);
+            mg_cluster_sync();
+        }
+        mg_interp(t, j, lt, p0, ps);
+        mg_cluster_sync();
+        mg_resid<true>(t, j, lt, 1, p0, ps);
+        mg_cluster_sync();
+        mg_psinv<true>(t, j, lt, p0, ps);
+        mg_cluster_sync();
+        mg_resid<true>(t, j, lt, 1, p0, ps);
+        mg_cluster_sync();
+    }
+    if (threadIdx.x < kMgThreads)
+        for (unsigned plane = rank; plane < t.nx; plane += kMgCluster) mg_norm_plane<true>(t, j, plane);
+    mg_cluster_sync();
+    if (rank == 0 && threadIdx.x == 0) mg_norm_fold(t, j);
 }
 
 }  // namespace vgk

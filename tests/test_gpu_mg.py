@@ -65,7 +65,8 @@ def _check(inp, out, cls):
 
 def test_nas_mg_class_s_batch_of_8_bit_exact():
     """The paper's configuration: class S (32^3, 4 V-cycles), 8 SPMD
-    processes in one batch (one table launch per grid operator)."""
+    processes in one batch (one launch: a thread-block cluster per job with
+    comm3 / zero3 fused into the operators, mg_cluster_kernel)."""
     inp = V.mg_input_for_class("S")
     sz = W.Sizes()
     outs, s = _run([inp] * 8, W.region_bytes("mg", sz))
@@ -89,3 +90,23 @@ def test_nas_mg_native_path_and_malformed_input():
     _check(inp, out, "S")
     with pytest.raises(Exception):
         V.output_size("nas-mg", inp[:-8])
+
+
+def test_nas_mg_class_s_both_device_paths_agree_bit_for_bit():
+    """Class S through the launch-per-operator path (VGPU_MG_CLUSTER=0, a
+    fresh process: the switch is read once) equals the oracle too, so both
+    device schedules of mg.f give the same bits."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1511_07658_b200 import vgpu as V\n"
+            "inp = V.mg_input_for_class('S')\n"
+            "out = V.native_run_task(inp, V.KernelDescriptor('nas-mg', 5000, 30000, 5000, 64))\n"
+            "sys.stdout.write(out.hex())\n") % repo
+    for flag in ("0", "1"):
+        env = dict(os.environ, VGPU_MG_CLUSTER=flag)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        _check(V.mg_input_for_class("S"), bytes.fromhex(r.stdout.strip()), "S")
