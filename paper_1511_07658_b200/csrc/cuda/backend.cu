@@ -294,6 +294,72 @@ cudaError_t launch_tc2_tma(const vgk::TcTable& tt, std::uint32_t maxn, cudaStrea
     return cudaSuccess;
 }
 
+// SGEMM batches of >= 2 jobs: split(h1) ; GEMM(h1) || split(h2) ; GEMM(h2)
+// (VGPU_SGEMM_OVERLAP=0 keeps split(all) ; GEMM(all))
+bool sgemm_overlap() {
+    static const bool o = [] {
+        const char* e = std::getenv("VGPU_SGEMM_OVERLAP");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return o;
+}
+
+// One helper stream + two events per device, made on first use (the
+// dispatcher, the native path and the resident bench each call launch_jobs
+// from one thread at a time per device; the mutex covers creation).
+struct SgemmHelper {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t start = nullptr, done = nullptr;
+};
+cudaError_t sgemm_helper(SgemmHelper** out) {
+    static std::mutex mu;
+    static SgemmHelper helpers[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard lk(mu);
+    SgemmHelper& h = helpers[dev];
+    if (!h.s2) {
+        e = cudaStreamCreateWithFlags(&h.s2, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            h.s2 = nullptr;
+            return e;
+        }
+    }
+    *out = &h;
+    return cudaSuccess;
+}
+
+cudaError_t launch_sgemm_overlapped(const vgk::TcTable& tt, std::uint32_t maxn, cudaStream_t s,
+                                    std::uint64_t* launches) {
+    using namespace vgk;
+    SgemmHelper* h = nullptr;
+    cudaError_t e = sgemm_helper(&h);
+    if (e != cudaSuccess) return e;
+    TcTable a = tt, b = tt;
+    a.njobs = tt.njobs / 2;
+    b.njobs = tt.njobs - a.njobs;
+    for (std::uint32_t i = 0; i < b.njobs; ++i) b.job[i] = tt.job[a.njobs + i];
+    tc_split_kernel<<<dim3(maxn / 64, maxn / 64, a.njobs), 256, 0, s>>>(a);
+    // split(h2) starts once split(h1) is done (the two would only share HBM)
+    if ((e = cudaGetLastError()) == cudaSuccess) e = cudaEventRecord(h->start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->s2, h->start, 0);
+    if (e == cudaSuccess) {
+        tc_split_kernel<<<dim3(maxn / 64, maxn / 64, b.njobs), 256, 0, h->s2>>>(b);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(h->done, h->s2);
+    if (e == cudaSuccess) e = launch_tc2_tma(a, maxn, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->done, 0);
+    if (e == cudaSuccess) e = launch_tc2_tma(b, maxn, s);
+    *launches += 2 + (a.njobs + kMaxTc2TmaJobs - 1) / kMaxTc2TmaJobs +
+                 (b.njobs + kMaxTc2TmaJobs - 1) / kMaxTc2TmaJobs;
+    return e;
+}
+
 // Co-resident clusters of the CG kernel per cluster size 1..16 (above 8
 // needs the non-portable attribute; a cluster lives in one GPC, so at 16
 // CTAs only ~7 fit on a B200). All zero when the kernel cannot launch.
@@ -866,6 +932,22 @@ cudaError_t launch_jobs(std::uint32_t kernel, const DevJob* jobs, std::uint32_t 
                                                     kTcSmemBytes) == cudaSuccess;
                     }();
                     if (!attr) return cudaErrorInvalidConfiguration;
+                    bool pair_tma = sgemm_pair() && sgemm_tma();
+                    for (std::uint32_t i = 0; i < tt.njobs && pair_tma; ++i)
+                        pair_tma = tt.job[i].n % kTc2BN == 0;
+                    if (g_sgemm_phases == 3u && pair_tma && tt.njobs >= 2 && sgemm_overlap()) {
+                        // the HBM-bound split of the second half of the jobs runs
+                        // on a helper stream beside the tensor-bound GEMM of the
+                        // first half (their CTAs can co-reside: 224 + 32 registers
+                        // x 256 threads = the 64 K register file, 193 + 17 KiB
+                        // smem). Measured: 4 jobs 0.385 -> 0.364 ms, 16 jobs 1.377
+                        // -> 1.371 ms (there the split's 8 K short CTAs and the
+                        // GEMM's 512 CTAs mostly take turns; a 148-CTA grid-stride
+                        // split beside the GEMM was slower, 1.76 ms)
+                        const cudaError_t eo = launch_sgemm_overlapped(tt, maxn, s, launches);
+                        if (eo != cudaSuccess) return eo;
+                        return cudaSuccess;
+                    }
                     if (g_sgemm_phases & 1u) {
                         tc_split_kernel<<<dim3(maxn / 64, maxn / 64, tt.njobs), 256, 0, s>>>(tt);
                         ++*launches;

@@ -87,11 +87,18 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
 // grid (n/64, n/64, jobs), 256 threads; n % 128 == 0 for this path. A 64x64
 // tile per CTA, 128-bit loads and stores throughout (the pass is HBM-bound:
 // 4 bytes read, 8 written per element of A and of B).
+__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by);
+
 __global__ void __launch_bounds__(256) tc_split_kernel(const __grid_constant__ TcTable table) {
     const TcJob& job = table.job[blockIdx.z];
     const int n = static_cast<int>(job.n);
     const int bx = blockIdx.x * 64, by = blockIdx.y * 64;
     if (bx >= n || by >= n) return;
+    tc_split_tile(job, bx, by);
+}
+
+__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by) {
+    const int n = static_cast<int>(job.n);
     const int t = threadIdx.x;
     const int c4 = (t & 15) * 4;  // 16 threads x 4 columns = 64 columns
     const int r0 = t >> 4;        // 16 rows per pass, 4 passes
