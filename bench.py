@@ -817,6 +817,12 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                   "launch_chaining": ("PDL: K independent steps back to back, each launch may "
                                       "ramp up under the previous one's tail") if d["pdl"]
                                      else "serialized"})
+        if kind == "mg":
+            # class S: 0.7 MB of grids per job, L2-resident; one launch runs mg.f's
+            # whole sequence as 74 dependent cluster-barrier steps per job
+            r["bound_note"] = ("NAS MG class S: the grids stay in L2; the launch is 74 dependent "
+                               "cluster-barrier steps per job (mg_cluster_kernel), so latency, not "
+                               "HBM bandwidth, bounds it: %.2f us per step" % (kernel_s * 1e6 / 74))
         if d.get("serial_kernel_ms_per_launch"):
             r["serial_us_per_launch"] = d["serial_kernel_ms_per_launch"] * 1e3
             r["serial_frac"] = (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"]
@@ -883,7 +889,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
     # the pipe view of the same kernel from its committed ncu capture: the
     # op count above is algorithmic; the hardware also runs the log's
     # reduction, the Newton steps of div/sqrt and the compaction
-    summ = os.path.join(REPO, "profiles", "r1_ncu_ep_summary_v7.txt")
+    summ = os.path.join(REPO, "profiles", "r2_ncu_ep_final_summary.txt")
     if os.path.exists(summ):
         vals = {}
         for line in open(summ):
@@ -896,7 +902,7 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                                                                "pct_of_peak_sustained_active"),
                               "issue_active_pct": vals.get("smsp__issue_active.avg."
                                                            "pct_of_peak_sustained_active"),
-                              "source": "profiles/r1_ncu_ep_summary_v7.txt (ncu --set full)"}
+                              "source": "profiles/r2_ncu_ep_final_summary.txt (ncu --set full)"}
     return r
 
 
@@ -919,7 +925,7 @@ def kernel_summary(V, W, workload, device, peaks, sizes, steps, warmup) -> dict:
                          W.EP_CLASS_A_ACCEPTED if kind == "ep" else None)
             out[kind] = {k: r.get(k) for k in ("bound", "kernel", "achieved", "peak", "unit",
                                                  "frac", "traffic", "kernel_us_per_launch",
-                                                 "fp32_equiv_tflops") if k in r}
+                                                 "fp32_equiv_tflops", "bound_note") if k in r}
             out[kind]["tasks_per_launch"] = procs
         except Exception as e:  # noqa: BLE001 - reported in the line
             out[kind] = {"error": str(e)[:200]}

@@ -1245,6 +1245,8 @@ struct vgpu_cu_dev {
     std::atomic<std::uint64_t> launches{0}, tasks{0}, h2d_bytes{0}, d2h_bytes{0}, nbatches{0};
 
     ncclComm_t comm = nullptr;
+    std::uint8_t* reduce_buf = nullptr;  // device buffer of the final all-gather, kept
+    std::uint64_t reduce_cap = 0;
     int nranks = 1;
 
     int pool_get(cudaEvent_t* out) {
@@ -1641,6 +1643,9 @@ void drop_state(vgpu_cu_dev* d, bool live) {
     d->arena = nullptr;
     if (live && d->comm && nccl().ok) nccl().comm_destroy(d->comm);
     d->comm = nullptr;
+    if (live && d->reduce_buf) cudaFree(d->reduce_buf);
+    d->reduce_buf = nullptr;
+    d->reduce_cap = 0;
 }
 
 // Sticky device fault (an illegal address, a trap, ...): the context is
@@ -2805,8 +2810,17 @@ int vgpu_cu_reduce_final(vgpu_cu_dev* d, const void* partial, std::uint64_t byte
         return VGPU_CU_EINVAL;
     }
     CK(cudaSetDevice(d->device));
-    std::uint8_t* buf = nullptr;
-    CK(cudaMalloc(&buf, bytes * (d->nranks + 1)));
+    // one device buffer per handle (a cudaMalloc / cudaFree per call would
+    // synchronize the device and cost milliseconds)
+    const std::uint64_t need = bytes * (static_cast<std::uint64_t>(d->nranks) + 1);
+    if (need > d->reduce_cap) {
+        if (d->reduce_buf) cudaFree(d->reduce_buf);
+        d->reduce_buf = nullptr;
+        d->reduce_cap = 0;
+        CK(cudaMalloc(&d->reduce_buf, need));
+        d->reduce_cap = need;
+    }
+    std::uint8_t* buf = d->reduce_buf;
     cudaStream_t s = d->anchor_stream;
     cudaError_t e = cudaMemcpyAsync(buf, partial, bytes, cudaMemcpyHostToDevice, s);
     ncclResult_t r = ncclSuccess;
@@ -2815,7 +2829,6 @@ int vgpu_cu_reduce_final(vgpu_cu_dev* d, const void* partial, std::uint64_t byte
     if (e == cudaSuccess && r == ncclSuccess)
         e = cudaMemcpyAsync(all_out, buf + bytes, bytes * d->nranks, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(buf);
     if (r != ncclSuccess) {
         set_err("ncclAllGather: %s", nccl().error_string ? nccl().error_string(r) : "?");
         return VGPU_CU_ENCCL;
