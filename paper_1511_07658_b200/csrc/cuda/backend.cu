@@ -311,14 +311,19 @@ struct SgemmHelper {
     cudaStream_t s2 = nullptr;
     cudaEvent_t start = nullptr, done = nullptr;
 };
-cudaError_t sgemm_helper(SgemmHelper** out) {
+std::mutex& sgemm_helper_mu() {
     static std::mutex mu;
+    return mu;
+}
+
+// (caller holds sgemm_helper_mu() across its whole enqueue sequence, so two
+// threads never interleave records and waits on the shared events)
+cudaError_t sgemm_helper(SgemmHelper** out) {
     static SgemmHelper helpers[64];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    std::lock_guard lk(mu);
     SgemmHelper& h = helpers[dev];
     if (!h.s2) {
         e = cudaStreamCreateWithFlags(&h.s2, cudaStreamNonBlocking);
@@ -336,6 +341,7 @@ cudaError_t sgemm_helper(SgemmHelper** out) {
 cudaError_t launch_sgemm_overlapped(const vgk::TcTable& tt, std::uint32_t maxn, cudaStream_t s,
                                     std::uint64_t* launches) {
     using namespace vgk;
+    std::lock_guard lk(sgemm_helper_mu());
     SgemmHelper* h = nullptr;
     cudaError_t e = sgemm_helper(&h);
     if (e != cudaSuccess) return e;
@@ -719,7 +725,7 @@ cudaError_t launch_mg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
                 }
                 return n;
             }();
-            const int forced = [] {
+            static const int forced = [] {
                 const char* v = std::getenv("VGPU_MG_THREADS");
                 return v ? std::atoi(v) : 0;
             }();
