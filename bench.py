@@ -819,10 +819,11 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                                      else "serialized"})
         if kind == "mg":
             # class S: 0.7 MB of grids per job, L2-resident; one launch runs mg.f's
-            # whole sequence as 74 dependent cluster-barrier steps per job
-            r["bound_note"] = ("NAS MG class S: the grids stay in L2; the launch is 74 dependent "
-                               "cluster-barrier steps per job (mg_cluster_kernel), so latency, not "
-                               "HBM bandwidth, bounds it: %.2f us per step" % (kernel_s * 1e6 / 74))
+            # whole sequence as 78 dependent barrier steps per job
+            r["bound_note"] = ("NAS MG class S: the grids stay in L2; the launch is 78 dependent "
+                               "steps per job (38 cluster barriers, 40 CTA barriers on the coarse "
+                               "levels; mg_cluster_kernel), so latency, not HBM bandwidth, bounds "
+                               "it: %.2f us per step" % (kernel_s * 1e6 / 78))
         if d.get("serial_kernel_ms_per_launch"):
             r["serial_us_per_launch"] = d["serial_kernel_ms_per_launch"] * 1e3
             r["serial_frac"] = (d["algo_bytes_per_launch"] / (d["serial_kernel_ms_per_launch"]
