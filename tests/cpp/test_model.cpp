@@ -248,6 +248,14 @@ TEST_CASE("device: B200 fluid block scheduler (DeviceSpec::fluid_blocks)") {
     p.grid_size = 2 * 592;
     CHECK(span(1) == 100);
     CHECK(span(2) == 200);
+    // the fixed part of a kernel span (launch probe) is paid once per kernel,
+    // concurrently, not per wave: two full-device kernels of 110 us with 10 us
+    // fixed take 10 + 2 x 100, not 2 x 110
+    p.grid_size = 592;
+    p.t_comp = 110;
+    dev.kernel_launch_us = 10;
+    CHECK(span(1) == 110);
+    CHECK(span(2) == 210);
 }
 
 TEST_CASE("DeviceSpec keeps the reference's layout (it sits inside GvmConfig)") {
