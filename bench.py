@@ -54,6 +54,9 @@ DTYPE = {"vecadd": "f32", "ep": "f64", "bs": "f32", "mm": "f32", "mixed": "f32+f
          "vmul": "f32", "es": "f32", "mg": "f64"}
 
 
+T_START = time.time()
+
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -1145,6 +1148,7 @@ def main():
     if clocks:
         clocks.mark(t0, time.time())
 
+    log(f"value leg done ({time.time() - T_START:.0f} s)")
     # ---- e2e: virtualized through the GVM ----------------------------------------------
     dist.barrier()
     # B200 policy: eager dispatch (barrier 1) — per-client hardware queues make
@@ -1180,6 +1184,7 @@ def main():
     d2h = sum(W.output_bytes(k, sizes) for k in kinds)
     launches_e2e = int(round(e2e["launches_total"] * args.steps / (args.steps + args.warmup)))
 
+    log(f"e2e legs done ({time.time() - T_START:.0f} s)")
     # ---- native baseline --------------------------------------------------------------
     native = None
     if not args.no_native:
@@ -1216,6 +1221,7 @@ def main():
                       "desc": "paper Figs. 13-22 turnaround: simultaneous start -> last process "
                               "has its result; virtualized includes REQ, native includes its "
                               "own CUDA context creation"}
+    log(f"native + turnaround legs done ({time.time() - T_START:.0f} s)")
     overhead = None
     if not args.no_native and world == 1:
         overhead = leg_overhead_n1(V, N, W, args.workload if args.workload != "mixed" else "vecadd",
@@ -1249,6 +1255,7 @@ def main():
     except Exception as e:  # noqa: BLE001 - reported in the line
         reduce_info = {"error": str(e)[:300], "local_record_jobs": record[0]}
 
+    log(f"overhead + final reduce done ({time.time() - T_START:.0f} s)")
     # ---- cpu baseline (rank 0, N = 1) -----------------------------------------------------
     cpu = None
     if dist.rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1272,6 +1279,7 @@ def main():
         accepted = record[13] if record[13] > 0 else None
         roof = roofline(W, dom, legs[dom], peaks, accepted)
         roof["link"] = link_roofline(V, device, h2d, d2h, args.steps, secs, world)
+        log(f"cpu baseline done ({time.time() - T_START:.0f} s)")
         kernels = None
         if not args.no_kernels:
             kernels = kernel_summary(V, W, args.workload, device, peaks, sizes, args.steps,
