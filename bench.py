@@ -294,7 +294,8 @@ def leg_value(V, W, workload, procs_per_gpu, gid0, total_workers, steps, warmup,
 
 
 def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, device, native,
-                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False, api="span"):
+                sizes, dist, cold=False, barrier=0, window=2000, snapshot=False, api="span",
+                timeline=False):
     """api: the SPMD program's client API (vgpu-spmd): 'span' = the
     reference's snd(span) + rcv(); 'inplace' = snd(span) + rcv_region();
     'resident' = input kept in the pinned region, snd_region_at +
@@ -342,6 +343,7 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         fold = gvm.fold() if gvm else None
         batches = gvm.batches() if gvm else []
         tasks = gvm.tasks() if gvm else []
+        tl_csv = gvm.timeline_csv() if gvm and timeline else None
     finally:
         if gvm:
             gvm.stop()
@@ -351,6 +353,8 @@ def leg_workers(V, N, W, workload, procs, gid0, total_workers, steps, warmup, de
         raise RuntimeError(f"worker errors: {bad[:2]}")
     t0, t1 = timed_window(res, warmup)
     info = {"results": res, "t0": t0, "t1": t1, "seconds": (t1 - t0) * 1e-9}
+    if tl_csv is not None:
+        info["timeline_csv"] = tl_csv
     if gvm:
         info["launches_total"] = after["kernel_launches"] - before["kernel_launches"]
         info["gvm_fold"] = fold
@@ -752,6 +756,55 @@ def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
     return out
 
 
+def timeline_report(V, N, W, workload, device, sizes, dist, steps, warmup, procs, path) -> dict:
+    """The measured schedule of the e2e leg (resident API, eager dispatch):
+    every task's H2D / kernel / D2H interval from its CUDA events, in the
+    reference's timeline CSV schema (proj/src/device.cpp:210-215), written
+    to `path`; the summary says how much of the timed window each stage kind
+    kept busy and how much the copies overlapped the kernels and each other
+    (the paper's copy/compute overlap, measured)."""
+    procs = procs or W.DEFAULT_PROCS[workload]
+    r = leg_workers(V, N, W, workload, procs, 0, procs, steps, warmup, device, False, sizes, dist,
+                    barrier=1, api="resident", timeline=True)
+    csv = r["timeline_csv"]
+    with open(path, "w") as f:
+        f.write(csv)
+    ivs = {"SendData": [], "Compute": [], "RtrvData": []}
+    for line in csv.strip().splitlines()[1:]:
+        _, _, kind, a, b = line.split(",")
+        ivs.setdefault(kind, []).append((float(a), float(b)))
+    t_end = max(b for v in ivs.values() for _, b in v)
+    span_t = r["seconds"] * 1e6
+    t0 = t_end - span_t  # the timed rounds: the last `seconds` of the schedule
+
+    def union(iv):
+        out, cur = 0.0, None
+        for a, b in sorted((max(a, t0), b) for a, b in iv if b > t0):
+            if cur is None or a > cur[1]:
+                if cur:
+                    out += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        return out + (cur[1] - cur[0] if cur else 0.0)
+
+    def both(x, y):  # time both kinds were active: |x| + |y| - |x or y|
+        return union(ivs[x]) + union(ivs[y]) - union(ivs[x] + ivs[y])
+
+    busy = {k: union(v) / span_t for k, v in ivs.items()}
+    return {"report": "timeline", "workload": W.CONFIG_NAME[workload], "procs": procs,
+            "timed_window_us": span_t, "csv": os.path.relpath(path, REPO) if path.startswith(REPO)
+            else path,
+            "busy_fraction": {"h2d": busy["SendData"], "kernel": busy["Compute"],
+                              "d2h": busy["RtrvData"]},
+            "overlap_fraction": {"h2d_and_d2h": both("SendData", "RtrvData") / span_t,
+                                 "h2d_and_kernel": both("SendData", "Compute") / span_t,
+                                 "d2h_and_kernel": both("RtrvData", "Compute") / span_t},
+            "jobs_per_s": procs * steps / r["seconds"],
+            "desc": "fractions of the timed window (the last K rounds) during which at least one "
+                    "H2D / kernel / D2H of any client ran, and during which two kinds ran at once"}
+
+
 def model_summary(batches):
     """Paper model (simulate() on the declared triples) vs CUDA-event batch
     makespans, §6 model validation."""
@@ -1057,6 +1110,9 @@ def main():
                     help="the reference's acceptance criteria 5-7 on B200 data (report)")
     ap.add_argument("--overhead-curve", action="store_true",
                     help="virtualization overhead across payload sizes, 1 process (report)")
+    ap.add_argument("--timeline", default="",
+                    help="measured schedule of the e2e leg -> this CSV path, plus an overlap "
+                         "summary line (report)")
     ap.add_argument("--ep-m", type=int, default=0, help="diagnostics: EP class m (default 28)")
     ap.add_argument("--vecadd-n", type=int, default=0, help="diagnostics: floats per vecadd job")
     ap.add_argument("--no-kernels", action="store_true",
@@ -1114,8 +1170,12 @@ def main():
     if V.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU fallback)")
     device = dist.device
-    if args.validate_model or args.sweep or args.overhead_curve or args.speedup or args.acceptance:
+    if (args.validate_model or args.sweep or args.overhead_curve or args.speedup or args.acceptance
+            or args.timeline):
         if dist.rank == 0:
+            if args.timeline:
+                emit(timeline_report(V, N, W, args.workload, device, sizes, dist, args.steps,
+                                     args.warmup, args.procs, os.path.abspath(args.timeline)))
             if args.acceptance:
                 emit(acceptance(V, N, W, device, dist, args.steps, args.warmup))
             if args.speedup:
