@@ -756,6 +756,40 @@ def overhead_curve(V, N, W, device, dist, steps, warmup) -> dict:
     return out
 
 
+def timeline_fractions(csv: str, span_us: float):
+    """Busy and pairwise-overlap fractions of the last `span_us` of a
+    timeline CSV (task_id,stream_id,kind,start_us,end_us): the fraction of
+    that window during which at least one interval of a kind (or of two kinds
+    at once) was open."""
+    ivs = {"SendData": [], "Compute": [], "RtrvData": []}
+    for line in csv.strip().splitlines()[1:]:
+        _, _, kind, a, b = line.split(",")
+        ivs.setdefault(kind, []).append((float(a), float(b)))
+    t_end = max((b for v in ivs.values() for _, b in v), default=0.0)
+    t0 = t_end - span_us
+
+    def union(iv):
+        out, cur = 0.0, None
+        for a, b in sorted((max(a, t0), b) for a, b in iv if b > t0):
+            if cur is None or a > cur[1]:
+                if cur:
+                    out += cur[1] - cur[0]
+                cur = [a, b]
+            else:
+                cur[1] = max(cur[1], b)
+        return out + (cur[1] - cur[0] if cur else 0.0)
+
+    def both(x, y):  # |x| + |y| - |x or y|
+        return union(ivs[x]) + union(ivs[y]) - union(ivs[x] + ivs[y])
+
+    busy = {"h2d": union(ivs["SendData"]) / span_us, "kernel": union(ivs["Compute"]) / span_us,
+            "d2h": union(ivs["RtrvData"]) / span_us}
+    overlap = {"h2d_and_d2h": both("SendData", "RtrvData") / span_us,
+               "h2d_and_kernel": both("SendData", "Compute") / span_us,
+               "d2h_and_kernel": both("RtrvData", "Compute") / span_us}
+    return busy, overlap
+
+
 def timeline_report(V, N, W, workload, device, sizes, dist, steps, warmup, procs, path) -> dict:
     """The measured schedule of the e2e leg (resident API, eager dispatch):
     every task's H2D / kernel / D2H interval from its CUDA events, in the
@@ -769,37 +803,12 @@ def timeline_report(V, N, W, workload, device, sizes, dist, steps, warmup, procs
     csv = r["timeline_csv"]
     with open(path, "w") as f:
         f.write(csv)
-    ivs = {"SendData": [], "Compute": [], "RtrvData": []}
-    for line in csv.strip().splitlines()[1:]:
-        _, _, kind, a, b = line.split(",")
-        ivs.setdefault(kind, []).append((float(a), float(b)))
-    t_end = max(b for v in ivs.values() for _, b in v)
     span_t = r["seconds"] * 1e6
-    t0 = t_end - span_t  # the timed rounds: the last `seconds` of the schedule
-
-    def union(iv):
-        out, cur = 0.0, None
-        for a, b in sorted((max(a, t0), b) for a, b in iv if b > t0):
-            if cur is None or a > cur[1]:
-                if cur:
-                    out += cur[1] - cur[0]
-                cur = [a, b]
-            else:
-                cur[1] = max(cur[1], b)
-        return out + (cur[1] - cur[0] if cur else 0.0)
-
-    def both(x, y):  # time both kinds were active: |x| + |y| - |x or y|
-        return union(ivs[x]) + union(ivs[y]) - union(ivs[x] + ivs[y])
-
-    busy = {k: union(v) / span_t for k, v in ivs.items()}
+    busy, overlap = timeline_fractions(csv, span_t)
     return {"report": "timeline", "workload": W.CONFIG_NAME[workload], "procs": procs,
             "timed_window_us": span_t, "csv": os.path.relpath(path, REPO) if path.startswith(REPO)
             else path,
-            "busy_fraction": {"h2d": busy["SendData"], "kernel": busy["Compute"],
-                              "d2h": busy["RtrvData"]},
-            "overlap_fraction": {"h2d_and_d2h": both("SendData", "RtrvData") / span_t,
-                                 "h2d_and_kernel": both("SendData", "Compute") / span_t,
-                                 "d2h_and_kernel": both("RtrvData", "Compute") / span_t},
+            "busy_fraction": busy, "overlap_fraction": overlap,
             "jobs_per_s": procs * steps / r["seconds"],
             "desc": "fractions of the timed window (the last K rounds) during which at least one "
                     "H2D / kernel / D2H of any client ran, and during which two kinds ran at once"}

@@ -188,3 +188,21 @@ def test_payload_bench_rows_parse(bench, monkeypatch):
     out = bench.payload_bench_ref()
     assert out["rows"][0] == {"kernel": "vector-add", "n": 8388608, "serial_gbs": 5.034, "omp_gbs": 51.539}
     assert len(out["rows"]) == 2
+
+
+def test_timeline_fractions_busy_and_overlap(bench):
+    # window = the last 100 us (t = 100 .. 200); H2D [100,200), kernel
+    # [150,160), D2H [120,170) and [190,210) (clipped at the end = 210)
+    csv = ("task_id,stream_id,kind,start_us,end_us\n"
+           "1,0,SendData,100,200\n"
+           "1,0,Compute,150,160\n"
+           "1,0,RtrvData,120,170\n"
+           "2,1,RtrvData,190,210\n"
+           "0,0,SendData,0,50\n")            # before the window: ignored
+    busy, overlap = bench.timeline_fractions(csv, 110.0)  # window 100 .. 210
+    assert abs(busy["h2d"] - 100 / 110) < 1e-12
+    assert abs(busy["kernel"] - 10 / 110) < 1e-12
+    assert abs(busy["d2h"] - 70 / 110) < 1e-12
+    assert abs(overlap["h2d_and_d2h"] - 60 / 110) < 1e-12      # 120..170 and 190..200
+    assert abs(overlap["h2d_and_kernel"] - 10 / 110) < 1e-12
+    assert abs(overlap["d2h_and_kernel"] - 10 / 110) < 1e-12
