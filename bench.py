@@ -882,6 +882,10 @@ def roofline(W, kind, d, peaks, ep_accepted=None) -> dict:
                   "launch_chaining": ("PDL: K independent steps back to back, each launch may "
                                       "ramp up under the previous one's tail") if d["pdl"]
                                      else "serialized"})
+        if traffic and traffic < d["algo_bytes_per_launch"]:
+            r["traffic_note"] = ("DRAM bytes (ncu) below the algorithmic bytes: part of the output "
+                                 "is still in L2 when the launch ends, so the algorithmic rate can "
+                                 "exceed the measured copy peak (frac > 1)")
         if kind == "mg":
             # class S: 0.7 MB of grids per job, L2-resident; one launch runs mg.f's
             # whole sequence as 78 dependent barrier steps per job
