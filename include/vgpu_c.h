@@ -143,10 +143,11 @@ uint64_t vgpu_model_simulate(int style, uint32_t n, uint64_t t_in, uint64_t t_co
 /* simulate() with DeviceSpec::fluid_blocks (B200 block scheduler as a
  * fluid): grid = the task's CTAs, ctas_per_sm = its resident CTAs per SM,
  * launch_us = the fixed part of a kernel's measured span (once per kernel,
- * not per wave; vgpu_cu_launch_probe) */
+ * not per wave; vgpu_cu_launch_probe); shared = 0: queue-order slots,
+ * 1: processor sharing among the kernels that run at once */
 uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
                                    uint64_t t_out, uint32_t grid, uint32_t sms,
-                                   uint32_t ctas_per_sm, uint64_t launch_us);
+                                   uint32_t ctas_per_sm, uint64_t launch_us, int shared);
 int vgpu_model_classify(uint64_t t_in, uint64_t t_comp, uint64_t t_out);
 uint64_t vgpu_model_no_vt(uint32_t n, uint64_t t_init, uint64_t t_ctx, uint64_t t_in,
                           uint64_t t_comp, uint64_t t_out);

@@ -180,7 +180,7 @@ HOST_API = {
     "vgpu_native_run_task": (C.c_int, [C.c_int, C.POINTER(DescriptorC), _P, _U64, _P, _U64,
                                        C.POINTER(_U64)]),
     "vgpu_model_simulate": (_U64, [C.c_int, _U32, _U64, _U64, _U64, _U32, _U32, _U32, _U32]),
-    "vgpu_model_simulate_fluid": (_U64, [C.c_int, _U32, _U64, _U64, _U64, _U32, _U32, _U32, _U64]),
+    "vgpu_model_simulate_fluid": (_U64, [C.c_int, _U32, _U64, _U64, _U64, _U32, _U32, _U32, _U64, C.c_int]),
     "vgpu_model_classify": (C.c_int, [_U64, _U64, _U64]),
     "vgpu_model_no_vt": (_U64, [_U32, _U64, _U64, _U64, _U64, _U64]),
     "vgpu_encode_frame": (C.c_int, [C.c_uint8, _U32, _U64, _P, _U64, _P, _U64, C.POINTER(_U64)]),

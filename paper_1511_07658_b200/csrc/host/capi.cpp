@@ -416,7 +416,7 @@ uint64_t vgpu_model_simulate(int style, uint32_t n, uint64_t t_in, uint64_t t_co
 
 uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_t t_comp,
                                    uint64_t t_out, uint32_t grid, uint32_t sms,
-                                   uint32_t ctas_per_sm, uint64_t launch_us) {
+                                   uint32_t ctas_per_sm, uint64_t launch_us, int shared) {
     try {
         KernelProfile p;
         p.t_data_in = t_in;
@@ -427,7 +427,7 @@ uint64_t vgpu_model_simulate_fluid(int style, uint32_t n, uint64_t t_in, uint64_
         DeviceSpec dev = DeviceSpec::b200();
         dev.num_sms = sms;
         dev.block_slots_per_sm = ctas_per_sm;
-        dev.fluid_blocks = true;
+        dev.fluid_blocks = shared ? 2 : 1;
         dev.kernel_launch_us = static_cast<std::uint16_t>(std::min<uint64_t>(launch_us, 65535));
         return simulate(build_work_queue(style ? ProgrammingStyle::PS2 : ProgrammingStyle::PS1, ps),
                         dev)

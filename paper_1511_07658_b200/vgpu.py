@@ -418,11 +418,12 @@ def link_probe(device: int = 0, nbytes: int = 256 << 20, reps: int = 8, shm: boo
 
 
 def model_simulate_fluid(style: int, n: int, t_in: int, t_comp: int, t_out: int, grid: int,
-                         sms: int, ctas_per_sm: int, launch_us: int = 0) -> int:
-    """simulate() with the B200 fluid block-scheduler spec (DeviceSpec::fluid_blocks);
-    launch_us = the fixed part of a kernel span (DeviceSpec::kernel_launch_us)."""
+                         sms: int, ctas_per_sm: int, launch_us: int = 0, shared: bool = False) -> int:
+    """simulate() with the B200 fluid block-scheduler spec (DeviceSpec::fluid_blocks: 1 queue
+    order, 2 = shared when `shared`); launch_us = the fixed part of a kernel span
+    (DeviceSpec::kernel_launch_us)."""
     return _libs().host.vgpu_model_simulate_fluid(style, n, t_in, t_comp, t_out, grid, sms,
-                                                  ctas_per_sm, launch_us)
+                                                  ctas_per_sm, launch_us, 1 if shared else 0)
 
 
 def launch_probe(device: int = 0) -> float:

@@ -256,6 +256,19 @@ TEST_CASE("device: B200 fluid block scheduler (DeviceSpec::fluid_blocks)") {
     dev.kernel_launch_us = 10;
     CHECK(span(1) == 110);
     CHECK(span(2) == 210);
+    // shared slots (processor sharing): two 512-CTA kernels on 592 slots run
+    // side by side and end together at 2 x 512 x 100 / 592, where queue order
+    // leaves the second one a tail on 512 slots
+    dev.kernel_launch_us = 0;
+    p.grid_size = 512;
+    p.t_comp = 100;
+    dev.fluid_blocks = 2;
+    CHECK(span(1) == 100);
+    CHECK(span(2) == static_cast<Micros>(std::ceil(2.0 * 512 * 100 / 592)));
+    const Micros shared8 = span(8);
+    CHECK(shared8 == static_cast<Micros>(std::ceil(8.0 * 512 * 100 / 592)));
+    dev.fluid_blocks = 1;
+    CHECK(span(8) > shared8);
 }
 
 TEST_CASE("DeviceSpec keeps the reference's layout (it sits inside GvmConfig)") {
