@@ -38,7 +38,7 @@ RPATH_LIB := -Wl,-rpath,'$$ORIGIN'
 RPATH_BIN := -Wl,-rpath,'$$ORIGIN/../lib'
 RPATH_TST := -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
-.PHONY: all product tests oracle ref clean
+.PHONY: all product tests oracle ref clean tsan
 all: product tests oracle
 
 product: $(LIBDIR)/libvgpu_cuda.so $(LIBDIR)/libvgpu.so \
@@ -76,6 +76,19 @@ oracle: oracle/_build/libvgpu_oracle.so
 oracle/_build/libvgpu_oracle.so: oracle/vgpu_oracle.c oracle/vgpu_oracle.h $(wildcard $(CSRC)/common/*.h)
 	@mkdir -p oracle/_build
 	$(OCC) $(CFLAGS) $(OMP) -shared -o $@ oracle/vgpu_oracle.c -lm
+
+# ThreadSanitizer build of the host layer (GVM, transports, client SDK,
+# model) and its C++ tests; the CUDA backend stays uninstrumented. Run the
+# CPU cases: `make tsan && TSAN_OPTIONS=halt_on_error=1 tests/_bin/vgpu-tests-tsan --exclude-gpu`
+TSAN_FLAGS := -O1 -g -std=c++20 -fPIC -pthread -fsanitize=thread -Iinclude -I$(CUDA_HOME)/include
+TSAN_CXX := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo $(CXX))
+tsan: $(TESTBIN)/vgpu-tests-tsan
+
+$(TESTBIN)/vgpu-tests-tsan: $(HOST_SRC) $(TEST_SRC) tests/cpp/minitest.hpp $(LIBDIR)/libvgpu_cuda.so oracle/_build/libvgpu_oracle.so $(HDRS)
+	@mkdir -p $(TESTBIN)
+	$(TSAN_CXX) $(TSAN_FLAGS) -Itests/cpp -Ioracle -o $@ $(HOST_SRC) $(TEST_SRC) \
+	    -L$(LIBDIR) -lvgpu_cuda -Loracle/_build -lvgpu_oracle \
+	    $(RPATH_TST) -Wl,-rpath,'$$ORIGIN/../../oracle/_build' -lrt
 
 ref:
 	$(MAKE) -f oracle/Makefile.ref
