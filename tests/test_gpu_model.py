@@ -42,12 +42,36 @@ def test_validate_model_reports_every_spec():
     sz = W.Sizes()
     sz.vecadd_n = 1 << 18
     out = bench.validate_model(V, N, W, "vecadd", 0, sz, bench.Dist(), reps=3, procs=3)
-    for spec in ("concurrent", "device_filling", "b200_blocks"):
+    for spec in ("concurrent", "device_filling", "b200_blocks", "b200_shared"):
         rows = out[spec]["rows"]
         assert [r["n"] for r in rows] == [1, 2, 3]
         assert all(r["model_us"] > 0 and r["measured_us"] > 0 for r in rows)
         assert out[spec]["mean_deviation_pct"] is not None
     assert out["b200_blocks_spec"]["ctas_per_task"] >= 1
+    # the launch probe: an empty kernel's event-timed span, a few microseconds
+    assert 0.5 < out["b200_blocks_spec"]["kernel_launch_us"] < 100.0
+    assert [s["n"] for s in out["measured_stage_us_per_n"]] == [1, 2, 3]
+
+
+def test_timeline_report_covers_every_task(tmp_path):
+    """bench.py --timeline: the e2e leg's measured schedule (reference CSV
+    schema) has an H2D, a kernel and a D2H interval per task, inside the run."""
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_1511_07658_b200 import _native as N
+    sz = W.Sizes()
+    sz.vecadd_n = 1 << 18
+    path = str(tmp_path / "tl.csv")
+    out = bench.timeline_report(V, N, W, "vecadd", 0, sz, bench.Dist(), 4, 2, 2, path)
+    lines = open(path).read().strip().splitlines()
+    assert lines[0] == "task_id,stream_id,kind,start_us,end_us"
+    kinds = [ln.split(",")[2] for ln in lines[1:]]
+    jobs = 2 * (4 + 3)  # procs x (steps + warmup; bench raises warmup to >= 3 only in main)
+    assert kinds.count("SendData") >= 2 * 4 and kinds.count("Compute") >= 2 * 4
+    assert kinds.count("RtrvData") >= 2 * 4 and len(kinds) <= 3 * jobs
+    for k in ("h2d", "kernel", "d2h"):
+        assert 0.0 < out["busy_fraction"][k] <= 1.0 + 1e-9
+    assert out["jobs_per_s"] > 0
 
 
 def test_span_inplace_resident_apis_agree():
