@@ -4,16 +4,22 @@
 // reference kernel: proj/src/bench/profiles.cpp:37 is a timing profile).
 //
 // Every grid operator of mg.f (resid, psinv, rprj3, interp, comm3, zero3)
-// is one launch over all jobs of a batch (blockIdx.y = job), one thread per
-// output point. Each point evaluates mg.f's expression in its order with
-// explicitly rounded binary64 operations (__dadd_rn / __dsub_rn /
-// __dmul_rn: no FMA contraction), the order the oracle restates
-// (oracle/vgpu_oracle.c vo_mg_run), so the grids match the oracle bit for
-// bit. The ghost layer (comm3) is a separate pass over the six faces: an
-// in-place resid (r = r - A u on the coarse levels) reads its own point
-// only, so a thread may overwrite its point, but filling a ghost from the
-// wrapped interior inside the same pass would race with that point's
-// thread. norm2u3 is a fixed-order reduction shared with the oracle: per
+// is a per-point device function. Two schedules run them: for small grids
+// (nx <= 64) mg_cluster_kernel, one thread-block cluster per job running
+// the whole timed sequence in one launch (comm3 / zero3 fused into the
+// writing operator, coarse levels on one CTA; below); for larger grids one
+// launch per operator over all jobs of a batch (blockIdx.y = job), one
+// thread per output point, with comm3 as a separate pass. Each point
+// evaluates mg.f's expression in its order with explicitly rounded binary64
+// operations (__dadd_rn / __dsub_rn / __dmul_rn: no FMA contraction), the
+// order the oracle restates (oracle/vgpu_oracle.c vo_mg_run), so both
+// schedules match the oracle bit for bit. In the per-operator schedule the
+// ghost layer (comm3) is a separate pass over the six faces: an in-place
+// resid (r = r - A u on the coarse levels) reads its own point only, so a
+// thread may overwrite its point, but filling a ghost from the wrapped
+// interior inside the same pass would race with that point's thread (the
+// fused form writes each ghost from the thread that owns its interior
+// mirror instead). norm2u3 is a fixed-order reduction shared with the oracle: per
 // i3 plane, lane l of 256 sums the plane's points l, l + 256, ... in order,
 // the lanes combine by the stride-doubling tree (warp shuffles, then the 8
 // warp sums), the planes add in i3 order.
