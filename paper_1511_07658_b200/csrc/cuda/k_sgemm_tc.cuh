@@ -19,9 +19,11 @@
 //   tc_gemm2_kernel      the same pair with cp.async loads (VGPU_SGEMM_TMA=0)
 //   tc_gemm_kernel       one CTA, 128 x 128 tiles (n % 128 == 0; VGPU_SGEMM=tc)
 //
-// Pre-pass (tc_split_kernel): A -> A_hi, A_lo (row-major M x K = K-major);
-// B -> B_hi^T, B_lo^T (N x K, K-major) through a 64x64 shared-memory
-// transpose, so both UMMA operands are K-major.
+// Pre-pass (tc_split_kernel): A -> A_lo (row-major M x K = K-major; A_hi is
+// A itself, which the MMA reads truncated to TF32, so A_lo = A - trunc(A);
+// with raw_ahi = 0, A_hi rounded to nearest is written too); B -> B_hi^T,
+// B_lo^T (N x K, K-major) through a 64x64 shared-memory transpose, so both
+// UMMA operands are K-major.
 //
 // 1-CTA kernel (tc_gemm_kernel), one 128 x 128 output tile per CTA, 256
 // threads, tiles of every task of a batch in one launch (blockIdx.z = task):
@@ -71,6 +73,7 @@ struct TcTable {
     TcJob job[kMaxTcJobs];
     std::uint32_t njobs;
     std::uint32_t chunk_kb;  // k-blocks (of kTcBK) per TMEM accumulation chunk
+    std::uint32_t raw_ahi;   // A_hi is A itself (the MMA truncates): the pre-pass writes A_lo only
 };
 
 // ---- pre-pass: split + transpose ---------------------------------------------
@@ -87,17 +90,22 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
 // grid (n/64, n/64, jobs), 256 threads; n % 128 == 0 for this path. A 64x64
 // tile per CTA, 128-bit loads and stores throughout (the pass is HBM-bound:
 // 4 bytes read, 8 written per element of A and of B).
-__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by);
+__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by, bool raw_ahi);
 
 __global__ void __launch_bounds__(256) tc_split_kernel(const __grid_constant__ TcTable table) {
     const TcJob& job = table.job[blockIdx.z];
     const int n = static_cast<int>(job.n);
     const int bx = blockIdx.x * 64, by = blockIdx.y * 64;
     if (bx >= n || by >= n) return;
-    tc_split_tile(job, bx, by);
+    tc_split_tile(job, bx, by, table.raw_ahi != 0);
 }
 
-__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by) {
+// lo = x - trunc_tf32(x): exact; the remainder the MMA drops when it reads x itself
+__device__ __forceinline__ float tf32_trunc_lo(float x) {
+    return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xffffe000u));
+}
+
+__device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by, bool raw_ahi) {
     const int n = static_cast<int>(job.n);
     const int t = threadIdx.x;
     const int c4 = (t & 15) * 4;  // 16 threads x 4 columns = 64 columns
@@ -108,11 +116,15 @@ __device__ __forceinline__ void tc_split_tile(const TcJob& job, int bx, int by) 
         const std::size_t idx = static_cast<std::size_t>(by + r0 + 16 * k) * n + bx + c4;
         const float4 v = __ldcs(reinterpret_cast<const float4*>(job.A + idx));
         float4 h, l;
-        tf32_split(v.x, h.x, l.x);
-        tf32_split(v.y, h.y, l.y);
-        tf32_split(v.z, h.z, l.z);
-        tf32_split(v.w, h.w, l.w);
-        *reinterpret_cast<float4*>(job.ahi + idx) = h;
+        if (raw_ahi) {
+            l = make_float4(tf32_trunc_lo(v.x), tf32_trunc_lo(v.y), tf32_trunc_lo(v.z), tf32_trunc_lo(v.w));
+        } else {
+            tf32_split(v.x, h.x, l.x);
+            tf32_split(v.y, h.y, l.y);
+            tf32_split(v.z, h.z, l.z);
+            tf32_split(v.w, h.w, l.w);
+            *reinterpret_cast<float4*>(job.ahi + idx) = h;
+        }
         *reinterpret_cast<float4*>(job.alo + idx) = l;
     }
     // B: transpose through shared memory; Bt[c][r] = B[r][c]
