@@ -155,7 +155,9 @@ std::uint64_t job_ws_bytes(std::uint32_t kernel, const void* h_in, std::uint64_t
     if (kernel == VGPU_CU_K_CG && h_in && in_bytes >= sizeof(vgpu_cg_header)) {
         vgpu_cg_header h;
         std::memcpy(&h, h_in, sizeof h);
-        // x, z, p, q, r, then the grid variant's barrier and partials
+        // x, z, p, q, r, then the grid variant's barrier and partials (or
+        // the group mode's state, k_cg.cuh)
+        static_assert(sizeof(vgk::CgGroupSync) <= sizeof(vgk::CgGridSync), "group state shares the grid state's room");
         return ((5ull * 8ull * h.n + 255) & ~255ull) + sizeof(vgk::CgGridSync);
     }
     if (kernel == VGPU_CU_K_MG && h_in && in_bytes >= sizeof(vgpu_mg_header)) {
@@ -380,7 +382,9 @@ const CgOccupancy& cg_occupancy() {
         using namespace vgk;
         for (auto k : {cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>, cg_kernel<kCgGlobal, 32>,
                        cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>, cg_kernel<kCgStaged, 32>,
-                       cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>, cg_kernel<kCgResident, 32>}) {
+                       cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>, cg_kernel<kCgResident, 32>,
+                       cg_kernel<kCgResident, 8, true>, cg_kernel<kCgResident, 16, true>,
+                       cg_kernel<kCgResident, 32, true>}) {
             if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
                 cudaGetLastError();
@@ -435,6 +439,64 @@ unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned jobs) {
         }
     }
     return cs;
+}
+
+// Clusters per job (k_cg.cuh group mode) and their width: a job over G
+// co-resident clusters instead of one, when that gives it at least 5/4 the
+// SMs, only when every vector is resident in shared memory at the
+// ONE-cluster row split too (the solo fallback's), and at least 256 rows per
+// CTA. Measured on B200 (scripts/cg_groups.py, profiles/r2_cg_groups.json):
+// the group-mode CTA runs its SpMV ~1.7x slower per SM than the plain
+// kernel (its body is a separate function, whose register budget lets the
+// scheduler batch only two of the four load chains), so it pays only where
+// the SM count gained is large: a launch with ONE class-A-size job (n >=
+// 10^4; 3 x 16 CTAs: 14.7 -> 11.1-11.7 ms). With 8 jobs (10-CTA clusters ->
+// 12-16 CTAs per job) it lost (22.3 -> 30.6 ms), so batches keep one
+// cluster per job. VGPU_CG_GROUPS=1 disables it, =k forces k groups.
+struct CgShape {
+    unsigned cs = 0, groups = 1;
+};
+
+CgShape cg_shape_for(const vgpu_cg_header& h, unsigned jobs, bool resident_ok) {
+    CgShape best{cg_cluster_for(h, jobs), 1};
+    static const int force = [] {
+        const char* e = std::getenv("VGPU_CG_GROUPS");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 1 && v <= vgk::kCgMaxGroups ? v : 0;
+    }();
+    if (!best.cs || !resident_ok || force == 1 || jobs == 0) return best;
+    if (!force && (jobs != 1 || h.n < 10000)) return best;
+    const CgOccupancy& o = cg_occupancy();
+    auto resident_at = [&](unsigned w) {
+        const std::uint64_t rows = (h.n + w - 1) / w + 2;
+        return 8ull * h.n + 32ull * rows + 4ull * rows <= vgk::kCgSmemBytes;
+    };
+    CgShape pick = best;
+    for (unsigned g = 2; g <= static_cast<unsigned>(vgk::kCgMaxGroups); ++g) {
+        if (force && g != static_cast<unsigned>(force)) continue;
+        unsigned w = vgk::kCgMaxCluster;
+        // at least 256 rows per CTA: below that the groups' barriers cost
+        // more than the SMs gain
+        auto fits = [&](unsigned w) {
+            return o.active[w] >= static_cast<int>(jobs * g) && 256ull * w * g <= h.n && resident_at(w);
+        };
+        while (w > 1 && !fits(w)) --w;
+        if (!fits(w)) continue;
+        const bool better = force ? true : 4ull * w * g >= 5ull * best.cs && w * g > pick.cs * pick.groups;
+        if (better) pick = CgShape{w, g};
+    }
+    return pick;
+}
+
+// how long a group-mode cluster waits for its job's other clusters before
+// it runs the job alone (VGPU_CG_JOIN_US, default 50 us)
+unsigned cg_join_ns() {
+    static const unsigned ns = [] {
+        const char* e = std::getenv("VGPU_CG_JOIN_US");
+        const long v = e ? std::atol(e) : 50;
+        return static_cast<unsigned>(std::max(0l, std::min(v, 4000000l)) * 1000);
+    }();
+    return ns;
 }
 
 // SMs of the current device; the grid CG kernels' shared-memory opt-in
@@ -579,9 +641,16 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
             if (e != cudaSuccess) return e;
         }
     }
+    // the clusters' shape of a job: width and groups (group mode needs the
+    // resident placement at the one-cluster split)
+    auto shape_for = [&](const vgpu_cg_header& h) {
+        const unsigned cs1 = cg_cluster_for(h, ncg);
+        return cg_shape_for(h, ncg, cs1 && mode_for(h, cs1) == kCgResident);
+    };
     for (std::uint32_t i = 0; i < n; ++i) {
         if (done[i] || !jobs[i].ws || jobs[i].cg.n == 0) continue;
-        const unsigned cs = cg_cluster_for(jobs[i].cg, ncg);
+        const CgShape shp = shape_for(jobs[i].cg);
+        const unsigned cs = shp.cs;
         if (!cs) return cudaErrorInvalidConfiguration;
         const int mode = mode_for(jobs[i].cg, cs);
         const unsigned seg = cg_seg_for(jobs[i].cg);
@@ -589,8 +658,9 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
         std::uint32_t maxn = 0, maxrows = 0;
         for (std::uint32_t k = i; k < n && t.njobs < kMaxCgJobs; ++k) {
             const vgpu_cg_header& h = jobs[k].cg;
-            if (done[k] || !jobs[k].ws || h.n == 0 || cg_cluster_for(h, ncg) != cs ||
-                mode_for(h, cs) != mode || cg_seg_for(h) != seg)
+            if (done[k] || !jobs[k].ws || h.n == 0) continue;
+            const CgShape sk = shape_for(h);
+            if (sk.cs != cs || sk.groups != shp.groups || mode_for(h, cs) != mode || cg_seg_for(h) != seg)
                 continue;
             done[k] = true;
             const std::uint8_t* in = jobs[k].in;
@@ -612,16 +682,27 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
             j.niter = h.niter;
             j.cgitmax = h.cgitmax;
             j.shift = h.shift;
+            if (shp.groups > 1) {  // the groups' barrier state, zeroed per launch
+                j.gsync = reinterpret_cast<CgGroupSync*>(jobs[k].ws + ((5ull * 8ull * h.n + 255) & ~255ull));
+                const cudaError_t e = cudaMemsetAsync(j.gsync, 0, sizeof(CgGroupSync), s);
+                if (e != cudaSuccess) return e;
+            }
             maxn = std::max(maxn, h.n);
+            // rows of one CTA at the one-cluster split (group mode's solo fallback)
             maxrows = std::max(maxrows, (h.n + cs - 1) / cs + 2);
         }
+        t.groups = shp.groups;
+        t.join_ns = cg_join_ns();
+        if (std::getenv("VGPU_CG_VERBOSE"))
+            std::fprintf(stderr, "nas-cg launch: jobs=%u width=%u groups=%u mode=%d seg=%u\n", t.njobs, cs,
+                         t.groups, mode, seg);
         // p (n doubles) | own x z r q slices | rowstr slice if it fits
         t.stage_n = mode != kCgGlobal ? maxn : 0;
         t.own_rows = mode == kCgResident ? maxrows : 0;
         const std::uint64_t base = 8ull * t.stage_n + 32ull * t.own_rows;
         t.srow_words = base + 4ull * maxrows <= kCgSmemBytes ? maxrows : 0;
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(t.njobs * cs);
+        cfg.gridDim = dim3(t.njobs * t.groups * cs);
         cfg.blockDim = dim3(kCgThreads);
         cfg.dynamicSmemBytes = base + 4ull * t.srow_words;
         cfg.stream = s;
@@ -638,8 +719,11 @@ cudaError_t launch_cg(const DevJob* jobs, std::uint32_t n, cudaStream_t s, std::
                                : cudaLaunchKernelEx(&cfg, k8, t);
         };
         const cudaError_t e =
-            mode == kCgResident ? go(cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>,
-                                     cg_kernel<kCgResident, 32>)
+            mode == kCgResident && t.groups > 1
+                ? go(cg_kernel<kCgResident, 8, true>, cg_kernel<kCgResident, 16, true>,
+                     cg_kernel<kCgResident, 32, true>)
+            : mode == kCgResident ? go(cg_kernel<kCgResident, 8>, cg_kernel<kCgResident, 16>,
+                                       cg_kernel<kCgResident, 32>)
             : mode == kCgStaged ? go(cg_kernel<kCgStaged, 8>, cg_kernel<kCgStaged, 16>,
                                      cg_kernel<kCgStaged, 32>)
                                 : go(cg_kernel<kCgGlobal, 8>, cg_kernel<kCgGlobal, 16>,

@@ -23,6 +23,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "vgpu_cuda.h"
 
@@ -37,6 +38,31 @@ constexpr int kCgMaxGridCtas = 32;  // CTAs per job in the grid variant (warp-0 
 constexpr std::uint32_t kCgStageMax = 24576;  // rows whose p fits in shared memory (192 KiB)
 constexpr std::uint32_t kCgSmemBytes = 224 * 1024;  // dynamic shared memory cap per CTA
 
+// Group mode (kCgResident only): a job spans G clusters of the launch's
+// width instead of one, so a batch that leaves SMs idle as one cluster per
+// job (clusters live inside a GPC) gets more of them. The clusters of a job
+// exchange what crosses them through the job's HBM/L2 workspace: each
+// cluster's dot-product partial (one slot per group, summed by every CTA in
+// group order, so all CTAs keep identical bits) and the new p / z slices
+// (written beside the DSMEM push, copied into each CTA's full copy after
+// the groups' barrier). The barrier between groups is a release counter
+// per group. A job's clusters are only co-resident when nothing else holds
+// the SMs, so the groups first JOIN: when all G arrive within the wait
+// budget the job runs grouped; otherwise the first arrival claims the job
+// and runs it alone (rows over its own cluster, the plain schedule) and the
+// late clusters exit. Nothing ever waits without a bound on a cluster that
+// may not be scheduled.
+constexpr int kCgMaxGroups = 4;
+enum CgGroupMode : unsigned { kCgGrouped = 1, kCgSolo = 2, kCgExit = 3 };
+
+struct CgGroupSync {          // per job, zeroed before every launch
+    unsigned state;           // arrivals (bits 0..15) | decision << 16 (1 grouped, 2 solo)
+    unsigned pad0[31];
+    unsigned seq[kCgMaxGroups];  // publish counter per group
+    unsigned pad1[32 - kCgMaxGroups];
+    double part[2][kCgMaxGroups][4];  // [slot][group][value]
+};
+
 struct CgJob {
     const std::uint32_t* rowstr;
     const std::uint32_t* colidx;
@@ -47,6 +73,7 @@ struct CgJob {
     double* q;
     double* r;
     vgpu_cg_result* out;
+    CgGroupSync* gsync;  // group mode only
     std::uint32_t n, nnz, niter, cgitmax;
     double shift;
 };
@@ -57,7 +84,118 @@ struct CgTable {
     std::uint32_t stage_n;     // doubles of staged p at the start of dynamic smem
     std::uint32_t own_rows;    // kCgResident: doubles per own vector slice after it
     std::uint32_t srow_words;  // room for a rowstr slice after them (u32 words)
+    std::uint32_t groups;      // clusters per job (1: plain)
+    std::uint32_t join_ns;     // group mode: how long the first arrival waits for the others
 };
+
+__device__ __forceinline__ unsigned cg_ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ std::uint64_t cg_globaltimer() {
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// A CTA's group-mode state, in shared memory (CTA-uniform; read only on
+// the group paths, so the SpMV loop keeps its registers).
+struct CgGroupCtx {
+    unsigned groups, gidx, c0, c1, gseq;  // c0..c1: this cluster's rows
+    CgGroupSync* gs;
+    double* gp;  // the workspace copies of p and z the other clusters read
+    double* gz;
+};
+
+// One thread per cluster (rank 0, thread 0): grouped, solo or exit.
+__device__ __forceinline__ unsigned cg_group_join(CgGroupSync* s, unsigned groups, unsigned join_ns) {
+    const unsigned old = atomicAdd(&s->state, 1u);
+    if (old >> 16) return kCgExit;  // decided without this cluster
+    const std::uint64_t t0 = cg_globaltimer();
+    for (;;) {
+        const unsigned st = cg_ld_acquire_u32(&s->state);
+        if ((st >> 16) == 1u) return kCgGrouped;
+        if ((st >> 16) == 2u) return kCgExit;
+        if ((st & 0xffffu) == groups) {
+            if (atomicCAS(&s->state, st, st | (1u << 16)) == st) return kCgGrouped;
+            continue;
+        }
+        if (cg_globaltimer() - t0 > join_ns) {
+            if (atomicCAS(&s->state, st, st | (2u << 16)) == st) return kCgSolo;
+            continue;
+        }
+    }
+}
+
+// After a cluster-wide barrier: the cluster's rank 0 publishes `target`
+// for its group, then every CTA waits until all groups have. The barrier
+// before made the whole cluster's global writes visible to rank 0; its
+// fence and release store carry them to the other groups.
+__device__ __forceinline__ void cg_group_barrier(CgGroupSync* s, unsigned groups, unsigned gidx,
+                                                 unsigned rank, unsigned target) {
+    if (threadIdx.x == 0) {
+        if (rank == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->seq[gidx]), "r"(target) : "memory");
+        }
+        for (unsigned g = 0; g < groups; ++g)
+            while (cg_ld_acquire_u32(&s->seq[g]) < target) {
+            }
+    }
+    __syncthreads();
+}
+
+// The group steps as separate (non-inlined) functions, called at CG phase
+// boundaries: inlined, their code made the scheduler interleave the SpMV's
+// loads with its gathers and FMAs one chain at a time (3.6x slower).
+//
+// v[0..W) holds the cluster's total (identical in every CTA): the job's
+// total over the groups, summed in group order.
+__device__ __noinline__ void cg_group_sum_fn(CgGroupCtx* gx, double* v, int W, unsigned rank) {
+    CgGroupSync* const gs = gx->gs;
+    const unsigned slot = gx->gseq & 1u, ng = gx->groups, target = gx->gseq + 1;
+    if (rank == 0 && threadIdx.x == 0)
+        for (int w = 0; w < W; ++w) gs->part[slot][gx->gidx][w] = v[w];
+    cg_group_barrier(gs, ng, gx->gidx, rank, target);  // ends in __syncthreads
+    if (threadIdx.x == 0) gx->gseq = target;
+    for (int w = 0; w < W; ++w) {
+        double t = 0.0;
+        for (unsigned g = 0; g < ng; ++g) t += __ldcg(&gs->part[slot][g][w]);
+        v[w] = t;
+    }
+}
+
+// After the cluster barrier that completed this cluster's part of p (or z,
+// `use_z`): the groups' barrier, then the rows outside this cluster's range
+// from the workspace into this CTA's full copy ps.
+__device__ __noinline__ void cg_group_exchange_fn(CgGroupCtx* gx, double* ps, std::uint32_t n, unsigned rank,
+                                                  bool use_z) {
+    const unsigned target = gx->gseq + 1;
+    cg_group_barrier(gx->gs, gx->groups, gx->gidx, rank, target);
+    const double* src = use_z ? gx->gz : gx->gp;
+    const std::uint32_t c0 = gx->c0, c1 = gx->c1;
+    const std::uint32_t nf = n - (c1 - c0);
+    for (std::uint32_t i0 = threadIdx.x; i0 < nf; i0 += 4 * kCgThreads) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const std::uint32_t k = i0 + u * kCgThreads;
+            const std::uint32_t i = k < c0 ? k : k + (c1 - c0);
+            if (k < nf) t[u] = __ldcg(src + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const std::uint32_t k = i0 + u * kCgThreads;
+            const std::uint32_t i = k < c0 ? k : k + (c1 - c0);
+            if (k < nf) ps[i] = t[u];
+        }
+    }
+    __syncthreads();  // also: every thread read gseq before it advances
+    if (threadIdx.x == 0) gx->gseq = target;
+    __syncthreads();
+}
 
 __device__ __forceinline__ double cg_warp_sum(double v) {
 #pragma unroll
@@ -191,19 +329,35 @@ __host__ __device__ __forceinline__ unsigned cg_segment(std::uint32_t n, std::ui
 //                (classes S..A at the widths the batch allows).
 enum CgMode { kCgGlobal = 0, kCgStaged = 1, kCgResident = 2 };
 
-template <int kMode, unsigned kSeg>
-__global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant__ CgTable table) {
+// The CG body of one CTA: kG = the grouped row split (G clusters per job,
+// this cluster group gidx), else the plain one (the job over this cluster).
+template <int kMode, unsigned kSeg, bool kG>
+__device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsigned gidx_in, unsigned G) {
     // dynamic shared memory: p (stage_n doubles) | x z r q slices (own_rows
     // doubles each, kCgResident) | this CTA's rowstr slice (srow_words)
     extern __shared__ double ps[];
     __shared__ CgReduce red;
+    __shared__ CgGroupCtx gx;  // group mode only
     cgx::cluster_group cluster = cgx::this_cluster();
     const unsigned csize = cluster.num_blocks();
-    const CgJob& job = table.job[blockIdx.x / csize];
     const unsigned rank = cluster.block_rank();
+    const CgJob& job = table.job[jid];
     const std::uint32_t n = job.n;
-    const std::uint32_t r0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * rank) / csize);
-    const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (rank + 1)) / csize);
+    const unsigned groups = kG ? G : 1u, gidx = kG ? gidx_in : 0u;
+    const std::uint32_t parts = groups * csize, part = gidx * csize + rank;
+    const std::uint32_t r0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * part) / parts);
+    const std::uint32_t r1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (part + 1)) / parts);
+    if (kG && threadIdx.x == 0) {
+        // this cluster's rows (the rest of p / z arrives through the workspace)
+        gx.groups = groups;
+        gx.gidx = gidx;
+        gx.c0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * gidx * csize) / parts);
+        gx.c1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (gidx + 1) * csize) / parts);
+        gx.gseq = 0;  // group barriers passed
+        gx.gs = job.gsync;
+        gx.gp = job.p;
+        gx.gz = job.z;
+    }
     unsigned parity = 0;
     const CgMatrix mat{job.colidx, job.a, n - 1, job.nnz};
     constexpr bool kStage = kMode != kCgGlobal;
@@ -256,12 +410,21 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
         else return __ldcg(job.p + c);
     };
     // resident: element i of the full vector in every CTA's copy (own too)
-    auto push = [&](std::uint32_t i, double v) {
+    // group mode: the vector also goes to the workspace for the job's other
+    // clusters (gbuf null: p's buffer, else z's)
+    auto push = [&](std::uint32_t i, double v, double* gbuf) {
         if constexpr (kRes) {
             for (unsigned c = 0; c < csize; ++c) cluster.map_shared_rank(ps, c)[i] = v;
+            if (kG) (gbuf ? gx.gz : gx.gp)[i] = v;
         } else {
             p[i] = v;
         }
+    };
+    // dot product over the job: the cluster's fixed tree, then (group mode)
+    // the clusters' partials in group order, the same bits in every CTA
+    auto job_sum = [&](auto& v) {
+        cg_cluster_sum(v, red, parity, cluster, csize);
+        if (kG) cg_group_sum_fn(&gx, v, sizeof(v) / sizeof(double), rank);
     };
 
     for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = 1.0;
@@ -274,10 +437,11 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
             const double xi = x[i];
             z[i] = 0.0;
             r[i] = xi;
-            push(i, xi);
+            push(i, xi, nullptr);
             v1[0] = fma(xi, xi, v1[0]);
         }
-        cg_cluster_sum(v1, red, parity, cluster, csize);  // also publishes p
+        job_sum(v1);  // also publishes p
+        if (kG) cg_group_exchange_fn(&gx, ps, n, rank, false);
         double rho = v1[0];
         stage_p();
         for (std::uint32_t cgit = 0; cgit < cgitmax; ++cgit) {
@@ -287,7 +451,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
                 q[row] = s;
                 d[0] = fma(gather_p(row), s, d[0]);
             });
-            cg_cluster_sum(d, red, parity, cluster, csize);
+            job_sum(d);
             const double alpha = rho / d[0];
             const double rho0 = rho;
             // z += alpha p, r -= alpha q, rho = r . r
@@ -299,18 +463,20 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
                 r[i] = ri;
                 rr[0] = fma(ri, ri, rr[0]);
             }
-            cg_cluster_sum(rr, red, parity, cluster, csize);
+            job_sum(rr);
             rho = rr[0];
             const double beta = rho / rho0;
-            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, fma(beta, p[i], r[i]));
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, fma(beta, p[i], r[i]), nullptr);
             cluster.sync();  // p complete before anyone gathers it
+            if (kG) cg_group_exchange_fn(&gx, ps, n, rank, false);
             stage_p();
         }
         // ||x - A z||, x . z, z . z: the residual SpMV gathers z — resident:
         // pushed into every CTA's (now unused) p copy; else from HBM
         if constexpr (kRes) {
-            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, z[i]);
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, z[i], reinterpret_cast<double*>(1));
             cluster.sync();
+            if (kG) cg_group_exchange_fn(&gx, ps, n, rank, true);
         }
         double s3[3] = {0.0, 0.0, 0.0};
         cg_spmv<kSeg, kChains>(mat, rs, r0, r1,
@@ -325,13 +491,13 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
                           s3[1] = fma(xi, zi, s3[1]);
                           s3[2] = fma(zi, zi, s3[2]);
                       });
-        cg_cluster_sum(s3, red, parity, cluster, csize);
+        job_sum(s3);
         rnorm = sqrt(s3[0]);
         zeta = job.shift + 1.0 / s3[1];
         const double scale = 1.0 / sqrt(s3[2]);
         for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = scale * z[i];
     }
-    if (rank == 0 && threadIdx.x == 0) {
+    if (gidx == 0 && rank == 0 && threadIdx.x == 0) {
         vgpu_cg_result res;
         res.zeta = zeta;
         res.rnorm = rnorm;
@@ -344,6 +510,41 @@ __global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant
     cluster.sync();
 }
 
+// The group-mode instance runs its body as a separate function: inlined
+// after the join (atomics, a timed spin, cluster barriers), the scheduler
+// interleaved the SpMV's loads with its gathers and FMAs one chain at a time
+// instead of issuing all chains' loads first.
+template <int kMode, unsigned kSeg, bool kG>
+__device__ __noinline__ void cg_body_call(const CgTable& table, unsigned jid, unsigned gidx, unsigned G) {
+    cg_body<kMode, kSeg, kG>(table, jid, gidx, G);
+}
+
+// kGroups: the group-mode instance (kCgResident only); the plain instance
+// compiles without any of its code, so the SpMV keeps its registers
+template <int kMode, unsigned kSeg, bool kGroups = false>
+__global__ void __launch_bounds__(kCgThreads, 1) cg_kernel(const __grid_constant__ CgTable table) {
+    static_assert(!kGroups || kMode == kCgResident, "group mode needs the resident placement");
+    cgx::cluster_group cluster = cgx::this_cluster();
+    const unsigned csize = cluster.num_blocks();
+    const unsigned cid = blockIdx.x / csize;
+    if constexpr (!kGroups) {
+        cg_body<kMode, kSeg, false>(table, cid, 0, 1);
+    } else {
+        const unsigned G = table.groups;
+        const unsigned jid = G == 1 ? cid : G == 2 ? cid >> 1 : G == 4 ? cid >> 2 : cid / 3u;
+        const CgJob& job = table.job[jid];
+        const unsigned rank = cluster.block_rank();
+        // join the job's other clusters, or run it alone, or leave
+        __shared__ unsigned s_mode;
+        if (rank == 0 && threadIdx.x == 0) s_mode = G > 1 ? cg_group_join(job.gsync, G, table.join_ns) : kCgSolo;
+        cluster.sync();
+        const unsigned m = *cluster.map_shared_rank(&s_mode, 0);
+        cluster.sync();  // rank 0's word is read before any CTA leaves
+        if (m == kCgExit) return;
+        if (m == kCgGrouped) cg_body_call<kMode, kSeg, true>(table, jid, cid - jid * G, G);
+        else cg_body_call<kMode, kSeg, false>(table, jid, 0, 1);
+    }
+}
 
 // ---- grid variant: a job spans plain CTAs on any SMs ------------------------
 // Clusters live inside one GPC (16-CTA clusters: 7 co-resident on a B200),

@@ -298,3 +298,71 @@ def test_every_payload_kind_in_one_gvm_batch(style):
     vg = np.frombuffer(outs[6], np.float32).astype(np.float64)
     ve = oracle.es(es).ravel()
     assert np.abs(vg - ve).sum() / np.abs(ve).sum() <= 1e-5
+
+
+@pytest.mark.parametrize("switch", ["auto", "groups2", "groups3", "solo", "off"])
+def test_nas_cg_group_mode_class_a(switch):
+    """Group mode (k_cg.cuh): a job over several clusters that exchange dot
+    partials and p / z slices through the workspace. Eight class-A jobs in
+    one GVM batch and one class-A job on the native path, each meeting
+    NPB's verification (1e-10) and the oracle (1e-12), the eight batch
+    results bit-identical (same input, same fixed reduction order; not under
+    solo, where arrival order picks each job's split). auto:
+    the host's shape (group mode for the single native job only);
+    groups2/3: VGPU_CG_GROUPS forces 2 / 3 clusters per job in the batch
+    too; solo: forced 2 with VGPU_CG_JOIN_US=0, so the first cluster of a
+    job usually claims it alone and its siblings exit (the fallback for
+    clusters that are not co-resident); off: VGPU_CG_GROUPS=1."""
+    import subprocess
+    import sys
+    code = r'''
+import threading
+from oracle import oracle
+from paper_1511_07658_b200 import vgpu as V
+inp = V.cg_input_for_class("A")
+want = V.cg_class("A").zeta_verify
+ref = oracle.cg_run(inp).zeta
+inst = "cgg8"
+V.unlink_os_instance(inst, 8)
+cfg = V.GvmConfig(instance=inst, max_clients=8, barrier_size=8, per_client_shm_bytes=len(inp) + (1 << 16),
+                  barrier_window=200000, clock=V.ClockMode.Real)
+outs = [None] * 8
+with V.GvmDaemon.start_os(cfg):
+    def w(k):
+        h = V.req(inst)
+        outs[k] = h.run_task(inp, V.KernelDescriptor("nas-cg"))
+        h.rls(); h.close()
+    ts = [threading.Thread(target=w, args=(k,)) for k in range(8)]
+    [t.start() for t in ts]; [t.join() for t in ts]
+outs.append(V.native_run_task(inp, V.KernelDescriptor("nas-cg")))
+for o in outs:
+    zeta = V.cg_result(o)[0]
+    print("job", abs(zeta - want) / want <= 1e-10 and abs(zeta - ref) / ref <= 1e-12, zeta)
+print("same", all(o == outs[0] for o in outs[:8]))
+'''
+    env = dict(os.environ, VGPU_CG_VERBOSE="1")
+    if switch == "solo":
+        env["VGPU_CG_JOIN_US"] = "0"
+        env["VGPU_CG_GROUPS"] = "2"
+    elif switch.startswith("groups"):
+        env["VGPU_CG_GROUPS"] = switch[-1]
+    elif switch == "off":
+        env["VGPU_CG_GROUPS"] = "1"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l.split() for l in out.stdout.splitlines() if l.strip()]
+    jobs = [l for l in lines if l[0] == "job"]
+    assert len(jobs) == 9 and all(l[1] == "True" for l in jobs), out.stdout
+    if switch != "solo":  # solo: each job grouped or alone by arrival order, so its sum order varies
+        assert ["same", "True"] in lines, out.stdout
+    if switch == "off":
+        assert "groups=1" in out.stderr and "groups=2" not in out.stderr, out.stderr[-2000:]
+    else:
+        import re
+        shapes = {(int(j), int(g)) for j, g in re.findall(r"jobs=(\d+) width=\d+ groups=(\d+)", out.stderr)}
+        if switch == "auto":  # the batch keeps one cluster per job, the single job is grouped
+            assert (8, 1) in shapes and any(j == 1 and g > 1 for j, g in shapes), shapes
+        else:
+            assert (8, int(switch[-1]) if switch != "solo" else 2) in shapes, shapes
