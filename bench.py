@@ -1176,7 +1176,8 @@ def main():
             else:
                 cores = os.cpu_count()
                 line = {"impl": "reference", "metric": METRIC, "value": r["jobs_per_s"],
-                        "unit": "jobs/s", "higher_is_better": True, "n_gpus": 0, "steps": r["rounds"],
+                        "unit": "jobs/s", "higher_is_better": True, "n_gpus": world,
+                        "device": "host CPU cores only (the reference has no GPU path)", "steps": r["rounds"],
                         "warmup": r["warmup"], "ms_per_step": r["ms_per_round"], "dtype": DTYPE[args.workload],
                         "data": "synthetic", "scaling": "weak", "vs_baseline": None,
                         "config": config,
