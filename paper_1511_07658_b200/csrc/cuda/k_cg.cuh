@@ -286,13 +286,17 @@ __device__ __forceinline__ void cg_spmv(const CgMatrix& m, const std::uint32_t* 
             for (std::uint32_t k = rs[row - r0] + sl; k < k1; k += kCgChains * seg) {
                 std::uint32_t col[kCgChains];
                 double av[kCgChains];
+                // one 64-bit address per array and iteration; the chains
+                // are immediate offsets from it (a 32-bit k + c * seg per
+                // chain cost a wide multiply-add and a register pair each)
+                const std::uint32_t* __restrict__ pc = colidx + k;
+                const double* __restrict__ pa = a + k;
 #pragma unroll
                 for (unsigned c = 0; c < kCgChains; ++c) {
-                    const std::uint32_t kk = k + c * seg;
-                    const bool in = kk < k1;
+                    const bool in = k + c * seg < k1;
                     // malformed column indices are clamped into bounds
-                    col[c] = in ? min(__ldg(colidx + kk), nm1) : 0u;
-                    av[c] = in ? __ldg(a + kk) : 0.0;
+                    col[c] = in ? min(__ldg(pc + c * seg), nm1) : 0u;
+                    av[c] = in ? __ldg(pa + c * seg) : 0.0;
                 }
 #pragma unroll
                 for (unsigned c = 0; c < kCgChains; ++c) acc[c] = fma(av[c], gather(col[c]), acc[c]);
