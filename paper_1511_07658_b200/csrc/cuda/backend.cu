@@ -450,8 +450,8 @@ unsigned cg_cluster_for(const vgpu_cg_header& h, unsigned jobs) {
 // kernel (its body is a separate function, whose register budget lets the
 // scheduler batch only two of the four load chains), so it pays only where
 // the SM count gained is large: a launch with ONE class-A-size job (n >=
-// 10^4; 3 x 16 CTAs: 14.7 -> 11.1-11.7 ms). With 8 jobs (10-CTA clusters ->
-// 12-16 CTAs per job) it lost (22.3 -> 30.6 ms), so batches keep one
+// 10^4; 4 x 13 CTAs: 14.7 -> 10.85 ms). With 8 jobs (10-CTA clusters ->
+// 12-15 CTAs per job) it lost (22.0 -> 30-33 ms), so batches keep one
 // cluster per job. VGPU_CG_GROUPS=1 disables it, =k forces k groups.
 struct CgShape {
     unsigned cs = 0, groups = 1;

@@ -103,10 +103,10 @@ __device__ __forceinline__ std::uint64_t cg_globaltimer() {
 // A CTA's group-mode state, in shared memory (CTA-uniform; read only on
 // the group paths, so the SpMV loop keeps its registers).
 struct CgGroupCtx {
-    unsigned groups, gidx, c0, c1, gseq;  // c0..c1: this cluster's rows
+    unsigned groups, gidx, gseq;
     CgGroupSync* gs;
-    double* gp;  // the workspace copies of p and z the other clusters read
-    double* gz;
+    double* gp;  // the workspace copies of r (every CG step) and z (every
+    double* gz;  // outer iteration) that all CTAs of the job read whole
 };
 
 // One thread per cluster (rank 0, thread 0): grouped, solo or exit.
@@ -152,48 +152,74 @@ __device__ __forceinline__ void cg_group_barrier(CgGroupSync* s, unsigned groups
 // loads with its gathers and FMAs one chain at a time (3.6x slower).
 //
 // v[0..W) holds the cluster's total (identical in every CTA): the job's
-// total over the groups, summed in group order.
-__device__ __noinline__ void cg_group_sum_fn(CgGroupCtx* gx, double* v, int W, unsigned rank) {
+// total over the groups, summed in group order (the partials are loaded at
+// once, then added in that order).
+template <int W>
+__device__ __noinline__ void cg_group_sum_fn(CgGroupCtx* gx, double* v, unsigned rank) {
     CgGroupSync* const gs = gx->gs;
     const unsigned slot = gx->gseq & 1u, ng = gx->groups, target = gx->gseq + 1;
     if (rank == 0 && threadIdx.x == 0)
         for (int w = 0; w < W; ++w) gs->part[slot][gx->gidx][w] = v[w];
     cg_group_barrier(gs, ng, gx->gidx, rank, target);  // ends in __syncthreads
     if (threadIdx.x == 0) gx->gseq = target;
+    double part[kCgMaxGroups][W];
+#pragma unroll
+    for (int g = 0; g < kCgMaxGroups; ++g)
+#pragma unroll
+        for (int w = 0; w < W; ++w) part[g][w] = g < static_cast<int>(ng) ? __ldcg(&gs->part[slot][g][w]) : 0.0;
+#pragma unroll
     for (int w = 0; w < W; ++w) {
         double t = 0.0;
-        for (unsigned g = 0; g < ng; ++g) t += __ldcg(&gs->part[slot][g][w]);
+#pragma unroll
+        for (int g = 0; g < kCgMaxGroups; ++g)
+            if (g < static_cast<int>(ng)) t += part[g][w];
         v[w] = t;
     }
 }
 
-// After the cluster barrier that completed this cluster's part of p (or z,
-// `use_z`): the groups' barrier, then the rows outside this cluster's range
-// from the workspace into this CTA's full copy ps.
-__device__ __noinline__ void cg_group_exchange_fn(CgGroupCtx* gx, double* ps, std::uint32_t n, unsigned rank,
-                                                  bool use_z) {
+// The groups' barrier alone (after a cluster barrier that completed this
+// cluster's writes to the workspace).
+__device__ __noinline__ void cg_group_sync_fn(CgGroupCtx* gx, unsigned rank) {
     const unsigned target = gx->gseq + 1;
     cg_group_barrier(gx->gs, gx->groups, gx->gidx, rank, target);
-    const double* src = use_z ? gx->gz : gx->gp;
-    const std::uint32_t c0 = gx->c0, c1 = gx->c1;
-    const std::uint32_t nf = n - (c1 - c0);
-    for (std::uint32_t i0 = threadIdx.x; i0 < nf; i0 += 4 * kCgThreads) {
-        double t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const std::uint32_t k = i0 + u * kCgThreads;
-            const std::uint32_t i = k < c0 ? k : k + (c1 - c0);
-            if (k < nf) t[u] = __ldcg(src + i);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const std::uint32_t k = i0 + u * kCgThreads;
-            const std::uint32_t i = k < c0 ? k : k + (c1 - c0);
-            if (k < nf) ps[i] = t[u];
-        }
-    }
-    __syncthreads();  // also: every thread read gseq before it advances
     if (threadIdx.x == 0) gx->gseq = target;
+    __syncthreads();
+}
+
+// ps[i] = src[i] (f == nullptr) or fma(beta, ps[i], src[i]) for the whole
+// vector: the workspace -> this CTA's full copy, 16-byte loads, eight in
+// flight per thread.
+__device__ __noinline__ void cg_full_vector_fn(double* ps, const double* src, std::uint32_t n, bool update,
+                                               double beta) {
+    if ((reinterpret_cast<std::uintptr_t>(src) & 15u) == 0) {
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        double2* p2 = reinterpret_cast<double2*>(ps);
+        const std::uint32_t n2 = n / 2;
+        for (std::uint32_t i0 = threadIdx.x; i0 < n2; i0 += 8 * kCgThreads) {
+            double2 t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const std::uint32_t i = i0 + u * kCgThreads;
+                if (i < n2) t[u] = __ldcg(s2 + i);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const std::uint32_t i = i0 + u * kCgThreads;
+                if (i < n2) {
+                    if (update) {
+                        const double2 o = p2[i];
+                        t[u].x = fma(beta, o.x, t[u].x);
+                        t[u].y = fma(beta, o.y, t[u].y);
+                    }
+                    p2[i] = t[u];
+                }
+            }
+        }
+        if ((n & 1u) && threadIdx.x == 0) ps[n - 1] = update ? fma(beta, ps[n - 1], __ldcg(src + n - 1)) : __ldcg(src + n - 1);
+    } else {
+        for (std::uint32_t i = threadIdx.x; i < n; i += kCgThreads)
+            ps[i] = update ? fma(beta, ps[i], __ldcg(src + i)) : __ldcg(src + i);
+    }
     __syncthreads();
 }
 
@@ -355,8 +381,6 @@ __device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsi
         // this cluster's rows (the rest of p / z arrives through the workspace)
         gx.groups = groups;
         gx.gidx = gidx;
-        gx.c0 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * gidx * csize) / parts);
-        gx.c1 = static_cast<std::uint32_t>((static_cast<std::uint64_t>(n) * (gidx + 1) * csize) / parts);
         gx.gseq = 0;  // group barriers passed
         gx.gs = job.gsync;
         gx.gp = job.p;
@@ -413,13 +437,12 @@ __device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsi
         if constexpr (kStage) return ps[c];
         else return __ldcg(job.p + c);
     };
-    // resident: element i of the full vector in every CTA's copy (own too)
-    // group mode: the vector also goes to the workspace for the job's other
-    // clusters (gbuf null: p's buffer, else z's)
-    auto push = [&](std::uint32_t i, double v, double* gbuf) {
+    // resident: element i of the full vector in every CTA's copy (own too).
+    // Group mode never pushes: every CTA computes the whole p itself from
+    // the full r the groups publish (below).
+    auto push = [&](std::uint32_t i, double v) {
         if constexpr (kRes) {
             for (unsigned c = 0; c < csize; ++c) cluster.map_shared_rank(ps, c)[i] = v;
-            if (kG) (gbuf ? gx.gz : gx.gp)[i] = v;
         } else {
             p[i] = v;
         }
@@ -428,24 +451,28 @@ __device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsi
     // the clusters' partials in group order, the same bits in every CTA
     auto job_sum = [&](auto& v) {
         cg_cluster_sum(v, red, parity, cluster, csize);
-        if (kG) cg_group_sum_fn(&gx, v, sizeof(v) / sizeof(double), rank);
+        if constexpr (kG) cg_group_sum_fn<sizeof(v) / sizeof(double)>(&gx, v, rank);
     };
 
     for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = 1.0;
-    double zeta = 0.0, rnorm = 0.0;
+    double zeta = 0.0, rnorm = 0.0, scale = 1.0;
     const std::uint32_t niter = job.niter, cgitmax = job.cgitmax;
     for (std::uint32_t it = 0; it < niter; ++it) {
         // conj_grad: q = z = 0, r = p = x, rho = r . r
         double v1[1] = {0.0};
+        if constexpr (kG) {
+            // p = x over the whole vector, from what every CTA holds: x = 1
+            // at first, then scale * z (the full z the residual gathered)
+            for (std::uint32_t i = threadIdx.x; i < n; i += kCgThreads) ps[i] = it == 0 ? 1.0 : scale * ps[i];
+        }
         for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) {
             const double xi = x[i];
             z[i] = 0.0;
             r[i] = xi;
-            push(i, xi, nullptr);
+            if constexpr (!kG) push(i, xi);
             v1[0] = fma(xi, xi, v1[0]);
         }
-        job_sum(v1);  // also publishes p
-        if (kG) cg_group_exchange_fn(&gx, ps, n, rank, false);
+        job_sum(v1);  // also publishes p (and orders the group-mode p writes)
         double rho = v1[0];
         stage_p();
         for (std::uint32_t cgit = 0; cgit < cgitmax; ++cgit) {
@@ -465,22 +492,33 @@ __device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsi
                 z[i] = fma(alpha, pi, z[i]);
                 const double ri = fma(-alpha, q[i], r[i]);
                 r[i] = ri;
+                if constexpr (kG) gx.gp[i] = ri;  // the groups' copy of r
                 rr[0] = fma(ri, ri, rr[0]);
             }
-            job_sum(rr);
+            job_sum(rr);  // group mode: its barrier also publishes r
             rho = rr[0];
             const double beta = rho / rho0;
-            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, fma(beta, p[i], r[i]), nullptr);
-            cluster.sync();  // p complete before anyone gathers it
-            if (kG) cg_group_exchange_fn(&gx, ps, n, rank, false);
+            if constexpr (kG) {
+                // p = r + beta p over the whole vector in every CTA (the same
+                // bits as the owner's), no push and no barrier of its own
+                cg_full_vector_fn(ps, gx.gp, n, true, beta);
+            } else {
+                for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, fma(beta, p[i], r[i]));
+                cluster.sync();  // p complete before anyone gathers it
+            }
             stage_p();
         }
         // ||x - A z||, x . z, z . z: the residual SpMV gathers z — resident:
         // pushed into every CTA's (now unused) p copy; else from HBM
-        if constexpr (kRes) {
-            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, z[i], reinterpret_cast<double*>(1));
+        if constexpr (kG) {
+            // z to the workspace, the groups' barrier, the whole z back
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) gx.gz[i] = z[i];
             cluster.sync();
-            if (kG) cg_group_exchange_fn(&gx, ps, n, rank, true);
+            cg_group_sync_fn(&gx, rank);
+            cg_full_vector_fn(ps, gx.gz, n, false, 0.0);
+        } else if constexpr (kRes) {
+            for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) push(i, z[i]);
+            cluster.sync();
         }
         double s3[3] = {0.0, 0.0, 0.0};
         cg_spmv<kSeg, kChains>(mat, rs, r0, r1,
@@ -498,7 +536,7 @@ __device__ __forceinline__ void cg_body(const CgTable& table, unsigned jid, unsi
         job_sum(s3);
         rnorm = sqrt(s3[0]);
         zeta = job.shift + 1.0 / s3[1];
-        const double scale = 1.0 / sqrt(s3[2]);
+        scale = 1.0 / sqrt(s3[2]);
         for (std::uint32_t i = r0 + threadIdx.x; i < r1; i += kCgThreads) x[i] = scale * z[i];
     }
     if (gidx == 0 && rank == 0 && threadIdx.x == 0) {
