@@ -39,14 +39,15 @@ constexpr std::uint32_t kCgStageMax = 24576;  // rows whose p fits in shared mem
 constexpr std::uint32_t kCgSmemBytes = 224 * 1024;  // dynamic shared memory cap per CTA
 
 // Group mode (kCgResident only): a job spans G clusters of the launch's
-// width instead of one, so a batch that leaves SMs idle as one cluster per
-// job (clusters live inside a GPC) gets more of them. The clusters of a job
-// exchange what crosses them through the job's HBM/L2 workspace: each
-// cluster's dot-product partial (one slot per group, summed by every CTA in
-// group order, so all CTAs keep identical bits) and the new p / z slices
-// (written beside the DSMEM push, copied into each CTA's full copy after
-// the groups' barrier). The barrier between groups is a release counter
-// per group. A job's clusters are only co-resident when nothing else holds
+// width instead of one, so a job that would get one GPC's worth of SMs gets
+// more of them (the host uses it for a launch with one large job). The
+// clusters of a job exchange what crosses them through the job's HBM/L2
+// workspace: each cluster's dot-product partial (one slot per group, summed
+// by every CTA in group order, so all CTAs keep identical bits), each CTA's
+// r slice (written before the r . r barrier, after which every CTA computes
+// the whole p = r + beta p itself: no p pushes, two group barriers per CG
+// step) and, once per outer iteration, z. The barrier between groups is a
+// release counter per group. A job's clusters are only co-resident when nothing else holds
 // the SMs, so the groups first JOIN: when all G arrive within the wait
 // budget the job runs grouped; otherwise the first arrival claims the job
 // and runs it alone (rows over its own cluster, the plain schedule) and the
